@@ -1,0 +1,496 @@
+/*
+ * oracle.cpp — TEST INFRASTRUCTURE ONLY.  Plain, slow, double-precision CPU
+ * Katsevich reconstruction for helical cone-beam CT with a curved detector,
+ * written directly from arXiv 2201.02309 §II.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs may load this library.  It shares no code with the
+ * CUDA product path (paper_2201_02309_b200/): its own geometry struct, its own
+ * PI-line solver (bisection), its own ψ̂ root finder (scan + bisection), its
+ * own filter (direct-sum Hilbert) and backprojection.
+ *
+ * Parity pins: see tests/test_oracle_*.py and DESIGN.md "Oracle pins".
+ * Every function cites the passage it follows; readings of silent / ambiguous
+ * points follow SURVEY.md §8(c) A1-A21 and are listed in DESIGN.md.
+ *
+ * Unlike the product (which uses pitch-periodic tables, P:l.174-185), the
+ * oracle evaluates PI-lines, v*, α*, w* and the BP weights at ABSOLUTE
+ * coordinates (z_j + kP, λ = v·Δλ) for every pitch k, solving afresh — the
+ * plain definition, so periodicity is a checked property, not an assumption.
+ */
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+extern "C" {
+
+/* Oracle-private geometry description (mirrors the problem statement of
+ * PAPER.md l.87-98, l.117, l.189, l.311-349).  Not shared with the product. */
+typedef struct {
+    double R, D, P, lambda0, z0, r_fov;      /* helix radius, src-det distance, pitch, start angle/height, FOV radius */
+    int32_t n_rows; double d_w;              /* w_m = (m-(n_rows-1)/2) d_w   (P:l.340) */
+    int32_t n_cols; double d_alpha, alpha_offset; /* α_l = (l-(n_cols-1)/2+off) d_alpha (P:l.328) */
+    int32_t views_per_turn;                  /* Δλ = 2π / views_per_turn */
+    int32_t nx, ny; double dx, dy;           /* x_i = (i - nx/2) dx  (P:l.316) */
+    int32_t nz;                              /* slices per pitch: z_j = j P / nz (P:l.357, l.740) */
+    int32_t n_psi;                           /* κ-lines (0 -> 2 n_rows + 1) */
+} ora_geom;
+
+}  // extern "C"
+
+namespace {
+
+const double PI = 3.14159265358979323846;
+
+struct G {
+    ora_geom g;
+    double dlam, h, r_fov, alpha_m, psi_max, dpsi, kappa_scale;
+    int n_psi;
+};
+
+G make(const ora_geom *in)
+{
+    G o; o.g = *in;
+    o.dlam = 2.0 * PI / in->views_per_turn;
+    o.h = in->P / (2.0 * PI);                               /* h = P/2π */
+    double hx = 0.5 * in->nx * in->dx, hy = 0.5 * in->ny * in->dy;
+    o.r_fov = in->r_fov > 0 ? in->r_fov : std::sqrt(hx * hx + hy * hy) * (1.0 + 1e-9);  /* A17 */
+    o.alpha_m = std::asin(o.r_fov / in->R);                 /* α_m = arcsin(r/R), P:l.133 */
+    o.psi_max = PI / 2 + o.alpha_m;                         /* ψ ∈ [-π/2-α_m, π/2+α_m], P:l.132 */
+    o.n_psi = in->n_psi > 0 ? in->n_psi : 2 * in->n_rows + 1;   /* A6 */
+    o.dpsi = 2.0 * o.psi_max / (o.n_psi - 1);
+    o.kappa_scale = in->D * in->P / (2.0 * PI * in->R);     /* DP/(2πR), Eq. (11) P:l.135 */
+    return o;
+}
+
+inline double alpha_l(const G &o, int l) { return (l - 0.5 * (o.g.n_cols - 1) + o.g.alpha_offset) * o.g.d_alpha; }
+inline double w_m(const G &o, int m) { return (m - 0.5 * (o.g.n_rows - 1)) * o.g.d_w; }
+inline double psi_i(const G &o, int i) { return -o.psi_max + i * o.dpsi; }
+inline double x_i(const G &o, int i) { return (i - 0.5 * o.g.nx) * o.g.dx; }
+inline double y_i(const G &o, int i) { return (i - 0.5 * o.g.ny) * o.g.dy; }
+inline double z_j(const G &o, int j, int pitch) { return j * o.g.P / o.g.nz + pitch * o.g.P; }
+inline bool in_fov(const G &o, double x, double y) { return x * x + y * y < o.r_fov * o.r_fov; }  /* U, A17 */
+
+/* A12: snap a floor/ceil argument to the nearest integer when within 1e-9. */
+inline double snap(double a)
+{
+    double r = std::nearbyint(a);
+    return std::fabs(a - r) < 1e-9 ? r : a;
+}
+
+/* Linear-interpolation index rule of A9/A12 on a grid of n nodes: returns
+ * false when pos lies outside [0, n-1] (zero contribution). */
+inline bool lin_index(double pos, int n, int *idx, double *frac)
+{
+    double a = snap(pos);
+    if (!(a >= 0.0 && a <= n - 1)) return false;
+    int m = (int)std::floor(a);
+    if (m >= n - 1) m = n - 2;
+    if (m < 0) m = 0;          /* n == 1 degenerate */
+    *idx = m; *frac = a - m;
+    return true;
+}
+
+/* ---------- PI-line (P:l.104, l.194) ----------
+ * The PI-line of x is the chord a(σ-δ)a(σ+δ) through x with 0 < 2δ < 2π.
+ * Chord points: xy = R cosδ e_r(σ) + u R sinδ e_t(σ), z = z0 + h(σ + uδ),
+ * e_r = (cos(σ+λ0), sin(σ+λ0)), e_t = (-sin(σ+λ0), cos(σ+λ0)), u ∈ [-1,1].
+ * Given σ, x fixes δ = arccos((x·e_r)/R) and u = (x·e_t)/(R sinδ); σ solves
+ * F(σ) = σ + u δ - (z - z0)/h = 0, bracketed by [ζ-π, ζ+π], ζ = (z-z0)/h.
+ * Solved by plain bisection to machine precision. */
+void pi_line(const G &o, double x, double y, double z, double *li, double *lo)
+{
+    const double R = o.g.R, lam0 = o.g.lambda0;
+    const double zeta = (z - o.g.z0) / o.h;
+    auto F = [&](double s, double *dd) {
+        double c = std::cos(s + lam0), sn = std::sin(s + lam0);
+        double cr = (x * c + y * sn) / R;
+        cr = std::max(-1.0, std::min(1.0, cr));
+        double d = std::acos(cr);
+        double u = (-x * sn + y * c) / (R * std::sin(d));
+        *dd = d;
+        return s + u * d - zeta;
+    };
+    double a = zeta - PI, b = zeta + PI, d;
+    for (int it = 0; it < 200; ++it) {
+        double m = 0.5 * (a + b);
+        if (m == a || m == b) break;
+        if (F(m, &d) < 0.0) a = m; else b = m;
+    }
+    double s = 0.5 * (a + b);
+    F(s, &d);
+    *li = s - d;
+    *lo = s + d;
+}
+
+/* ---------- κ-line height, Eq. (11) P:l.134-136 ---------- */
+double w_kappa(const G &o, double alpha, double psi)
+{
+    double r = std::fabs(psi) < 1e-8 ? 1.0 - psi * psi / 3.0 : psi / std::tan(psi);  /* ψ/tanψ -> 1 */
+    return o.kappa_scale * (psi * std::cos(alpha) + r * std::sin(alpha));
+}
+
+/* ---------- ψ̂(α, w): "angle ψ of the smallest absolute value" with
+ * w = w_κ(α, ψ)  (P:l.147-150).  Reading A8: the first root met moving out
+ * from ψ = 0 (toward +ψ if w > w_κ(α,0), else toward -ψ) within
+ * [-ψ_max, ψ_max]; none -> undefined.  Fine scan + bisection. */
+bool psi_hat(const G &o, double alpha, double w, double *out)
+{
+    double f0 = w_kappa(o, alpha, 0.0) - w;
+    if (f0 == 0.0) { *out = 0.0; return true; }
+    const double dir = f0 < 0.0 ? 1.0 : -1.0;   /* w above w_κ(α,0): go to +ψ */
+    const int NS = 20000;
+    double prev_p = 0.0, prev_f = f0;
+    for (int k = 1; k <= NS; ++k) {
+        double p = dir * o.psi_max * k / NS;
+        double f = w_kappa(o, alpha, p) - w;
+        if ((f >= 0.0) != (prev_f >= 0.0) || f == 0.0) {
+            double a = prev_p, b = p, fa = prev_f;
+            for (int it = 0; it < 200; ++it) {
+                double m = 0.5 * (a + b);
+                if (m == a || m == b) break;
+                double fm = w_kappa(o, alpha, m) - w;
+                if ((fm >= 0.0) == (fa >= 0.0) && fm != 0.0) { a = m; fa = fm; } else b = m;
+            }
+            *out = 0.5 * (a + b);
+            return true;
+        }
+        prev_p = p; prev_f = f;
+    }
+    return false;
+}
+
+/* ---------- BP end weights (A11, A12) ----------
+ * t_i = λ_i/Δλ, t_o = λ_o/Δλ, view k owns the cell [k-½, k+½];
+ * ω_k = |[k-½,k+½] ∩ [t_i,t_o]|, k_first = ⌊t_i+½⌋, k_last = ⌈t_o-½⌉. */
+void bp_weights(const G &o, double li, double lo, int64_t *kf, int64_t *kl, double *wf, double *wl)
+{
+    double ti = li / o.dlam, to = lo / o.dlam;
+    int64_t a = (int64_t)std::floor(snap(ti + 0.5));
+    int64_t b = (int64_t)std::ceil(snap(to - 0.5));
+    auto omega = [&](int64_t k) {
+        double lo_ = std::max((double)k - 0.5, ti), hi_ = std::min((double)k + 0.5, to);
+        return std::max(0.0, hi_ - lo_);
+    };
+    *kf = a; *kl = b; *wf = omega(a); *wl = omega(b);
+}
+
+/* Slab of pitch k (P:l.234-246): BP views [K_lo, K_hi] over
+ * all in-FOV voxels of the pitch, plus one derivative halo view each side. */
+void pitch_bp_range(const G &o, int pitch, int64_t *Klo, int64_t *Khi)
+{
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    const int nx = o.g.nx, ny = o.g.ny, nz = o.g.nz;
+    #pragma omp parallel for collapse(2) reduction(min:lo) reduction(max:hi) schedule(dynamic, 4)
+    for (int j = 0; j < nz; ++j)
+        for (int iy = 0; iy < ny; ++iy)
+            for (int ix = 0; ix < nx; ++ix) {
+                double x = x_i(o, ix), y = y_i(o, iy);
+                if (!in_fov(o, x, y)) continue;
+                double li, lo_;
+                pi_line(o, x, y, z_j(o, j, pitch), &li, &lo_);
+                int64_t kf, kl; double wf, wl;
+                bp_weights(o, li, lo_, &kf, &kl, &wf, &wl);
+                lo = std::min(lo, kf); hi = std::max(hi, kl);
+            }
+    *Klo = lo; *Khi = hi;
+}
+
+/* ---------- Rebinning maps, pre-calculated once (P:l.174, l.193) ----------
+ * Forward: row position of w_κ(α_l, ψ_i) (Eq. 11) on the w grid.
+ * Backward: ψ-grid position of ψ̂(α_l, w_m) (Eq. 14, reading A8).
+ * Index/fraction in the canonical A12 form; idx = -1 marks "0 contribution". */
+struct Rebin {
+    std::vector<int32_t> fi, bi;
+    std::vector<double> ff, bf;
+};
+
+Rebin rebin_maps(const G &o)
+{
+    const int nr = o.g.n_rows, nc = o.g.n_cols, np = o.n_psi;
+    Rebin rb;
+    rb.fi.assign((size_t)np * nc, -1); rb.ff.assign((size_t)np * nc, 0.0);
+    rb.bi.assign((size_t)nr * nc, -1); rb.bf.assign((size_t)nr * nc, 0.0);
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < np; ++i)
+        for (int l = 0; l < nc; ++l) {
+            double pos = w_kappa(o, alpha_l(o, l), psi_i(o, i)) / o.g.d_w + 0.5 * (nr - 1);
+            int m; double f;
+            if (lin_index(pos, nr, &m, &f)) { rb.fi[(size_t)i * nc + l] = m; rb.ff[(size_t)i * nc + l] = f; }
+        }
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            double ph; int i; double f;
+            if (psi_hat(o, alpha_l(o, l), w_m(o, m), &ph) && lin_index((ph + o.psi_max) / o.dpsi, np, &i, &f)) {
+                rb.bi[(size_t)m * nc + l] = i; rb.bf[(size_t)m * nc + l] = f;
+            }
+        }
+    return rb;
+}
+
+/* ---------- Filtering steps 1-6 for one view (P:l.117-154, Eqs. 8-15) ----------
+ * g(v) at sino[v - s0]; writes optional stage outputs (double, [rows][cols] or
+ * [n_psi][cols]).  Discretisation readings: A5 (centred differences, one-sided
+ * at the α edges), A9 (linear rebins, 0 outside), A10 (band-limited Hilbert). */
+void filter_view(const G &o, const float *sino, int64_t s0, int64_t v,
+                 const std::vector<double> &Kh, const Rebin &rb,
+                 double *g2o, double *g3o, double *g4o, double *gFo)
+{
+    const int nr = o.g.n_rows, nc = o.g.n_cols, np = o.n_psi;
+    auto g = [&](int64_t vv, int m, int l) { return (double)sino[((vv - s0) * nr + m) * (int64_t)nc + l]; };
+    std::vector<double> g2((size_t)nr * nc), g3((size_t)np * nc), g4((size_t)np * nc);
+    /* Step 1, Eq. (8): g1 = (∂_q + ∂_α) g |_{q=λ}; step 2, Eq. (9): g2 = D/sqrt(D²+w²) g1 */
+    for (int m = 0; m < nr; ++m) {
+        double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + w_m(o, m) * w_m(o, m));
+        for (int l = 0; l < nc; ++l) {
+            double dq = (g(v + 1, m, l) - g(v - 1, m, l)) / (2.0 * o.dlam);
+            double da;
+            if (l == 0) da = (g(v, m, 1) - g(v, m, 0)) / o.g.d_alpha;
+            else if (l == nc - 1) da = (g(v, m, nc - 1) - g(v, m, nc - 2)) / o.g.d_alpha;
+            else da = (g(v, m, l + 1) - g(v, m, l - 1)) / (2.0 * o.g.d_alpha);
+            g2[(size_t)m * nc + l] = wgt * (dq + da);
+        }
+    }
+    /* Step 3, Eqs. (10)-(11): g3(α,ψ) = g2(α, w_κ(α,ψ)), linear in w, 0 outside */
+    for (int i = 0; i < np; ++i)
+        for (int l = 0; l < nc; ++l) {
+            size_t t = (size_t)i * nc + l;
+            int m = rb.fi[t]; double f = rb.ff[t];
+            g3[t] = m < 0 ? 0.0 : (1.0 - f) * g2[(size_t)m * nc + l] + f * g2[(size_t)(m + 1) * nc + l];
+        }
+    /* Step 4, Eq. (12) with h_H(s) = 1/(πs) (Eq. e4): g4(α_l) = Σ_l' K[l-l'] g3(α_l') */
+    for (int i = 0; i < np; ++i)
+        for (int l = 0; l < nc; ++l) {
+            double acc = 0.0;
+            for (int lp = 0; lp < nc; ++lp) acc += Kh[(size_t)(l - lp + nc - 1)] * g3[(size_t)i * nc + lp];
+            g4[(size_t)i * nc + l] = acc;
+        }
+    /* Steps 5-6, Eqs. (13)-(15): g5 = g4(α, ψ̂(α,w)), linear in ψ; gF = cosα g5 */
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            size_t t = (size_t)m * nc + l;
+            int i = rb.bi[t]; double f = rb.bf[t];
+            double val = i < 0 ? 0.0 : (1.0 - f) * g4[(size_t)i * nc + l] + f * g4[(size_t)(i + 1) * nc + l];
+            if (gFo) gFo[t] = std::cos(alpha_l(o, l)) * val;
+        }
+    if (g2o) std::memcpy(g2o, g2.data(), sizeof(double) * g2.size());
+    if (g3o) std::memcpy(g3o, g3.data(), sizeof(double) * g3.size());
+    if (g4o) std::memcpy(g4o, g4.data(), sizeof(double) * g4.size());
+}
+
+/* Band-limited kernel of h_H(sin(α-α')) dα' (A10):
+ * K[d] = Δα (1 - cos πd) / (π sin(dΔα)), K[0] = 0; 1 - cos πd = 1 - (-1)^d. */
+std::vector<double> hilbert_kernel(const G &o)
+{
+    const int nc = o.g.n_cols;
+    std::vector<double> K((size_t)(2 * nc - 1), 0.0);
+    for (int d = -(nc - 1); d <= nc - 1; ++d) {
+        if (d == 0) continue;
+        double one_minus_cos = (d % 2 == 0) ? 0.0 : 2.0;
+        K[(size_t)(d + nc - 1)] = o.g.d_alpha * one_minus_cos / (PI * std::sin(d * o.g.d_alpha));
+    }
+    return K;
+}
+
+/* Bilinear sample of gF(view) at (α*, w*); 0 outside the sample range (A9). */
+inline double sample(const G &o, const double *gv, double alpha, double w)
+{
+    int l, m; double fa, fw;
+    if (!lin_index(alpha / o.g.d_alpha + 0.5 * (o.g.n_cols - 1) - o.g.alpha_offset, o.g.n_cols, &l, &fa)) return 0.0;
+    if (!lin_index(w / o.g.d_w + 0.5 * (o.g.n_rows - 1), o.g.n_rows, &m, &fw)) return 0.0;
+    const int nc = o.g.n_cols;
+    double a0 = (1.0 - fa) * gv[(size_t)m * nc + l] + fa * gv[(size_t)m * nc + l + 1];
+    double a1 = (1.0 - fa) * gv[(size_t)(m + 1) * nc + l] + fa * gv[(size_t)(m + 1) * nc + l + 1];
+    return (1.0 - fw) * a0 + fw * a1;
+}
+
+/* ---------- Step 7 backprojection for one voxel (P:l.155-171; O5) ----------
+ * f(x) = (1/2π) ∫_{λi}^{λo} dλ gF(λ, α*, w*)/v*  with the rectangle rule and
+ * fractional end weights (A11):  f = Δλ/2π Σ_k ω_k gF_k(α*_k, w*_k) / v*_k,
+ * v* = R - x cos(λ+λ0) - y sin(λ+λ0)                       (P:l.161)
+ * α* = arctan((-x sin(λ+λ0) + y cos(λ+λ0)) / v*)           (P:l.166)
+ * w* = D cos α* / v* · (z - z0 - P λ / 2π)                 (P:l.170)
+ * gF views are indexed absolutely: view k at gF + (k - gF0) * rows*cols. */
+double bp_voxel(const G &o, double x, double y, double z, const double *gF, int64_t gF0, int64_t gFn, int *oob)
+{
+    if (!in_fov(o, x, y)) return 0.0;
+    double li, lo;
+    pi_line(o, x, y, z, &li, &lo);
+    int64_t kf, kl; double wf, wl;
+    bp_weights(o, li, lo, &kf, &kl, &wf, &wl);
+    if (kf < gF0 || kl >= gF0 + gFn) { if (oob) *oob = 1; return 0.0; }
+    const size_t vs = (size_t)o.g.n_rows * o.g.n_cols;
+    double acc = 0.0;
+    for (int64_t k = kf; k <= kl; ++k) {
+        double om = (k == kf) ? wf : (k == kl) ? wl : 1.0;   /* kf == kl: wf = t_o - t_i */
+        double lam = k * o.dlam;
+        double c = std::cos(lam + o.g.lambda0), s = std::sin(lam + o.g.lambda0);
+        double vstar = o.g.R - x * c - y * s;
+        double astar = std::atan((-x * s + y * c) / vstar);
+        double wstar = o.g.D * std::cos(astar) / vstar * (z - o.g.z0 - o.h * lam);
+        acc += om * sample(o, gF + (size_t)(k - gF0) * vs, astar, wstar) / vstar;
+    }
+    return acc * o.dlam / (2.0 * PI);      /* +1/2π (step 7, P:l.157; reading A3) */
+}
+
+}  // namespace
+
+extern "C" {
+
+/* Derived scalars for tests: [dlam, h, r_fov, alpha_m, psi_max, dpsi, kappa_scale, n_psi] */
+void ora_derived(const ora_geom *g, double *out)
+{
+    G o = make(g);
+    out[0] = o.dlam; out[1] = o.h; out[2] = o.r_fov; out[3] = o.alpha_m;
+    out[4] = o.psi_max; out[5] = o.dpsi; out[6] = o.kappa_scale; out[7] = o.n_psi;
+}
+
+void ora_pi_line(const ora_geom *g, double x, double y, double z, double *li, double *lo)
+{
+    G o = make(g);
+    pi_line(o, x, y, z, li, lo);
+}
+
+void ora_pi_lines(const ora_geom *g, const double *pts, int64_t n, double *li, double *lo)
+{
+    G o = make(g);
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) pi_line(o, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], li + i, lo + i);
+}
+
+double ora_w_kappa(const ora_geom *g, double alpha, double psi) { G o = make(g); return w_kappa(o, alpha, psi); }
+
+int ora_psi_hat(const ora_geom *g, double alpha, double w, double *psi)
+{
+    G o = make(g);
+    return psi_hat(o, alpha, w, psi) ? 1 : 0;
+}
+
+/* Hilbert kernel K[d], d = -(nc-1)..nc-1 (2nc-1 values). */
+void ora_hilbert_kernel(const ora_geom *g, double *K)
+{
+    G o = make(g);
+    std::vector<double> k = hilbert_kernel(o);
+    std::memcpy(K, k.data(), sizeof(double) * k.size());
+}
+
+/* Integer/fraction tables in the canonical A12 form, for the bit-exact test.
+ * fr_idx/fr_frac [n_psi][n_cols]: row index m of w_κ(α_l, ψ_i) (-1 = outside)
+ * br_idx/br_frac [n_rows][n_cols]: ψ index of ψ̂(α_l, w_m) (-1 = none/outside) */
+void ora_rebin_tables(const ora_geom *g, int32_t *fr_idx, double *fr_frac, int32_t *br_idx, double *br_frac)
+{
+    G o = make(g);
+    Rebin rb = rebin_maps(o);
+    std::memcpy(fr_idx, rb.fi.data(), sizeof(int32_t) * rb.fi.size());
+    std::memcpy(fr_frac, rb.ff.data(), sizeof(double) * rb.ff.size());
+    std::memcpy(br_idx, rb.bi.data(), sizeof(int32_t) * rb.bi.size());
+    std::memcpy(br_frac, rb.bf.data(), sizeof(double) * rb.bf.size());
+}
+
+/* PI-window BP weights for every voxel of pitch `pitch` at absolute
+ * coordinates (no periodicity used).  Out-of-FOV voxels get
+ * kf = 0, kl = -1, weights 0.  Arrays [nz][ny][nx]. */
+void ora_bp_weights(const ora_geom *g, int32_t pitch, int64_t *kf, int64_t *kl, double *wf, double *wl)
+{
+    G o = make(g);
+    const int nx = g->nx, ny = g->ny, nz = g->nz;
+    #pragma omp parallel for collapse(2) schedule(dynamic, 4)
+    for (int j = 0; j < nz; ++j)
+        for (int iy = 0; iy < ny; ++iy)
+            for (int ix = 0; ix < nx; ++ix) {
+                size_t id = ((size_t)j * ny + iy) * nx + ix;
+                double x = x_i(o, ix), y = y_i(o, iy);
+                if (!in_fov(o, x, y)) { kf[id] = 0; kl[id] = -1; wf[id] = 0; wl[id] = 0; continue; }
+                double li, lo;
+                pi_line(o, x, y, z_j(o, j, pitch), &li, &lo);
+                bp_weights(o, li, lo, kf + id, kl + id, wf + id, wl + id);
+            }
+}
+
+/* Views a pitch needs: slab [K_lo - 1, K_hi + 1]. */
+void ora_pitch_slab(const ora_geom *g, int32_t pitch, int64_t *first_view, int64_t *n_views)
+{
+    G o = make(g);
+    int64_t lo, hi;
+    pitch_bp_range(o, pitch, &lo, &hi);
+    *first_view = lo - 1;
+    *n_views = hi - lo + 3;
+}
+
+/* Filter views [v_first, v_first + n_out) of a sinogram whose first view is
+ * s0 (needs views v_first-1 .. v_first+n_out).  Optional outputs (double):
+ * g2 [n_out][rows][cols], g3/g4 [n_out][n_psi][cols], gF [n_out][rows][cols]. */
+int ora_filter(const ora_geom *g, const float *sino, int64_t s0, int64_t sn,
+               int64_t v_first, int64_t n_out, double *g2, double *g3, double *g4, double *gF)
+{
+    G o = make(g);
+    if (v_first - 1 < s0 || v_first + n_out + 1 > s0 + sn) return -1;
+    std::vector<double> K = hilbert_kernel(o);
+    Rebin rb = rebin_maps(o);
+    const size_t rs = (size_t)g->n_rows * g->n_cols, ps = (size_t)o.n_psi * g->n_cols;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n_out; ++i)
+        filter_view(o, sino, s0, v_first + i, K, rb,
+                    g2 ? g2 + i * rs : nullptr, g3 ? g3 + i * ps : nullptr,
+                    g4 ? g4 + i * ps : nullptr, gF ? gF + i * rs : nullptr);
+    return 0;
+}
+
+/* Backproject a full pitch volume [nz][ny][nx] from filtered views gF
+ * (views gF0 .. gF0+gFn-1, absolute).  Returns 1 if some voxel's PI-window
+ * fell outside the provided views (those voxels are 0). */
+int ora_backproject(const ora_geom *g, int32_t pitch, const double *gF, int64_t gF0, int64_t gFn, double *vol)
+{
+    G o = make(g);
+    const int nx = g->nx, ny = g->ny, nz = g->nz;
+    int oob_any = 0;
+    #pragma omp parallel for collapse(2) schedule(dynamic, 1) reduction(|:oob_any)
+    for (int j = 0; j < nz; ++j)
+        for (int iy = 0; iy < ny; ++iy)
+            for (int ix = 0; ix < nx; ++ix) {
+                int oob = 0;
+                vol[((size_t)j * ny + iy) * nx + ix] = bp_voxel(o, x_i(o, ix), y_i(o, iy), z_j(o, j, pitch), gF, gF0, gFn, &oob);
+                oob_any |= oob;
+            }
+    return oob_any;
+}
+
+/* Backproject selected voxels: idx[n][3] = (ix, iy, j). */
+int ora_backproject_voxels(const ora_geom *g, int32_t pitch, const double *gF, int64_t gF0, int64_t gFn,
+                           const int32_t *idx, int64_t n, double *out)
+{
+    G o = make(g);
+    int oob_any = 0;
+    #pragma omp parallel for schedule(dynamic, 16) reduction(|:oob_any)
+    for (int64_t i = 0; i < n; ++i) {
+        int oob = 0;
+        out[i] = bp_voxel(o, x_i(o, idx[3 * i]), y_i(o, idx[3 * i + 1]), z_j(o, idx[3 * i + 2], pitch), gF, gF0, gFn, &oob);
+        oob_any |= oob;
+    }
+    return oob_any;
+}
+
+/* Whole reconstruction of pitches [k0, k0+np) from a sinogram (first view s0):
+ * for each pitch, slice its slab (P:l.246-248), filter steps 1-6 on the slab,
+ * backproject (P:l.249-262).  vol [np*nz][ny][nx] (double).
+ * Returns -1 if a slab is not covered by the sinogram. */
+int ora_reconstruct(const ora_geom *g, const float *sino, int64_t s0, int64_t sn,
+                    int32_t k0, int32_t np, double *vol)
+{
+    const size_t vs = (size_t)g->nx * g->ny * g->nz;
+    const size_t rs = (size_t)g->n_rows * g->n_cols;
+    for (int32_t k = k0; k < k0 + np; ++k) {
+        int64_t fv, nv;
+        ora_pitch_slab(g, k, &fv, &nv);
+        if (fv < s0 || fv + nv > s0 + sn) return -1;
+        std::vector<double> gF((size_t)(nv - 2) * rs);
+        ora_filter(g, sino, s0, sn, fv + 1, nv - 2, nullptr, nullptr, nullptr, gF.data());
+        ora_backproject(g, k, gF.data(), fv + 1, nv - 2, vol + (size_t)(k - k0) * vs);
+    }
+    return 0;
+}
+
+}  // extern "C"

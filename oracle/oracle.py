@@ -1,0 +1,208 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes wrapper over oracle/liboracle.so, the plain
+double-precision CPU Katsevich reconstruction written from arXiv 2201.02309 §II
+(see oracle.cpp for the per-function citations).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline/reference
+legs may import this module.  It shares no code with paper_2201_02309_b200/.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+
+
+class OraGeom(ctypes.Structure):
+    _fields_ = [
+        ("R", ctypes.c_double), ("D", ctypes.c_double), ("P", ctypes.c_double),
+        ("lambda0", ctypes.c_double), ("z0", ctypes.c_double), ("r_fov", ctypes.c_double),
+        ("n_rows", ctypes.c_int32), ("d_w", ctypes.c_double),
+        ("n_cols", ctypes.c_int32), ("d_alpha", ctypes.c_double), ("alpha_offset", ctypes.c_double),
+        ("views_per_turn", ctypes.c_int32),
+        ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("dx", ctypes.c_double), ("dy", ctypes.c_double),
+        ("nz", ctypes.c_int32), ("n_psi", ctypes.c_int32),
+    ]
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.cpp")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-fPIC", "-shared",
+                               "-o", _SO, src])
+    return _SO
+
+
+_lib = None
+_D = ctypes.POINTER(ctypes.c_double)
+_F = ctypes.POINTER(ctypes.c_float)
+_I32 = ctypes.POINTER(ctypes.c_int32)
+_I64 = ctypes.POINTER(ctypes.c_int64)
+_G = ctypes.POINTER(OraGeom)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        l = ctypes.CDLL(_SO)
+        sig = {
+            "ora_derived": (None, [_G, _D]),
+            "ora_pi_line": (None, [_G, ctypes.c_double, ctypes.c_double, ctypes.c_double, _D, _D]),
+            "ora_pi_lines": (None, [_G, _D, ctypes.c_int64, _D, _D]),
+            "ora_w_kappa": (ctypes.c_double, [_G, ctypes.c_double, ctypes.c_double]),
+            "ora_psi_hat": (ctypes.c_int, [_G, ctypes.c_double, ctypes.c_double, _D]),
+            "ora_hilbert_kernel": (None, [_G, _D]),
+            "ora_rebin_tables": (None, [_G, _I32, _D, _I32, _D]),
+            "ora_bp_weights": (None, [_G, ctypes.c_int32, _I64, _I64, _D, _D]),
+            "ora_pitch_slab": (None, [_G, ctypes.c_int32, _I64, _I64]),
+            "ora_filter": (ctypes.c_int, [_G, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int64, _D, _D, _D, _D]),
+            "ora_backproject": (ctypes.c_int, [_G, ctypes.c_int32, _D, ctypes.c_int64, ctypes.c_int64, _D]),
+            "ora_backproject_voxels": (ctypes.c_int, [_G, ctypes.c_int32, _D, ctypes.c_int64, ctypes.c_int64,
+                                                      _I32, ctypes.c_int64, _D]),
+            "ora_reconstruct": (ctypes.c_int, [_G, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                               ctypes.c_int32, _D]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(l, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = l
+    return _lib
+
+
+def geom(cfg: dict) -> OraGeom:
+    return OraGeom(cfg["R"], cfg["D"], cfg["P"], cfg.get("lambda0", 0.0), cfg.get("z0", 0.0),
+                   cfg.get("r_fov", 0.0), cfg["n_rows"], cfg["d_w"], cfg["n_cols"], cfg["d_alpha"],
+                   cfg.get("alpha_offset", 0.0), cfg["views_per_turn"], cfg["nx"], cfg["ny"],
+                   cfg["dx"], cfg.get("dy", cfg["dx"]), cfg["nz"], cfg.get("n_psi", 0))
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def derived(cfg):
+    out = np.zeros(8)
+    g = geom(cfg)
+    lib().ora_derived(ctypes.byref(g), _p(out, _D))
+    keys = ["dlam", "h", "r_fov", "alpha_m", "psi_max", "dpsi", "kappa_scale", "n_psi"]
+    d = dict(zip(keys, out.tolist()))
+    d["n_psi"] = int(d["n_psi"])
+    return d
+
+
+def pi_line(cfg, x, y, z):
+    g = geom(cfg)
+    li, lo = ctypes.c_double(), ctypes.c_double()
+    lib().ora_pi_line(ctypes.byref(g), x, y, z, ctypes.byref(li), ctypes.byref(lo))
+    return li.value, lo.value
+
+
+def pi_lines(cfg, pts):
+    g = geom(cfg)
+    p = np.ascontiguousarray(np.asarray(pts, dtype=np.float64).reshape(-1, 3))
+    li = np.empty(p.shape[0]); lo = np.empty(p.shape[0])
+    lib().ora_pi_lines(ctypes.byref(g), _p(p, _D), p.shape[0], _p(li, _D), _p(lo, _D))
+    return li, lo
+
+
+def w_kappa(cfg, alpha, psi):
+    g = geom(cfg)
+    return lib().ora_w_kappa(ctypes.byref(g), alpha, psi)
+
+
+def psi_hat(cfg, alpha, w):
+    g = geom(cfg)
+    out = ctypes.c_double()
+    ok = lib().ora_psi_hat(ctypes.byref(g), alpha, w, ctypes.byref(out))
+    return out.value if ok else None
+
+
+def hilbert_kernel(cfg):
+    g = geom(cfg)
+    K = np.empty(2 * cfg["n_cols"] - 1)
+    lib().ora_hilbert_kernel(ctypes.byref(g), _p(K, _D))
+    return K
+
+
+def rebin_tables(cfg):
+    d = derived(cfg)
+    npsi, nr, nc = d["n_psi"], cfg["n_rows"], cfg["n_cols"]
+    fi = np.empty((npsi, nc), np.int32); ff = np.empty((npsi, nc))
+    bi = np.empty((nr, nc), np.int32); bf = np.empty((nr, nc))
+    g = geom(cfg)
+    lib().ora_rebin_tables(ctypes.byref(g), _p(fi, _I32), _p(ff, _D), _p(bi, _I32), _p(bf, _D))
+    return fi, ff, bi, bf
+
+
+def bp_weights(cfg, pitch):
+    shape = (cfg["nz"], cfg["ny"], cfg["nx"])
+    kf = np.empty(shape, np.int64); kl = np.empty(shape, np.int64)
+    wf = np.empty(shape); wl = np.empty(shape)
+    g = geom(cfg)
+    lib().ora_bp_weights(ctypes.byref(g), pitch, _p(kf, _I64), _p(kl, _I64), _p(wf, _D), _p(wl, _D))
+    return kf, kl, wf, wl
+
+
+def pitch_slab(cfg, pitch):
+    g = geom(cfg)
+    fv, nv = ctypes.c_int64(), ctypes.c_int64()
+    lib().ora_pitch_slab(ctypes.byref(g), pitch, ctypes.byref(fv), ctypes.byref(nv))
+    return fv.value, nv.value
+
+
+def filter_views(cfg, sino, s0, v_first, n_out, stages=("gF",)):
+    """Filter views [v_first, v_first+n_out).  Returns dict of requested stages
+    among g2, g3, g4, gF (float64)."""
+    d = derived(cfg)
+    nr, nc, npsi = cfg["n_rows"], cfg["n_cols"], d["n_psi"]
+    sino = np.ascontiguousarray(sino, dtype=np.float32)
+    out = {}
+    shapes = {"g2": (n_out, nr, nc), "g3": (n_out, npsi, nc), "g4": (n_out, npsi, nc), "gF": (n_out, nr, nc)}
+    for s in stages:
+        out[s] = np.empty(shapes[s])
+    g = geom(cfg)
+    rc = lib().ora_filter(ctypes.byref(g), _p(sino, _F), s0, sino.shape[0], v_first, n_out,
+                          _p(out.get("g2"), _D), _p(out.get("g3"), _D), _p(out.get("g4"), _D),
+                          _p(out.get("gF"), _D))
+    if rc != 0:
+        raise ValueError("oracle filter: sinogram does not cover the requested views")
+    return out
+
+
+def backproject(cfg, pitch, gF, gF0):
+    gF = np.ascontiguousarray(gF, dtype=np.float64)
+    vol = np.empty((cfg["nz"], cfg["ny"], cfg["nx"]))
+    g = geom(cfg)
+    rc = lib().ora_backproject(ctypes.byref(g), pitch, _p(gF, _D), gF0, gF.shape[0], _p(vol, _D))
+    if rc:
+        raise ValueError("oracle backproject: filtered views do not cover a PI-window")
+    return vol
+
+
+def backproject_voxels(cfg, pitch, gF, gF0, idx):
+    gF = np.ascontiguousarray(gF, dtype=np.float64)
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int32).reshape(-1, 3))
+    out = np.empty(idx.shape[0])
+    g = geom(cfg)
+    rc = lib().ora_backproject_voxels(ctypes.byref(g), pitch, _p(gF, _D), gF0, gF.shape[0],
+                                      _p(idx, _I32), idx.shape[0], _p(out, _D))
+    if rc:
+        raise ValueError("oracle backproject: filtered views do not cover a PI-window")
+    return out
+
+
+def reconstruct(cfg, sino, s0, k0, n_pitches):
+    sino = np.ascontiguousarray(sino, dtype=np.float32)
+    vol = np.empty((n_pitches * cfg["nz"], cfg["ny"], cfg["nx"]))
+    g = geom(cfg)
+    rc = lib().ora_reconstruct(ctypes.byref(g), _p(sino, _F), s0, sino.shape[0], k0, n_pitches, _p(vol, _D))
+    if rc:
+        raise ValueError("oracle reconstruct: sinogram does not cover a requested pitch slab")
+    return vol

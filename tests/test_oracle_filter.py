@@ -1,0 +1,209 @@
+"""Oracle pins — κ-line rebinning maps and filtering steps 1-6 (Eqs. 8-15).
+
+Inputs are constructed so that the exact stage outputs are known in closed
+form (affine data, the derivative-annihilating view 0 trick), or compared with
+an independent dense principal-value quadrature of Eq. (12)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from synth import configs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_numbers.json")))
+
+
+def _cfg(**kw):
+    base = dict(R=595.0, D=1085.6, P=38.4, lambda0=0.3, z0=0.0, n_rows=64, d_w=1.0947, n_cols=96,
+                d_alpha=9.0805e-3, alpha_offset=0.25, views_per_turn=360, nx=16, ny=16, dx=10.0, dy=10.0, nz=4)
+    base.update(kw)
+    return base
+
+
+def _grid(cfg):
+    nr, nc = cfg["n_rows"], cfg["n_cols"]
+    al = (np.arange(nc) - (nc - 1) / 2 + cfg["alpha_offset"]) * cfg["d_alpha"]
+    w = (np.arange(nr) - (nr - 1) / 2) * cfg["d_w"]
+    return al, w
+
+
+def test_w_kappa_special_cases():
+    """w_κ(α, 0) = (DP/2πR) sin α and w_κ(0, ψ) = (DP/2πR) ψ (Eq. 11 limits)."""
+    cfg = _cfg()
+    Dk = cfg["D"] * cfg["P"] / (2 * math.pi * cfg["R"])
+    for a in np.linspace(-0.4, 0.4, 9):
+        assert abs(oracle.w_kappa(cfg, a, 0.0) - Dk * math.sin(a)) < 1e-12 * Dk
+    for p in np.linspace(-1.9, 1.9, 9):
+        assert abs(oracle.w_kappa(cfg, 0.0, p) - Dk * p) < 1e-12 * Dk
+
+
+def test_kappa_line_touches_td_window_at_fan_edge():
+    """κ-line ψ = π/2 + α_m meets the TD top boundary Δ(π/2-α)/cos α at α = -α_m (reading A7)."""
+    for name in ("C3", "C5", "T3"):
+        cfg = configs.get(name)
+        d = oracle.derived(cfg)
+        Dk = d["kappa_scale"]
+        am = d["alpha_m"]
+        w = oracle.w_kappa(cfg, -am, d["psi_max"])
+        assert abs(w - Dk * (math.pi / 2 + am) / math.cos(am)) < 1e-10 * Dk
+        w = oracle.w_kappa(cfg, am, -d["psi_max"])
+        assert abs(w + Dk * (math.pi / 2 + am) / math.cos(am)) < 1e-10 * Dk
+
+
+def test_psi_hat_roundtrip_and_first_root():
+    """ψ̂(α, w_κ(α, ψ)) = ψ on a 100×100 grid, |ψ| <= π/2 (SPEC criterion 5), and for
+    the wide-fan C3 geometry every tabulated ψ̂ is a root with no earlier crossing (A8)."""
+    cfg = configs.get("C3")
+    d = oracle.derived(cfg)
+    amax = cfg["n_cols"] / 2 * cfg["d_alpha"]
+    for a in np.linspace(-amax, amax, 100):
+        for p in np.linspace(-math.pi / 2, math.pi / 2, 100):
+            got = oracle.psi_hat(cfg, a, oracle.w_kappa(cfg, a, p))
+            assert got is not None and abs(got - p) < 1e-9
+    al, w = _grid(cfg)
+    rng = np.random.default_rng(0)
+    for l in rng.integers(0, cfg["n_cols"], 40):
+        for m in rng.integers(0, cfg["n_rows"], 8):
+            ph = oracle.psi_hat(cfg, al[l], w[m])
+            if ph is None:
+                continue
+            assert abs(oracle.w_kappa(cfg, al[l], ph) - w[m]) < 1e-9
+            grid = np.linspace(0.0, ph, 2001)[1:-1]
+            f = np.array([oracle.w_kappa(cfg, al[l], q) for q in grid]) - w[m]
+            f0 = oracle.w_kappa(cfg, al[l], 0.0) - w[m]
+            assert (np.sign(f) == np.sign(f0)).all()
+
+
+def test_rebin_tables_consistent_with_maps():
+    """Tables hold the canonical (index, fraction) of the maps: index + frac is the
+    node position of w_κ on the row grid / of ψ̂ on the ψ grid (reading A12)."""
+    cfg = configs.get("T3")
+    d = oracle.derived(cfg)
+    fi, ff, bi, bf = oracle.rebin_tables(cfg)
+    al, w = _grid(cfg)
+    psi = -d["psi_max"] + np.arange(d["n_psi"]) * d["dpsi"]
+    for i in range(0, d["n_psi"], 5):
+        for l in range(0, cfg["n_cols"], 7):
+            pos = oracle.w_kappa(cfg, al[l], psi[i]) / cfg["d_w"] + (cfg["n_rows"] - 1) / 2
+            if fi[i, l] < 0:
+                assert pos < -1e-9 or pos > cfg["n_rows"] - 1 + 1e-9
+            else:
+                assert abs(fi[i, l] + ff[i, l] - pos) < 1e-9 and 0 <= ff[i, l] <= 1
+    for m in range(cfg["n_rows"]):
+        for l in range(0, cfg["n_cols"], 3):
+            ph = oracle.psi_hat(cfg, al[l], w[m])
+            if bi[m, l] >= 0:
+                assert abs(bi[m, l] + bf[m, l] - (ph + d["psi_max"]) / d["dpsi"]) < 1e-9
+
+
+def _view_trick_sino(cfg, cw, H, nviews=3):
+    """g(v, m, l) = λ_v c(w_m) H(α_l) with views -1, 0, +1: at view 0 the α-derivative
+    vanishes and the λ-difference is exact, so g1(0) = c(w) H(α) exactly."""
+    lam = (np.arange(nviews) - nviews // 2) * 2 * math.pi / cfg["views_per_turn"]
+    return (lam[:, None, None] * cw[None, :, None] * H[None, None, :]).astype(np.float64)
+
+
+def test_derivative_and_length_weight_exact_on_affine_data():
+    """g = λ + α: centred/one-sided differences are exact, g1 = 2, g2 = 2 D/sqrt(D²+w²) (Eqs. 8-9)."""
+    cfg = _cfg()
+    al, w = _grid(cfg)
+    lam = (np.arange(5) - 2) * 2 * math.pi / cfg["views_per_turn"]
+    g = (lam[:, None, None] + al[None, None, :] + 0 * w[None, :, None]).astype(np.float32)
+    out = oracle.filter_views(cfg, g, -2, -1, 3, stages=("g2",))["g2"]
+    # inputs were rounded to fp32: exactness up to that rounding
+    want = 2 * cfg["D"] / np.sqrt(cfg["D"] ** 2 + w ** 2)
+    assert np.abs(out - want[None, :, None]).max() < 2e-4
+
+
+def test_length_weight_value():
+    """D = 1085.6, w = 3.8819 -> D/sqrt(D²+w²) = 0.99999361."""
+    gold = GOLD["length_weight"]
+    cfg = _cfg(n_rows=3, d_w=gold["w"], D=gold["D"])
+    al, w = _grid(cfg)
+    g = (((np.arange(3) - 1) * 2 * math.pi / cfg["views_per_turn"])[:, None, None] * np.ones((1, 3, cfg["n_cols"]))).astype(np.float32)
+    out = oracle.filter_views(cfg, g, -1, 0, 1, stages=("g2",))["g2"][0]
+    # g1 = 1 (pure λ ramp); the fp32 ramp rounds λ by < 6e-8 relative
+    assert abs(out[0, 10] / out[1, 10] - gold["value"]) < gold["tol"]
+
+
+def test_forward_rebin_exact_on_affine_rows():
+    """g2 = a + b w -> g3 = a + b w_κ(α_l, ψ_i) inside the rows, 0 outside (Eqs. 10-11, A9)."""
+    cfg = _cfg(n_rows=24, d_w=3.0)
+    d = oracle.derived(cfg)
+    al, w = _grid(cfg)
+    a, b = 0.7, -0.05
+    cw = (a + b * w) * np.sqrt(cfg["D"] ** 2 + w ** 2) / cfg["D"]
+    g = _view_trick_sino(cfg, cw, np.ones(cfg["n_cols"])).astype(np.float32)
+    g3 = oracle.filter_views(cfg, g, -1, 0, 1, stages=("g3",))["g3"][0]
+    psi = -d["psi_max"] + np.arange(d["n_psi"]) * d["dpsi"]
+    for i in range(d["n_psi"]):
+        for l in range(cfg["n_cols"]):
+            wk = oracle.w_kappa(cfg, al[l], psi[i])
+            inside = w[0] - 1e-9 <= wk <= w[-1] + 1e-9
+            want = a + b * wk if inside else 0.0
+            assert abs(g3[i, l] - want) < 2e-6
+
+
+def test_hilbert_delta_response_is_closed_form_kernel():
+    """A delta on one column returns K[d] = 2Δα/(π sin(dΔα)) for odd d, 0 for even d
+    (band-limited h_H(sin ·), Eq. 12 / e4, reading A10) on every κ-line."""
+    cfg = _cfg(n_rows=64, d_w=40.0, n_cols=31)
+    d = oracle.derived(cfg)
+    al, w = _grid(cfg)
+    l0 = 12
+    H = np.zeros(cfg["n_cols"]); H[l0] = 1.0
+    cw = np.sqrt(cfg["D"] ** 2 + w ** 2) / cfg["D"]
+    g = _view_trick_sino(cfg, cw, H).astype(np.float32)
+    g4 = oracle.filter_views(cfg, g, -1, 0, 1, stages=("g4",))["g4"][0]
+    dd = np.arange(cfg["n_cols"]) - l0
+    with np.errstate(divide="ignore", invalid="ignore"):
+        K = np.where(dd % 2 == 1, 2 * cfg["d_alpha"] / (np.pi * np.sin(dd * cfg["d_alpha"])), 0.0)
+    K[l0] = 0.0
+    for i in range(d["n_psi"]):
+        assert np.abs(g4[i] - K).max() < 1e-6 * np.abs(K).max()
+    assert np.allclose(oracle.hilbert_kernel(cfg)[::-1], -oracle.hilbert_kernel(cfg))   # odd kernel
+
+
+@pytest.mark.parametrize("omega", [20.0, 60.0])
+def test_hilbert_matches_principal_value_quadrature(omega):
+    """g3 = cos(ωα) on the paper's 627-column detector: g4 matches a dense
+    principal-value quadrature of Eq. (12) over the detector's α support to < 1 %
+    in the interior (SPEC criterion 7)."""
+    from scipy.integrate import quad
+    cfg = _cfg(n_rows=40, d_w=60.0, n_cols=627, d_alpha=math.pi / 2880, R=1085.6, D=595.0, P=7 * math.pi)
+    al, w = _grid(cfg)
+    cw = np.sqrt(cfg["D"] ** 2 + w ** 2) / cfg["D"]
+    H = np.cos(omega * al)
+    g = _view_trick_sino(cfg, cw, H).astype(np.float32)
+    d = oracle.derived(cfg)
+    g4 = oracle.filter_views(cfg, g, -1, 0, 1, stages=("g4",))["g4"][0][d["n_psi"] // 2]
+    lo_a, hi_a = al[0] - cfg["d_alpha"] / 2, al[-1] + cfg["d_alpha"] / 2
+    idx = np.arange(150, 480, 15)
+    errs = []
+    for l in idx:
+        a = al[l]
+        f = lambda t: -(1 / np.pi) * np.cos(omega * t) * ((t - a) / np.sin(t - a) if t != a else 1.0)
+        pv, _ = quad(f, lo_a, hi_a, weight="cauchy", wvar=a, limit=400)
+        errs.append(abs(g4[l] - pv))
+    scale = np.abs(g4[idx]).max()
+    assert max(errs) < 1e-2 * scale
+
+
+def test_backward_rebin_of_constant_lines_returns_constant():
+    """When every κ-line carries the same g4 (constant along ψ), g5 = g4 wherever ψ̂ is
+    defined and inside the ψ grid (Eqs. 13-14 with linear interpolation), else 0."""
+    cfg = _cfg(n_rows=64, d_w=40.0, n_cols=41)
+    al, w = _grid(cfg)
+    rng = np.random.default_rng(5)
+    H = rng.standard_normal(cfg["n_cols"])
+    cw = np.sqrt(cfg["D"] ** 2 + w ** 2) / cfg["D"]
+    g = _view_trick_sino(cfg, cw, H).astype(np.float32)
+    out = oracle.filter_views(cfg, g, -1, 0, 1, stages=("g4", "gF"))
+    g4, gF = out["g4"][0], out["gF"][0]
+    fi, ff, bi, bf = oracle.rebin_tables(cfg)
+    assert np.abs(g4 - g4[0][None, :]).max() < 1e-9 * np.abs(g4).max()
+    want = np.where(bi >= 0, np.cos(al)[None, :] * g4[0][None, :], 0.0)
+    assert np.abs(gF - want).max() < 1e-9 * np.abs(g4).max()
