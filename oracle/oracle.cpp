@@ -410,6 +410,21 @@ void ora_bp_weights(const ora_geom *g, int32_t pitch, int64_t *kf, int64_t *kl, 
             }
 }
 
+/* BP weights of selected voxels idx[n][3] = (ix, iy, j) of pitch `pitch`. */
+void ora_bp_weights_voxels(const ora_geom *g, int32_t pitch, const int32_t *idx, int64_t n,
+                           int64_t *kf, int64_t *kl, double *wf, double *wl)
+{
+    G o = make(g);
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double x = x_i(o, idx[3 * i]), y = y_i(o, idx[3 * i + 1]);
+        if (!in_fov(o, x, y)) { kf[i] = 0; kl[i] = -1; wf[i] = 0; wl[i] = 0; continue; }
+        double li, lo;
+        pi_line(o, x, y, z_j(o, idx[3 * i + 2], pitch), &li, &lo);
+        bp_weights(o, li, lo, kf + i, kl + i, wf + i, wl + i);
+    }
+}
+
 /* Views a pitch needs: slab [K_lo - 1, K_hi + 1]. */
 void ora_pitch_slab(const ora_geom *g, int32_t pitch, int64_t *first_view, int64_t *n_views)
 {

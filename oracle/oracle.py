@@ -60,6 +60,7 @@ def lib():
             "ora_rebin_tables": (None, [_G, _I32, _D, _I32, _D]),
             "ora_bp_weights": (None, [_G, ctypes.c_int32, _I64, _I64, _D, _D]),
             "ora_pitch_slab": (None, [_G, ctypes.c_int32, _I64, _I64]),
+            "ora_bp_weights_voxels": (None, [_G, ctypes.c_int32, _I32, ctypes.c_int64, _I64, _I64, _D, _D]),
             "ora_filter": (ctypes.c_int, [_G, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                           ctypes.c_int64, _D, _D, _D, _D]),
             "ora_backproject": (ctypes.c_int, [_G, ctypes.c_int32, _D, ctypes.c_int64, ctypes.c_int64, _D]),
@@ -147,6 +148,16 @@ def bp_weights(cfg, pitch):
     wf = np.empty(shape); wl = np.empty(shape)
     g = geom(cfg)
     lib().ora_bp_weights(ctypes.byref(g), pitch, _p(kf, _I64), _p(kl, _I64), _p(wf, _D), _p(wl, _D))
+    return kf, kl, wf, wl
+
+
+def bp_weights_voxels(cfg, pitch, idx):
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int32).reshape(-1, 3))
+    n = idx.shape[0]
+    kf = np.empty(n, np.int64); kl = np.empty(n, np.int64); wf = np.empty(n); wl = np.empty(n)
+    g = geom(cfg)
+    lib().ora_bp_weights_voxels(ctypes.byref(g), pitch, _p(idx, _I32), n, _p(kf, _I64), _p(kl, _I64),
+                                _p(wf, _D), _p(wl, _D))
     return kf, kl, wf, wl
 
 

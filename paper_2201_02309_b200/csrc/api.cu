@@ -1,0 +1,522 @@
+// api.cu — the C ABI declared in include/katsevich.h.
+//
+// Host plumbing only: argument checking, device table upload, workspace
+// carving, launch sequencing and optional CUDA-event timing.  Every step of
+// the method runs in the kernels of filter.cu / backproject.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "kernels.cuh"
+
+using namespace kats;
+
+namespace {
+
+constexpr int kFilterChunk = 256;   // views per filter chunk (g3/g4 stay L2-resident)
+
+enum Stage { ST_K12 = 0, ST_K3 = 1, ST_K4 = 2, ST_K5 = 3, ST_FIX = 4, ST_OTHER = 5 };
+
+int cuda_fail(katsevich_plan *p, cudaError_t e, const char *where)
+{
+    if (p) {
+        p->detail = std::string(where) + ": " + cudaGetErrorString(e);
+    }
+    return KATS_ERR_CUDA;
+}
+
+#define KCHECK(p, call)                                          \
+    do {                                                         \
+        cudaError_t _e = (call);                                 \
+        if (_e != cudaSuccess) return cuda_fail((p), _e, #call); \
+    } while (0)
+
+// Records CUDA events around one launch when profiling is on; counts launches.
+struct LaunchScope {
+    katsevich_plan *p;
+    int stage;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    LaunchScope(katsevich_plan *p_, int st, cudaStream_t s_) : p(p_), stage(st), s(s_)
+    {
+        p->total_launches++;
+        p->stage_launches[stage]++;
+        if (p->profiling) {
+            e0 = take(); e1 = take();
+            cudaEventRecord(e0, s);
+        }
+    }
+    cudaEvent_t take()
+    {
+        if (!p->event_pool.empty()) {
+            cudaEvent_t e = (cudaEvent_t)p->event_pool.back();
+            p->event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    ~LaunchScope()
+    {
+        if (e0) {
+            cudaEventRecord(e1, s);
+            p->prof.push_back({stage, (void *)e0, (void *)e1});
+        }
+    }
+};
+
+template <typename T>
+int upload(katsevich_plan *p, T **dst, const std::vector<T> &src)
+{
+    if (src.empty()) { *dst = nullptr; return KATS_OK; }
+    KCHECK(p, cudaMalloc((void **)dst, sizeof(T) * src.size()));
+    KCHECK(p, cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+    return KATS_OK;
+}
+
+void free_device(katsevich_plan *p)
+{
+    if (p->device < 0) return;
+    cudaSetDevice(p->device);
+    void *ptrs[] = {p->d.pi_k, p->d.pi_w, p->d.view, p->d.fr, p->d.br, p->d.cos_alpha, p->d.wlen, p->d.hilbert};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    p->d = DeviceTables{};
+    for (auto &r : p->prof) { cudaEventDestroy((cudaEvent_t)r.ev0); cudaEventDestroy((cudaEvent_t)r.ev1); }
+    p->prof.clear();
+    for (void *e : p->event_pool) cudaEventDestroy((cudaEvent_t)e);
+    p->event_pool.clear();
+}
+
+int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
+{
+    const HostTables &t = p->t;
+    return (int64_t)(n_pitches - 1) * p->g.views_per_turn + (t.bp_hi - t.bp_lo + 1);
+}
+
+size_t filter_chunk_bytes(const katsevich_plan *p)
+{
+    return 2 * sizeof(float) * (size_t)kFilterChunk * p->t.n_psi * p->g.n_cols;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+FilterParams filter_params(const katsevich_plan *p)
+{
+    FilterParams f{};
+    f.nr = p->g.n_rows; f.nc = p->g.n_cols; f.npsi = p->t.n_psi;
+    f.inv_2dlam = (float)(1.0 / (2.0 * p->t.dlam));
+    f.inv_dalpha = (float)(1.0 / p->g.d_alpha);
+    f.inv_2dalpha = (float)(1.0 / (2.0 * p->g.d_alpha));
+    f.wlen = p->d.wlen; f.fr = p->d.fr; f.br = p->d.br;
+    f.cos_alpha = p->d.cos_alpha; f.hilbert = p->d.hilbert;
+    return f;
+}
+
+// Filter n_out views whose raw data (with ±1 halo) is at sino_v0 - rows*cols
+// .. ; writes gF (and optionally full g3/g4 when dbg3/dbg4 are given).
+int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float *gF,
+               float *scratch, float *dbg3, float *dbg4, cudaStream_t s)
+{
+    FilterParams f = filter_params(p);
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t ps = (size_t)p->t.n_psi * p->g.n_cols;
+    for (int64_t v0 = 0; v0 < n_out; v0 += kFilterChunk) {
+        const int nv = (int)std::min<int64_t>(kFilterChunk, n_out - v0);
+        f.sino = raw_first_out + v0 * rs;
+        f.n_views = nv;
+        f.g3 = dbg3 ? dbg3 + v0 * ps : scratch;
+        f.g4 = dbg4 ? dbg4 + v0 * ps : scratch + (size_t)kFilterChunk * ps;
+        f.gF = gF + v0 * rs;
+        { LaunchScope ls(p, ST_K12, s); launch_deriv_fwd_rebin(f, s); }
+        KCHECK(p, cudaGetLastError());
+        { LaunchScope ls(p, ST_K3, s); launch_hilbert(f, s); }
+        KCHECK(p, cudaGetLastError());
+        { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos(f, s); }
+        KCHECK(p, cudaGetLastError());
+    }
+    return KATS_OK;
+}
+
+BPParams bp_params(const katsevich_plan *p)
+{
+    BPParams b{};
+    const katsevich_geometry &g = p->g;
+    b.nr = g.n_rows; b.nc = g.n_cols; b.nx = g.nx; b.ny = g.ny; b.nz = g.nz_per_pitch;
+    b.pi_k = p->d.pi_k; b.pi_w = p->d.pi_w; b.view = p->d.view;
+    b.view_lo = (int)p->t.bp_lo;
+    b.R = (float)g.R; b.D = (float)g.D;
+    b.inv_dalpha = (float)(1.0 / g.d_alpha);
+    b.col_c = (float)(0.5 * (g.n_cols - 1) - g.alpha_offset);
+    b.inv_dw = (float)(1.0 / g.d_w);
+    b.row_c = (float)(0.5 * (g.n_rows - 1));
+    b.x0 = (float)(-0.5 * g.nx * g.dx); b.dx = (float)g.dx;
+    b.y0 = (float)(-0.5 * g.ny * g.dy); b.dy = (float)g.dy;
+    b.dz = (float)(g.pitch / g.nz_per_pitch);
+    b.scale = (float)(p->t.dlam / (2.0 * kPi));      // +1/2π (P:l.157; A3)
+    return b;
+}
+
+int check_device_plan(katsevich_plan *p)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (p->device < 0) { p->detail = "host-only plan"; return KATS_ERR_NO_DEVICE; }
+    if (!p->precomputed) { p->detail = "katsevich_precompute has not run"; return KATS_ERR_NOT_PRECOMPUTED; }
+    if (cudaSetDevice(p->device) != cudaSuccess) return cuda_fail(p, cudaGetLastError(), "cudaSetDevice");
+    return KATS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int katsevich_plan_create(const katsevich_geometry *geom, int cuda_device, katsevich_plan **out)
+{
+    if (!out) return KATS_ERR_NULL;
+    *out = nullptr;
+    if (!geom) return KATS_ERR_NULL;
+    std::string detail;
+    int rc = validate(*geom, detail);
+    if (rc != KATS_OK) return rc;
+    if (cuda_device >= 0) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || cuda_device >= n) return KATS_ERR_NO_DEVICE;
+    }
+    katsevich_plan *p = new (std::nothrow) katsevich_plan;
+    if (!p) return KATS_ERR_ARGUMENT;
+    p->g = *geom;
+    p->device = cuda_device;
+    *out = p;
+    return KATS_OK;
+}
+
+int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
+{
+    if (!p) return KATS_ERR_NULL;
+    (void)cuda_stream;
+    p->precomputed = false;
+    int rc = compute_host_tables(p->g, p->t, p->detail);
+    if (rc < 0) return rc;
+    if (!p->t.td_covered && p->detail.empty())
+        p->detail = "detector rows do not cover the Tam-Danielsson window";
+    if (p->device >= 0) {
+        KCHECK(p, cudaSetDevice(p->device));
+        free_device(p);
+        const katsevich_geometry &g = p->g;
+        const HostTables &t = p->t;
+        const size_t nvox = t.pi_first.size();
+        std::vector<int2> pik(nvox);
+        std::vector<float2> piw(nvox);
+        for (size_t i = 0; i < nvox; ++i) {
+            pik[i] = make_int2(t.pi_first[i], t.pi_last[i]);
+            piw[i] = make_float2((float)t.w_first[i], (float)t.w_last[i]);
+        }
+        std::vector<ViewGeom> vg;
+        for (int64_t k = t.bp_lo; k <= t.bp_hi; ++k) {
+            double lam = (double)k * t.dlam;    // pitch-relative λ'
+            vg.push_back({(float)std::cos(lam + g.lambda0), (float)std::sin(lam + g.lambda0),
+                          (float)(g.z0 + t.h * lam), 0.f});
+        }
+        std::vector<RebinEntry> fr(t.fr_idx.size()), br(t.br_idx.size());
+        for (size_t i = 0; i < fr.size(); ++i) fr[i] = {t.fr_idx[i], (float)t.fr_frac[i]};
+        for (size_t i = 0; i < br.size(); ++i) br[i] = {t.br_idx[i], (float)t.br_frac[i]};
+        std::vector<float> cosa(g.n_cols), wlen(g.n_rows), hk(2 * (size_t)g.n_cols - 1);
+        for (int l = 0; l < g.n_cols; ++l)
+            cosa[l] = (float)std::cos(((double)l - 0.5 * (g.n_cols - 1) + g.alpha_offset) * g.d_alpha);
+        for (int m = 0; m < g.n_rows; ++m) {
+            double w = ((double)m - 0.5 * (g.n_rows - 1)) * g.d_w;
+            wlen[m] = (float)(g.D / std::sqrt(g.D * g.D + w * w));          // Eq. (9)
+        }
+        for (int d = -(g.n_cols - 1); d <= g.n_cols - 1; ++d) {            // reading A10
+            double kd = (d & 1) ? 2.0 * g.d_alpha / (kPi * std::sin(d * g.d_alpha)) : 0.0;
+            hk[(size_t)(d + g.n_cols - 1)] = (float)kd;
+        }
+        if ((rc = upload(p, &p->d.pi_k, pik)) || (rc = upload(p, &p->d.pi_w, piw)) ||
+            (rc = upload(p, &p->d.view, vg)) || (rc = upload(p, &p->d.fr, fr)) ||
+            (rc = upload(p, &p->d.br, br)) || (rc = upload(p, &p->d.cos_alpha, cosa)) ||
+            (rc = upload(p, &p->d.wlen, wlen)) || (rc = upload(p, &p->d.hilbert, hk)))
+            return rc;
+        KCHECK(p, cudaDeviceSynchronize());
+    }
+    p->precomputed = true;
+    return p->t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
+}
+
+int katsevich_pitch_views(const katsevich_plan *p, int32_t pitch, int64_t *first_view, int32_t *n_views)
+{
+    if (!p || !first_view || !n_views) return KATS_ERR_NULL;
+    if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
+    *first_view = (int64_t)pitch * p->g.views_per_turn + p->t.bp_lo - 1;
+    *n_views = (int32_t)(p->t.bp_hi - p->t.bp_lo + 3);
+    return KATS_OK;
+}
+
+int katsevich_scan_views(const katsevich_plan *p, int32_t first_pitch, int32_t n_pitches,
+                         int64_t *first_view, int64_t *n_views)
+{
+    if (!p || !first_view || !n_views) return KATS_ERR_NULL;
+    if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
+    if (n_pitches < 1) return KATS_ERR_ARGUMENT;
+    *first_view = (int64_t)first_pitch * p->g.views_per_turn + p->t.bp_lo - 1;
+    *n_views = n_union_views(p, n_pitches) + 2;
+    return KATS_OK;
+}
+
+int katsevich_workspace_bytes(const katsevich_plan *p, int32_t n_pitches, size_t *bytes)
+{
+    if (!p || !bytes) return KATS_ERR_NULL;
+    if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
+    if (n_pitches < 1) return KATS_ERR_ARGUMENT;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const int64_t nslab = p->t.bp_hi - p->t.bp_lo + 1;
+    // reconstruct: gF over the union of views; batch: gF per slab
+    size_t gf = sizeof(float) * rs * (size_t)std::max<int64_t>(n_union_views(p, n_pitches), nslab * n_pitches);
+    *bytes = align_up(gf) + align_up(filter_chunk_bytes(p));
+    return KATS_OK;
+}
+
+int katsevich_workspace_bytes_host(const katsevich_plan *p, int32_t n_pitches, size_t *bytes)
+{
+    int rc = katsevich_workspace_bytes(p, n_pitches, bytes);
+    if (rc) return rc;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t vol = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch * n_pitches;
+    *bytes += align_up(sizeof(float) * rs * (size_t)(n_union_views(p, n_pitches) + 2)) + align_up(sizeof(float) * vol);
+    return KATS_OK;
+}
+
+int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int64_t sn,
+                          int32_t first_pitch, int32_t n_pitches, float *vol,
+                          void *workspace, size_t workspace_bytes, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!sino || !vol || !workspace) return KATS_ERR_NULL;
+    if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
+    size_t need;
+    katsevich_workspace_bytes(p, n_pitches, &need);
+    if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
+    const int vt = p->g.views_per_turn;
+    const HostTables &t = p->t;
+    const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;                  // first filtered view
+    const int64_t nu = n_union_views(p, n_pitches);
+    if (u0 - 1 < s0 || u0 + nu + 1 > s0 + sn) {
+        // reconstructible pitches k need [k vt + bp_lo - 1, k vt + bp_hi + 1] inside the scan
+        double ka = std::ceil((double)(s0 - (t.bp_lo - 1)) / vt);
+        double kb = std::floor((double)(s0 + sn - 1 - (t.bp_hi + 1)) / vt);
+        char buf[200];
+        std::snprintf(buf, sizeof buf, "sinogram views [%lld, %lld) do not cover pitches [%d, %d); reconstructible pitches: %.0f..%.0f",
+                      (long long)s0, (long long)(s0 + sn), first_pitch, first_pitch + n_pitches, ka, kb);
+        p->detail = buf;
+        return KATS_ERR_COVERAGE;
+    }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    float *gF = (float *)workspace;
+    float *scratch = (float *)((char *)workspace + align_up(sizeof(float) * rs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
+    rc = run_filter(p, sino + (u0 - s0) * rs, nu, gF, scratch, nullptr, nullptr, s);
+    if (rc) return rc;
+    BPParams b = bp_params(p);
+    b.gF = gF;
+    b.off0 = (int64_t)first_pitch * vt - u0;
+    b.item_views = vt;
+    b.n_items = n_pitches;
+    b.vol = vol;
+    { LaunchScope ls(p, ST_K5, s); launch_backproject(b, s); }
+    KCHECK(p, cudaGetLastError());
+    return KATS_OK;
+}
+
+int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B, float *vols,
+                                void *workspace, size_t workspace_bytes, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!slabs || !vols || !workspace) return KATS_ERR_NULL;
+    if (B < 1) return KATS_ERR_ARGUMENT;
+    size_t need;
+    katsevich_workspace_bytes(p, B, &need);
+    if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const HostTables &t = p->t;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const int64_t nbp = t.bp_hi - t.bp_lo + 1;        // filtered views per slab
+    const int64_t nslab = nbp + 2;                     // raw views per slab
+    float *gF = (float *)workspace;
+    float *scratch = (float *)((char *)workspace + align_up(sizeof(float) * rs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
+    for (int b = 0; b < B; ++b) {
+        rc = run_filter(p, slabs + ((size_t)b * nslab + 1) * rs, nbp, gF + (size_t)b * nbp * rs, scratch, nullptr, nullptr, s);
+        if (rc) return rc;
+    }
+    BPParams bp = bp_params(p);
+    bp.gF = gF;
+    bp.off0 = -t.bp_lo;
+    bp.item_views = nbp;
+    bp.n_items = B;
+    bp.vol = vols;
+    { LaunchScope ls(p, ST_K5, s); launch_backproject(bp, s); }
+    KCHECK(p, cudaGetLastError());
+    return KATS_OK;
+}
+
+int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_t s0, int64_t sn,
+                               int32_t first_pitch, int32_t n_pitches, float *host_vol,
+                               void *workspace, size_t workspace_bytes, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!host_sino || !host_vol || !workspace) return KATS_ERR_NULL;
+    if (n_pitches < 1) return KATS_ERR_ARGUMENT;
+    size_t need, base;
+    katsevich_workspace_bytes_host(p, n_pitches, &need);
+    katsevich_workspace_bytes(p, n_pitches, &base);
+    if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
+    int64_t fv, nv;
+    katsevich_scan_views(p, first_pitch, n_pitches, &fv, &nv);
+    if (fv < s0 || fv + nv > s0 + sn) return katsevich_reconstruct(p, host_sino, s0, sn, first_pitch, n_pitches,
+                                                                   host_vol, workspace, workspace_bytes, cuda_stream);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t volsz = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch * n_pitches;
+    float *dsino = (float *)((char *)workspace + base);
+    float *dvol = (float *)((char *)dsino + align_up(sizeof(float) * rs * (size_t)nv));
+    KCHECK(p, cudaMemcpyAsync(dsino, host_sino + (fv - s0) * rs, sizeof(float) * rs * nv, cudaMemcpyHostToDevice, s));
+    rc = katsevich_reconstruct(p, dsino, fv, nv, first_pitch, n_pitches, dvol, workspace, base, cuda_stream);
+    if (rc) return rc;
+    KCHECK(p, cudaMemcpyAsync(host_vol, dvol, sizeof(float) * volsz, cudaMemcpyDeviceToHost, s));
+    KCHECK(p, cudaStreamSynchronize(s));
+    return KATS_OK;
+}
+
+int katsevich_filter(katsevich_plan *p, const float *sino, int64_t s0, int64_t sn,
+                     int64_t out_first_view, int32_t n_out, float *g3, float *g4, float *gF, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!sino || !gF) return KATS_ERR_NULL;
+    if (n_out < 1) return KATS_ERR_ARGUMENT;
+    if (out_first_view - 1 < s0 || out_first_view + n_out + 1 > s0 + sn) {
+        p->detail = "sinogram does not hold the ±1 halo of the requested views";
+        return KATS_ERR_COVERAGE;
+    }
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    float *scratch = nullptr;
+    if (!g3 || !g4) KCHECK(p, cudaMallocAsync((void **)&scratch, filter_chunk_bytes(p), s));
+    rc = run_filter(p, sino + (out_first_view - s0) * rs, n_out, gF, scratch, g3, g4, s);
+    if (scratch) cudaFreeAsync(scratch, s);
+    return rc;
+}
+
+int katsevich_backproject(katsevich_plan *p, const float *gF, int64_t gF0, int64_t gFn,
+                          int32_t pitch, float *vol, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!gF || !vol) return KATS_ERR_NULL;
+    const int vt = p->g.views_per_turn;
+    const int64_t a = (int64_t)pitch * vt + p->t.bp_lo, b = (int64_t)pitch * vt + p->t.bp_hi;
+    if (a < gF0 || b >= gF0 + gFn) { p->detail = "filtered views do not cover the pitch"; return KATS_ERR_COVERAGE; }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    BPParams bp = bp_params(p);
+    bp.gF = gF;
+    bp.off0 = (int64_t)pitch * vt - gF0;
+    bp.item_views = 0;
+    bp.n_items = 1;
+    bp.vol = vol;
+    { LaunchScope ls(p, ST_K5, s); launch_backproject(bp, s); }
+    KCHECK(p, cudaGetLastError());
+    return KATS_OK;
+}
+
+int katsevich_table_info(const katsevich_plan *p, int32_t *n_psi, int64_t *lo, int64_t *hi)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
+    if (n_psi) *n_psi = p->t.n_psi;
+    if (lo) *lo = p->t.bp_lo;
+    if (hi) *hi = p->t.bp_hi;
+    return KATS_OK;
+}
+
+int katsevich_export_tables(const katsevich_plan *p, int32_t *pi_first, int32_t *pi_last,
+                            double *w_first, double *w_last, int32_t *fr_idx, double *fr_frac,
+                            int32_t *br_idx, double *br_frac)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
+    const HostTables &t = p->t;
+    auto cp = [](auto *dst, const auto &v) {
+        if (dst) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
+    };
+    cp(pi_first, t.pi_first); cp(pi_last, t.pi_last); cp(w_first, t.w_first); cp(w_last, t.w_last);
+    cp(fr_idx, t.fr_idx); cp(fr_frac, t.fr_frac); cp(br_idx, t.br_idx); cp(br_frac, t.br_frac);
+    return KATS_OK;
+}
+
+int katsevich_profile_enable(katsevich_plan *p, int enable)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (p->device < 0) return KATS_ERR_NO_DEVICE;
+    p->profiling = enable != 0;
+    return KATS_OK;
+}
+
+int katsevich_profile_read(katsevich_plan *p, katsevich_stats *out, int reset)
+{
+    if (!p || !out) return KATS_ERR_NULL;
+    if (p->device >= 0) {
+        cudaSetDevice(p->device);
+        for (auto &r : p->prof) {
+            float ms = 0.f;
+            KCHECK(p, cudaEventSynchronize((cudaEvent_t)r.ev1));
+            KCHECK(p, cudaEventElapsedTime(&ms, (cudaEvent_t)r.ev0, (cudaEvent_t)r.ev1));
+            p->stage_ms[r.stage] += ms;
+            p->event_pool.push_back(r.ev0);
+            p->event_pool.push_back(r.ev1);
+        }
+        p->prof.clear();
+    }
+    for (int i = 0; i < 6; ++i) { out->launches[i] = p->stage_launches[i]; out->ms[i] = p->stage_ms[i]; }
+    out->total_launches = p->total_launches;
+    if (reset) {
+        for (int i = 0; i < 6; ++i) { p->stage_launches[i] = 0; p->stage_ms[i] = 0; }
+        p->total_launches = 0;
+    }
+    return KATS_OK;
+}
+
+void katsevich_destroy(katsevich_plan *p)
+{
+    if (!p) return;
+    free_device(p);
+    delete p;
+}
+
+const char *katsevich_error_string(int code)
+{
+    switch (code) {
+    case KATS_OK: return "ok";
+    case KATS_WARN_TD_NOT_COVERED: return "warning: detector does not cover the Tam-Danielsson window";
+    case KATS_ERR_NULL: return "null pointer argument";
+    case KATS_ERR_INVALID_GEOMETRY: return "invalid geometry";
+    case KATS_ERR_NOT_PRECOMPUTED: return "plan not precomputed";
+    case KATS_ERR_COVERAGE: return "sinogram does not cover the requested pitches";
+    case KATS_ERR_PI_NONCONVERGENCE: return "PI-line / kappa-line solver did not converge";
+    case KATS_ERR_WORKSPACE: return "workspace too small";
+    case KATS_ERR_CUDA: return "CUDA error";
+    case KATS_ERR_NO_DEVICE: return "no CUDA device for this plan";
+    case KATS_ERR_ARGUMENT: return "invalid argument";
+    default: return "unknown error code";
+    }
+}
+
+const char *katsevich_last_error_detail(const katsevich_plan *p)
+{
+    return p ? p->detail.c_str() : "";
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// kernels.cuh — launch interfaces of the sm_100a kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "plan.hpp"
+
+namespace kats {
+
+// Filter steps 1-6 over `n_views` consecutive views.
+struct FilterParams {
+    const float *sino;        // raw view v at sino + v * rows*cols (v relative to the output range; halo at v = -1 and n_views)
+    int n_views;
+    int nr, nc, npsi;
+    float inv_2dlam, inv_dalpha, inv_2dalpha;
+    const float *wlen;        // D/sqrt(D²+w_m²)
+    const RebinEntry *fr;     // [npsi][nc]
+    const RebinEntry *br;     // [nr][nc]
+    const float *cos_alpha;   // [nc]
+    const float *hilbert;     // [2nc-1]
+    float *g3, *g4, *gF;      // outputs ([n_views][npsi][nc] / [n_views][nr][nc])
+};
+
+void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
+void launch_hilbert(const FilterParams &p, cudaStream_t s);           // K3:  Eq. 12
+void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s);     // K4:  Eqs. 13-15
+
+// Step 7 backprojection over `n_items`
+// independent pitches/slabs sharing the periodic tables.
+struct BPParams {
+    const float *gF;          // filtered views
+    int64_t off0, item_views; // gF view index of pitch-relative view k for item b: k + off0 + b*item_views
+    int n_items;
+    int nr, nc, nx, ny, nz;
+    const int2 *pi_k;         // [nz][ny][nx] (k_first, k_last)
+    const float2 *pi_w;       // [nz][ny][nx] (ω_first, ω_last)
+    const ViewGeom *view;     // [k - view_lo]
+    int view_lo;
+    float R, D, inv_dalpha, col_c, inv_dw, row_c;
+    float x0, dx, y0, dy, dz;
+    float scale;              // Δλ / 2π
+    float *vol;               // [n_items][nz][ny][nx]
+};
+
+void launch_backproject(const BPParams &p, cudaStream_t s);           // K5
+
+}  // namespace kats

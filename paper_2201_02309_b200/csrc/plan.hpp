@@ -1,0 +1,70 @@
+// plan.hpp — internal plan of the B200 Katsevich library (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>
+
+#include "../../include/katsevich.h"
+
+namespace kats {
+
+constexpr double kPi = 3.14159265358979323846;
+
+// Host-side periodic tables (double precision, pitch 0).
+struct HostTables {
+    int32_t n_psi = 0;
+    double dlam = 0, h = 0, r_fov = 0, alpha_m = 0, psi_max = 0, dpsi = 0, kappa = 0;
+    // T_pi per voxel [nz][ny][nx], pitch-relative view indices
+    std::vector<int32_t> pi_first, pi_last;
+    std::vector<double> w_first, w_last;
+    int64_t bp_lo = 0, bp_hi = -1;          // min k_first / max k_last over the pitch
+    // T_fr [n_psi][n_cols], T_br [n_rows][n_cols]
+    std::vector<int32_t> fr_idx, br_idx;
+    std::vector<double> fr_frac, br_frac;
+    bool td_covered = true;
+};
+
+// Per-view geometry for the backprojection (pitch-relative view k in [bp_lo, bp_hi]).
+struct ViewGeom { float c, s, zc, pad; };    // cos(λ'+λ0), sin(λ'+λ0), z0 + hλ'
+
+struct RebinEntry { int32_t idx; float frac; };
+
+struct DeviceTables {
+    int2 *pi_k = nullptr;          // (k_first, k_last) per voxel [nz][ny][nx]
+    float2 *pi_w = nullptr;        // (ω_first, ω_last)
+    ViewGeom *view = nullptr;      // [bp_hi - bp_lo + 1]
+    RebinEntry *fr = nullptr;      // [n_psi][n_cols]
+    RebinEntry *br = nullptr;      // [n_rows][n_cols]
+    float *cos_alpha = nullptr;    // [n_cols]
+    float *wlen = nullptr;         // [n_rows]  D / sqrt(D² + w²)
+    float *hilbert = nullptr;      // [2 n_cols - 1]  K[d], d = -(nc-1)..nc-1
+};
+
+struct ProfRecord { int stage; void *ev0; void *ev1; };
+
+}  // namespace kats
+
+struct katsevich_plan {
+    katsevich_geometry g{};
+    int device = -1;
+    bool precomputed = false;
+    kats::HostTables t;
+    kats::DeviceTables d;
+    std::string detail;
+    // profiling
+    bool profiling = false;
+    std::vector<kats::ProfRecord> prof;
+    std::vector<void *> event_pool;
+    int64_t total_launches = 0;
+    int64_t stage_launches[6] = {0, 0, 0, 0, 0, 0};
+    double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace kats {
+// precompute.cpp
+int validate(const katsevich_geometry &g, std::string &detail);
+int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string &detail);
+}  // namespace kats

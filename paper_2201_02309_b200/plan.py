@@ -1,0 +1,203 @@
+"""Python face of the C ABI: `Plan` wraps katsevich_plan_* with the same names.
+
+PyTorch is used only for device memory (workspace, outputs) and stream
+handles; all arithmetic runs in libkatsevich.so's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import warnings
+
+import numpy as np
+
+from ._lib import (KATS_ERR_NO_DEVICE, KATS_OK, KATS_WARN_TD_NOT_COVERED, KatsevichError,
+                   KatsevichGeometry, KatsevichStats, lib)
+
+STAGES = ("K12_deriv_fwd_rebin", "K3_hilbert", "K4_bwd_rebin_cos", "K5_backproject", "fixup", "other")
+
+
+def geometry_from_config(cfg: dict) -> KatsevichGeometry:
+    """Build the C geometry from a config dict (synth/configs.py keys)."""
+    return KatsevichGeometry(
+        R=cfg["R"], D=cfg["D"], pitch=cfg["P"], lambda0=cfg.get("lambda0", 0.0), z0=cfg.get("z0", 0.0),
+        r_fov=cfg.get("r_fov", 0.0), n_rows=cfg["n_rows"], d_w=cfg["d_w"], n_cols=cfg["n_cols"],
+        d_alpha=cfg["d_alpha"], alpha_offset=cfg.get("alpha_offset", 0.0),
+        views_per_turn=cfg["views_per_turn"], nx=cfg["nx"], ny=cfg["ny"], dx=cfg["dx"],
+        dy=cfg.get("dy", cfg["dx"]), nz_per_pitch=cfg["nz"], n_psi=cfg.get("n_psi", 0), flags=0)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """katsevich_plan: geometry + periodic tables (host double, device fp32)."""
+
+    def __init__(self, geometry, device: int = 0):
+        if isinstance(geometry, dict):
+            geometry = geometry_from_config(geometry)
+        self.geometry = geometry
+        self.device = device
+        self._h = ctypes.c_void_p()
+        rc = lib().katsevich_plan_create(ctypes.byref(geometry), device, ctypes.byref(self._h))
+        if rc != KATS_OK:
+            raise KatsevichError(rc, "katsevich_plan_create")
+        self.td_covered = None
+        self._ws = None
+
+    # -- lifecycle ---------------------------------------------------------
+    def _check(self, rc, what=""):
+        if rc < 0:
+            raise KatsevichError(rc, lib().katsevich_last_error_detail(self._h).decode() or what)
+        return rc
+
+    def precompute(self, stream=None):
+        s = ctypes.c_void_p(0) if self.device < 0 else _stream_handle(stream)
+        rc = self._check(lib().katsevich_precompute(self._h, s))
+        self.td_covered = rc != KATS_WARN_TD_NOT_COVERED
+        if not self.td_covered:
+            warnings.warn("detector rows do not cover the Tam-Danielsson window")
+        return rc
+
+    def close(self):
+        if self._h:
+            lib().katsevich_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- queries -----------------------------------------------------------
+    def pitch_views(self, pitch: int = 0):
+        fv, nv = ctypes.c_int64(), ctypes.c_int32()
+        self._check(lib().katsevich_pitch_views(self._h, pitch, ctypes.byref(fv), ctypes.byref(nv)))
+        return fv.value, nv.value
+
+    def scan_views(self, first_pitch: int, n_pitches: int):
+        fv, nv = ctypes.c_int64(), ctypes.c_int64()
+        self._check(lib().katsevich_scan_views(self._h, first_pitch, n_pitches, ctypes.byref(fv), ctypes.byref(nv)))
+        return fv.value, nv.value
+
+    def workspace_bytes(self, n_pitches: int = 1, host: bool = False) -> int:
+        b = ctypes.c_size_t()
+        f = lib().katsevich_workspace_bytes_host if host else lib().katsevich_workspace_bytes
+        self._check(f(self._h, n_pitches, ctypes.byref(b)))
+        return b.value
+
+    def table_info(self):
+        n, lo, hi = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        self._check(lib().katsevich_table_info(self._h, ctypes.byref(n), ctypes.byref(lo), ctypes.byref(hi)))
+        return dict(n_psi=n.value, bp_lo=lo.value, bp_hi=hi.value)
+
+    def export_tables(self):
+        g = self.geometry
+        info = self.table_info()
+        nvox = (g.nz_per_pitch, g.ny, g.nx)
+        out = dict(pi_first=np.empty(nvox, np.int32), pi_last=np.empty(nvox, np.int32),
+                   w_first=np.empty(nvox), w_last=np.empty(nvox),
+                   fr_idx=np.empty((info["n_psi"], g.n_cols), np.int32), fr_frac=np.empty((info["n_psi"], g.n_cols)),
+                   br_idx=np.empty((g.n_rows, g.n_cols), np.int32), br_frac=np.empty((g.n_rows, g.n_cols)))
+        P32, PD = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)
+        self._check(lib().katsevich_export_tables(
+            self._h, out["pi_first"].ctypes.data_as(P32), out["pi_last"].ctypes.data_as(P32),
+            out["w_first"].ctypes.data_as(PD), out["w_last"].ctypes.data_as(PD),
+            out["fr_idx"].ctypes.data_as(P32), out["fr_frac"].ctypes.data_as(PD),
+            out["br_idx"].ctypes.data_as(P32), out["br_frac"].ctypes.data_as(PD)))
+        return out
+
+    # -- device entry points (torch tensors for memory) --------------------
+    def _workspace(self, nbytes: int):
+        import torch
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def _vol_shape(self, n):
+        g = self.geometry
+        return (n * g.nz_per_pitch, g.ny, g.nx)
+
+    def reconstruct(self, sino, sino_first_view: int, first_pitch: int = 0, n_pitches: int = 1,
+                    out=None, stream=None):
+        """sino: cuda float32 tensor [views][rows][cols] holding views from sino_first_view."""
+        import torch
+        assert sino.is_cuda and sino.dtype == torch.float32 and sino.is_contiguous()
+        if out is None:
+            out = torch.empty(self._vol_shape(n_pitches), dtype=torch.float32, device=sino.device)
+        nb = self.workspace_bytes(n_pitches)
+        ws = self._workspace(nb)
+        self._check(lib().katsevich_reconstruct(self._h, _ptr(sino), sino_first_view, sino.shape[0],
+                                                first_pitch, n_pitches, _ptr(out), _ptr(ws), ws.numel(),
+                                                _stream_handle(stream)))
+        return out
+
+    def reconstruct_batch(self, slabs, out=None, stream=None):
+        """slabs: cuda float32 [B][n_views][rows][cols] of pitch-0 slabs."""
+        import torch
+        B = slabs.shape[0]
+        assert slabs.is_cuda and slabs.dtype == torch.float32 and slabs.is_contiguous()
+        assert slabs.shape[1] == self.pitch_views(0)[1]
+        if out is None:
+            g = self.geometry
+            out = torch.empty((B, g.nz_per_pitch, g.ny, g.nx), dtype=torch.float32, device=slabs.device)
+        ws = self._workspace(self.workspace_bytes(B))
+        self._check(lib().katsevich_reconstruct_batch(self._h, _ptr(slabs), B, _ptr(out), _ptr(ws), ws.numel(),
+                                                      _stream_handle(stream)))
+        return out
+
+    def reconstruct_host(self, sino_host, sino_first_view: int, first_pitch: int = 0, n_pitches: int = 1,
+                         out_host=None, stream=None):
+        """Host (numpy or pinned torch CPU) sinogram in, host volume out; copies inside the call."""
+        import torch
+        if isinstance(sino_host, np.ndarray):
+            sino_host = torch.from_numpy(np.ascontiguousarray(sino_host, dtype=np.float32))
+        if out_host is None:
+            out_host = torch.empty(self._vol_shape(n_pitches), dtype=torch.float32)
+        ws = self._workspace(self.workspace_bytes(n_pitches, host=True))
+        self._check(lib().katsevich_reconstruct_host(self._h, _ptr(sino_host), sino_first_view, sino_host.shape[0],
+                                                     first_pitch, n_pitches, _ptr(out_host), _ptr(ws), ws.numel(),
+                                                     _stream_handle(stream)))
+        return out_host
+
+    def filter(self, sino, sino_first_view: int, out_first_view: int, n_out: int, stages=("gF",), stream=None):
+        import torch
+        g = self.geometry
+        npsi = self.table_info()["n_psi"]
+        dev = sino.device
+        gF = torch.empty((n_out, g.n_rows, g.n_cols), dtype=torch.float32, device=dev)
+        g3 = torch.empty((n_out, npsi, g.n_cols), dtype=torch.float32, device=dev) if "g3" in stages else None
+        g4 = torch.empty((n_out, npsi, g.n_cols), dtype=torch.float32, device=dev) if "g4" in stages else None
+        self._check(lib().katsevich_filter(self._h, _ptr(sino), sino_first_view, sino.shape[0], out_first_view, n_out,
+                                           _ptr(g3) if g3 is not None else None,
+                                           _ptr(g4) if g4 is not None else None, _ptr(gF), _stream_handle(stream)))
+        return {"g3": g3, "g4": g4, "gF": gF}
+
+    def backproject(self, gF, gF_first_view: int, pitch: int = 0, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty(self._vol_shape(1), dtype=torch.float32, device=gF.device)
+        self._check(lib().katsevich_backproject(self._h, _ptr(gF), gF_first_view, gF.shape[0], pitch, _ptr(out),
+                                                _stream_handle(stream)))
+        return out
+
+    # -- in-run timing -------------------------------------------------------
+    def profile_enable(self, enable: bool = True):
+        self._check(lib().katsevich_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self, reset: bool = True):
+        st = KatsevichStats()
+        self._check(lib().katsevich_profile_read(self._h, ctypes.byref(st), 1 if reset else 0))
+        return {"launches": {STAGES[i]: st.launches[i] for i in range(6)},
+                "ms": {STAGES[i]: st.ms[i] for i in range(6)},
+                "total_launches": st.total_launches}

@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded synthetic inputs.  Bar (BASELINE.json north_star): integer tables
+bit-exact; fp32 volume rel L2 <= 1e-4 and max-abs <= 1e-3 x phantom contrast.
+Per-stage intermediates: rel L2 <= 1e-5 (fp32 arithmetic vs fp64)."""
+import functools
+
+import numpy as np
+import pytest
+
+from tests.conftest import cuda_ok
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-4
+MAX_ABS_FRAC = 1e-3
+STAGE_REL = 1e-5
+
+
+@functools.lru_cache(maxsize=None)
+def _case(name):
+    from oracle import oracle
+    from synth import configs, synth
+    cfg = configs.get(name)
+    sino = synth.project(cfg, cfg["phantom"], cfg["scan_v0"], cfg["scan_nv"])
+    ref = oracle.reconstruct(cfg, sino, cfg["scan_v0"], 0, cfg["n_pitches"])
+    truth = np.concatenate([synth.volume_truth(cfg, cfg["phantom"], k) for k in range(cfg["n_pitches"])])
+    return cfg, sino, ref, float(truth.max() - truth.min())
+
+
+def _plan(cfg):
+    import paper_2201_02309_b200 as k
+    p = k.Plan(cfg, device=0)
+    p.precompute()
+    return p
+
+
+def _check(got, ref, contrast, rel=REL_L2, frac=MAX_ABS_FRAC):
+    got = np.asarray(got, dtype=np.float64)
+    e = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)
+    m = np.abs(got - ref).max()
+    assert e <= rel, f"rel L2 {e:.3e} > {rel}"
+    assert m <= frac * contrast, f"max abs {m:.3e} > {frac} x contrast {contrast:.3g}"
+    return e, m
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not cuda_ok():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("name", ["T1", "T2", "T3", "C1"])
+def test_reconstruct_matches_oracle(name):
+    import torch
+    cfg, sino, ref, contrast = _case(name)
+    p = _plan(cfg)
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    _check(vol.cpu().numpy(), ref, contrast)
+
+
+@pytest.mark.parametrize("name", ["T1", "T3"])
+def test_filter_stages_match_oracle(name):
+    import torch
+    from oracle import oracle
+    cfg, sino, _, _ = _case(name)
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    out = p.filter(torch.from_numpy(sino).cuda(), cfg["scan_v0"], v0 + 1, nv - 2, stages=("g3", "g4", "gF"))
+    torch.cuda.synchronize()
+    ref = oracle.filter_views(cfg, sino, cfg["scan_v0"], v0 + 1, nv - 2, stages=("g3", "g4", "gF"))
+    for s in ("g3", "g4", "gF"):
+        got = out[s].cpu().numpy().astype(np.float64)
+        e = np.linalg.norm(got - ref[s]) / np.linalg.norm(ref[s])
+        assert e <= STAGE_REL, f"{s}: rel L2 {e:.3e}"
+
+
+@pytest.mark.parametrize("name", ["T1", "T2", "C1"])
+def test_backproject_only_matches_oracle(name):
+    """K5 alone, fed with the oracle's filtered views (rounded to fp32)."""
+    import torch
+    from oracle import oracle
+    cfg, sino, _, contrast = _case(name)
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    gF = oracle.filter_views(cfg, sino, cfg["scan_v0"], v0 + 1, nv - 2)["gF"]
+    gF32 = gF.astype(np.float32)
+    ref = oracle.backproject(cfg, 0, gF32.astype(np.float64), v0 + 1)
+    got = p.backproject(torch.from_numpy(gF32).cuda(), v0 + 1, 0)
+    torch.cuda.synchronize()
+    _check(got.cpu().numpy(), ref, contrast)
+
+
+def test_batch_matches_oracle():
+    """Independent one-pitch slabs (C5-shaped, small): reconstruct_batch."""
+    import torch
+    from oracle import oracle
+    from synth import configs, synth
+    cfg = configs.get("T2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    slabs, refs, contrasts = [], [], []
+    for s in range(3):
+        ph = configs.random_ellipsoids(s, 6, 180.0, -5.0, cfg["P"] + 5.0)
+        sino = synth.project(cfg, ph, v0, nv)
+        slabs.append(sino)
+        refs.append(oracle.reconstruct(cfg, sino, v0, 0, 1))
+        t = synth.volume_truth(cfg, ph, 0)
+        contrasts.append(t.max() - t.min())
+    got = p.reconstruct_batch(torch.from_numpy(np.stack(slabs)).cuda())
+    torch.cuda.synchronize()
+    for b in range(3):
+        _check(got[b].cpu().numpy(), refs[b], contrasts[b])
+
+
+def test_host_entry_point_matches_device():
+    import torch
+    cfg, sino, ref, contrast = _case("T3")
+    p = _plan(cfg)
+    h = p.reconstruct_host(sino, cfg["scan_v0"], 0, cfg["n_pitches"])
+    d = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    assert np.array_equal(h.numpy(), d.cpu().numpy())
+    _check(h.numpy(), ref, contrast)
+
+
+def test_deterministic_and_pitch_periodic():
+    """Bitwise determinism; identical slabs at different pitches give bitwise
+    identical volumes (same periodic tables, pitch-relative arithmetic)."""
+    import torch
+    cfg, sino, _, _ = _case("T2")
+    p = _plan(cfg)
+    vt = cfg["views_per_turn"]
+    v0, nv = p.pitch_views(0)
+    slab = sino[v0 - cfg["scan_v0"]: v0 - cfg["scan_v0"] + nv]
+    a = p.reconstruct(torch.from_numpy(np.ascontiguousarray(slab)).cuda(), v0, 0, 1)
+    b = p.reconstruct(torch.from_numpy(np.ascontiguousarray(slab)).cuda(), v0 + 5 * vt, 5, 1)
+    c = p.reconstruct(torch.from_numpy(np.ascontiguousarray(slab)).cuda(), v0, 0, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(a, c)
+
+
+def test_coverage_error_names_pitches():
+    import torch
+    import paper_2201_02309_b200 as k
+    cfg, sino, _, _ = _case("T1")
+    p = _plan(cfg)
+    with pytest.raises(k.KatsevichError) as ei:
+        p.reconstruct(torch.from_numpy(sino[:40]).cuda(), cfg["scan_v0"], 0, 1)
+    assert ei.value.code == -4 and "reconstructible" in str(ei.value)
