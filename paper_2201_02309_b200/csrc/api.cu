@@ -104,6 +104,9 @@ size_t filter_chunk_bytes(const katsevich_plan *p)
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// filtered view as tap quads: (n_rows + 2) x n_cols float4 (two zero rows below)
+size_t quad_view_elems(const katsevich_plan *p) { return (size_t)(p->g.n_rows + 2) * p->g.n_cols; }
+
 FilterParams filter_params(const katsevich_plan *p)
 {
     FilterParams f{};
@@ -118,11 +121,12 @@ FilterParams filter_params(const katsevich_plan *p)
 
 // Filter n_out views whose raw data (with ±1 halo) is at sino_v0 - rows*cols
 // .. ; writes gF (and optionally full g3/g4 when dbg3/dbg4 are given).
-int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float *gF,
-               float *scratch, float *dbg3, float *dbg4, cudaStream_t s)
+int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float4 *gq,
+               float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s)
 {
     FilterParams f = filter_params(p);
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t qs = quad_view_elems(p);
     const size_t ps = (size_t)p->t.n_psi * p->g.n_cols;
     for (int64_t v0 = 0; v0 < n_out; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, n_out - v0);
@@ -130,7 +134,8 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
         f.n_views = nv;
         f.g3 = dbg3 ? dbg3 + v0 * ps : scratch;
         f.g4 = dbg4 ? dbg4 + v0 * ps : scratch + (size_t)kFilterChunk * ps;
-        f.gF = gF + v0 * rs;
+        f.gq = gq + v0 * qs;
+        f.gF = dbgF ? dbgF + v0 * rs : nullptr;
         { LaunchScope ls(p, ST_K12, s); launch_deriv_fwd_rebin(f, s); }
         KCHECK(p, cudaGetLastError());
         { LaunchScope ls(p, ST_K3, s); launch_hilbert(f, s); }
@@ -146,13 +151,24 @@ BPParams bp_params(const katsevich_plan *p)
     BPParams b{};
     const katsevich_geometry &g = p->g;
     b.nr = g.n_rows; b.nc = g.n_cols; b.nx = g.nx; b.ny = g.ny; b.nz = g.nz_per_pitch;
+    b.colbytes = 16u * (unsigned)(g.n_rows + 2);
+    b.viewbytes = 16 * (int64_t)quad_view_elems(p);
     b.pi_k = p->d.pi_k; b.pi_w = p->d.pi_w; b.view = p->d.view;
     b.view_lo = (int)p->t.bp_lo;
-    b.R = (float)g.R; b.D = (float)g.D;
+    b.R = (float)g.R;
+    b.D_over_dw = (float)(g.D / g.d_w);
     b.inv_dalpha = (float)(1.0 / g.d_alpha);
     b.col_c = (float)(0.5 * (g.n_cols - 1) - g.alpha_offset);
-    b.inv_dw = (float)(1.0 / g.d_w);
-    b.row_c = (float)(0.5 * (g.n_rows - 1));
+    b.row_c15 = (float)(0.5 * (g.n_rows - 1) + 1.5);   // quad row = row + 2, minus ½ for round-to-nearest
+    b.colmax = (float)(g.n_cols - 1);
+    b.rowmax = (float)(g.n_rows - 1);
+    // minimax fit of atan(t) = t·Σ c_i t^(2i) on |t| <= 0.75 (max error 9.4e-9 rad), scaled by 1/Δα
+    static const double c[7] = {0.99999980689595702, -0.33331974824996929, 0.19972144187876958,
+                                -0.14029432575638814, 0.098575642092481805, -0.055588999310759703,
+                                0.016795583727292406};
+    for (int i = 0; i < 7; ++i) b.at[i] = (float)(c[i] / g.d_alpha);
+    b.poly = std::tan(p->t.alpha_m) <= 0.75;
+    b.checked = !p->t.interior_in_detector;
     b.x0 = (float)(-0.5 * g.nx * g.dx); b.dx = (float)g.dx;
     b.y0 = (float)(-0.5 * g.ny * g.dy); b.dy = (float)g.dy;
     b.dz = (float)(g.pitch / g.nz_per_pitch);
@@ -270,10 +286,10 @@ int katsevich_workspace_bytes(const katsevich_plan *p, int32_t n_pitches, size_t
     if (!p || !bytes) return KATS_ERR_NULL;
     if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
     if (n_pitches < 1) return KATS_ERR_ARGUMENT;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t qs = quad_view_elems(p);
     const int64_t nslab = p->t.bp_hi - p->t.bp_lo + 1;
-    // reconstruct: gF over the union of views; batch: gF per slab
-    size_t gf = sizeof(float) * rs * (size_t)std::max<int64_t>(n_union_views(p, n_pitches), nslab * n_pitches);
+    // reconstruct: filtered quads over the union of views; batch: per slab
+    size_t gf = sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, n_pitches), nslab * n_pitches);
     *bytes = align_up(gf) + align_up(filter_chunk_bytes(p));
     return KATS_OK;
 }
@@ -315,12 +331,12 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     }
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
-    float *gF = (float *)workspace;
-    float *scratch = (float *)((char *)workspace + align_up(sizeof(float) * rs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
-    rc = run_filter(p, sino + (u0 - s0) * rs, nu, gF, scratch, nullptr, nullptr, s);
+    float4 *gq = (float4 *)workspace;
+    float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * quad_view_elems(p) * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
+    rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s);
     if (rc) return rc;
     BPParams b = bp_params(p);
-    b.gF = gF;
+    b.gq = gq;
     b.off0 = (int64_t)first_pitch * vt - u0;
     b.item_views = vt;
     b.n_items = n_pitches;
@@ -345,14 +361,15 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     const int64_t nbp = t.bp_hi - t.bp_lo + 1;        // filtered views per slab
     const int64_t nslab = nbp + 2;                     // raw views per slab
-    float *gF = (float *)workspace;
-    float *scratch = (float *)((char *)workspace + align_up(sizeof(float) * rs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
+    float4 *gq = (float4 *)workspace;
+    const size_t qs = quad_view_elems(p);
+    float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
     for (int b = 0; b < B; ++b) {
-        rc = run_filter(p, slabs + ((size_t)b * nslab + 1) * rs, nbp, gF + (size_t)b * nbp * rs, scratch, nullptr, nullptr, s);
+        rc = run_filter(p, slabs + ((size_t)b * nslab + 1) * rs, nbp, gq + (size_t)b * nbp * qs, scratch, nullptr, nullptr, nullptr, s);
         if (rc) return rc;
     }
     BPParams bp = bp_params(p);
-    bp.gF = gF;
+    bp.gq = gq;
     bp.off0 = -t.bp_lo;
     bp.item_views = nbp;
     bp.n_items = B;
@@ -405,9 +422,12 @@ int katsevich_filter(katsevich_plan *p, const float *sino, int64_t s0, int64_t s
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     cudaStream_t s = (cudaStream_t)cuda_stream;
     float *scratch = nullptr;
+    float4 *gq = nullptr;
     if (!g3 || !g4) KCHECK(p, cudaMallocAsync((void **)&scratch, filter_chunk_bytes(p), s));
-    rc = run_filter(p, sino + (out_first_view - s0) * rs, n_out, gF, scratch, g3, g4, s);
+    KCHECK(p, cudaMallocAsync((void **)&gq, sizeof(float4) * quad_view_elems(p) * (size_t)n_out, s));
+    rc = run_filter(p, sino + (out_first_view - s0) * rs, n_out, gq, scratch, g3, g4, gF, s);
     if (scratch) cudaFreeAsync(scratch, s);
+    cudaFreeAsync(gq, s);
     return rc;
 }
 
@@ -421,14 +441,20 @@ int katsevich_backproject(katsevich_plan *p, const float *gF, int64_t gF0, int64
     const int64_t a = (int64_t)pitch * vt + p->t.bp_lo, b = (int64_t)pitch * vt + p->t.bp_hi;
     if (a < gF0 || b >= gF0 + gFn) { p->detail = "filtered views do not cover the pitch"; return KATS_ERR_COVERAGE; }
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    float4 *gq = nullptr;
+    const int nr = p->g.n_rows, nc = p->g.n_cols;
+    KCHECK(p, cudaMallocAsync((void **)&gq, sizeof(float4) * quad_view_elems(p) * gFn, s));
+    { LaunchScope ls(p, ST_OTHER, s); launch_make_quads(gF, gq, gFn, nr, nc, s); }
+    KCHECK(p, cudaGetLastError());
     BPParams bp = bp_params(p);
-    bp.gF = gF;
+    bp.gq = gq;
     bp.off0 = (int64_t)pitch * vt - gF0;
     bp.item_views = 0;
     bp.n_items = 1;
     bp.vol = vol;
     { LaunchScope ls(p, ST_K5, s); launch_backproject(bp, s); }
     KCHECK(p, cudaGetLastError());
+    cudaFreeAsync(gq, s);
     return KATS_OK;
 }
 

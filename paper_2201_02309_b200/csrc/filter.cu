@@ -45,50 +45,120 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin(FilterParams p)
 // ---------------------------------------------------------------------------
 // K3: g4 = Σ_l' K[l-l'] g3[l'] along each κ-line (Eq. 12, h_H = 1/(πs) of
 //     Eq. e4, band-limited kernel of DESIGN.md reading A10: only odd
-//     distances contribute).  One CTA per line; line and kernel staged in
-//     shared memory; direct convolution (n_cols/2 MACs per output).
+//     distances contribute, so an output of parity p sums the inputs of
+//     parity 1-p).  Direct convolution, register-tiled: a thread owns HR
+//     consecutive same-parity outputs l0, l0+2, ..., keeps the HR kernel taps
+//     they need in a register window that slides by one tap per input, so
+//     each input costs 2 shared-memory loads for HR FMAs.  A CTA holds
+//     several κ-lines (and the kernel) in shared memory.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_hilbert_direct(FilterParams p)
+constexpr int HR = 8;
+
+__device__ __forceinline__ int hilbert_threads_per_line(int nc) { return 2 * ((nc + 1) / 2 + HR - 1) / HR; }
+
+__global__ void __launch_bounds__(256) k_hilbert(FilterParams p, int64_t n_lines, int lines_per_block)
 {
     extern __shared__ float smem[];
     const int nc = p.nc;
-    float *gl = smem;             // [nc]
-    float *ks = smem + nc;        // [2nc-1]
-    const size_t line = blockIdx.x;
-    const float *src = p.g3 + line * nc;
-    for (int t = threadIdx.x; t < nc; t += blockDim.x) gl[t] = src[t];
-    for (int t = threadIdx.x; t < 2 * nc - 1; t += blockDim.x) ks[t] = __ldg(p.hilbert + t);
+    constexpr int PAD = 2 * HR + 4;            // zero taps beyond |d| = nc-1 (windows of discarded outputs)
+    float *ks = smem + PAD;                    // K[d] at ks[d + nc - 1], d = -(nc-1) .. nc-1
+    float *gl = smem + 2 * nc - 1 + 2 * PAD;   // lines_per_block x nc
+    const int64_t line0 = (int64_t)blockIdx.x * lines_per_block;
+    const int nl = (n_lines - line0 < lines_per_block) ? (int)(n_lines - line0) : lines_per_block;
+    for (int t = threadIdx.x; t < 2 * nc - 1 + 2 * PAD; t += blockDim.x)
+        smem[t] = (t >= PAD && t < PAD + 2 * nc - 1) ? __ldg(p.hilbert + t - PAD) : 0.f;
+    const float *src = p.g3 + line0 * nc;
+    for (int t = threadIdx.x; t < nl * nc; t += blockDim.x) gl[t] = src[t];
     __syncthreads();
-    for (int l = threadIdx.x; l < nc; l += blockDim.x) {
-        float acc0 = 0.f, acc1 = 0.f;
-        const float *kk = ks + l + nc - 1;
-        int lp = (l & 1) ^ 1;
-        for (; lp + 2 < nc; lp += 4) {
-            acc0 = fmaf(kk[-lp], gl[lp], acc0);
-            acc1 = fmaf(kk[-lp - 2], gl[lp + 2], acc1);
+    const int tpl = hilbert_threads_per_line(nc);
+    const int li = threadIdx.x / tpl, r = threadIdx.x - li * tpl;
+    if (li >= nl) return;
+    const int half = tpl / 2;
+    const int par = r / half;                  // output parity
+    const int l0 = par + 2 * HR * (r - par * half);
+    if (l0 >= nc) return;
+    const float *g = gl + li * nc;
+    // inputs l' = 1-par, 3-par, ...; tap for output l0+2j and input l' is K[l0 + 2j - l']
+    float acc[HR];
+#pragma unroll
+    for (int j = 0; j < HR; ++j) acc[j] = 0.f;
+    const float *kk = ks + nc - 1 + l0;        // kk[2j - l'] = K[l0 + 2j - l']
+    int lp = 1 - par;
+    // window w[j] = K[l0 + 2j - lp]
+    float w[HR];
+#pragma unroll
+    for (int j = 0; j < HR; ++j) w[j] = kk[2 * j - lp];
+    for (; lp + 2 * (HR - 1) < nc; lp += 2 * HR) {
+#pragma unroll
+        for (int s = 0; s < HR; ++s) {
+            const float gv = g[lp + 2 * s];
+            // window for input lp + 2s: w[(j - s) mod HR] holds K[l0 + 2j - lp - 2s]
+#pragma unroll
+            for (int j = 0; j < HR; ++j) acc[j] = fmaf(w[(j - s + HR) % HR], gv, acc[j]);
+            // slide: input lp+2s+2 needs slot i = -s-1, i.e. K[l0 - 2s - 2 - lp], in the slot
+            // ((-s-1) mod HR) that held the tap of output HR-1-s just consumed
+            w[(HR - 1 - s) % HR] = kk[-2 * s - 2 - lp];
         }
-        for (; lp < nc; lp += 2) acc0 = fmaf(kk[-lp], gl[lp], acc0);
-        p.g4[line * nc + l] = acc0 + acc1;
     }
+    // remainder inputs (at most HR-1 of them)
+    for (; lp < nc; lp += 2) {
+        const float gv = g[lp];
+#pragma unroll
+        for (int j = 0; j < HR; ++j) acc[j] = fmaf(kk[2 * j - lp], gv, acc[j]);
+    }
+    float *dst = p.g4 + (line0 + li) * nc;
+#pragma unroll
+    for (int j = 0; j < HR; ++j)
+        if (l0 + 2 * j < nc) dst[l0 + 2 * j] = acc[j];
 }
 
 // ---------------------------------------------------------------------------
 // K4: gF[v][m][l] = cos α_l · lerp_ψ(g4[v][·][l], ψ̂(α_l, w_m))   (Eqs. 13-15)
+//
+// Output for the backprojection: per view, column-major 2x2 tap quads in
+// sum/difference form
+//   Q[v][l][r] = (½(g[m][l] + g[m+1][l]), ½(g[m][l+1] + g[m+1][l+1]),
+//                 g[m+1][l] - g[m][l],     g[m+1][l+1] - g[m][l+1]),   m = r - 2,
+// r = 0 .. nr+1 (two zero rows below the detector; taps beyond the last row or
+// column are 0).  A bilinear sample at (l + fa, m + f) is then
+//   Q.x w0 + Q.y w1 + (f - ½)(Q.z w0 + Q.w w1),   w0 = 1 - fa, w1 = fa,
+// i.e. one 128-bit load and two paired FMAs (FFMA2) in the BP.
+// Optionally also the plain gF (debug / parity entry point).
+// One CTA per (view, 32-column block): the block's (nr + 3) x 33 gF values are
+// formed in shared memory, then written as contiguous quad columns.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_bwd_rebin_cos(FilterParams p)
+constexpr int K4_COLS = 32;
+
+__global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
 {
-    const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = blockIdx.y;
-    const int v = blockIdx.z;
-    if (l >= p.nc) return;
-    const RebinEntry e = p.br[m * p.nc + l];
-    float out = 0.f;
-    if (e.idx >= 0) {
-        const float *g = p.g4 + ((size_t)v * p.npsi + e.idx) * p.nc + l;
-        float a = g[0], b = g[p.nc];
-        out = __ldg(p.cos_alpha + l) * fmaf(e.frac, b - a, a);
+    extern __shared__ float tile[];            // [nr + 3][K4_COLS + 1], rows m = -2 .. nr
+    const int nc = p.nc, nr = p.nr, nq = nr + 2;
+    const int l0 = blockIdx.x * K4_COLS;
+    const int v = blockIdx.y;
+    const int cols = min(K4_COLS, nc - l0);
+    const int ld = K4_COLS + 1;
+    for (int e = threadIdx.x; e < (nr + 3) * ld; e += blockDim.x) {
+        const int mm = e / ld, ll = e - mm * ld, m = mm - 2, l = l0 + ll;
+        float out = 0.f;
+        if (m >= 0 && m < nr && l < nc && ll <= cols) {
+            const RebinEntry r = p.br[m * nc + l];
+            if (r.idx >= 0) {
+                const float *g = p.g4 + ((size_t)v * p.npsi + r.idx) * nc + l;
+                const float a = g[0], b = g[nc];
+                out = __ldg(p.cos_alpha + l) * fmaf(r.frac, b - a, a);
+            }
+            if (p.gF && ll < cols) p.gF[((size_t)v * nr + m) * nc + l] = out;
+        }
+        tile[e] = out;
     }
-    p.gF[((size_t)v * p.nr + m) * p.nc + l] = out;
+    __syncthreads();
+    float4 *q = p.gq + ((size_t)v * nc + l0) * nq;
+    for (int e = threadIdx.x; e < cols * nq; e += blockDim.x) {
+        const int ll = e / nq, r = e - ll * nq;        // r = quad row; taps rows r-2, r-1
+        const float *t0 = tile + r * ld + ll;
+        const float a0 = t0[0], a1 = t0[1], c0 = t0[ld], c1 = t0[ld + 1];
+        q[e] = make_float4(0.5f * (a0 + c0), 0.5f * (a1 + c1), c0 - a0, c1 - a1);
+    }
 }
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
@@ -99,20 +169,29 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
 
 void launch_hilbert(const FilterParams &p, cudaStream_t s)
 {
-    size_t smem = sizeof(float) * (3 * (size_t)p.nc - 1);
-    int threads = p.nc >= 256 ? 256 : ((p.nc + 31) / 32) * 32;
+    const int tpl = 2 * (((p.nc + 1) / 2 + HR - 1) / HR);
+    const int lpb = tpl >= 256 ? 1 : 256 / tpl;
+    const int64_t n_lines = (int64_t)p.n_views * p.npsi;
+    size_t smem = sizeof(float) * (2 * (size_t)p.nc - 1 + 2 * (2 * HR + 4) + (size_t)lpb * p.nc);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_hilbert_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_hilbert, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    k_hilbert_direct<<<(unsigned)((size_t)p.n_views * p.npsi), threads, smem, s>>>(p);
+    const int threads = ((lpb * tpl + 31) / 32) * 32;
+    k_hilbert<<<(unsigned)((n_lines + lpb - 1) / lpb), threads, smem, s>>>(p, n_lines, lpb);
 }
 
 void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
 {
-    dim3 grid((p.nc + 127) / 128, p.nr, p.n_views);
-    k_bwd_rebin_cos<<<grid, 128, 0, s>>>(p);
+    dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, p.n_views);
+    size_t smem = sizeof(float) * (size_t)(p.nr + 3) * (K4_COLS + 1);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_bwd_rebin_cos, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    k_bwd_rebin_cos<<<grid, 256, smem, s>>>(p);
 }
 
 }  // namespace kats

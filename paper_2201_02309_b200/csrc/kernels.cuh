@@ -18,7 +18,9 @@ struct FilterParams {
     const RebinEntry *br;     // [nr][nc]
     const float *cos_alpha;   // [nc]
     const float *hilbert;     // [2nc-1]
-    float *g3, *g4, *gF;      // outputs ([n_views][npsi][nc] / [n_views][nr][nc])
+    float *g3, *g4;           // κ-line intermediates [n_views][npsi][nc]
+    float4 *gq;               // filtered views as column-major 2x2 sum/difference tap quads [n_views][nc][nr+2] (BP input)
+    float *gF;                // optional plain filtered views [n_views][nr][nc] (debug), may be null
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
@@ -28,20 +30,26 @@ void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s);     // K4:  Eq
 // Step 7 backprojection over `n_items`
 // independent pitches/slabs sharing the periodic tables.
 struct BPParams {
-    const float *gF;          // filtered views
-    int64_t off0, item_views; // gF view index of pitch-relative view k for item b: k + off0 + b*item_views
+    const float4 *gq;         // filtered views as column-major sum/difference tap quads [views][nc][nr+2]
+    int64_t off0, item_views; // view index of pitch-relative view k for item b: k + off0 + b*item_views
     int n_items;
     int nr, nc, nx, ny, nz;
+    unsigned colbytes;        // (nr + 2) * 16: one quad column (rows contiguous)
+    int64_t viewbytes;        // nc * (nr + 2) * 16: one quad view
     const int2 *pi_k;         // [nz][ny][nx] (k_first, k_last)
     const float2 *pi_w;       // [nz][ny][nx] (ω_first, ω_last)
     const ViewGeom *view;     // [k - view_lo]
     int view_lo;
-    float R, D, inv_dalpha, col_c, inv_dw, row_c;
+    float R, D_over_dw, inv_dalpha, col_c, row_c15, colmax, rowmax;
+    float at[7];              // α*/Δα polynomial in t = u/v*: t·Σ at[i] t^(2i)
     float x0, dx, y0, dy, dz;
     float scale;              // Δλ / 2π
+    bool poly;                // use the polynomial arctangent (|α| <= 36.8°)
+    bool checked;             // per-sample detector test on interior views (margin check failed)
     float *vol;               // [n_items][nz][ny][nx]
 };
 
 void launch_backproject(const BPParams &p, cudaStream_t s);           // K5
+void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cudaStream_t s);
 
 }  // namespace kats

@@ -25,6 +25,8 @@ struct HostTables {
     std::vector<int32_t> fr_idx, br_idx;
     std::vector<double> fr_frac, br_frac;
     bool td_covered = true;
+    double w_L = 0;                         // max |w*| over grid views inside PI windows (P:l.336)
+    bool interior_in_detector = false;      // interior BP samples provably inside rows and columns (fp32 margin)
 };
 
 // Per-view geometry for the backprojection (pitch-relative view k in [bp_lo, bp_hi]).

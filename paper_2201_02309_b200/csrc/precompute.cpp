@@ -273,7 +273,14 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
     if (lo > hi) { lo = 0; hi = -1; }
     t.bp_lo = lo;
     t.bp_hi = hi;
+    t.w_L = wL;
     t.td_covered = wL <= 0.5 * (nr - 1) * o.dw * (1.0 + 1e-9);
+    // Interior views (k_first < k < k_last) sample inside [λ_i, λ_o], so |w*| <= w_L and
+    // |α*| <= α_m; with a relative margin well above fp32 rounding the kernel may skip the
+    // per-sample detector test.
+    const double a_lo = (-0.5 * (nc - 1) + o.aoff) * o.da, a_hi = (0.5 * (nc - 1) + o.aoff) * o.da;
+    t.interior_in_detector = wL <= 0.5 * (nr - 1) * o.dw * (1.0 - 1e-5) &&
+                             a_lo <= -t.alpha_m - 1e-5 * o.da && a_hi >= t.alpha_m + 1e-5 * o.da;
     (void)root_fail;
     return t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }

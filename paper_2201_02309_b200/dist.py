@@ -1,0 +1,78 @@
+"""Multi-GPU pitch sharding (host logic; one process per GPU, torch.distributed).
+
+Pitches are independent given their slab and share every periodic table
+(PAPER.md l.174-185, l.246, l.265), so a long scan shards by pitch (z-slab):
+rank r reconstructs a contiguous block of pitches from the views that block
+needs (its pitches plus the PI-window overlap).  The only collective is the
+optional gather of the volume slabs (NCCL over NVLink on B200; gloo in the
+CPU tests).  Nothing here computes: reconstruction runs in libkatsevich.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    first_pitch: int
+    n_pitches: int
+
+
+def pitch_shards(total_pitches: int, world: int, first_pitch: int = 0):
+    """Contiguous, balanced split of pitches [first_pitch, first_pitch + total) over
+    `world` ranks (the first total % world ranks get one extra pitch)."""
+    if world < 1 or total_pitches < 0:
+        raise ValueError("world >= 1 and total_pitches >= 0 required")
+    base, extra = divmod(total_pitches, world)
+    out, p = [], first_pitch
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append(Shard(r, p, n))
+        p += n
+    return out
+
+
+def weak_shard(pitches_per_rank: int, rank: int) -> Shard:
+    """Weak scaling: every rank owns the same number of pitches of a longer scan."""
+    return Shard(rank, rank * pitches_per_rank, pitches_per_rank)
+
+
+def shard_views(pitch_views, shard: Shard):
+    """Views [v0, v0 + nv) shard needs, from `pitch_views(k) -> (first_view, n_views)`
+    (e.g. Plan.pitch_views): union of its pitches' slabs (halo included)."""
+    if shard.n_pitches == 0:
+        return 0, 0
+    f0, n0 = pitch_views(shard.first_pitch)
+    f1, n1 = pitch_views(shard.first_pitch + shard.n_pitches - 1)
+    return f0, f1 + n1 - f0
+
+
+def slice_scan(scan, scan_first_view: int, v0: int, nv: int):
+    """The rank's sub-range of a full scan array [views][rows][cols]."""
+    a = v0 - scan_first_view
+    if a < 0 or a + nv > scan.shape[0]:
+        raise ValueError(f"scan views [{scan_first_view}, {scan_first_view + scan.shape[0]}) "
+                         f"do not cover [{v0}, {v0 + nv})")
+    return scan[a:a + nv]
+
+
+def gather_volumes(local, shards, nz: int, dst: int = 0, group=None):
+    """Gather per-rank volume slabs [n_pitches*nz][ny][nx] to rank `dst`.
+    Unequal shards are padded to the largest for the collective and trimmed.
+    Returns the stacked volume on `dst`, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    assert len(shards) == world
+    max_p = max(s.n_pitches for s in shards)
+    ny, nx = local.shape[-2], local.shape[-1]
+    buf = torch.zeros((max_p * nz, ny, nx), dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]] = local
+    if rank == dst:
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.gather(buf, parts, dst=dst, group=group)
+        return torch.cat([parts[s.rank][: s.n_pitches * nz] for s in shards], dim=0)
+    dist.gather(buf, None, dst=dst, group=group)
+    return None
