@@ -7,7 +7,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -169,6 +171,11 @@ BPParams bp_params(const katsevich_plan *p)
     for (int i = 0; i < 7; ++i) b.at[i] = (float)(c[i] / g.d_alpha);
     b.poly = std::tan(p->t.alpha_m) <= 0.75;
     b.checked = !p->t.interior_in_detector;
+    b.fp_cols = p->t.fp_cols;
+    b.max_cta_views = (int)(p->t.bp_hi - p->t.bp_lo + 1);
+    b.fp_rows = p->t.fp_rows;
+    const char *ev = std::getenv("KATS_BP_KERNEL");          // "l1" forces the L1-path kernel (A/B tests)
+    b.staged = !(ev && std::string(ev) == "l1");
     b.x0 = (float)(-0.5 * g.nx * g.dx); b.dx = (float)g.dx;
     b.y0 = (float)(-0.5 * g.ny * g.dy); b.dy = (float)g.dy;
     b.dz = (float)(g.pitch / g.nz_per_pitch);
@@ -258,6 +265,11 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
         KCHECK(p, cudaDeviceSynchronize());
     }
     p->precomputed = true;
+    if (const char *v = std::getenv("KATS_VERBOSE"); v && *v == '1')
+        std::fprintf(stderr, "[katsevich] n_psi %d, bp views [%lld, %lld], w_L %.6f, interior_in_detector %d, "
+                             "footprint box %d cols x %d quad rows\n",
+                     p->t.n_psi, (long long)p->t.bp_lo, (long long)p->t.bp_hi, p->t.w_L,
+                     (int)p->t.interior_in_detector, p->t.fp_cols, p->t.fp_rows);
     return p->t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }
 
@@ -337,6 +349,7 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     if (rc) return rc;
     BPParams b = bp_params(p);
     b.gq = gq;
+    b.gq_views = nu;
     b.off0 = (int64_t)first_pitch * vt - u0;
     b.item_views = vt;
     b.n_items = n_pitches;
@@ -370,6 +383,7 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     }
     BPParams bp = bp_params(p);
     bp.gq = gq;
+    bp.gq_views = nbp * B;
     bp.off0 = -t.bp_lo;
     bp.item_views = nbp;
     bp.n_items = B;
@@ -448,6 +462,7 @@ int katsevich_backproject(katsevich_plan *p, const float *gF, int64_t gF0, int64
     KCHECK(p, cudaGetLastError());
     BPParams bp = bp_params(p);
     bp.gq = gq;
+    bp.gq_views = gFn;
     bp.off0 = (int64_t)pitch * vt - gF0;
     bp.item_views = 0;
     bp.n_items = 1;

@@ -26,6 +26,9 @@
 //  * which slices of the chunk see view k is a bitmask recomputed only at the
 //    2·JZ events where a slice's interior window opens or closes.
 #include <climits>
+#include <cstdio>
+
+#include <cuda.h>
 
 #include "kernels.cuh"
 
@@ -33,7 +36,7 @@ namespace kats {
 
 namespace {
 
-constexpr int TX = 16, TY = 16, JZ = 8;
+constexpr int TX = kTileX, TY = kTileY, JZ = kChunkZ;
 constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23: x + kMagic rounds x to an integer
 constexpr unsigned kMagicBits = 0x4B400000u;
 
@@ -60,8 +63,15 @@ __device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm("add.rn.f32x2 %0,
 __device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 __device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
+__device__ __forceinline__ void fma2_acc(u64 &acc, u64 a, u64 b) { asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b)); }
 
 __device__ __forceinline__ float4 ldq(u64 addr) { return __ldg(reinterpret_cast<const float4 *>(addr)); }
+__device__ __forceinline__ float4 lds128(unsigned saddr)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+    return v;
+}
 
 struct ViewSetup {
     u64 colbase;         // &Q[k][l][0] - kMagicBits*16  (quad row r at colbase + (kMagicBits + r) * 16)
@@ -111,10 +121,10 @@ __device__ __forceinline__ void tap2(const ViewSetup &s, u64 PM, u64 &acc0, u64 
     upk(FW, f0, f1);
     const float4 g0 = ldq(s.colbase + ((u64)__float_as_uint(q0) << 4));
     const float4 g1 = ldq(s.colbase + ((u64)__float_as_uint(q1) << 4));
-    acc0 = fma2(pk(g0.x, g0.y), s.W, acc0);
-    acc0 = fma2(pk(g0.z, g0.w), mul2(s.W, pk(f0, f0)), acc0);
-    acc1 = fma2(pk(g1.x, g1.y), s.W, acc1);
-    acc1 = fma2(pk(g1.z, g1.w), mul2(s.W, pk(f1, f1)), acc1);
+    fma2_acc(acc0, pk(g0.x, g0.y), s.W);
+    fma2_acc(acc0, pk(g0.z, g0.w), mul2(s.W, pk(f0, f0)));
+    fma2_acc(acc1, pk(g1.x, g1.y), s.W);
+    fma2_acc(acc1, pk(g1.z, g1.w), mul2(s.W, pk(f1, f1)));
 }
 
 __device__ __forceinline__ void tap1(const ViewSetup &s, float pm, u64 &acc)
@@ -122,8 +132,8 @@ __device__ __forceinline__ void tap1(const ViewSetup &s, float pm, u64 &acc)
     const float q = pm + kMagic;
     const float f = pm - (q - kMagic);
     const float4 g = ldq(s.colbase + ((u64)__float_as_uint(q) << 4));
-    acc = fma2(pk(g.x, g.y), s.W, acc);
-    acc = fma2(pk(g.z, g.w), mul2(s.W, pk(f, f)), acc);
+    fma2_acc(acc, pk(g.x, g.y), s.W);
+    fma2_acc(acc, pk(g.z, g.w), mul2(s.W, pk(f, f)));
 }
 
 // checked end-view sample with weight ω (reading A9: zero outside the closed node range)
@@ -235,6 +245,300 @@ __global__ void __launch_bounds__(TX *TY, 3) k_backproject(BPParams p)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory staged, warp-specialized variant (interior views, detector
+// margin check passed) — the default.  Per CTA, a producer warp plans the quad
+// box (fp_cols x fp_rows) each view of the CTA's view range needs (from the
+// tile's corner rays; 32 views per planning step, one per lane) and streams
+// it with bulk async copies (cp.async.bulk, TMA engine) into a ring of slots
+// guarded by full/empty mbarriers; 8 consumer warps read the taps with
+// LDS.128 (4 wavefronts per warp instead of ~8 for scattered 128-bit global
+// loads through L1) and release each slot with one mbarrier arrive.  No CTA
+// barrier inside the view loop, so warps drift freely within the ring depth.
+// ---------------------------------------------------------------------------
+constexpr int kBoxesBytes = 128;  // (unused head); keeps the stage 128-B aligned for TMA
+static_assert(kBoxesBytes % 16 == 0, "stage buffer must stay 16-byte aligned");
+
+__device__ __forceinline__ void mbar_init(unsigned addr, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned addr, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes) : "memory");
+}
+// producer-side wait: back off between polls so the spinning warp does not steal issue slots
+__device__ __forceinline__ void mbar_wait_sleep(unsigned addr, unsigned parity)
+{
+    unsigned done;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+        if (done) return;
+        __nanosleep(256);
+    }
+}
+__device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n}" ::"r"(addr), "r"(parity) : "memory");
+}
+// bulk async copy global -> shared (TMA engine), completion counted on an mbarrier
+// 3-D tensor TMA: box {4*fp_rows floats, fp_cols columns, 1 view} at (4*r0, c0, view)
+__device__ __forceinline__ void tma_box(unsigned dst, const CUtensorMap *map, int c_row, int c_col, int c_view, unsigned mbar)
+{
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c_row), "r"(c_col), "r"(c_view), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+template <bool POLY>
+__device__ __forceinline__ float col_of(const BPParams &p, float x, float y, float c, float s)
+{
+    const float vstar = fmaf(-x, c, fmaf(-y, s, p.R));
+    const float u = fmaf(y, c, -x * s);
+    if (POLY) {
+        const float t = u * rcp_approx(vstar), q = t * t;
+        float a = p.at[6];
+        a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+        a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+        return fmaf(t, a, p.col_c);
+    }
+    return fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+}
+
+// quad box origin (first column, first quad row) for view k of a CTA tile
+template <bool POLY>
+__device__ __forceinline__ int2 plan_box(const BPParams &p, int k, float xa, float ya, float zb)
+{
+    const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+    const float xb = xa + (TX - 1) * p.dx, yb = ya + (TY - 1) * p.dy;
+    float cmin = 1e30f, pmin = 1e30f;
+    const float cx[4] = {xa, xb, xa, xb}, cy[4] = {ya, ya, yb, yb};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        cmin = fminf(cmin, col_of<POLY>(p, cx[q], cy[q], vg.x, vg.y));
+        const float vstar = fmaf(-cx[q], vg.x, fmaf(-cy[q], vg.y, p.R));
+        const float u = fmaf(cy[q], vg.x, -cx[q] * vg.y);
+        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+        const float p0 = fmaf(sc, zb - vg.z, p.row_c15);
+        pmin = fminf(pmin, fminf(p0, fmaf(sc, (JZ - 1) * p.dz, p0)));
+    }
+    int c0 = (int)floorf(cmin) - 1, r0 = (int)floorf(pmin) - 1;
+    c0 = max(0, min(c0, p.nc - p.fp_cols));
+    r0 = max(0, min(r0, p.nr + 2 - p.fp_rows));
+    return make_int2(c0, r0);
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned addr)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+
+// Warp-specialized: warps 0..7 consume (16x16 columns, 8x4 per warp), warp 8 produces.
+constexpr int kConsumerWarps = (TX * TY) / 32;
+constexpr int kWsThreads = TX * TY + 32;
+constexpr int kMaxSlots = 16;
+
+template <bool POLY>
+__global__ void __launch_bounds__(kWsThreads, 2) k_backproject_smem(BPParams p, const __grid_constant__ CUtensorMap qmap)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);         // [nslots][slot_quads]
+    int2 *boxes = reinterpret_cast<int2 *>(smem + kBoxesBytes + (size_t)p.nbatch * (((size_t)p.fp_cols * p.fp_rows + 7) & ~(size_t)7) * 16);  // [max_views] box origin per view of the CTA range
+    __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
+    __shared__ int s_k0, s_k1;
+    const int BW = p.fp_cols, BH = p.fp_rows, box = BW * BH, S = p.nbatch;
+    const int slot_quads = (box + 7) & ~7;     // 128-B aligned slots
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = warp == kConsumerWarps;
+    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
+    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int nchunk = (p.nz + JZ - 1) / JZ;
+    const int chunk = blockIdx.z % nchunk;
+    const int item = blockIdx.z / nchunk;
+    const bool inside = !producer && ix < p.nx && iy < p.ny;
+    const int j0 = chunk * JZ;
+    const int nzc = min(JZ, p.nz - j0);
+    const size_t plane = (size_t)p.nx * p.ny;
+    const int2 *pik = p.pi_k + (size_t)j0 * plane + (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
+    const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
+
+    if (tid == 0) {
+        s_k0 = INT_MAX; s_k1 = INT_MIN;
+        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, kConsumerWarps); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int K0 = INT_MAX, K1 = INT_MIN;
+    if (inside)
+        for (int t = 0; t < nzc; ++t) {
+            const int2 e = pik[t * plane];
+            if (e.x + 1 <= e.y - 1) { K0 = min(K0, e.x + 1); K1 = max(K1, e.y - 1); }
+        }
+    int wk0 = K0, wk1 = K1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wk0 = min(wk0, __shfl_xor_sync(0xffffffffu, wk0, o));
+        wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
+    }
+    if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    const float zb = j0 * p.dz;
+    const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
+    __syncthreads();                          // the only CTA-wide barrier after setup
+    const int KC0 = s_k0, KC1 = s_k1;
+    const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
+
+    // plan every view's quad box of the CTA range up front (all threads, a few views each)
+    {
+        const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
+        for (int k = KC0 + tid; k <= KC1; k += kWsThreads) boxes[k - KC0] = plan_box<POLY>(p, k, xa, ya, zb);
+    }
+    __syncthreads();
+
+    if (producer) {
+        // ---- producer warp: lanes 0..3 each stream one view's box per iteration into the slot ring ----
+        const int vbase = (int)(p.off0 + (int64_t)item * p.item_views);   // tensor view coordinate of k = 0
+        constexpr int G = 4;
+        if (lane < G) {
+            int sl = lane;
+            unsigned phase = 0;
+            for (int n = lane; KC0 + n <= KC1; n += G) {
+                if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);   // consumers released this slot
+                const unsigned full = full0 + 8u * sl;
+                const int2 bo = boxes[n];
+                mbar_expect_tx(full, (unsigned)box * 16u);
+                tma_box(stage_sa + (unsigned)(sl * slot_quads) * 16u, &qmap, 4 * bo.y, bo.x, vbase + KC0 + n, full);
+                sl += G;
+                if (sl >= S) { sl -= S; phase ^= 1u; }
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps ----
+    u64 acc[JZ];
+#pragma unroll
+    for (int t = 0; t < JZ; ++t) acc[t] = 0ull;
+    unsigned mask = 0;
+    int next_ev = K0;
+    int sl = 0;
+    unsigned phase = 0;
+    for (int k = KC0; k <= KC1; ++k) {
+        mbar_wait(full0 + 8u * sl, phase);
+        if (k >= K0 && k <= K1) {
+            if (k >= next_ev) {
+                mask = 0;
+                next_ev = INT_MAX;
+                for (int t = 0; t < nzc; ++t) {
+                    const int2 e = pik[t * plane];
+                    const int a = e.x + 1, bb = e.y - 1;
+                    if (a <= bb) {
+                        if (a <= k && k <= bb) mask |= 1u << t;
+                        if (a > k) next_ev = min(next_ev, a);
+                        if (bb >= k) next_ev = min(next_ev, bb + 1);
+                    }
+                }
+            }
+            if (mask != 0) {
+                const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+                const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+                const float u = fmaf(y, vg.x, -x * vg.y);
+                const float inv_v = rcp_approx(vstar);
+                float colpos;
+                if (POLY) {
+                    const float tt = u * inv_v, q = tt * tt;
+                    float a = p.at[6];
+                    a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+                    a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+                    colpos = fmaf(tt, a, p.col_c);
+                } else {
+                    colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+                }
+                const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
+                const int l = __float2int_rz(cp);
+                const float fa = cp - __int2float_rn(l);
+                const float w1 = fa * inv_v;
+                const u64 W = pk(inv_v - w1, w1);
+                const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+                const float base = fmaf(sc, zb - vg.z, p.row_c15), step = sc * p.dz;
+                const int2 bo = boxes[k - KC0];
+                const int ci = min(max(l - bo.x, 0), BW - 1);
+                // shared byte address of quad row r: colbase + (kMagicBits + r) * 16  (mod 2^32)
+                unsigned colbase = stage_sa + (unsigned)(sl * slot_quads + ci * BH) * 16u -
+                                   (kMagicBits + (unsigned)bo.y) * 16u;
+                asm("" : "+r"(colbase));      // keep the magic offset folded (one LEA per sample)
+                if (mask == (1u << JZ) - 1) {
+                    const u64 B = pk(base, base), Sd = pk(step, step);
+#pragma unroll
+                    for (int t = 0; t < JZ; t += 2) {
+                        const u64 PM = fma2(pk((float)t, (float)(t + 1)), Sd, B);
+                        const u64 Q = add2(PM, pk(kMagic, kMagic));
+                        const u64 FW = sub2(PM, sub2(Q, pk(kMagic, kMagic)));
+                        float q0, q1, f0, f1;
+                        upk(Q, q0, q1);
+                        upk(FW, f0, f1);
+                        const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+                        const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+                        fma2_acc(acc[t], pk(g0.x, g0.y), W);
+                        fma2_acc(acc[t], pk(g0.z, g0.w), mul2(W, pk(f0, f0)));
+                        fma2_acc(acc[t + 1], pk(g1.x, g1.y), W);
+                        fma2_acc(acc[t + 1], pk(g1.z, g1.w), mul2(W, pk(f1, f1)));
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < JZ; ++t)
+                        if (mask & (1u << t)) {
+                            const float pm = fmaf((float)t, step, base);
+                            const float q = pm + kMagic;
+                            const float f = pm - (q - kMagic);
+                            const float4 g = lds128(colbase + __float_as_uint(q) * 16u);
+                            fma2_acc(acc[t], pk(g.x, g.y), W);
+                            fma2_acc(acc[t], pk(g.z, g.w), mul2(W, pk(f, f)));
+                        }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8u * sl);   // this warp is done with the slot
+        if (++sl == S) { sl = 0; phase ^= 1u; }
+    }
+    if (!inside) return;
+    // end views: fractional weights ω_first, ω_last and the full range test (global loads)
+    const float2 *piw = p.pi_w + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
+#pragma unroll
+    for (int t = 0; t < JZ; ++t) {
+        if (t < nzc) {
+            const int2 e = pik[t * plane];
+            if (e.x <= e.y) {
+                const float2 w = piw[t * plane];
+                tap_checked<POLY>(p, qbase, e.x, x, y, zb, t, w.x, acc[t]);
+                if (e.y != e.x) tap_checked<POLY>(p, qbase, e.y, x, y, zb, t, w.y, acc[t]);
+            }
+        }
+    }
+    float *out = p.vol + (size_t)item * p.nz * plane + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
+#pragma unroll
+    for (int t = 0; t < JZ; ++t) {
+        if (t < nzc) {
+            float a, b;
+            upk(acc[t], a, b);
+            out[t * plane] = (a + b) * p.scale;
+        }
+    }
+}
+
 // plain gF [n][nr][nc] -> column-major sum/difference tap quads [n][nc][nr+2] (debug entry point)
 __global__ void k_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc)
 {
@@ -257,11 +561,70 @@ void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cu
     k_make_quads<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(gF, q, n, nr, nc);
 }
 
+size_t backproject_smem_bytes(const BPParams &p)
+{
+    const size_t slot = (((size_t)p.fp_cols * p.fp_rows + 7) & ~(size_t)7) * sizeof(float4);
+    return kBoxesBytes + (size_t)p.nbatch * slot + sizeof(int2) * (size_t)p.max_cta_views;
+}
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled()
+{
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    return fn;
+}
+
+// the quad array as a 3-D fp32 tensor: (4 * (nr+2) floats per column, nc columns, n_views)
+bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
+{
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)4 * (p.nr + 2), (cuuint64_t)p.nc, (cuuint64_t)n_views};
+    const cuuint64_t strides[2] = {(cuuint64_t)(p.nr + 2) * 16, (cuuint64_t)p.viewbytes};
+    const cuuint32_t box[3] = {(cuuint32_t)(4 * p.fp_rows), (cuuint32_t)p.fp_cols, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
 void launch_backproject(const BPParams &p, cudaStream_t s)
 {
     const int nchunk = (p.nz + JZ - 1) / JZ;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk * p.n_items);
     const int block = TX * TY;
+    BPParams q = p;
+    // deepest slot ring (<= kMaxSlots views) that lets 2 CTAs share an SM
+    q.nbatch = kMaxSlots;
+    while (q.nbatch > 4 && backproject_smem_bytes(q) > 100 * 1024) q.nbatch /= 2;
+    const size_t sm = backproject_smem_bytes(q);
+    CUtensorMap qmap;
+    const bool box_ok = p.fp_rows * 4 <= 256 && p.fp_cols <= 256;
+    if (p.staged && !p.checked && sm <= 200 * 1024 && box_ok && p.gq_views > 0 && make_quad_map(p, p.gq_views, &qmap)) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_backproject_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_backproject_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+        if (p.poly) k_backproject_smem<true><<<grid, kWsThreads, sm, s>>>(q, qmap);
+        else k_backproject_smem<false><<<grid, kWsThreads, sm, s>>>(q, qmap);
+        return;
+    }
     if (p.poly) {
         if (p.checked) k_backproject<true, true><<<grid, block, 0, s>>>(p);
         else k_backproject<true, false><<<grid, block, 0, s>>>(p);

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin(FilterParams p)
 // ---------------------------------------------------------------------------
 constexpr int HR = 8;
 
-__device__ __forceinline__ int hilbert_threads_per_line(int nc) { return 2 * ((nc + 1) / 2 + HR - 1) / HR; }
+__device__ __forceinline__ int hilbert_threads_per_line(int nc) { return 2 * (((nc + 1) / 2 + HR - 1) / HR); }
 
 __global__ void __launch_bounds__(256) k_hilbert(FilterParams p, int64_t n_lines, int lines_per_block)
 {

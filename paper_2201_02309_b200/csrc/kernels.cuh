@@ -46,6 +46,11 @@ struct BPParams {
     float scale;              // Δλ / 2π
     bool poly;                // use the polynomial arctangent (|α| <= 36.8°)
     bool checked;             // per-sample detector test on interior views (margin check failed)
+    bool staged;              // use the shared-memory staged kernel
+    int fp_cols, fp_rows;     // per-view quad box of one CTA (staged kernel)
+    int nbatch;               // slots in the staged kernel's ring (set by the launcher)
+    int64_t gq_views;         // views in the gq array (TMA tensor extent)
+    int max_cta_views;        // upper bound of a CTA's interior view range (box table size)
     float *vol;               // [n_items][nz][ny][nx]
 };
 

@@ -13,6 +13,10 @@ namespace kats {
 
 constexpr double kPi = 3.14159265358979323846;
 
+// Backprojection work decomposition (backproject.cu): a CTA owns a TILE_X x TILE_Y
+// tile of (x, y) columns and a chunk of CHUNK_Z slices.
+constexpr int kTileX = 16, kTileY = 16, kChunkZ = 8;
+
 // Host-side periodic tables (double precision, pitch 0).
 struct HostTables {
     int32_t n_psi = 0;
@@ -27,6 +31,7 @@ struct HostTables {
     bool td_covered = true;
     double w_L = 0;                         // max |w*| over grid views inside PI windows (P:l.336)
     bool interior_in_detector = false;      // interior BP samples provably inside rows and columns (fp32 margin)
+    int32_t fp_cols = 0, fp_rows = 0;       // quad box (columns x quad rows) covering any CTA's interior samples of one view
 };
 
 // Per-view geometry for the backprojection (pitch-relative view k in [bp_lo, bp_hi]).

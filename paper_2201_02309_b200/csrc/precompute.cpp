@@ -282,6 +282,54 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
     t.interior_in_detector = wL <= 0.5 * (nr - 1) * o.dw * (1.0 - 1e-5) &&
                              a_lo <= -t.alpha_m - 1e-5 * o.da && a_hi >= t.alpha_m + 1e-5 * o.da;
     (void)root_fail;
+
+    // ---- footprint box of one CTA (kTileX x kTileY columns, kChunkZ slices) on one
+    // interior view: columns/quad rows spanned by the tile's corner rays (the
+    // extreme α* and |r| over a square are at its corners), over every tile, chunk
+    // and interior view; +margins for the kernel's fp32 arithmetic.
+    {
+        const int ntx = (o.nx + kTileX - 1) / kTileX, nty = (o.ny + kTileY - 1) / kTileY;
+        const int nch = (o.nz + kChunkZ - 1) / kChunkZ;
+        int bw = 0, bh = 0;
+        #pragma omp parallel for collapse(2) schedule(dynamic, 1) reduction(max:bw, bh)
+        for (int ty = 0; ty < nty; ++ty)
+            for (int tx = 0; tx < ntx; ++tx)
+                for (int ch = 0; ch < nch; ++ch) {
+                    int64_t k0 = INT64_MAX, k1 = INT64_MIN;
+                    for (int j = ch * kChunkZ; j < std::min(o.nz, (ch + 1) * kChunkZ); ++j)
+                        for (int iy = ty * kTileY; iy < std::min(o.ny, (ty + 1) * kTileY); ++iy)
+                            for (int ix = tx * kTileX; ix < std::min(o.nx, (tx + 1) * kTileX); ++ix) {
+                                size_t id = ((size_t)j * o.ny + iy) * o.nx + ix;
+                                if (t.pi_first[id] + 1 <= t.pi_last[id] - 1) {
+                                    k0 = std::min<int64_t>(k0, t.pi_first[id] + 1);
+                                    k1 = std::max<int64_t>(k1, t.pi_last[id] - 1);
+                                }
+                            }
+                    const double xa = ((double)tx * kTileX - 0.5 * o.nx) * o.dx, xb = xa + (kTileX - 1) * o.dx;
+                    const double ya = ((double)ty * kTileY - 0.5 * o.ny) * o.dy, yb = ya + (kTileY - 1) * o.dy;
+                    const double zb = (double)ch * kChunkZ * o.dz;
+                    for (int64_t k = k0; k <= k1; ++k) {
+                        const double lam = (double)k * o.dlam;
+                        const double c = std::cos(lam + o.lam0), s = std::sin(lam + o.lam0);
+                        const double zc = o.z0 + o.h * lam;
+                        double cmin = 1e300, cmax = -1e300, pmin = 1e300, pmax = -1e300;
+                        const double cx[4] = {xa, xb, xa, xb}, cy[4] = {ya, ya, yb, yb};
+                        for (int q = 0; q < 4; ++q) {
+                            const double vs = o.R - cx[q] * c - cy[q] * s, us = -cx[q] * s + cy[q] * c;
+                            const double col = std::atan2(us, vs) / o.da + 0.5 * (nc - 1) - o.aoff;
+                            const double sc = o.D / std::hypot(us, vs) / o.dw;
+                            const double p0 = sc * (zb - zc) + 0.5 * (nr - 1) + 1.5;
+                            const double p1 = p0 + sc * (kChunkZ - 1) * o.dz;
+                            cmin = std::min(cmin, col); cmax = std::max(cmax, col);
+                            pmin = std::min(pmin, std::min(p0, p1)); pmax = std::max(pmax, std::max(p0, p1));
+                        }
+                        bw = std::max(bw, (int)(std::floor(cmax) - std::floor(cmin)) + 3);
+                        bh = std::max(bh, (int)(std::floor(pmax) - std::floor(pmin)) + 4);
+                    }
+                }
+        t.fp_cols = std::min(bw, nc);
+        t.fp_rows = std::min(bh, nr + 2);
+    }
     return t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }
 
