@@ -173,6 +173,15 @@ BPParams bp_params(const katsevich_plan *p)
     b.checked = !p->t.interior_in_detector;
     b.fp_cols = p->t.fp_cols;
     b.max_cta_views = (int)(p->t.bp_hi - p->t.bp_lo + 1);
+    b.fp_cols_column = p->t.fp_cols_column;
+    b.max_active = p->t.max_active;
+    b.windows_monotone = p->t.windows_monotone;
+    {   // rows an inactive window entry (up to 3 slices above the top open one) can overshoot
+        const double r_near = g.R - p->t.r_fov;
+        const double step_max = g.D / (r_near * g.d_w) * (g.pitch / g.nz_per_pitch);
+        b.tail_quads = 8 + (int)std::ceil(3.0 * step_max) + 2;
+    }
+    b.zero = 0u;
     b.fp_rows = p->t.fp_rows;
     const char *ev = std::getenv("KATS_BP_KERNEL");          // "l1" forces the L1-path kernel (A/B tests)
     b.staged = !(ev && std::string(ev) == "l1");
@@ -267,9 +276,10 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
     p->precomputed = true;
     if (const char *v = std::getenv("KATS_VERBOSE"); v && *v == '1')
         std::fprintf(stderr, "[katsevich] n_psi %d, bp views [%lld, %lld], w_L %.6f, interior_in_detector %d, "
-                             "footprint box %d cols x %d quad rows\n",
+                             "footprint box %d cols x %d quad rows, column box %d cols, max active slices %d, monotone %d\n",
                      p->t.n_psi, (long long)p->t.bp_lo, (long long)p->t.bp_hi, p->t.w_L,
-                     (int)p->t.interior_in_detector, p->t.fp_cols, p->t.fp_rows);
+                     (int)p->t.interior_in_detector, p->t.fp_cols, p->t.fp_rows, p->t.fp_cols_column,
+                     p->t.max_active, (int)p->t.windows_monotone);
     return p->t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }
 

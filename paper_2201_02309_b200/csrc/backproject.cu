@@ -36,7 +36,8 @@ namespace kats {
 
 namespace {
 
-constexpr int TX = kTileX, TY = kTileY, JZ = kChunkZ;
+constexpr int TX = kTileX, TY = kTileY, JZ = kChunkZ;   // staged kernel: 16 slices per thread
+constexpr int JZL = 8;                                    // L1-path fallback kernel: 8 slices per thread
 constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23: x + kMagic rounds x to an integer
 constexpr unsigned kMagicBits = 0x4B400000u;
 
@@ -159,12 +160,12 @@ __global__ void __launch_bounds__(TX *TY, 3) k_backproject(BPParams p)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
     const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
-    const int nchunk = (p.nz + JZ - 1) / JZ;
+    const int nchunk = (p.nz + JZL - 1) / JZL;
     const int chunk = blockIdx.z % nchunk;
     const int item = blockIdx.z / nchunk;
     if (ix >= p.nx || iy >= p.ny) return;
-    const int j0 = chunk * JZ;
-    const int nzc = min(JZ, p.nz - j0);
+    const int j0 = chunk * JZL;
+    const int nzc = min(JZL, p.nz - j0);
     const size_t plane = (size_t)p.nx * p.ny;
     const int2 *pik = p.pi_k + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
 
@@ -178,9 +179,9 @@ __global__ void __launch_bounds__(TX *TY, 3) k_backproject(BPParams p)
     const float zb = j0 * p.dz;
     const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
 
-    u64 acc[JZ];
+    u64 acc[JZL];
 #pragma unroll
-    for (int t = 0; t < JZ; ++t) acc[t] = 0ull;
+    for (int t = 0; t < JZL; ++t) acc[t] = 0ull;
 
     unsigned mask = 0;
     int next_ev = K0;
@@ -206,25 +207,25 @@ __global__ void __launch_bounds__(TX *TY, 3) k_backproject(BPParams p)
         if (CHECK) {
             if (!(s.colpos >= 0.f && s.colpos <= p.colmax)) continue;
 #pragma unroll
-            for (int t = 0; t < JZ; ++t) {
+            for (int t = 0; t < JZL; ++t) {
                 const float pm = fmaf((float)t, s.step, s.base);
                 if ((mask & (1u << t)) && pm >= 1.5f && pm <= p.rowmax + 1.5f) tap1(s, pm, acc[t]);
             }
-        } else if (mask == (1u << JZ) - 1) {
+        } else if (mask == (1u << JZL) - 1) {
             const u64 B = pk(s.base, s.base), S = pk(s.step, s.step);
 #pragma unroll
-            for (int t = 0; t < JZ; t += 2)
+            for (int t = 0; t < JZL; t += 2)
                 tap2(s, fma2(pk((float)t, (float)(t + 1)), S, B), acc[t], acc[t + 1]);
         } else {
 #pragma unroll
-            for (int t = 0; t < JZ; ++t)
+            for (int t = 0; t < JZL; ++t)
                 if (mask & (1u << t)) tap1(s, fmaf((float)t, s.step, s.base), acc[t]);
         }
     }
     // end views: fractional weights ω_first, ω_last and the full range test
     const float2 *piw = p.pi_w + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
 #pragma unroll
-    for (int t = 0; t < JZ; ++t) {
+    for (int t = 0; t < JZL; ++t) {
         if (t < nzc) {
             const int2 e = pik[t * plane];
             if (e.x <= e.y) {
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(TX *TY, 3) k_backproject(BPParams p)
     }
     float *out = p.vol + (size_t)item * p.nz * plane + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
 #pragma unroll
-    for (int t = 0; t < JZ; ++t) {
+    for (int t = 0; t < JZL; ++t) {
         if (t < nzc) {
             float a, b;
             upk(acc[t], a, b);
@@ -267,16 +268,15 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned addr, unsigned bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes) : "memory");
 }
-// producer-side wait: back off between polls so the spinning warp does not steal issue slots
+// producer-side wait: suspend in hardware until the phase completes (time hint 1 ms) so the
+// waiting warp does not spin on issue slots
 __device__ __forceinline__ void mbar_wait_sleep(unsigned addr, unsigned parity)
 {
-    unsigned done;
-    for (;;) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(done) : "r"(addr), "r"(parity) : "memory");
-        if (done) return;
-        __nanosleep(256);
-    }
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, 1000000;\n\t"
+        "@!done bra WAITS_%=;\n}" ::"r"(addr), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned addr, unsigned parity)
 {
@@ -347,44 +347,63 @@ constexpr int kConsumerWarps = (TX * TY) / 32;
 constexpr int kWsThreads = TX * TY + 32;
 constexpr int kMaxSlots = 16;
 
+// column of the tile's quad box for view k (rows: the whole detector)
 template <bool POLY>
-__global__ void __launch_bounds__(kWsThreads, 2) k_backproject_smem(BPParams p, const __grid_constant__ CUtensorMap qmap)
+__device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, float ya)
+{
+    const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+    const float xb = xa + (TX - 1) * p.dx, yb = ya + (TY - 1) * p.dy;
+    float cmin = fminf(fminf(col_of<POLY>(p, xa, ya, vg.x, vg.y), col_of<POLY>(p, xb, ya, vg.x, vg.y)),
+                       fminf(col_of<POLY>(p, xa, yb, vg.x, vg.y), col_of<POLY>(p, xb, yb, vg.x, vg.y)));
+    int c0 = (int)floorf(cmin) - 1;
+    return max(0, min(c0, p.nc - p.fp_cols_column));
+}
+
+// ---------------------------------------------------------------------------
+// Sliding-window kernel.  A thread owns a whole (x, y) column of the pitch and
+// keeps W scalar accumulators for exactly the slices whose interior PI windows
+// contain the current view (a contiguous, monotonically advancing slice range
+// [t_lo, t_hi]; requires the host's monotone-window check).  Slices enter the
+// window when their window opens and are flushed from its bottom (end views
+// with their fractional weights added, volume written, registers shifted)
+// when it closes, so no view does partial work and the per-(x, y, view) setup
+// is shared by every active slice (~40 at C3/C4).
+// ---------------------------------------------------------------------------
+template <bool POLY, int W>
+__global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const __grid_constant__ CUtensorMap qmap)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);         // [nslots][slot_quads]
-    int2 *boxes = reinterpret_cast<int2 *>(smem + kBoxesBytes + (size_t)p.nbatch * (((size_t)p.fp_cols * p.fp_rows + 7) & ~(size_t)7) * 16);  // [max_views] box origin per view of the CTA range
+    const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch;
+    const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged view (128-B aligned)
+    const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
+    float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
+    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vq * 16);   // first column per view
     __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
     __shared__ int s_k0, s_k1;
-    const int BW = p.fp_cols, BH = p.fp_rows, box = BW * BH, S = p.nbatch;
-    const int slot_quads = (box + 7) & ~7;     // 128-B aligned slots
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = warp == kConsumerWarps;
     const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
     const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
-    const int nchunk = (p.nz + JZ - 1) / JZ;
-    const int chunk = blockIdx.z % nchunk;
-    const int item = blockIdx.z / nchunk;
+    const int item = blockIdx.z;
     const bool inside = !producer && ix < p.nx && iy < p.ny;
-    const int j0 = chunk * JZ;
-    const int nzc = min(JZ, p.nz - j0);
     const size_t plane = (size_t)p.nx * p.ny;
-    const int2 *pik = p.pi_k + (size_t)j0 * plane + (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const int2 *pik = p.pi_k + col;
     const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
     const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
 
     if (tid == 0) {
         s_k0 = INT_MAX; s_k1 = INT_MIN;
-        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, kConsumerWarps); }
+        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, TX * TY); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     int K0 = INT_MAX, K1 = INT_MIN;
-    if (inside)
-        for (int t = 0; t < nzc; ++t) {
-            const int2 e = pik[t * plane];
-            if (e.x + 1 <= e.y - 1) { K0 = min(K0, e.x + 1); K1 = max(K1, e.y - 1); }
-        }
+    if (inside) {
+        const int2 e0 = pik[0];
+        if (e0.x <= e0.y) { K0 = e0.x + 1; K1 = pik[(size_t)(p.nz - 1) * plane].y - 1; }
+    }
     int wk0 = K0, wk1 = K1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -392,34 +411,31 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_backproject_smem(BPParams p, 
         wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
     }
     if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
-
     const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
-    const float zb = j0 * p.dz;
     const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
-    __syncthreads();                          // the only CTA-wide barrier after setup
+    __syncthreads();
     const int KC0 = s_k0, KC1 = s_k1;
+    const int NV = KC1 - KC0 + 1;
     const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
-
-    // plan every view's quad box of the CTA range up front (all threads, a few views each)
     {
         const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
-        for (int k = KC0 + tid; k <= KC1; k += kWsThreads) boxes[k - KC0] = plan_box<POLY>(p, k, xa, ya, zb);
+        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col<POLY>(p, KC0 + n, xa, ya);
     }
     __syncthreads();
 
     if (producer) {
-        // ---- producer warp: lanes 0..3 each stream one view's box per iteration into the slot ring ----
-        const int vbase = (int)(p.off0 + (int64_t)item * p.item_views);   // tensor view coordinate of k = 0
+        if (NV <= 0) return;
+        // ---- producer warp: lanes 0..3 stream one view's full-height column box each per round ----
+        const int vbase = (int)(p.off0 + (int64_t)item * p.item_views) + KC0;
         constexpr int G = 4;
         if (lane < G) {
             int sl = lane;
             unsigned phase = 0;
-            for (int n = lane; KC0 + n <= KC1; n += G) {
-                if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);   // consumers released this slot
+            for (int n = lane; n < NV; n += G) {
+                if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
                 const unsigned full = full0 + 8u * sl;
-                const int2 bo = boxes[n];
-                mbar_expect_tx(full, (unsigned)box * 16u);
-                tma_box(stage_sa + (unsigned)(sl * slot_quads) * 16u, &qmap, 4 * bo.y, bo.x, vbase + KC0 + n, full);
+                mbar_expect_tx(full, box_bytes);
+                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 0, boxc[n], vbase + n, full);
                 sl += G;
                 if (sl >= S) { sl -= S; phase ^= 1u; }
             }
@@ -428,30 +444,46 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_backproject_smem(BPParams p, 
     }
 
     // ---- consumer warps ----
-    u64 acc[JZ];
+    float acc[W];
 #pragma unroll
-    for (int t = 0; t < JZ; ++t) acc[t] = 0ull;
-    unsigned mask = 0;
-    int next_ev = K0;
+    for (int i = 0; i < W; ++i) acc[i] = 0.f;
+    const float2 *piw = p.pi_w + col;
+    float *out = p.vol + (size_t)item * p.nz * plane + col;
+    const bool active_col = inside && K0 <= K1;
+    int t_lo = 0, t_hi = -1;
+    int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
+
+    // slice t_lo's window is closed: add its two end views, write it, shift the register window
+    auto flush = [&]() {
+        const int2 e = pik[(size_t)t_lo * plane];
+        const float2 w = piw[(size_t)t_lo * plane];
+        u64 ends = 0ull;
+        tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t_lo, w.x, ends);
+        tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t_lo, w.y, ends);
+        float ea, eb;
+        upk(ends, ea, eb);
+        out[(size_t)t_lo * plane] = (acc[0] + ea + eb) * p.scale;
+#pragma unroll
+        for (int i = 0; i < W - 1; ++i) acc[i] = acc[i + 1];
+        acc[W - 1] = 0.f;
+        ++t_lo;
+        next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;   // b + 1 = k_last
+    };
+
     int sl = 0;
     unsigned phase = 0;
-    for (int k = KC0; k <= KC1; ++k) {
+    for (int n = 0; n < NV; ++n) {
+        const int k = KC0 + n;
         mbar_wait(full0 + 8u * sl, phase);
-        if (k >= K0 && k <= K1) {
-            if (k >= next_ev) {
-                mask = 0;
-                next_ev = INT_MAX;
-                for (int t = 0; t < nzc; ++t) {
-                    const int2 e = pik[t * plane];
-                    const int a = e.x + 1, bb = e.y - 1;
-                    if (a <= bb) {
-                        if (a <= k && k <= bb) mask |= 1u << t;
-                        if (a > k) next_ev = min(next_ev, a);
-                        if (bb >= k) next_ev = min(next_ev, bb + 1);
-                    }
-                }
+        if (active_col) {
+            while (k >= next_open) {                              // slice t_hi+1's interior window opens
+                ++t_hi;
+                if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+                next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
             }
-            if (mask != 0) {
+            while (k >= next_close) flush();                      // slice t_lo's window closed
+            const int n_act = t_hi - t_lo + 1;
+            if (n_act > 0 && k <= K1) {
                 const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
                 const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
                 const float u = fmaf(y, vg.x, -x * vg.y);
@@ -470,73 +502,56 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_backproject_smem(BPParams p, 
                 const int l = __float2int_rz(cp);
                 const float fa = cp - __int2float_rn(l);
                 const float w1 = fa * inv_v;
-                const u64 W = pk(inv_v - w1, w1);
+                const u64 Wp = pk(inv_v - w1, w1);
                 const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
-                const float base = fmaf(sc, zb - vg.z, p.row_c15), step = sc * p.dz;
-                const int2 bo = boxes[k - KC0];
-                const int ci = min(max(l - bo.x, 0), BW - 1);
-                // shared byte address of quad row r: colbase + (kMagicBits + r) * 16  (mod 2^32)
-                unsigned colbase = stage_sa + (unsigned)(sl * slot_quads + ci * BH) * 16u -
-                                   (kMagicBits + (unsigned)bo.y) * 16u;
-                asm("" : "+r"(colbase));      // keep the magic offset folded (one LEA per sample)
-                if (mask == (1u << JZ) - 1) {
-                    const u64 B = pk(base, base), Sd = pk(step, step);
+                const float step = sc * p.dz;
+                const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_c15));   // entry 0 = slice t_lo
+                const int ci = min(max(l - boxc[n], 0), BW - 1);
+                // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
+                const unsigned colbase = (stage_sa + (unsigned)(sl * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
+                const u64 S2 = pk(2.f * step, 2.f * step);
+                u64 PM = pk(base, base + step);
 #pragma unroll
-                    for (int t = 0; t < JZ; t += 2) {
-                        const u64 PM = fma2(pk((float)t, (float)(t + 1)), Sd, B);
-                        const u64 Q = add2(PM, pk(kMagic, kMagic));
-                        const u64 FW = sub2(PM, sub2(Q, pk(kMagic, kMagic)));
-                        float q0, q1, f0, f1;
-                        upk(Q, q0, q1);
-                        upk(FW, f0, f1);
-                        const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
-                        const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                        fma2_acc(acc[t], pk(g0.x, g0.y), W);
-                        fma2_acc(acc[t], pk(g0.z, g0.w), mul2(W, pk(f0, f0)));
-                        fma2_acc(acc[t + 1], pk(g1.x, g1.y), W);
-                        fma2_acc(acc[t + 1], pk(g1.z, g1.w), mul2(W, pk(f1, f1)));
-                    }
-                } else {
+                for (int g = 0; g < W; g += 4) {
+                    if (g < n_act) {
 #pragma unroll
-                    for (int t = 0; t < JZ; ++t)
-                        if (mask & (1u << t)) {
-                            const float pm = fmaf((float)t, step, base);
-                            const float q = pm + kMagic;
-                            const float f = pm - (q - kMagic);
-                            const float4 g = lds128(colbase + __float_as_uint(q) * 16u);
-                            fma2_acc(acc[t], pk(g.x, g.y), W);
-                            fma2_acc(acc[t], pk(g.z, g.w), mul2(W, pk(f, f)));
+                        for (int j = 0; j < 4; j += 2) {
+                            const int i = g + j;
+                            // entries >= n_act (not yet open) read at most a few quad rows past the
+                            // column (a tail pad keeps them inside the allocation); their sums are dropped
+                            const u64 Q = add2(PM, pk(kMagic, kMagic));
+                            const u64 FW = sub2(PM, sub2(Q, pk(kMagic, kMagic)));
+                            float q0, q1, f0, f1;
+                            upk(Q, q0, q1);
+                            upk(FW, f0, f1);
+                            const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+                            const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+                            u64 T0 = fma2(pk(g0.z, g0.w), mul2(Wp, pk(f0, f0)), mul2(pk(g0.x, g0.y), Wp));
+                            u64 T1 = fma2(pk(g1.z, g1.w), mul2(Wp, pk(f1, f1)), mul2(pk(g1.x, g1.y), Wp));
+                            float a0, b0, a1, b1;
+                            upk(T0, a0, b0);
+                            upk(T1, a1, b1);
+                            if (i < n_act) acc[i] += a0 + b0;
+                            if (i + 1 < n_act) acc[i + 1] += a1 + b1;
+                            PM = add2(PM, S2);
                         }
+                    } else {
+                        PM = add2(PM, S2);
+                        PM = add2(PM, S2);
+                    }
                 }
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8u * sl);   // this warp is done with the slot
+        mbar_arrive(empty0 + 8u * sl);
         if (++sl == S) { sl = 0; phase ^= 1u; }
     }
     if (!inside) return;
-    // end views: fractional weights ω_first, ω_last and the full range test (global loads)
-    const float2 *piw = p.pi_w + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
-#pragma unroll
-    for (int t = 0; t < JZ; ++t) {
-        if (t < nzc) {
-            const int2 e = pik[t * plane];
-            if (e.x <= e.y) {
-                const float2 w = piw[t * plane];
-                tap_checked<POLY>(p, qbase, e.x, x, y, zb, t, w.x, acc[t]);
-                if (e.y != e.x) tap_checked<POLY>(p, qbase, e.y, x, y, zb, t, w.y, acc[t]);
-            }
-        }
+    if (!active_col) {                                            // outside U: the column is 0
+        for (int t = 0; t < p.nz; ++t) out[(size_t)t * plane] = 0.f;
+        return;
     }
-    float *out = p.vol + (size_t)item * p.nz * plane + (size_t)j0 * plane + (size_t)iy * p.nx + ix;
-#pragma unroll
-    for (int t = 0; t < JZ; ++t) {
-        if (t < nzc) {
-            float a, b;
-            upk(acc[t], a, b);
-            out[t * plane] = (a + b) * p.scale;
-        }
-    }
+    while (t_hi + 1 < p.nz) ++t_hi;                               // (all windows opened by K1)
+    while (t_lo <= t_hi) flush();
 }
 
 // plain gF [n][nr][nc] -> column-major sum/difference tap quads [n][nc][nr+2] (debug entry point)
@@ -563,8 +578,22 @@ void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cu
 
 size_t backproject_smem_bytes(const BPParams &p)
 {
-    const size_t slot = (((size_t)p.fp_cols * p.fp_rows + 7) & ~(size_t)7) * sizeof(float4);
-    return kBoxesBytes + (size_t)p.nbatch * slot + sizeof(int2) * (size_t)p.max_cta_views;
+    const size_t vq = ((size_t)p.fp_cols_column * (p.nr + 2) + 7) & ~(size_t)7;
+    return kBoxesBytes + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
+           16 * (size_t)p.tail_quads;
+}
+
+template <int W>
+void launch_window(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &qmap, cudaStream_t s)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bp_window<true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_window<false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    if (q.poly) k_bp_window<true, W><<<grid, kWsThreads, sm, s>>>(q, qmap);
+    else k_bp_window<false, W><<<grid, kWsThreads, sm, s>>>(q, qmap);
 }
 
 namespace {
@@ -587,16 +616,17 @@ EncodeTiledFn encode_tiled()
     return fn;
 }
 
-// the quad array as a 3-D fp32 tensor: (4 * (nr+2) floats per column, nc columns, n_views)
+// the quad array as a 3-D tensor of 8-byte elements: (2 * (nr+2) per column, nc columns, n_views);
+// box = full column height x fp_cols_column columns x 1 view
 bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
 {
     EncodeTiledFn fn = encode_tiled();
     if (!fn) return false;
-    const cuuint64_t dims[3] = {(cuuint64_t)4 * (p.nr + 2), (cuuint64_t)p.nc, (cuuint64_t)n_views};
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * (p.nr + 2), (cuuint64_t)p.nc, (cuuint64_t)n_views};
     const cuuint64_t strides[2] = {(cuuint64_t)(p.nr + 2) * 16, (cuuint64_t)p.viewbytes};
-    const cuuint32_t box[3] = {(cuuint32_t)(4 * p.fp_rows), (cuuint32_t)p.fp_cols, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * (p.nr + 2)), (cuuint32_t)p.fp_cols_column, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -606,31 +636,34 @@ void launch_backproject(const BPParams &p, cudaStream_t s)
 {
     const int nchunk = (p.nz + JZ - 1) / JZ;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk * p.n_items);
+    const int nchunk_l1 = (p.nz + JZL - 1) / JZL;
+    dim3 grid_l1((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk_l1 * p.n_items);
     const int block = TX * TY;
     BPParams q = p;
-    // deepest slot ring (<= kMaxSlots views) that lets 2 CTAs share an SM
+    // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 2 CTAs share an SM
     q.nbatch = kMaxSlots;
-    while (q.nbatch > 4 && backproject_smem_bytes(q) > 100 * 1024) q.nbatch /= 2;
+    while (q.nbatch > 2 && backproject_smem_bytes(q) > 100 * 1024) q.nbatch /= 2;
     const size_t sm = backproject_smem_bytes(q);
+    const int W = p.max_active <= 8 ? 8 : p.max_active <= 16 ? 16 : p.max_active <= 32 ? 32 : p.max_active <= 48 ? 48 : 0;
     CUtensorMap qmap;
-    const bool box_ok = p.fp_rows * 4 <= 256 && p.fp_cols <= 256;
-    if (p.staged && !p.checked && sm <= 200 * 1024 && box_ok && p.gq_views > 0 && make_quad_map(p, p.gq_views, &qmap)) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_backproject_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(k_backproject_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr = true;
+    if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * (p.nr + 2) <= 256 &&
+        p.tail_quads <= 4096 &&
+        p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_map(p, p.gq_views, &qmap)) {
+        dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
+        switch (W) {
+        case 8: launch_window<8>(q, gw, sm, qmap, s); break;
+        case 16: launch_window<16>(q, gw, sm, qmap, s); break;
+        case 32: launch_window<32>(q, gw, sm, qmap, s); break;
+        default: launch_window<48>(q, gw, sm, qmap, s); break;
         }
-        if (p.poly) k_backproject_smem<true><<<grid, kWsThreads, sm, s>>>(q, qmap);
-        else k_backproject_smem<false><<<grid, kWsThreads, sm, s>>>(q, qmap);
         return;
     }
     if (p.poly) {
-        if (p.checked) k_backproject<true, true><<<grid, block, 0, s>>>(p);
-        else k_backproject<true, false><<<grid, block, 0, s>>>(p);
+        if (p.checked) k_backproject<true, true><<<grid_l1, block, 0, s>>>(p);
+        else k_backproject<true, false><<<grid_l1, block, 0, s>>>(p);
     } else {
-        if (p.checked) k_backproject<false, true><<<grid, block, 0, s>>>(p);
-        else k_backproject<false, false><<<grid, block, 0, s>>>(p);
+        if (p.checked) k_backproject<false, true><<<grid_l1, block, 0, s>>>(p);
+        else k_backproject<false, false><<<grid_l1, block, 0, s>>>(p);
     }
 }
 

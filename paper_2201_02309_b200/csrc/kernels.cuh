@@ -51,6 +51,11 @@ struct BPParams {
     int nbatch;               // slots in the staged kernel's ring (set by the launcher)
     int64_t gq_views;         // views in the gq array (TMA tensor extent)
     int max_cta_views;        // upper bound of a CTA's interior view range (box table size)
+    int fp_cols_column;       // quad columns of a tile's full-column box (sliding-window kernel)
+    int max_active;           // max slices of a column sharing an interior view
+    bool windows_monotone;    // host check: per-column interior windows non-empty and monotone in z
+    int tail_quads;           // shared-memory pad after the ring for reads of not-yet-open window entries
+    unsigned zero;            // runtime 0 (opaque to ptxas)
     float *vol;               // [n_items][nz][ny][nx]
 };
 

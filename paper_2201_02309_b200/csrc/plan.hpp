@@ -15,7 +15,7 @@ constexpr double kPi = 3.14159265358979323846;
 
 // Backprojection work decomposition (backproject.cu): a CTA owns a TILE_X x TILE_Y
 // tile of (x, y) columns and a chunk of CHUNK_Z slices.
-constexpr int kTileX = 16, kTileY = 16, kChunkZ = 8;
+constexpr int kTileX = 16, kTileY = 16, kChunkZ = 16;
 
 // Host-side periodic tables (double precision, pitch 0).
 struct HostTables {
@@ -32,6 +32,9 @@ struct HostTables {
     double w_L = 0;                         // max |w*| over grid views inside PI windows (P:l.336)
     bool interior_in_detector = false;      // interior BP samples provably inside rows and columns (fp32 margin)
     int32_t fp_cols = 0, fp_rows = 0;       // quad box (columns x quad rows) covering any CTA's interior samples of one view
+    int32_t max_active = 0;                 // max slices of one column whose interior windows share a view
+    bool windows_monotone = false;          // per column: k_first, k_last nondecreasing in z, interior windows non-empty
+    int32_t fp_cols_column = 0;             // quad columns covering a tile's full-column samples of one view
 };
 
 // Per-view geometry for the backprojection (pitch-relative view k in [bp_lo, bp_hi]).

@@ -330,6 +330,61 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
         t.fp_cols = std::min(bw, nc);
         t.fp_rows = std::min(bh, nr + 2);
     }
+    // ---- sliding-window backprojection prerequisites (backproject.cu k_bp_window):
+    // per column, interior windows [k_first+1, k_last-1] non-empty and nondecreasing in z,
+    // and the largest number of slices whose interior windows contain a common view.
+    {
+        bool mono = true;
+        int mact = 0;
+        #pragma omp parallel for schedule(static) reduction(&&:mono) reduction(max:mact)
+        for (int iy = 0; iy < o.ny; ++iy)
+            for (int ix = 0; ix < o.nx; ++ix) {
+                const size_t c = (size_t)iy * o.nx + ix, plane = (size_t)o.nx * o.ny;
+                if (t.pi_last[c] < t.pi_first[c]) continue;            // outside U: whole column empty
+                int lo = 0;
+                for (int j = 0; j < o.nz; ++j) {
+                    const int a = t.pi_first[c + j * plane] + 1, b = t.pi_last[c + j * plane] - 1;
+                    if (a > b) mono = false;
+                    if (j > 0 && (a < t.pi_first[c + (j - 1) * plane] + 1 || b < t.pi_last[c + (j - 1) * plane] - 1))
+                        mono = false;
+                    // slices active at view a (the newest): those with b_j' >= a
+                    while (lo < j && t.pi_last[c + lo * plane] - 1 < a) ++lo;
+                    mact = std::max(mact, j - lo + 1);
+                }
+            }
+        t.windows_monotone = mono;
+        t.max_active = mact;
+        // full-column tile footprint: column span only (rows = the whole detector)
+        const int ntx = (o.nx + kTileX - 1) / kTileX, nty = (o.ny + kTileY - 1) / kTileY;
+        int bw = 0;
+        #pragma omp parallel for collapse(2) schedule(dynamic, 1) reduction(max:bw)
+        for (int ty = 0; ty < nty; ++ty)
+            for (int tx = 0; tx < ntx; ++tx) {
+                int64_t k0 = INT64_MAX, k1 = INT64_MIN;
+                for (int iy = ty * kTileY; iy < std::min(o.ny, (ty + 1) * kTileY); ++iy)
+                    for (int ix = tx * kTileX; ix < std::min(o.nx, (tx + 1) * kTileX); ++ix) {
+                        const size_t c = (size_t)iy * o.nx + ix, plane = (size_t)o.nx * o.ny;
+                        if (t.pi_last[c] < t.pi_first[c]) continue;
+                        k0 = std::min<int64_t>(k0, t.pi_first[c] + 1);
+                        k1 = std::max<int64_t>(k1, t.pi_last[c + (o.nz - 1) * plane] - 1);
+                    }
+                const double xa = ((double)tx * kTileX - 0.5 * o.nx) * o.dx, xb = xa + (kTileX - 1) * o.dx;
+                const double ya = ((double)ty * kTileY - 0.5 * o.ny) * o.dy, yb = ya + (kTileY - 1) * o.dy;
+                for (int64_t k = k0; k <= k1; ++k) {
+                    const double lam = (double)k * o.dlam;
+                    const double c = std::cos(lam + o.lam0), s = std::sin(lam + o.lam0);
+                    double cmin = 1e300, cmax = -1e300;
+                    const double cx[4] = {xa, xb, xa, xb}, cy[4] = {ya, ya, yb, yb};
+                    for (int q = 0; q < 4; ++q) {
+                        const double vs = o.R - cx[q] * c - cy[q] * s, us = -cx[q] * s + cy[q] * c;
+                        const double col = std::atan2(us, vs) / o.da + 0.5 * (nc - 1) - o.aoff;
+                        cmin = std::min(cmin, col); cmax = std::max(cmax, col);
+                    }
+                    bw = std::max(bw, (int)(std::floor(cmax) - std::floor(cmin)) + 3);
+                }
+            }
+        t.fp_cols_column = std::min(bw, nc);
+    }
     return t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }
 
