@@ -290,7 +290,7 @@ def run_ours(args):
         "gpu_launches": stats["total_launches"],
         "stage_ms_share": share,
         "precompute_s": t_pre,
-        "roofline": {"bound": "alu", "kernel": "k_backproject", "achieved": achieved_tflops, "peak": fp32_peak,
+        "roofline": {"bound": "alu", "kernel": "k_bp_window", "achieved": achieved_tflops, "peak": fp32_peak,
                      "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak,
                      "traffic": ncu_traffic(cfg["name"]),
                      "flops_per_update": bp_flops_per_update(), "k5_ms_per_launch": k5_ms,

@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
         if (NV <= 0) return;
         // ---- producer warp: lanes 0..3 stream one view's full-height column box each per round ----
         const int vbase = (int)(p.off0 + (int64_t)item * p.item_views) + KC0;
-        constexpr int G = 4;
+        const int G = min(4, S);                              // lanes in flight; divides S (powers of 2)
         if (lane < G) {
             int sl = lane;
             unsigned phase = 0;
