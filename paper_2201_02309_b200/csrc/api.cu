@@ -91,6 +91,10 @@ void free_device(katsevich_plan *p)
     p->prof.clear();
     for (void *e : p->event_pool) cudaEventDestroy((cudaEvent_t)e);
     p->event_pool.clear();
+    for (void *e : p->sync_events) cudaEventDestroy((cudaEvent_t)e);
+    p->sync_events.clear();
+    if (p->copy_stream) { cudaStreamDestroy((cudaStream_t)p->copy_stream); p->copy_stream = nullptr; }
+    if (p->copy_stream2) { cudaStreamDestroy((cudaStream_t)p->copy_stream2); p->copy_stream2 = nullptr; }
 }
 
 int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
@@ -419,15 +423,75 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
     katsevich_scan_views(p, first_pitch, n_pitches, &fv, &nv);
     if (fv < s0 || fv + nv > s0 + sn) return katsevich_reconstruct(p, host_sino, s0, sn, first_pitch, n_pitches,
                                                                    host_vol, workspace, workspace_bytes, cuda_stream);
+    // Pipelined over groups of pitches on two streams: H2D of the views the next group needs and
+    // D2H of finished volumes (copy stream) overlap filtering + backprojection (caller's stream).
     cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (!p->copy_stream) {
+        cudaStream_t a, b;
+        KCHECK(p, cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        KCHECK(p, cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        p->copy_stream = a;
+        p->copy_stream2 = b;
+    }
+    cudaStream_t cs = (cudaStream_t)p->copy_stream, ds = (cudaStream_t)p->copy_stream2;
+    const int G = 2;                                          // pitches per group (>= 2 BP waves)
+    const int ngroups = (n_pitches + G - 1) / G;
+    while ((int)p->sync_events.size() < 2 * ngroups + 1) {
+        cudaEvent_t e;
+        KCHECK(p, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->sync_events.push_back(e);
+    }
+    const HostTables &t = p->t;
+    const int vt = p->g.views_per_turn;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
-    const size_t volsz = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch * n_pitches;
+    const size_t qs = quad_view_elems(p);
+    const size_t vpitch = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
+    const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;   // first filtered view (= fv + 1)
+    const int64_t nu = n_union_views(p, n_pitches);
+    float4 *gq = (float4 *)workspace;
+    float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
     float *dsino = (float *)((char *)workspace + base);
     float *dvol = (float *)((char *)dsino + align_up(sizeof(float) * rs * (size_t)nv));
-    KCHECK(p, cudaMemcpyAsync(dsino, host_sino + (fv - s0) * rs, sizeof(float) * rs * nv, cudaMemcpyHostToDevice, s));
-    rc = katsevich_reconstruct(p, dsino, fv, nv, first_pitch, n_pitches, dvol, workspace, base, cuda_stream);
-    if (rc) return rc;
-    KCHECK(p, cudaMemcpyAsync(host_vol, dvol, sizeof(float) * volsz, cudaMemcpyDeviceToHost, s));
+    // the caller's pending work on s (e.g. earlier writes to the workspace) precedes our copies
+    cudaEvent_t e_start = (cudaEvent_t)p->sync_events[2 * ngroups];
+    KCHECK(p, cudaEventRecord(e_start, s));
+    KCHECK(p, cudaStreamWaitEvent(cs, e_start, 0));
+    // all host->device copies up front on their own stream, one event per group
+    int64_t copied_to = fv;
+    for (int gi = 0; gi < ngroups; ++gi) {
+        const int g0 = gi * G, np_g = std::min(G, n_pitches - g0);
+        const int64_t raw_end = (int64_t)(first_pitch + g0 + np_g - 1) * vt + t.bp_hi + 2;
+        KCHECK(p, cudaMemcpyAsync(dsino + (copied_to - fv) * rs, host_sino + (copied_to - s0) * rs,
+                                  sizeof(float) * rs * (size_t)(raw_end - copied_to), cudaMemcpyHostToDevice, cs));
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[2 * gi], cs));
+        copied_to = raw_end;
+    }
+    int64_t filtered_to = u0;
+    for (int gi = 0; gi < ngroups; ++gi) {
+        const int g0 = gi * G, np_g = std::min(G, n_pitches - g0);
+        const int64_t filt_end = (int64_t)(first_pitch + g0 + np_g - 1) * vt + t.bp_hi + 1;
+        cudaEvent_t e_h2d = (cudaEvent_t)p->sync_events[2 * gi], e_bp = (cudaEvent_t)p->sync_events[2 * gi + 1];
+        KCHECK(p, cudaStreamWaitEvent(s, e_h2d, 0));
+        rc = run_filter(p, dsino + (filtered_to - fv) * rs, filt_end - filtered_to, gq + (filtered_to - u0) * qs,
+                        scratch, nullptr, nullptr, nullptr, s);
+        if (rc) return rc;
+        filtered_to = filt_end;
+        BPParams b = bp_params(p);
+        b.gq = gq;
+        b.gq_views = nu;
+        b.off0 = (int64_t)(first_pitch + g0) * vt - u0;
+        b.item_views = vt;
+        b.n_items = np_g;
+        b.vol = dvol + (size_t)g0 * vpitch;
+        { LaunchScope ls(p, ST_K5, s); launch_backproject(b, s); }
+        KCHECK(p, cudaGetLastError());
+        KCHECK(p, cudaEventRecord(e_bp, s));
+        KCHECK(p, cudaStreamWaitEvent(ds, e_bp, 0));
+        KCHECK(p, cudaMemcpyAsync(host_vol + (size_t)g0 * vpitch, b.vol, sizeof(float) * vpitch * np_g,
+                                  cudaMemcpyDeviceToHost, ds));
+    }
+    KCHECK(p, cudaStreamSynchronize(ds));
+    KCHECK(p, cudaStreamSynchronize(cs));
     KCHECK(p, cudaStreamSynchronize(s));
     return KATS_OK;
 }

@@ -346,6 +346,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned addr)
 constexpr int kConsumerWarps = (TX * TY) / 32;
 constexpr int kWsThreads = TX * TY + 32;
 constexpr int kMaxSlots = 16;
+constexpr int kGroup = 8;          // window entries per conditional block (ILP vs. predicated-off waste)
 
 // column of the tile's quad box for view k (rows: the whole detector)
 template <bool POLY>
@@ -512,10 +513,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
                 const u64 S2 = pk(2.f * step, 2.f * step);
                 u64 PM = pk(base, base + step);
 #pragma unroll
-                for (int g = 0; g < W; g += 4) {
+                for (int g = 0; g < W; g += kGroup) {
                     if (g < n_act) {
 #pragma unroll
-                        for (int j = 0; j < 4; j += 2) {
+                        for (int j = 0; j < kGroup; j += 2) {
                             const int i = g + j;
                             // entries >= n_act (not yet open) read at most a few quad rows past the
                             // column (a tail pad keeps them inside the allocation); their sums are dropped
@@ -536,8 +537,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
                             PM = add2(PM, S2);
                         }
                     } else {
-                        PM = add2(PM, S2);
-                        PM = add2(PM, S2);
+#pragma unroll
+                        for (int j = 0; j < kGroup; j += 2) PM = add2(PM, S2);
                     }
                 }
             }

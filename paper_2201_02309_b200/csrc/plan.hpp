@@ -71,6 +71,10 @@ struct katsevich_plan {
     int64_t total_launches = 0;
     int64_t stage_launches[6] = {0, 0, 0, 0, 0, 0};
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+    // host entry point: copy stream + sync events (created on first use)
+    void *copy_stream = nullptr;            // host->device
+    void *copy_stream2 = nullptr;           // device->host
+    std::vector<void *> sync_events;
 };
 
 namespace kats {
