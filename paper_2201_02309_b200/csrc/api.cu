@@ -168,6 +168,13 @@ BPParams bp_params(const katsevich_plan *p)
     b.row_c15 = (float)(0.5 * (g.n_rows - 1) + 1.5);   // quad row = row + 2, minus ½ for round-to-nearest
     b.colmax = (float)(g.n_cols - 1);
     b.rowmax = (float)(g.n_rows - 1);
+    {
+        const int c = (g.n_rows + 2) / 2;                      // quad centring row (must match K4)
+        b.row_cc = b.row_c15 - (float)c;
+        b.qmagic = 12582912.0f + (float)c;
+        b.pm_lo = 1.5f - (float)c;
+        b.pm_hi = b.rowmax + 1.5f - (float)c;
+    }
     // minimax fit of atan(t) = t·Σ c_i t^(2i) on |t| <= 0.75 (max error 9.4e-9 rad), scaled by 1/Δα
     static const double c[7] = {0.99999980689595702, -0.33331974824996929, 0.19972144187876958,
                                 -0.14029432575638814, 0.098575642092481805, -0.055588999310759703,
@@ -184,8 +191,10 @@ BPParams bp_params(const katsevich_plan *p)
         const double r_near = g.R - p->t.r_fov;
         const double step_max = g.D / (r_near * g.d_w) * (g.pitch / g.nz_per_pitch);
         b.tail_quads = 8 + (int)std::ceil(3.0 * step_max) + 2;
+        b.pad_quads = 12 + (int)std::ceil(8.0 * step_max);
     }
     b.zero = 0u;
+    b.warp_span = p->t.warp_span;
     b.fp_rows = p->t.fp_rows;
     const char *ev = std::getenv("KATS_BP_KERNEL");          // "l1" forces the L1-path kernel (A/B tests)
     b.staged = !(ev && std::string(ev) == "l1");
@@ -280,10 +289,10 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
     p->precomputed = true;
     if (const char *v = std::getenv("KATS_VERBOSE"); v && *v == '1')
         std::fprintf(stderr, "[katsevich] n_psi %d, bp views [%lld, %lld], w_L %.6f, interior_in_detector %d, "
-                             "footprint box %d cols x %d quad rows, column box %d cols, max active slices %d, monotone %d\n",
+                             "footprint box %d cols x %d quad rows, column box %d cols, max active slices %d, monotone %d, warp span %d\n",
                      p->t.n_psi, (long long)p->t.bp_lo, (long long)p->t.bp_hi, p->t.w_L,
                      (int)p->t.interior_in_detector, p->t.fp_cols, p->t.fp_rows, p->t.fp_cols_column,
-                     p->t.max_active, (int)p->t.windows_monotone);
+                     p->t.max_active, (int)p->t.windows_monotone, p->t.warp_span);
     return p->t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }
 

@@ -27,6 +27,8 @@
 //    2·JZ events where a slice's interior window opens or closes.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include <cuda.h>
 
@@ -64,6 +66,13 @@ __device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm("add.rn.f32x2 %0,
 __device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 __device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
+// acc += a * b where (mask & bit) != 0, in place (one predicated FFMA2)
+__device__ __forceinline__ void fma2_if(u64 &acc, u64 a, u64 b, unsigned mask, unsigned bit)
+{
+    asm("{\n\t.reg .pred q;\n\t.reg .b32 m;\n\tand.b32 m, %3, %4;\n\tsetp.ne.b32 q, m, 0;\n\t"
+        "@q fma.rn.f32x2 %0, %1, %2, %0;\n\t}"
+        : "+l"(acc) : "l"(a), "l"(b), "r"(mask), "r"(bit));
+}
 __device__ __forceinline__ void fma2_acc(u64 &acc, u64 a, u64 b) { asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b)); }
 
 __device__ __forceinline__ float4 ldq(u64 addr) { return __ldg(reinterpret_cast<const float4 *>(addr)); }
@@ -77,7 +86,8 @@ __device__ __forceinline__ float4 lds128(unsigned saddr)
 struct ViewSetup {
     u64 colbase;         // &Q[k][l][0] - kMagicBits*16  (quad row r at colbase + (kMagicBits + r) * 16)
     u64 W;               // ((1 - frac_α)/v*, frac_α/v*)
-    float base, step;    // quad-row position (= row position + 1.5) of slice 0 of the chunk, increment
+    float base, step;    // centred quad-row position (row + 1.5 - c) of slice 0 of the chunk, increment
+    float qmagic;        // kMagic + c: (position + qmagic) has the quad row's index in its low bits
     float colpos;        // column position (checked path)
 };
 
@@ -106,7 +116,8 @@ __device__ __forceinline__ ViewSetup view_setup(const BPParams &p, u64 viewbase,
     const float w1 = fa * inv_v;
     s.W = pk(inv_v - w1, w1);
     const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
-    s.base = fmaf(sc, zb - vg.z, p.row_c15);
+    s.base = fmaf(sc, zb - vg.z, p.row_cc);
+    s.qmagic = p.qmagic;
     s.step = sc * p.dz;
     s.colbase = viewbase + (u64)l * p.colbytes - (u64)kMagicBits * 16ull;
     return s;
@@ -115,26 +126,21 @@ __device__ __forceinline__ ViewSetup view_setup(const BPParams &p, u64 viewbase,
 // accumulate two slices (quad-row positions pm0, pm1 as a pair) into acc pairs
 __device__ __forceinline__ void tap2(const ViewSetup &s, u64 PM, u64 &acc0, u64 &acc1)
 {
-    const u64 Q = add2(PM, pk(kMagic, kMagic));
-    const u64 FW = sub2(PM, sub2(Q, pk(kMagic, kMagic)));    // fraction - ½ for both slices
-    float q0, q1, f0, f1;
+    const u64 Q = add2(PM, pk(s.qmagic, s.qmagic));
+    float q0, q1, p0, p1;
     upk(Q, q0, q1);
-    upk(FW, f0, f1);
+    upk(PM, p0, p1);
     const float4 g0 = ldq(s.colbase + ((u64)__float_as_uint(q0) << 4));
     const float4 g1 = ldq(s.colbase + ((u64)__float_as_uint(q1) << 4));
-    fma2_acc(acc0, pk(g0.x, g0.y), s.W);
-    fma2_acc(acc0, pk(g0.z, g0.w), mul2(s.W, pk(f0, f0)));
-    fma2_acc(acc1, pk(g1.x, g1.y), s.W);
-    fma2_acc(acc1, pk(g1.z, g1.w), mul2(s.W, pk(f1, f1)));
+    fma2_acc(acc0, s.W, fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)));
+    fma2_acc(acc1, s.W, fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)));
 }
 
 __device__ __forceinline__ void tap1(const ViewSetup &s, float pm, u64 &acc)
 {
-    const float q = pm + kMagic;
-    const float f = pm - (q - kMagic);
+    const float q = pm + s.qmagic;
     const float4 g = ldq(s.colbase + ((u64)__float_as_uint(q) << 4));
-    fma2_acc(acc, pk(g.x, g.y), s.W);
-    fma2_acc(acc, pk(g.z, g.w), mul2(s.W, pk(f, f)));
+    fma2_acc(acc, s.W, fma2(pk(g.z, g.w), pk(pm, pm), pk(g.x, g.y)));
 }
 
 // checked end-view sample with weight ω (reading A9: zero outside the closed node range)
@@ -146,7 +152,7 @@ __device__ __forceinline__ void tap_checked(const BPParams &p, u64 qbase, int k,
     ViewSetup s = view_setup<POLY>(p, qbase + (u64)((int64_t)k * p.viewbytes), vg, x, y, zb);
     if (!(s.colpos >= 0.f && s.colpos <= p.colmax)) return;
     const float pm = fmaf((float)t, s.step, s.base);
-    if (!(pm >= 1.5f && pm <= p.rowmax + 1.5f)) return;
+    if (!(pm >= p.pm_lo && pm <= p.pm_hi)) return;
     s.W = mul2(s.W, pk(weight, weight));
     tap1(s, pm, acc);
 }
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(TX *TY, 3) k_backproject(BPParams p)
 #pragma unroll
             for (int t = 0; t < JZL; ++t) {
                 const float pm = fmaf((float)t, s.step, s.base);
-                if ((mask & (1u << t)) && pm >= 1.5f && pm <= p.rowmax + 1.5f) tap1(s, pm, acc[t]);
+                if ((mask & (1u << t)) && pm >= p.pm_lo && pm <= p.pm_hi) tap1(s, pm, acc[t]);
             }
         } else if (mask == (1u << JZL) - 1) {
             const u64 B = pk(s.base, s.base), S = pk(s.step, s.step);
@@ -502,11 +508,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
                 const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
                 const int l = __float2int_rz(cp);
                 const float fa = cp - __int2float_rn(l);
-                const float w1 = fa * inv_v;
-                const u64 Wp = pk(inv_v - w1, w1);
+                const float w1 = fa * inv_v, w0 = inv_v - w1;
                 const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
                 const float step = sc * p.dz;
-                const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_c15));   // entry 0 = slice t_lo
+                const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));    // entry 0 = slice t_lo
                 const int ci = min(max(l - boxc[n], 0), BW - 1);
                 // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
                 const unsigned colbase = (stage_sa + (unsigned)(sl * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
@@ -520,20 +525,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
                             const int i = g + j;
                             // entries >= n_act (not yet open) read at most a few quad rows past the
                             // column (a tail pad keeps them inside the allocation); their sums are dropped
-                            const u64 Q = add2(PM, pk(kMagic, kMagic));
-                            const u64 FW = sub2(PM, sub2(Q, pk(kMagic, kMagic)));
-                            float q0, q1, f0, f1;
+                            const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
+                            float q0, q1, p0, p1;
                             upk(Q, q0, q1);
-                            upk(FW, f0, f1);
+                            upk(PM, p0, p1);
                             const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
                             const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                            u64 T0 = fma2(pk(g0.z, g0.w), mul2(Wp, pk(f0, f0)), mul2(pk(g0.x, g0.y), Wp));
-                            u64 T1 = fma2(pk(g1.z, g1.w), mul2(Wp, pk(f1, f1)), mul2(pk(g1.x, g1.y), Wp));
+                            // the two columns' row samples s' + p d, then their α weights
                             float a0, b0, a1, b1;
-                            upk(T0, a0, b0);
-                            upk(T1, a1, b1);
-                            if (i < n_act) acc[i] += a0 + b0;
-                            if (i + 1 < n_act) acc[i + 1] += a1 + b1;
+                            upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), a0, b0);
+                            upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), a1, b1);
+                            if (i < n_act) acc[i] = fmaf(a0, w0, fmaf(b0, w1, acc[i]));
+                            if (i + 1 < n_act) acc[i + 1] = fmaf(a1, w0, fmaf(b1, w1, acc[i + 1]));
                             PM = add2(PM, S2);
                         }
                     } else {
@@ -555,6 +558,318 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
     while (t_lo <= t_hi) flush();
 }
 
+// ---------------------------------------------------------------------------
+// TMEM-window kernel (opt-in: KATS_BP_KERNEL=tmem): the sliding window of
+// per-slice accumulators lives in tensor memory instead of registers.  Each
+// lane owns one TMEM lane (row); slice t of the column accumulates in TMEM
+// column t mod Wc of the warp's column range, so the window is a true circular
+// buffer (no register shifts, no static unrolling over the window).  A warp
+// walks the union of its lanes' open slices in groups of 8 columns
+// (tcgen05.ld.32x32b.x8 -> FFMA work -> tcgen05.st.x8); a slice is flushed
+// (end views, write, column zeroed) warp-uniformly once every lane has closed
+// it.  Each slice keeps its two detector columns' partial sums (a TMEM column
+// pair), so an update is two FFMA2.  Measured on C4 it is ~15% slower than the
+// register window (per-group TMEM ld/st + mask overhead); kept for A/B.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tm_ld8(unsigned ta, float (&v)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st8(unsigned ta, const float (&v)[8])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(ta), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld16(unsigned ta, u64 (&v)[8])
+{
+    float a[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]), "=f"(a[4]), "=f"(a[5]), "=f"(a[6]), "=f"(a[7]),
+                   "=f"(a[8]), "=f"(a[9]), "=f"(a[10]), "=f"(a[11]), "=f"(a[12]), "=f"(a[13]), "=f"(a[14]), "=f"(a[15])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = pk(a[2 * j], a[2 * j + 1]);
+}
+__device__ __forceinline__ void tm_st16(unsigned ta, const u64 (&v)[8])
+{
+    float a[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) upk(v[j], a[2 * j], a[2 * j + 1]);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(ta), "f"(a[0]), "f"(a[1]), "f"(a[2]), "f"(a[3]), "f"(a[4]), "f"(a[5]), "f"(a[6]), "f"(a[7]),
+                   "f"(a[8]), "f"(a[9]), "f"(a[10]), "f"(a[11]), "f"(a[12]), "f"(a[13]), "f"(a[14]), "f"(a[15])
+                 : "memory");
+}
+__device__ __forceinline__ float tm_ld2sum(unsigned ta)
+{
+    float a, b;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=f"(a), "=f"(b) : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return a + b;
+}
+__device__ __forceinline__ void tm_st2zero(unsigned ta)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%1};" ::"r"(ta), "f"(0.f) : "memory");
+}
+__device__ __forceinline__ float tm_ld1(unsigned ta)
+{
+    float v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=f"(v) : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return v;
+}
+__device__ __forceinline__ void tm_st1(unsigned ta, float v)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta), "f"(v) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__host__ __device__ inline size_t tmem_head_bytes(const BPParams &p)
+{
+    return (16 * (size_t)p.pad_quads + 127) & ~(size_t)127;
+}
+
+size_t tmem_smem_bytes(const BPParams &p)
+{
+    const int vq = (p.fp_cols_column * (p.nr + 2) + 7) & ~7;
+    return tmem_head_bytes(p) + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
+           16 * (size_t)p.pad_quads;
+}
+
+template <bool POLY>
+__global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __grid_constant__ CUtensorMap qmap)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch, Wc = p.tmem_cols;
+    const int vq = (BW * NQ + 7) & ~7;
+    const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
+    const size_t head = tmem_head_bytes(p);                   // pad for reads below the first column
+    float4 *stage = reinterpret_cast<float4 *>(smem + head);
+    int *boxc = reinterpret_cast<int *>(smem + head + (size_t)S * vq * 16);
+    __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
+    __shared__ int s_k0, s_k1;
+    __shared__ unsigned s_tmem;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = warp == kConsumerWarps;
+    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
+    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int item = blockIdx.z;
+    const bool inside = !producer && ix < p.nx && iy < p.ny;
+    const size_t plane = (size_t)p.nx * p.ny;
+    const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const int2 *pik = p.pi_k + col;
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
+    const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
+
+    if (warp == 0) {    // TMEM for the CTA: 2 x Wc columns (warps w and w+4 share a lane quarter)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"((unsigned)p.tmem_alloc));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        s_k0 = INT_MAX; s_k1 = INT_MIN;
+        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, TX * TY); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int K0 = INT_MAX, K1 = INT_MIN;
+    if (inside) {
+        const int2 e0 = pik[0];
+        if (e0.x <= e0.y) { K0 = e0.x + 1; K1 = pik[(size_t)(p.nz - 1) * plane].y - 1; }
+    }
+    int wk0 = K0, wk1 = K1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wk0 = min(wk0, __shfl_xor_sync(0xffffffffu, wk0, o));
+        wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
+    }
+    if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
+    __syncthreads();
+    const int KC0 = s_k0, KC1 = s_k1;
+    const int NV = KC1 - KC0 + 1;
+    const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
+    {
+        const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
+        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col<POLY>(p, KC0 + n, xa, ya);
+    }
+    __syncthreads();
+
+    if (producer) {
+        if (NV <= 0) return;
+        const int vbase = (int)(p.off0 + (int64_t)item * p.item_views) + KC0;
+        if (lane == 0) {
+            int sl = 0;
+            unsigned phase = 0;
+            for (int n = 0; n < NV; ++n) {
+                if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
+                const unsigned full = full0 + 8u * sl;
+                mbar_expect_tx(full, box_bytes);
+                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 0, boxc[n], vbase + n, full);
+                if (++sl == S) { sl = 0; phase ^= 1u; }
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps ----
+    // slice t -> TMEM column pair 2 (t mod Wc), 2 (t mod Wc) + 1: the two detector columns' partial sums
+    const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * 2 * Wc);
+    {
+        float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < 2 * Wc; c += 8) tm_st8(tw + c, z);
+        tm_wait_st();
+    }
+    const float2 *piw = p.pi_w + col;
+    float *out = p.vol + (size_t)item * p.nz * plane + col;
+    const bool active_col = inside && K0 <= K1;
+    int t_lo = 0, t_hi = -1, t_f = 0;                 // lane window [t_lo, t_hi]; warp flush point t_f
+    int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
+
+    // warp-uniform: slice t is closed in every lane -> finish and write it, zero its columns
+    auto flush_slice = [&](int t) {
+        const unsigned tc = tw + 2u * (unsigned)(t % Wc);
+        const float a = tm_ld2sum(tc);
+        if (active_col && t < p.nz) {
+            const int2 e = pik[(size_t)t * plane];
+            const float2 w = piw[(size_t)t * plane];
+            u64 ends = 0ull;
+            tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t, w.x, ends);
+            tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t, w.y, ends);
+            float ea, eb;
+            upk(ends, ea, eb);
+            out[(size_t)t * plane] = (a + ea + eb) * p.scale;
+        }
+        tm_st2zero(tc);
+    };
+
+    int sl = 0;
+    unsigned phase = 0;
+    for (int n = 0; n < NV; ++n) {
+        const int k = KC0 + n;
+        mbar_wait(full0 + 8u * sl, phase);
+        if (active_col) {
+            while (k >= next_open) {
+                ++t_hi;
+                if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+                next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
+            }
+            while (k >= next_close) {                                // closes at k_last (end view)
+                ++t_lo;
+                next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
+            }
+        }
+        const int lo_all = __reduce_min_sync(0xffffffffu, active_col ? t_lo : INT_MAX);
+        while (t_f < lo_all && t_f < p.nz) flush_slice(t_f++);
+        const bool work = active_col && t_hi >= t_lo && k <= K1;
+        const int lo_w = __reduce_min_sync(0xffffffffu, work ? t_lo : INT_MAX);
+        const int hi_w = __reduce_max_sync(0xffffffffu, work ? t_hi : -1);
+        if (hi_w >= lo_w) {
+            u64 Wp = 0ull;
+            float base = 0.f, step = 0.f;
+            unsigned colbase = (stage_sa + (unsigned)(sl * vq) * 16u - kMagicBits * 16u) ^ p.zero;
+            if (work) {
+                const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+                const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+                const float u = fmaf(y, vg.x, -x * vg.y);
+                const float inv_v = rcp_approx(vstar);
+                float colpos;
+                if (POLY) {
+                    const float tt = u * inv_v, q = tt * tt;
+                    float a = p.at[6];
+                    a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+                    a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+                    colpos = fmaf(tt, a, p.col_c);
+                } else {
+                    colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+                }
+                const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
+                const int l = __float2int_rz(cp);
+                const float fa = cp - __int2float_rn(l);
+                const float w1 = fa * inv_v;
+                Wp = pk(inv_v - w1, w1);
+                const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+                step = sc * p.dz;
+                base = fmaf(sc, -vg.z, p.row_cc);                   // slice 0 (centred quad-row position)
+                const int ci = min(max(l - boxc[n], 0), BW - 1);
+                colbase = (stage_sa + (unsigned)(sl * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
+            }
+            const u64 S2 = pk(2.f * step, 2.f * step);
+            const int m0 = lo_w & ~7;
+            unsigned cc = 2u * (unsigned)(m0 % Wc);                  // column of the group's first slice
+            for (int tb = m0; tb <= hi_w; tb += 8) {                 // warp-uniform groups of 8 slices
+                u64 acc[8];
+                tm_ld16(tw + cc, acc);
+                // a group that misses this lane's window is evaluated next to it instead (its sums are
+                // dropped), so every read stays within 7 slices of an open slice: head/tail pads cover that
+                const int tg = work ? min(max(tb, t_lo - 7), t_hi) : tb;
+                const int jl = min(max(t_lo - tb, 0), 8), jh = min(max(t_hi - tb + 1, 0), 8);
+                const unsigned mask = work ? ((0xffu << jl) & ((1u << jh) - 1u)) : 0u;
+                const float t0 = (float)tg;
+                u64 PM = pk(fmaf(t0, step, base), fmaf(t0 + 1.f, step, base));
+                if (__all_sync(0xffffffffu, mask == 0xffu || !work)) {
+                    // every working lane has all 8 slices open; idle lanes add exactly 0 (Wp = 0, finite reads)
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
+                        float q0, q1, f0, f1;
+                        upk(Q, q0, q1);
+                        upk(PM, f0, f1);
+                        const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+                        const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+                        acc[j] = fma2(Wp, fma2(pk(g0.z, g0.w), pk(f0, f0), pk(g0.x, g0.y)), acc[j]);
+                        acc[j + 1] = fma2(Wp, fma2(pk(g1.z, g1.w), pk(f1, f1), pk(g1.x, g1.y)), acc[j + 1]);
+                        PM = add2(PM, S2);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
+                        float q0, q1, f0, f1;
+                        upk(Q, q0, q1);
+                        upk(PM, f0, f1);
+                        const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+                        const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+                        // value = sum over the two columns c of W_c (s_c + f d_c): kept as a column pair
+                        const u64 I0 = fma2(pk(g0.z, g0.w), pk(f0, f0), pk(g0.x, g0.y));
+                        const u64 I1 = fma2(pk(g1.z, g1.w), pk(f1, f1), pk(g1.x, g1.y));
+                        fma2_if(acc[j], Wp, I0, mask, 1u << j);
+                        fma2_if(acc[j + 1], Wp, I1, mask, 2u << j);
+                        PM = add2(PM, S2);
+                    }
+                }
+                tm_st16(tw + cc, acc);
+                cc += 16u;
+                if (cc == 2u * (unsigned)Wc) cc = 0u;
+            }
+            tm_wait_st();
+        }
+        mbar_arrive(empty0 + 8u * sl);
+        if (++sl == S) { sl = 0; phase ^= 1u; }
+    }
+    // every window has closed by K1 + 1: flush the rest
+    const int hi_all = __reduce_max_sync(0xffffffffu, active_col ? p.nz - 1 : -1);
+    while (t_f <= hi_all) flush_slice(t_f++);
+    tm_wait_st();
+    if (inside && !active_col)
+        for (int t = 0; t < p.nz; ++t) out[(size_t)t * plane] = 0.f;
+    // release TMEM once every consumer warp is done with it
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(TX * TY));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"((unsigned)p.tmem_alloc));
+}
+
 // plain gF [n][nr][nc] -> column-major sum/difference tap quads [n][nc][nr+2] (debug entry point)
 __global__ void k_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc)
 {
@@ -568,7 +883,8 @@ __global__ void k_make_quads(const float *gF, float4 *q, int64_t n, int nr, int 
     auto at = [&](int mm, int ll) { return (mm >= 0 && mm < nr && ll < nc) ? g[(int64_t)mm * nc + ll] : 0.f; };
     const int m = r - 2;
     const float a0 = at(m, l), c0 = at(m + 1, l), a1 = at(m, l + 1), c1 = at(m + 1, l + 1);
-    q[i] = make_float4(0.5f * (a0 + c0), 0.5f * (a1 + c1), c0 - a0, c1 - a1);
+    const float rc = (float)(r - (nr + 2) / 2);          // centred quad row (as K4)
+    q[i] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0, c1 - a1);
 }
 
 void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cudaStream_t s)
@@ -582,6 +898,17 @@ size_t backproject_smem_bytes(const BPParams &p)
     const size_t vq = ((size_t)p.fp_cols_column * (p.nr + 2) + 7) & ~(size_t)7;
     return kBoxesBytes + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
            16 * (size_t)p.tail_quads;
+}
+
+template <bool POLY>
+void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &qmap, cudaStream_t s)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bp_tmem<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    k_bp_tmem<POLY><<<grid, kWsThreads, sm, s>>>(q, qmap);
 }
 
 template <int W>
@@ -640,6 +967,28 @@ void launch_backproject(const BPParams &p, cudaStream_t s)
     const int nchunk_l1 = (p.nz + JZL - 1) / JZL;
     dim3 grid_l1((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk_l1 * p.n_items);
     const int block = TX * TY;
+    const char *kv = std::getenv("KATS_BP_KERNEL");
+    const bool want_tmem = kv && std::string(kv) == "tmem";
+    // TMEM-window kernel (opt-in, A/B): accumulators in tensor memory
+    if (want_tmem && p.staged && !p.checked && p.windows_monotone && p.warp_span > 0 && 2 * (p.nr + 2) <= 256 &&
+        p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
+        BPParams q = p;
+        q.tmem_cols = ((p.warp_span + 7) & ~7) + 16;             // circular window + 2 alias-free groups
+        int alloc = 32;
+        while (alloc < 2 * 2 * q.tmem_cols) alloc *= 2;           // 2 columns per slice, 2 warps per lane quarter
+        q.tmem_alloc = alloc;
+        // deepest ring (<= kMaxSlots views) such that 2 CTAs fit in shared memory and TMEM (2 x alloc <= 512)
+        q.nbatch = kMaxSlots;
+        while (q.nbatch > 2 && tmem_smem_bytes(q) > 100 * 1024) --q.nbatch;
+        const size_t sm = tmem_smem_bytes(q);
+        CUtensorMap qmap;
+        if (alloc <= 256 && sm <= 200 * 1024 && make_quad_map(p, p.gq_views, &qmap)) {
+            dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
+            if (p.poly) launch_tmem_kernel<true>(q, gw, sm, qmap, s);
+            else launch_tmem_kernel<false>(q, gw, sm, qmap, s);
+            return;
+        }
+    }
     BPParams q = p;
     // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 2 CTAs share an SM
     q.nbatch = kMaxSlots;

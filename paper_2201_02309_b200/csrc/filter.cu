@@ -117,12 +117,13 @@ __global__ void __launch_bounds__(256) k_hilbert(FilterParams p, int64_t n_lines
 //
 // Output for the backprojection: per view, column-major 2x2 tap quads in
 // sum/difference form
-//   Q[v][l][r] = (½(g[m][l] + g[m+1][l]), ½(g[m][l+1] + g[m+1][l+1]),
-//                 g[m+1][l] - g[m][l],     g[m+1][l+1] - g[m][l+1]),   m = r - 2,
+//   Q[v][l][r] = (s_0 - ρ d_0, s_1 - ρ d_1, d_0, d_1),   ρ = r - c,  c = (nr + 2) / 2,
+//   s_j = ½(g[m][l+j] + g[m+1][l+j]),  d_j = g[m+1][l+j] - g[m][l+j],  m = r - 2,
 // r = 0 .. nr+1 (two zero rows below the detector; taps beyond the last row or
-// column are 0).  A bilinear sample at (l + fa, m + f) is then
-//   Q.x w0 + Q.y w1 + (f - ½)(Q.z w0 + Q.w w1),   w0 = 1 - fa, w1 = fa,
-// i.e. one 128-bit load and two paired FMAs (FFMA2) in the BP.
+// column are 0).  With the centred quad-row position P = (m + f) + 1.5 - c of a
+// sample at (l + fa, m + f) and r = round(P + c), the bilinear sample is
+//   w0 (Q.x + P Q.z) + w1 (Q.y + P Q.w),   w0 = 1 - fa, w1 = fa,
+// i.e. one 128-bit load and two paired FMAs (FFMA2) in the BP, no fraction.
 // Optionally also the plain gF (debug / parity entry point).
 // One CTA per (view, 32-column block): the block's (nr + 3) x 33 gF values are
 // formed in shared memory, then written as contiguous quad columns.
@@ -157,7 +158,8 @@ __global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
         const int ll = e / nq, r = e - ll * nq;        // r = quad row; taps rows r-2, r-1
         const float *t0 = tile + r * ld + ll;
         const float a0 = t0[0], a1 = t0[1], c0 = t0[ld], c1 = t0[ld + 1];
-        q[e] = make_float4(0.5f * (a0 + c0), 0.5f * (a1 + c1), c0 - a0, c1 - a1);
+        const float rc = (float)(r - (nr + 2) / 2);      // centred quad row
+        q[e] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0, c1 - a1);
     }
 }
 

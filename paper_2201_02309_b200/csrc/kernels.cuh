@@ -41,6 +41,8 @@ struct BPParams {
     const ViewGeom *view;     // [k - view_lo]
     int view_lo;
     float R, D_over_dw, inv_dalpha, col_c, row_c15, colmax, rowmax;
+    float row_cc, qmagic;     // centred quad-row origin row_c15 - c and kMagic + c, c = (nr + 2) / 2
+    float pm_lo, pm_hi;       // centred quad-row range of an in-detector sample (checked taps)
     float at[7];              // α*/Δα polynomial in t = u/v*: t·Σ at[i] t^(2i)
     float x0, dx, y0, dy, dz;
     float scale;              // Δλ / 2π
@@ -56,6 +58,9 @@ struct BPParams {
     bool windows_monotone;    // host check: per-column interior windows non-empty and monotone in z
     int tail_quads;           // shared-memory pad after the ring for reads of not-yet-open window entries
     unsigned zero;            // runtime 0 (opaque to ptxas)
+    int warp_span;            // max live slices of a warp (host, TMEM-window kernel)
+    int pad_quads;            // head/tail pad (quads) for the TMEM-window kernel: 7 slices of row travel
+    int tmem_cols, tmem_alloc;// TMEM columns per warp / allocated per CTA (set by the launcher)
     float *vol;               // [n_items][nz][ny][nx]
 };
 

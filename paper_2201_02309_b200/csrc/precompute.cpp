@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <vector>
 
 #include "plan.hpp"
 
@@ -384,6 +385,45 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
                 }
             }
         t.fp_cols_column = std::min(bw, nc);
+
+        // TMEM-window kernel: per warp (8x4 columns), the span of slices between the oldest slice
+        // not closed by every lane (warp-uniform flush point) and the newest slice open in any lane
+        int span = 0;
+        if (t.windows_monotone) {
+            const int nwx = (o.nx + 7) / 8, nwy = (o.ny + 3) / 4;
+            #pragma omp parallel for collapse(2) schedule(dynamic, 4) reduction(max:span)
+            for (int wy = 0; wy < nwy; ++wy)
+                for (int wx = 0; wx < nwx; ++wx) {
+                    std::vector<size_t> cols;
+                    for (int ly = 0; ly < 4; ++ly)
+                        for (int lx = 0; lx < 8; ++lx) {
+                            const int ix = wx * 8 + lx, iy = wy * 4 + ly;
+                            if (ix >= o.nx || iy >= o.ny) continue;
+                            const size_t c = (size_t)iy * o.nx + ix;
+                            if (t.pi_last[c] >= t.pi_first[c]) cols.push_back(c);
+                        }
+                    if (cols.empty()) continue;
+                    const size_t plane = (size_t)o.nx * o.ny;
+                    int64_t kmin = INT64_MAX, kmax = INT64_MIN;
+                    for (size_t c : cols) {
+                        kmin = std::min<int64_t>(kmin, t.pi_first[c] + 1);
+                        kmax = std::max<int64_t>(kmax, t.pi_last[c + (o.nz - 1) * plane]);
+                    }
+                    std::vector<int> lo(cols.size(), 0), hi(cols.size(), -1);
+                    for (int64_t k = kmin; k <= kmax; ++k) {
+                        int tf = INT32_MAX, th = -1;
+                        for (size_t q = 0; q < cols.size(); ++q) {
+                            const size_t c = cols[q];
+                            while (hi[q] + 1 < o.nz && t.pi_first[c + (hi[q] + 1) * plane] + 1 <= k) ++hi[q];
+                            while (lo[q] <= hi[q] && t.pi_last[c + lo[q] * plane] <= k) ++lo[q];   // closes at k_last
+                            tf = std::min(tf, lo[q]);
+                            th = std::max(th, hi[q]);
+                        }
+                        if (th >= tf) span = std::max(span, th - tf + 1);
+                    }
+                }
+        }
+        t.warp_span = span;
     }
     return t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }

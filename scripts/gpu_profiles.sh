@@ -11,6 +11,6 @@ timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches_$R.log 2>&1
 # full capture: the BP launch of the first timed step (3 warm-up steps -> skip 3 launches)
-ncu --set full --clock-control none --import-source on -k regex:"k_bp_window|k_backproject" -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"k_bp_tmem|k_bp_window|k_backproject" -s 3 -c 1 \
     -o gpurun_out/k5_full_$R -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$R.log 2>&1
 echo done
