@@ -124,6 +124,17 @@ def bp_flops_per_update():
     return 13.0
 
 
+def bp_smem_bytes_per_update():
+    # algorithmic on-chip gather of one update: the bilinear sample of gF at (α*, w*) reads
+    # 4 fp32 neighbours = 16 B (held as one (s', s', d, d) quad)
+    return 16.0
+
+
+def smem_peak_gbs(sm_mhz):
+    # shared-memory data pipe: 128 B/clk per SM (1 LSU wavefront/clk), 148 SMs
+    return 148 * 128 * sm_mhz * 1e6 / 1e9
+
+
 def ncu_traffic(config_name):
     """dram bytes per K5 launch from the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "ncu_k5_traffic.json")
@@ -265,6 +276,9 @@ def run_ours(args):
     achieved_tflops = k5_updates * bp_flops_per_update() / (k5_ms * 1e-3) / 1e12
     peaks, src = _peaks()
     fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    smem_peak = smem_peak_gbs(peaks.get("sm_max_mhz", 1965.0))
+    achieved_smem = k5_updates * bp_smem_bytes_per_update() / (k5_ms * 1e-3) / 1e9
+    bp_kernel = plan.bp_kernel()
     share = {s: stats["ms"][s] / max(1e-9, sum(stats["ms"].values())) for s in stats["ms"] if stats["ms"][s] > 0}
     line = {
         "metric": "voxel-view updates/s",
@@ -290,12 +304,16 @@ def run_ours(args):
         "gpu_launches": stats["total_launches"],
         "stage_ms_share": share,
         "precompute_s": t_pre,
-        "roofline": {"bound": "alu", "kernel": "k_bp_window", "achieved": achieved_tflops, "peak": fp32_peak,
-                     "unit": "TFLOP/s", "frac": achieved_tflops / fp32_peak,
+        "roofline": {"bound": "smem", "kernel": bp_kernel, "achieved": achieved_smem, "peak": smem_peak,
+                     "unit": "GB/s", "frac": achieved_smem / smem_peak,
                      "traffic": ncu_traffic(cfg["name"]),
-                     "flops_per_update": bp_flops_per_update(), "k5_ms_per_launch": k5_ms,
+                     "bytes_per_update": bp_smem_bytes_per_update(), "k5_ms_per_launch": k5_ms,
                      "k5_updates_per_s": k5_updates / (k5_ms * 1e-3),
-                     "peak_source": f"148 SMs x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0)} MHz ({src} sm_max)"},
+                     "peak_source": f"148 SMs x 128 B/clk shared-memory pipe x {peaks.get('sm_max_mhz', 1965.0)} MHz "
+                                    f"({src} sm_max); DESIGN.md §5",
+                     "secondary_alu": {"achieved": achieved_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+                                       "frac": achieved_tflops / fp32_peak,
+                                       "flops_per_update": bp_flops_per_update()}},
         "clocks": clk,
     }
     if e2e:

@@ -176,6 +176,18 @@ typedef struct {
 int katsevich_profile_enable(katsevich_plan *plan, int enable);   /* 1: record events around each launch */
 int katsevich_profile_read(katsevich_plan *plan, katsevich_stats *out, int reset); /* synchronises recorded events */
 
+/* ---- which backprojection kernel ran ---- */
+
+/* Variant of the most recent step-7 (K5) launch of this plan: 0 none yet,
+ * KATS_BP_L1 (chunked kernel, global-memory reads; used for plans whose
+ * footprints leave the detector), KATS_BP_WINDOW (register sliding window),
+ * KATS_BP_TMEM (tensor-memory sliding window, the default).  The environment
+ * variable KATS_BP_KERNEL=window|l1 forces a variant for A/B tests. */
+#define KATS_BP_L1 1
+#define KATS_BP_WINDOW 2
+#define KATS_BP_TMEM 3
+int katsevich_bp_kernel(const katsevich_plan *plan);
+
 void katsevich_destroy(katsevich_plan *plan);
 const char *katsevich_error_string(int code);
 const char *katsevich_last_error_detail(const katsevich_plan *plan);

@@ -61,6 +61,7 @@ SIGNATURES = {
     "katsevich_export_tables": (ctypes.c_int, [_P, _PI32, _PI32, _PD, _PD, _PI32, _PD, _PI32, _PD]),
     "katsevich_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
     "katsevich_profile_read": (ctypes.c_int, [_P, ctypes.POINTER(KatsevichStats), ctypes.c_int]),
+    "katsevich_bp_kernel": (ctypes.c_int, [_P]),
     "katsevich_destroy": (None, [_P]),
     "katsevich_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "katsevich_last_error_detail": (ctypes.c_char_p, [_P]),

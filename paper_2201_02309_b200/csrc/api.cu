@@ -191,7 +191,7 @@ BPParams bp_params(const katsevich_plan *p)
         const double r_near = g.R - p->t.r_fov;
         const double step_max = g.D / (r_near * g.d_w) * (g.pitch / g.nz_per_pitch);
         b.tail_quads = 8 + (int)std::ceil(3.0 * step_max) + 2;
-        b.pad_quads = 12 + (int)std::ceil(8.0 * step_max);
+        b.pad_quads = 12 + (int)std::ceil((p->t.warp_span + 8) * step_max);   // TMEM kernel: warp-union groups
     }
     b.zero = 0u;
     b.warp_span = p->t.warp_span;
@@ -377,7 +377,7 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     b.item_views = vt;
     b.n_items = n_pitches;
     b.vol = vol;
-    { LaunchScope ls(p, ST_K5, s); launch_backproject(b, s); }
+    { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
     KCHECK(p, cudaGetLastError());
     return KATS_OK;
 }
@@ -411,7 +411,7 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     bp.item_views = nbp;
     bp.n_items = B;
     bp.vol = vols;
-    { LaunchScope ls(p, ST_K5, s); launch_backproject(bp, s); }
+    { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(bp, s); }
     KCHECK(p, cudaGetLastError());
     return KATS_OK;
 }
@@ -492,7 +492,7 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
         b.item_views = vt;
         b.n_items = np_g;
         b.vol = dvol + (size_t)g0 * vpitch;
-        { LaunchScope ls(p, ST_K5, s); launch_backproject(b, s); }
+        { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
         KCHECK(p, cudaGetLastError());
         KCHECK(p, cudaEventRecord(e_bp, s));
         KCHECK(p, cudaStreamWaitEvent(ds, e_bp, 0));
@@ -550,7 +550,7 @@ int katsevich_backproject(katsevich_plan *p, const float *gF, int64_t gF0, int64
     bp.item_views = 0;
     bp.n_items = 1;
     bp.vol = vol;
-    { LaunchScope ls(p, ST_K5, s); launch_backproject(bp, s); }
+    { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(bp, s); }
     KCHECK(p, cudaGetLastError());
     cudaFreeAsync(gq, s);
     return KATS_OK;
@@ -579,6 +579,12 @@ int katsevich_export_tables(const katsevich_plan *p, int32_t *pi_first, int32_t 
     cp(pi_first, t.pi_first); cp(pi_last, t.pi_last); cp(w_first, t.w_first); cp(w_last, t.w_last);
     cp(fr_idx, t.fr_idx); cp(fr_frac, t.fr_frac); cp(br_idx, t.br_idx); cp(br_frac, t.br_frac);
     return KATS_OK;
+}
+
+int katsevich_bp_kernel(const katsevich_plan *plan)
+{
+    if (!plan) return KATS_ERR_NULL;
+    return plan->last_bp_kernel;
 }
 
 int katsevich_profile_enable(katsevich_plan *p, int enable)

@@ -477,11 +477,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
         next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;   // b + 1 = k_last
     };
 
-    int sl = 0;
-    unsigned phase = 0;
+    const int lgS = __ffs(S) - 1;                                   // ring size is a power of two
     for (int n = 0; n < NV; ++n) {
         const int k = KC0 + n;
-        mbar_wait(full0 + 8u * sl, phase);
+        const int sl = n & (S - 1);                                 // slot and parity from n: no live state
+        mbar_wait(full0 + 8u * sl, (unsigned)(n >> lgS) & 1u);
         if (active_col) {
             while (k >= next_open) {                              // slice t_hi+1's interior window opens
                 ++t_hi;
@@ -547,7 +547,6 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
             }
         }
         mbar_arrive(empty0 + 8u * sl);
-        if (++sl == S) { sl = 0; phase ^= 1u; }
     }
     if (!inside) return;
     if (!active_col) {                                            // outside U: the column is 0
@@ -559,7 +558,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
 }
 
 // ---------------------------------------------------------------------------
-// TMEM-window kernel (opt-in: KATS_BP_KERNEL=tmem): the sliding window of
+// TMEM-window kernel (default; KATS_BP_KERNEL=window selects the register window): the sliding window of
 // per-slice accumulators lives in tensor memory instead of registers.  Each
 // lane owns one TMEM lane (row); slice t of the column accumulates in TMEM
 // column t mod Wc of the warp's column range, so the window is a true circular
@@ -567,9 +566,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const _
 // walks the union of its lanes' open slices in groups of 8 columns
 // (tcgen05.ld.32x32b.x8 -> FFMA work -> tcgen05.st.x8); a slice is flushed
 // (end views, write, column zeroed) warp-uniformly once every lane has closed
-// it.  Each slice keeps its two detector columns' partial sums (a TMEM column
-// pair), so an update is two FFMA2.  Measured on C4 it is ~15% slower than the
-// register window (per-group TMEM ld/st + mask overhead); kept for A/B.
+// it.  Without the ~48 accumulator registers three CTAs share an SM.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void tm_ld8(unsigned ta, float (&v)[8])
 {
@@ -577,6 +574,19 @@ __device__ __forceinline__ void tm_ld8(unsigned ta, float (&v)[8])
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
                  : "r"(ta));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_ld8_nowait(unsigned ta, float (&v)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(ta));
+}
+// wait for the loads in flight; the registers are tied in so no use is scheduled before the wait
+__device__ __forceinline__ void tm_wait_ld8(float (&v)[8])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7])
+                 :: "memory");
 }
 __device__ __forceinline__ void tm_st8(unsigned ta, const float (&v)[8])
 {
@@ -642,7 +652,7 @@ size_t tmem_smem_bytes(const BPParams &p)
 }
 
 template <bool POLY>
-__global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __grid_constant__ CUtensorMap qmap)
+__global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __grid_constant__ CUtensorMap qmap)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch, Wc = p.tmem_cols;
@@ -722,11 +732,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __g
     }
 
     // ---- consumer warps ----
-    // slice t -> TMEM column pair 2 (t mod Wc), 2 (t mod Wc) + 1: the two detector columns' partial sums
-    const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * 2 * Wc);
+    // slice t -> TMEM column t mod Wc of the warp's range (lane = TMEM lane)
+    const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * Wc);
     {
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int c = 0; c < 2 * Wc; c += 8) tm_st8(tw + c, z);
+        for (int c = 0; c < Wc; c += 8) tm_st8(tw + c, z);
         tm_wait_st();
     }
     const float2 *piw = p.pi_w + col;
@@ -735,10 +745,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __g
     int t_lo = 0, t_hi = -1, t_f = 0;                 // lane window [t_lo, t_hi]; warp flush point t_f
     int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
 
-    // warp-uniform: slice t is closed in every lane -> finish and write it, zero its columns
+    // warp-uniform: slice t is closed in every lane -> finish and write it, zero its column
     auto flush_slice = [&](int t) {
-        const unsigned tc = tw + 2u * (unsigned)(t % Wc);
-        const float a = tm_ld2sum(tc);
+        const unsigned tc = tw + ((unsigned)t & (unsigned)(Wc - 1));
+        const float a = tm_ld1(tc);
         if (active_col && t < p.nz) {
             const int2 e = pik[(size_t)t * plane];
             const float2 w = piw[(size_t)t * plane];
@@ -749,14 +759,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __g
             upk(ends, ea, eb);
             out[(size_t)t * plane] = (a + ea + eb) * p.scale;
         }
-        tm_st2zero(tc);
+        tm_st1(tc, 0.f);
     };
 
-    int sl = 0;
-    unsigned phase = 0;
     for (int n = 0; n < NV; ++n) {
         const int k = KC0 + n;
-        mbar_wait(full0 + 8u * sl, phase);
+        const int sl = n & (S - 1);                   // ring size is a power of two
+        mbar_wait(full0 + 8u * sl, (unsigned)(n >> p.lg_nbatch) & 1u);
         if (active_col) {
             while (k >= next_open) {
                 ++t_hi;
@@ -774,8 +783,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __g
         const int lo_w = __reduce_min_sync(0xffffffffu, work ? t_lo : INT_MAX);
         const int hi_w = __reduce_max_sync(0xffffffffu, work ? t_hi : -1);
         if (hi_w >= lo_w) {
-            u64 Wp = 0ull;
-            float base = 0.f, step = 0.f;
+            float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f;
             unsigned colbase = (stage_sa + (unsigned)(sl * vq) * 16u - kMagicBits * 16u) ^ p.zero;
             if (work) {
                 const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
@@ -795,66 +803,57 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_tmem(BPParams p, const __g
                 const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
                 const int l = __float2int_rz(cp);
                 const float fa = cp - __int2float_rn(l);
-                const float w1 = fa * inv_v;
-                Wp = pk(inv_v - w1, w1);
+                w1 = fa * inv_v;
+                w0 = inv_v - w1;
                 const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
                 step = sc * p.dz;
                 base = fmaf(sc, -vg.z, p.row_cc);                   // slice 0 (centred quad-row position)
                 const int ci = min(max(l - boxc[n], 0), BW - 1);
                 colbase = (stage_sa + (unsigned)(sl * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
             }
+            // slices open in every working lane: groups inside [lo_full, hi_full] need no mask
+            const int lo_full = __reduce_max_sync(0xffffffffu, work ? t_lo : INT_MIN);
+            const int hi_full = __reduce_min_sync(0xffffffffu, work ? t_hi : INT_MAX);
             const u64 S2 = pk(2.f * step, 2.f * step);
             const int m0 = lo_w & ~7;
-            unsigned cc = 2u * (unsigned)(m0 % Wc);                  // column of the group's first slice
+            const unsigned wmask = (unsigned)Wc - 1u;                // Wc is a power of two
+            unsigned cc = (unsigned)m0 & wmask;                      // column of the group's first slice
+            // every read stays within (warp span + 7) slices of an open slice: the pads cover that
+            u64 PM = pk(fmaf((float)m0, step, base), fmaf((float)(m0 + 1), step, base));
             for (int tb = m0; tb <= hi_w; tb += 8) {                 // warp-uniform groups of 8 slices
-                u64 acc[8];
-                tm_ld16(tw + cc, acc);
-                // a group that misses this lane's window is evaluated next to it instead (its sums are
-                // dropped), so every read stays within 7 slices of an open slice: head/tail pads cover that
-                const int tg = work ? min(max(tb, t_lo - 7), t_hi) : tb;
-                const int jl = min(max(t_lo - tb, 0), 8), jh = min(max(t_hi - tb + 1, 0), 8);
-                const unsigned mask = work ? ((0xffu << jl) & ((1u << jh) - 1u)) : 0u;
-                const float t0 = (float)tg;
-                u64 PM = pk(fmaf(t0, step, base), fmaf(t0 + 1.f, step, base));
-                if (__all_sync(0xffffffffu, mask == 0xffu || !work)) {
-                    // every working lane has all 8 slices open; idle lanes add exactly 0 (Wp = 0, finite reads)
+                float a8[8];
+                tm_ld8_nowait(tw + cc, a8);
+                float v[8][2];
 #pragma unroll
-                    for (int j = 0; j < 8; j += 2) {
-                        const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
-                        float q0, q1, f0, f1;
-                        upk(Q, q0, q1);
-                        upk(PM, f0, f1);
-                        const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
-                        const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                        acc[j] = fma2(Wp, fma2(pk(g0.z, g0.w), pk(f0, f0), pk(g0.x, g0.y)), acc[j]);
-                        acc[j + 1] = fma2(Wp, fma2(pk(g1.z, g1.w), pk(f1, f1), pk(g1.x, g1.y)), acc[j + 1]);
-                        PM = add2(PM, S2);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 8; j += 2) {
-                        const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
-                        float q0, q1, f0, f1;
-                        upk(Q, q0, q1);
-                        upk(PM, f0, f1);
-                        const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
-                        const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                        // value = sum over the two columns c of W_c (s_c + f d_c): kept as a column pair
-                        const u64 I0 = fma2(pk(g0.z, g0.w), pk(f0, f0), pk(g0.x, g0.y));
-                        const u64 I1 = fma2(pk(g1.z, g1.w), pk(f1, f1), pk(g1.x, g1.y));
-                        fma2_if(acc[j], Wp, I0, mask, 1u << j);
-                        fma2_if(acc[j + 1], Wp, I1, mask, 2u << j);
-                        PM = add2(PM, S2);
-                    }
+                for (int j = 0; j < 8; j += 2) {
+                    const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
+                    float q0, q1, p0, p1;
+                    upk(Q, q0, q1);
+                    upk(PM, p0, p1);
+                    const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+                    const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+                    upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), v[j][0], v[j][1]);
+                    upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), v[j + 1][0], v[j + 1][1]);
+                    PM = add2(PM, S2);
                 }
-                tm_st16(tw + cc, acc);
-                cc += 16u;
-                if (cc == 2u * (unsigned)Wc) cc = 0u;
+                tm_wait_ld8(a8);
+                if (tb >= lo_full && tb + 7 <= hi_full) {
+                    // all 8 slices open in every working lane; idle lanes add exactly 0 (w = 0, finite reads)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
+                } else {
+                    const int jl = min(max(t_lo - tb, 0), 8), jh = min(max(t_hi - tb + 1, 0), 8);
+                    const unsigned mask = work ? ((0xffu << jl) & ((1u << jh) - 1u)) : 0u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (mask & (1u << j)) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
+                }
+                tm_st8(tw + cc, a8);
+                cc = (cc + 8u) & wmask;
             }
             tm_wait_st();
         }
         mbar_arrive(empty0 + 8u * sl);
-        if (++sl == S) { sl = 0; phase ^= 1u; }
     }
     // every window has closed by K1 + 1: flush the rest
     const int hi_all = __reduce_max_sync(0xffffffffu, active_col ? p.nz - 1 : -1);
@@ -960,7 +959,7 @@ bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
 }
 }  // namespace
 
-void launch_backproject(const BPParams &p, cudaStream_t s)
+int launch_backproject(const BPParams &p, cudaStream_t s)
 {
     const int nchunk = (p.nz + JZ - 1) / JZ;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk * p.n_items);
@@ -968,25 +967,27 @@ void launch_backproject(const BPParams &p, cudaStream_t s)
     dim3 grid_l1((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk_l1 * p.n_items);
     const int block = TX * TY;
     const char *kv = std::getenv("KATS_BP_KERNEL");
-    const bool want_tmem = kv && std::string(kv) == "tmem";
-    // TMEM-window kernel (opt-in, A/B): accumulators in tensor memory
-    if (want_tmem && p.staged && !p.checked && p.windows_monotone && p.warp_span > 0 && 2 * (p.nr + 2) <= 256 &&
+    const bool want_window = kv && std::string(kv) == "window";
+    // TMEM-window kernel (default): accumulators in tensor memory, 3 CTAs per SM
+    if (!want_window && p.staged && !p.checked && p.windows_monotone && p.warp_span > 0 && 2 * (p.nr + 2) <= 256 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
         BPParams q = p;
-        q.tmem_cols = ((p.warp_span + 7) & ~7) + 16;             // circular window + 2 alias-free groups
+        q.tmem_cols = 16;                                         // power of two >= span + 2 alias-free groups
+        while (q.tmem_cols < ((p.warp_span + 7) & ~7) + 16) q.tmem_cols *= 2;
         int alloc = 32;
-        while (alloc < 2 * 2 * q.tmem_cols) alloc *= 2;           // 2 columns per slice, 2 warps per lane quarter
+        while (alloc < 2 * q.tmem_cols) alloc *= 2;               // 2 warps per TMEM lane quarter
         q.tmem_alloc = alloc;
-        // deepest ring (<= kMaxSlots views) such that 2 CTAs fit in shared memory and TMEM (2 x alloc <= 512)
+        // deepest power-of-two ring such that 3 CTAs fit in shared memory (and TMEM: 3 x alloc <= 512)
         q.nbatch = kMaxSlots;
-        while (q.nbatch > 2 && tmem_smem_bytes(q) > 100 * 1024) --q.nbatch;
+        while (q.nbatch > 2 && tmem_smem_bytes(q) > 74 * 1024) q.nbatch /= 2;
+        q.lg_nbatch = __builtin_ctz((unsigned)q.nbatch);
         const size_t sm = tmem_smem_bytes(q);
         CUtensorMap qmap;
-        if (alloc <= 256 && sm <= 200 * 1024 && make_quad_map(p, p.gq_views, &qmap)) {
+        if (alloc <= 128 && sm <= 200 * 1024 && make_quad_map(p, p.gq_views, &qmap)) {
             dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
             if (p.poly) launch_tmem_kernel<true>(q, gw, sm, qmap, s);
             else launch_tmem_kernel<false>(q, gw, sm, qmap, s);
-            return;
+            return KATS_BP_TMEM;
         }
     }
     BPParams q = p;
@@ -1006,7 +1007,7 @@ void launch_backproject(const BPParams &p, cudaStream_t s)
         case 32: launch_window<32>(q, gw, sm, qmap, s); break;
         default: launch_window<48>(q, gw, sm, qmap, s); break;
         }
-        return;
+        return KATS_BP_WINDOW;
     }
     if (p.poly) {
         if (p.checked) k_backproject<true, true><<<grid_l1, block, 0, s>>>(p);
@@ -1015,6 +1016,7 @@ void launch_backproject(const BPParams &p, cudaStream_t s)
         if (p.checked) k_backproject<false, true><<<grid_l1, block, 0, s>>>(p);
         else k_backproject<false, false><<<grid_l1, block, 0, s>>>(p);
     }
+    return KATS_BP_L1;
 }
 
 }  // namespace kats

@@ -60,11 +60,12 @@ struct BPParams {
     unsigned zero;            // runtime 0 (opaque to ptxas)
     int warp_span;            // max live slices of a warp (host, TMEM-window kernel)
     int pad_quads;            // head/tail pad (quads) for the TMEM-window kernel: 7 slices of row travel
-    int tmem_cols, tmem_alloc;// TMEM columns per warp / allocated per CTA (set by the launcher)
+    int tmem_cols, tmem_alloc;
+    int lg_nbatch;            // log2(nbatch) (TMEM kernel: slot parity from the view counter)// TMEM columns per warp / allocated per CTA (set by the launcher)
     float *vol;               // [n_items][nz][ny][nx]
 };
 
-void launch_backproject(const BPParams &p, cudaStream_t s);           // K5
+int launch_backproject(const BPParams &p, cudaStream_t s);            // K5; returns the KATS_BP_* variant
 void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cudaStream_t s);
 
 }  // namespace kats

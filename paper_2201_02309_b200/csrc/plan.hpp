@@ -70,6 +70,7 @@ struct katsevich_plan {
     std::vector<kats::ProfRecord> prof;
     std::vector<void *> event_pool;
     int64_t total_launches = 0;
+    int last_bp_kernel = 0;                 // KATS_BP_* variant of the last K5 launch
     int64_t stage_launches[6] = {0, 0, 0, 0, 0, 0};
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
     // host entry point: copy stream + sync events (created on first use)

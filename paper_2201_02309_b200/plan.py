@@ -191,6 +191,16 @@ class Plan:
                                                 _stream_handle(stream)))
         return out
 
+    BP_KERNELS = {0: None, 1: "k_backproject", 2: "k_bp_window", 3: "k_bp_tmem"}
+
+    def bp_kernel(self):
+        """Name of the step-7 kernel variant the last backprojection launched
+        (katsevich_bp_kernel), or None before the first one."""
+        r = lib().katsevich_bp_kernel(self._h)
+        if r < 0:
+            self._check(r)
+        return self.BP_KERNELS[r]
+
     # -- in-run timing -------------------------------------------------------
     def profile_enable(self, enable: bool = True):
         self._check(lib().katsevich_profile_enable(self._h, 1 if enable else 0))

@@ -148,3 +148,21 @@ def test_coverage_error_names_pitches():
     with pytest.raises(k.KatsevichError) as ei:
         p.reconstruct(torch.from_numpy(sino[:40]).cuda(), cfg["scan_v0"], 0, 1)
     assert ei.value.code == -4 and "reconstructible" in str(ei.value)
+
+
+@pytest.mark.parametrize("variant,kernel", [(None, "k_bp_tmem"), ("window", "k_bp_window"), ("l1", "k_backproject")])
+def test_every_bp_kernel_variant_matches_oracle(variant, kernel, monkeypatch):
+    """Each step-7 kernel (TMEM window = default, register window, chunked L1
+    path) on C1 against the oracle, and the plan reports that
+    the forced variant is the one that ran (katsevich_bp_kernel)."""
+    import torch
+    if variant is None:
+        monkeypatch.delenv("KATS_BP_KERNEL", raising=False)
+    else:
+        monkeypatch.setenv("KATS_BP_KERNEL", variant)
+    cfg, sino, ref, contrast = _case("C1")
+    p = _plan(cfg)
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    assert p.bp_kernel() == kernel
+    _check(vol.cpu().numpy(), ref, contrast)
