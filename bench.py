@@ -238,6 +238,30 @@ def run_ours(args):
             dist.barrier()
     ms_step = ms / args.steps
 
+    # ---- K5 in isolation: the same step with one backprojection launch over all of the rank's
+    # pitches after all filtering (KATS_PIPELINE=0), so no other kernel shares the GPU with it ----
+    iso = None
+    if not batch:
+        old_env = os.environ.get("KATS_PIPELINE")
+        os.environ["KATS_PIPELINE"] = "0"
+        step()
+        torch.cuda.synchronize()
+        plan.profile_read(reset=True)
+        plan.profile_enable(True)
+        n_iso = 3
+        for _ in range(n_iso):
+            step()
+        torch.cuda.synchronize()
+        st_iso = plan.profile_read(reset=True)
+        plan.profile_enable(False)
+        if old_env is None:
+            del os.environ["KATS_PIPELINE"]
+        else:
+            os.environ["KATS_PIPELINE"] = old_env
+        k = "K5_backproject"
+        iso = {"k5_ms_per_launch": st_iso["ms"][k] / max(1, st_iso["launches"][k]),
+               "launches": st_iso["launches"][k] // n_iso}
+
     # ---- e2e: host (pinned) in -> host out through katsevich_reconstruct_host ----
     e2e = None
     if not batch:
@@ -269,17 +293,20 @@ def run_ours(args):
     U_all = U_rank * world
     vols_all = (n_items * world) / (cfg["n_pitches"] if not batch else batch)
     value = U_all / (ms_step * 1e-3)
-    # roofline of the dominant kernel (K5 backprojection), CUDA events on the launching stream
+    # roofline of the dominant kernel (K5 backprojection), CUDA events recorded by the library on
+    # the launching streams. Per-pitch K5 launches run on two alternating streams and overlap, so
+    # the K5 time is its busy time (union of its launch intervals) per step, not a sum of durations.
     k5 = "K5_backproject"
-    k5_ms = stats["ms"][k5] / max(1, stats["launches"][k5])
-    k5_updates = U_rank / max(1, stats["launches"][k5] // args.steps)
-    achieved_tflops = k5_updates * bp_flops_per_update() / (k5_ms * 1e-3) / 1e12
+    k5_launches_per_step = max(1, stats["launches"][k5] // args.steps)
+    k5_ms_launch = stats["ms"][k5] / max(1, stats["launches"][k5])
+    k5_busy = stats["busy_ms"][k5] / args.steps
+    achieved_tflops = U_rank * bp_flops_per_update() / (k5_busy * 1e-3) / 1e12
     peaks, src = _peaks()
     fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     smem_peak = smem_peak_gbs(peaks.get("sm_max_mhz", 1965.0))
-    achieved_smem = k5_updates * bp_smem_bytes_per_update() / (k5_ms * 1e-3) / 1e9
+    achieved_smem = U_rank * bp_smem_bytes_per_update() / (k5_busy * 1e-3) / 1e9
     bp_kernel = plan.bp_kernel()
-    share = {s: stats["ms"][s] / max(1e-9, sum(stats["ms"].values())) for s in stats["ms"] if stats["ms"][s] > 0}
+    share = {s: stats["busy_ms"][s] / args.steps / ms_step for s in stats["busy_ms"] if stats["busy_ms"][s] > 0}
     line = {
         "metric": "voxel-view updates/s",
         "value": value,
@@ -302,18 +329,26 @@ def run_ours(args):
         "volumes_per_s": vols_all / (ms_step * 1e-3),
         "updates_per_step": U_all,
         "gpu_launches": stats["total_launches"],
-        "stage_ms_share": share,
+        "stage_busy_share_of_step": share,
         "precompute_s": t_pre,
         "roofline": {"bound": "smem", "kernel": bp_kernel, "achieved": achieved_smem, "peak": smem_peak,
                      "unit": "GB/s", "frac": achieved_smem / smem_peak,
                      "traffic": ncu_traffic(cfg["name"]),
-                     "bytes_per_update": bp_smem_bytes_per_update(), "k5_ms_per_launch": k5_ms,
-                     "k5_updates_per_s": k5_updates / (k5_ms * 1e-3),
+                     "bytes_per_update": bp_smem_bytes_per_update(),
+                     "k5_busy_ms_per_step": k5_busy, "k5_launches_per_step": k5_launches_per_step,
+                     "k5_ms_per_launch": k5_ms_launch, "k5_updates_per_s": U_rank / (k5_busy * 1e-3),
                      "peak_source": f"148 SMs x 128 B/clk shared-memory pipe x {peaks.get('sm_max_mhz', 1965.0)} MHz "
                                     f"({src} sm_max); DESIGN.md §5",
                      "secondary_alu": {"achieved": achieved_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
                                        "frac": achieved_tflops / fp32_peak,
-                                       "flops_per_update": bp_flops_per_update()}},
+                                       "flops_per_update": bp_flops_per_update()},
+                     "note": "achieved = 16 B x updates per step / K5 busy time per step in the timed "
+                             "region (per-pitch K5 launches overlap each other and the filter there, so "
+                             "this is a lower bound); isolated = one K5 launch for all pitches, alone",
+                     "isolated": None if iso is None else {
+                         "k5_ms_per_launch": iso["k5_ms_per_launch"],
+                         "achieved": U_rank * bp_smem_bytes_per_update() / (iso["k5_ms_per_launch"] * 1e-3) / 1e9,
+                         "frac": U_rank * bp_smem_bytes_per_update() / (iso["k5_ms_per_launch"] * 1e-3) / 1e9 / smem_peak}},
         "clocks": clk,
     }
     if e2e:

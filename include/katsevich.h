@@ -170,6 +170,8 @@ typedef struct {
     int64_t launches[6];     /* 0: K12 deriv+length weight+forward rebin, 1: K3 Hilbert,
                                 2: K4 backward rebin+cos, 3: K5 backprojection, 4: end-weight fix-up, 5: other */
     double  ms[6];           /* summed CUDA-event durations per stage */
+    double  busy_ms[6];      /* union of the stage's launch intervals (launches overlapping on
+                                different streams count once), per profile_read batch */
     int64_t total_launches;  /* all kernel launches issued by the plan since the last reset (always counted) */
 } katsevich_stats;
 

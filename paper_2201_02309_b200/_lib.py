@@ -37,7 +37,7 @@ class KatsevichGeometry(ctypes.Structure):
 
 class KatsevichStats(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6),
-                ("total_launches", ctypes.c_int64)]
+                ("busy_ms", ctypes.c_double * 6), ("total_launches", ctypes.c_int64)]
 
 
 # every symbol include/katsevich.h declares, with (restype, argtypes)

@@ -95,6 +95,9 @@ void free_device(katsevich_plan *p)
     p->sync_events.clear();
     if (p->copy_stream) { cudaStreamDestroy((cudaStream_t)p->copy_stream); p->copy_stream = nullptr; }
     if (p->copy_stream2) { cudaStreamDestroy((cudaStream_t)p->copy_stream2); p->copy_stream2 = nullptr; }
+    for (void *&b : p->bp_streams)
+        if (b) { cudaStreamDestroy((cudaStream_t)b); b = nullptr; }
+    if (p->filter_stream) { cudaStreamDestroy((cudaStream_t)p->filter_stream); p->filter_stream = nullptr; }
 }
 
 int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
@@ -339,6 +342,36 @@ int katsevich_workspace_bytes_host(const katsevich_plan *p, int32_t n_pitches, s
     return KATS_OK;
 }
 
+// two low-priority streams for per-pitch backprojections and one highest-priority stream for
+// the filter chunks that must finish before the next pitch's backprojection can start
+static int ensure_bp_streams(katsevich_plan *p)
+{
+    int lo = 0, hi = 0;
+    KCHECK(p, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (void *&b : p->bp_streams)
+        if (!b) {
+            cudaStream_t c;
+            KCHECK(p, cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, lo));
+            b = c;
+        }
+    if (!p->filter_stream) {
+        cudaStream_t c;
+        KCHECK(p, cudaStreamCreateWithPriority(&c, cudaStreamNonBlocking, hi));
+        p->filter_stream = c;
+    }
+    return KATS_OK;
+}
+
+static int ensure_events(katsevich_plan *p, size_t n)
+{
+    while (p->sync_events.size() < n) {
+        cudaEvent_t e;
+        KCHECK(p, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->sync_events.push_back(e);
+    }
+    return KATS_OK;
+}
+
 int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int64_t sn,
                           int32_t first_pitch, int32_t n_pitches, float *vol,
                           void *workspace, size_t workspace_bytes, void *cuda_stream)
@@ -368,17 +401,63 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     float4 *gq = (float4 *)workspace;
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * quad_view_elems(p) * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
-    rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s);
+    const char *pe = std::getenv("KATS_PIPELINE");
+    if (n_pitches == 1 || (pe && pe[0] == '0')) {
+        // filter every needed view, then one backprojection launch over all pitches
+        rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s);
+        if (rc) return rc;
+        BPParams b = bp_params(p);
+        b.gq = gq;
+        b.gq_views = nu;
+        b.off0 = (int64_t)first_pitch * vt - u0;
+        b.item_views = vt;
+        b.n_items = n_pitches;
+        b.vol = vol;
+        { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
+        KCHECK(p, cudaGetLastError());
+        return KATS_OK;
+    }
+    // Pipelined: pitch k is backprojected as soon as its views are filtered, on one of two
+    // streams forked from the caller's, so a launch's last wave overlaps the filtering and the
+    // backprojection of the next pitch; joined back into the caller's stream (still asynchronous).
+    rc = ensure_bp_streams(p);
     if (rc) return rc;
-    BPParams b = bp_params(p);
-    b.gq = gq;
-    b.gq_views = nu;
-    b.off0 = (int64_t)first_pitch * vt - u0;
-    b.item_views = vt;
-    b.n_items = n_pitches;
-    b.vol = vol;
-    { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
-    KCHECK(p, cudaGetLastError());
+    const size_t qs = quad_view_elems(p);
+    const size_t vpitch = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
+    const int64_t nchunks = (nu + kFilterChunk - 1) / kFilterChunk;
+    rc = ensure_events(p, 2 * (size_t)n_pitches + 1);
+    if (rc) return rc;
+    cudaStream_t fs = (cudaStream_t)p->filter_stream;
+    KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[2 * n_pitches], s));     // fork
+    KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[2 * n_pitches], 0));
+    int64_t c_next = 0;
+    for (int k = 0; k < n_pitches; ++k) {
+        const int64_t filt_end = (int64_t)(first_pitch + k) * vt + t.bp_hi + 1;   // exclusive
+        if (c_next < nchunks && u0 + c_next * kFilterChunk < filt_end) {
+            int64_t c_end = c_next;
+            while (c_end < nchunks && u0 + c_end * kFilterChunk < filt_end) ++c_end;
+            const int64_t a = u0 + c_next * kFilterChunk, n = std::min<int64_t>(c_end * kFilterChunk, nu) - c_next * kFilterChunk;
+            rc = run_filter(p, sino + (a - s0) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs);
+            if (rc) return rc;
+            c_next = c_end;
+        }
+        cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[n_pitches + k];
+        KCHECK(p, cudaEventRecord(e_filt, fs));
+        cudaStream_t bs = (cudaStream_t)p->bp_streams[k & 1];
+        KCHECK(p, cudaStreamWaitEvent(bs, e_filt, 0));
+        BPParams b = bp_params(p);
+        b.gq = gq;
+        b.gq_views = nu;
+        b.off0 = (int64_t)(first_pitch + k) * vt - u0;
+        b.item_views = vt;
+        b.n_items = 1;
+        b.vol = vol + (size_t)k * vpitch;
+        { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(b, bs); }
+        KCHECK(p, cudaGetLastError());
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[k], bs));
+    }
+    for (int k = std::max(0, n_pitches - 2); k < n_pitches; ++k)       // join
+        KCHECK(p, cudaStreamWaitEvent(s, (cudaEvent_t)p->sync_events[k], 0));
     return KATS_OK;
 }
 
@@ -432,8 +511,10 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
     katsevich_scan_views(p, first_pitch, n_pitches, &fv, &nv);
     if (fv < s0 || fv + nv > s0 + sn) return katsevich_reconstruct(p, host_sino, s0, sn, first_pitch, n_pitches,
                                                                    host_vol, workspace, workspace_bytes, cuda_stream);
-    // Pipelined over groups of pitches on two streams: H2D of the views the next group needs and
-    // D2H of finished volumes (copy stream) overlap filtering + backprojection (caller's stream).
+    // Pipelined on three streams: every host->device copy is enqueued up front on the copy stream,
+    // one piece per 256-view filter chunk with an event each, so filtering trails the copy chunk by
+    // chunk; each pitch is backprojected as soon as its views are filtered and its volume goes back
+    // on a second copy stream while the next pitch runs (caller's stream: filter + BP).
     cudaStream_t s = (cudaStream_t)cuda_stream;
     if (!p->copy_stream) {
         cudaStream_t a, b;
@@ -442,14 +523,9 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
         p->copy_stream = a;
         p->copy_stream2 = b;
     }
+    rc = ensure_bp_streams(p);
+    if (rc) return rc;
     cudaStream_t cs = (cudaStream_t)p->copy_stream, ds = (cudaStream_t)p->copy_stream2;
-    const int G = 2;                                          // pitches per group (>= 2 BP waves)
-    const int ngroups = (n_pitches + G - 1) / G;
-    while ((int)p->sync_events.size() < 2 * ngroups + 1) {
-        cudaEvent_t e;
-        KCHECK(p, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        p->sync_events.push_back(e);
-    }
     const HostTables &t = p->t;
     const int vt = p->g.views_per_turn;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
@@ -457,50 +533,66 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
     const size_t vpitch = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
     const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;   // first filtered view (= fv + 1)
     const int64_t nu = n_union_views(p, n_pitches);
+    const int64_t nchunks = (nu + kFilterChunk - 1) / kFilterChunk;
+    while ((int64_t)p->sync_events.size() < nchunks + 2 * n_pitches + 1) {
+        cudaEvent_t e;
+        KCHECK(p, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->sync_events.push_back(e);
+    }
     float4 *gq = (float4 *)workspace;
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
     float *dsino = (float *)((char *)workspace + base);
     float *dvol = (float *)((char *)dsino + align_up(sizeof(float) * rs * (size_t)nv));
     // the caller's pending work on s (e.g. earlier writes to the workspace) precedes our copies
-    cudaEvent_t e_start = (cudaEvent_t)p->sync_events[2 * ngroups];
+    cudaEvent_t e_start = (cudaEvent_t)p->sync_events[nchunks + 2 * n_pitches];
     KCHECK(p, cudaEventRecord(e_start, s));
     KCHECK(p, cudaStreamWaitEvent(cs, e_start, 0));
-    // all host->device copies up front on their own stream, one event per group
+    cudaStream_t fs = (cudaStream_t)p->filter_stream;
+    KCHECK(p, cudaStreamWaitEvent(fs, e_start, 0));
+    // chunk c filters views [u0 + 256 c, u0 + 256 c + n) and needs raw views up to one past its end
     int64_t copied_to = fv;
-    for (int gi = 0; gi < ngroups; ++gi) {
-        const int g0 = gi * G, np_g = std::min(G, n_pitches - g0);
-        const int64_t raw_end = (int64_t)(first_pitch + g0 + np_g - 1) * vt + t.bp_hi + 2;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t raw_end = u0 + std::min<int64_t>((c + 1) * kFilterChunk, nu) + 1;   // exclusive
         KCHECK(p, cudaMemcpyAsync(dsino + (copied_to - fv) * rs, host_sino + (copied_to - s0) * rs,
                                   sizeof(float) * rs * (size_t)(raw_end - copied_to), cudaMemcpyHostToDevice, cs));
-        KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[2 * gi], cs));
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[c], cs));
         copied_to = raw_end;
     }
-    int64_t filtered_to = u0;
-    for (int gi = 0; gi < ngroups; ++gi) {
-        const int g0 = gi * G, np_g = std::min(G, n_pitches - g0);
-        const int64_t filt_end = (int64_t)(first_pitch + g0 + np_g - 1) * vt + t.bp_hi + 1;
-        cudaEvent_t e_h2d = (cudaEvent_t)p->sync_events[2 * gi], e_bp = (cudaEvent_t)p->sync_events[2 * gi + 1];
-        KCHECK(p, cudaStreamWaitEvent(s, e_h2d, 0));
-        rc = run_filter(p, dsino + (filtered_to - fv) * rs, filt_end - filtered_to, gq + (filtered_to - u0) * qs,
-                        scratch, nullptr, nullptr, nullptr, s);
-        if (rc) return rc;
-        filtered_to = filt_end;
+    int64_t c_next = 0;                                       // next chunk to filter
+    for (int k = 0; k < n_pitches; ++k) {
+        const int64_t filt_end = (int64_t)(first_pitch + k) * vt + t.bp_hi + 1;   // exclusive
+        while (c_next < nchunks && u0 + c_next * kFilterChunk < filt_end) {
+            const int64_t a = u0 + c_next * kFilterChunk, n = std::min<int64_t>(kFilterChunk, nu - c_next * kFilterChunk);
+            KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[c_next], 0));
+            rc = run_filter(p, dsino + (a - fv) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs);
+            if (rc) return rc;
+            ++c_next;
+        }
+        // pitch k's BP on alternating streams: its tail overlaps the next pitch's filter and BP
+        cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[nchunks + n_pitches + k];
+        KCHECK(p, cudaEventRecord(e_filt, fs));
+        cudaStream_t bs = (cudaStream_t)p->bp_streams[k & 1];
+        KCHECK(p, cudaStreamWaitEvent(bs, e_filt, 0));
         BPParams b = bp_params(p);
         b.gq = gq;
         b.gq_views = nu;
-        b.off0 = (int64_t)(first_pitch + g0) * vt - u0;
+        b.off0 = (int64_t)(first_pitch + k) * vt - u0;
         b.item_views = vt;
-        b.n_items = np_g;
-        b.vol = dvol + (size_t)g0 * vpitch;
-        { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
+        b.n_items = 1;
+        b.vol = dvol + (size_t)k * vpitch;
+        { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(b, bs); }
         KCHECK(p, cudaGetLastError());
-        KCHECK(p, cudaEventRecord(e_bp, s));
+        cudaEvent_t e_bp = (cudaEvent_t)p->sync_events[nchunks + k];
+        KCHECK(p, cudaEventRecord(e_bp, bs));
         KCHECK(p, cudaStreamWaitEvent(ds, e_bp, 0));
-        KCHECK(p, cudaMemcpyAsync(host_vol + (size_t)g0 * vpitch, b.vol, sizeof(float) * vpitch * np_g,
+        KCHECK(p, cudaMemcpyAsync(host_vol + (size_t)k * vpitch, b.vol, sizeof(float) * vpitch,
                                   cudaMemcpyDeviceToHost, ds));
     }
     KCHECK(p, cudaStreamSynchronize(ds));
     KCHECK(p, cudaStreamSynchronize(cs));
+    KCHECK(p, cudaStreamSynchronize((cudaStream_t)p->bp_streams[0]));
+    KCHECK(p, cudaStreamSynchronize((cudaStream_t)p->bp_streams[1]));
+    KCHECK(p, cudaStreamSynchronize(fs));
     KCHECK(p, cudaStreamSynchronize(s));
     return KATS_OK;
 }
@@ -600,20 +692,42 @@ int katsevich_profile_read(katsevich_plan *p, katsevich_stats *out, int reset)
     if (!p || !out) return KATS_ERR_NULL;
     if (p->device >= 0) {
         cudaSetDevice(p->device);
+        // per launch: duration, and its interval against the first recorded event so that
+        // launches overlapping on different streams count once in the stage's busy time
+        std::vector<std::pair<float, float>> iv[6];
         for (auto &r : p->prof) {
-            float ms = 0.f;
+            float ms = 0.f, a = 0.f, b = 0.f;
             KCHECK(p, cudaEventSynchronize((cudaEvent_t)r.ev1));
             KCHECK(p, cudaEventElapsedTime(&ms, (cudaEvent_t)r.ev0, (cudaEvent_t)r.ev1));
+            KCHECK(p, cudaEventElapsedTime(&a, (cudaEvent_t)p->prof[0].ev0, (cudaEvent_t)r.ev0));
+            KCHECK(p, cudaEventElapsedTime(&b, (cudaEvent_t)p->prof[0].ev0, (cudaEvent_t)r.ev1));
             p->stage_ms[r.stage] += ms;
+            iv[r.stage].push_back({a, b});
+        }
+        for (int st = 0; st < 6; ++st) {
+            std::sort(iv[st].begin(), iv[st].end());
+            double busy = 0.0, lo = 0.0, hi = -1e300;
+            for (auto &x : iv[st]) {
+                if (x.first > hi) { if (hi > lo) busy += hi - lo; lo = x.first; hi = x.second; }
+                else hi = std::max<double>(hi, x.second);
+            }
+            if (hi > lo) busy += hi - lo;
+            p->stage_busy_ms[st] += busy;
+        }
+        for (auto &r : p->prof) {
             p->event_pool.push_back(r.ev0);
             p->event_pool.push_back(r.ev1);
         }
         p->prof.clear();
     }
-    for (int i = 0; i < 6; ++i) { out->launches[i] = p->stage_launches[i]; out->ms[i] = p->stage_ms[i]; }
+    for (int i = 0; i < 6; ++i) {
+        out->launches[i] = p->stage_launches[i];
+        out->ms[i] = p->stage_ms[i];
+        out->busy_ms[i] = p->stage_busy_ms[i];
+    }
     out->total_launches = p->total_launches;
     if (reset) {
-        for (int i = 0; i < 6; ++i) { p->stage_launches[i] = 0; p->stage_ms[i] = 0; }
+        for (int i = 0; i < 6; ++i) { p->stage_launches[i] = 0; p->stage_ms[i] = 0; p->stage_busy_ms[i] = 0; }
         p->total_launches = 0;
     }
     return KATS_OK;

@@ -73,9 +73,12 @@ struct katsevich_plan {
     int last_bp_kernel = 0;                 // KATS_BP_* variant of the last K5 launch
     int64_t stage_launches[6] = {0, 0, 0, 0, 0, 0};
     double stage_ms[6] = {0, 0, 0, 0, 0, 0};
+    double stage_busy_ms[6] = {0, 0, 0, 0, 0, 0};
     // host entry point: copy stream + sync events (created on first use)
     void *copy_stream = nullptr;            // host->device
     void *copy_stream2 = nullptr;           // device->host
+    void *bp_streams[2] = {nullptr, nullptr};  // alternating per-pitch backprojection streams (low priority)
+    void *filter_stream = nullptr;          // filter chunks (highest priority)
     std::vector<void *> sync_events;
 };
 

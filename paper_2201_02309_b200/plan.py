@@ -210,4 +210,5 @@ class Plan:
         self._check(lib().katsevich_profile_read(self._h, ctypes.byref(st), 1 if reset else 0))
         return {"launches": {STAGES[i]: st.launches[i] for i in range(6)},
                 "ms": {STAGES[i]: st.ms[i] for i in range(6)},
+                "busy_ms": {STAGES[i]: st.busy_ms[i] for i in range(6)},
                 "total_launches": st.total_launches}
