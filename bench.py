@@ -239,7 +239,8 @@ def run_ours(args):
     ms_step = ms / args.steps
 
     # ---- K5 in isolation: the same step with one backprojection launch over all of the rank's
-    # pitches after all filtering (KATS_PIPELINE=0), so no other kernel shares the GPU with it ----
+    # pitches after all filtering (KATS_PIPELINE=0, the default), so no other kernel shares the GPU
+    # with it (differs from the timed region only when KATS_PIPELINE=1 is set) ----
     iso = None
     if not batch:
         old_env = os.environ.get("KATS_PIPELINE")

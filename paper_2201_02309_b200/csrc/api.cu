@@ -83,7 +83,8 @@ void free_device(katsevich_plan *p)
 {
     if (p->device < 0) return;
     cudaSetDevice(p->device);
-    void *ptrs[] = {p->d.pi_k, p->d.pi_w, p->d.view, p->d.fr, p->d.br, p->d.cos_alpha, p->d.wlen, p->d.hilbert};
+    void *ptrs[] = {p->d.pi_k, p->d.pi_w, p->d.view, p->d.fr, p->d.br, p->d.cos_alpha, p->d.wlen, p->d.hilbert,
+                    p->d.hilbert_tc};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     p->d = DeviceTables{};
@@ -124,7 +125,7 @@ FilterParams filter_params(const katsevich_plan *p)
     f.inv_dalpha = (float)(1.0 / p->g.d_alpha);
     f.inv_2dalpha = (float)(1.0 / (2.0 * p->g.d_alpha));
     f.wlen = p->d.wlen; f.fr = p->d.fr; f.br = p->d.br;
-    f.cos_alpha = p->d.cos_alpha; f.hilbert = p->d.hilbert;
+    f.cos_alpha = p->d.cos_alpha; f.hilbert = p->d.hilbert; f.hilbert_tc = p->d.hilbert_tc;
     return f;
 }
 
@@ -287,6 +288,9 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
             (rc = upload(p, &p->d.br, br)) || (rc = upload(p, &p->d.cos_alpha, cosa)) ||
             (rc = upload(p, &p->d.wlen, wlen)) || (rc = upload(p, &p->d.hilbert, hk)))
             return rc;
+        std::vector<float> htc;
+        hilbert_tc_table(g.n_cols, hk.data(), htc);
+        if ((rc = upload(p, &p->d.hilbert_tc, htc))) return rc;
         KCHECK(p, cudaDeviceSynchronize());
     }
     p->precomputed = true;
@@ -402,7 +406,7 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     float4 *gq = (float4 *)workspace;
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * quad_view_elems(p) * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
     const char *pe = std::getenv("KATS_PIPELINE");
-    if (n_pitches == 1 || (pe && pe[0] == '0')) {
+    if (n_pitches == 1 || !(pe && pe[0] == '1')) {
         // filter every needed view, then one backprojection launch over all pitches
         rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s);
         if (rc) return rc;
@@ -417,7 +421,8 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
         KCHECK(p, cudaGetLastError());
         return KATS_OK;
     }
-    // Pipelined: pitch k is backprojected as soon as its views are filtered, on one of two
+    // Pipelined (KATS_PIPELINE=1; worthwhile when filtering is a large share of the step): pitch k
+    // is backprojected as soon as its views are filtered, on one of two
     // streams forked from the caller's, so a launch's last wave overlaps the filtering and the
     // backprojection of the next pitch; joined back into the caller's stream (still asynchronous).
     rc = ensure_bp_streams(p);

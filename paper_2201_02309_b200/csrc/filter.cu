@@ -2,6 +2,12 @@
 // PAPER.md §II (l.117-154) as sm_100a kernels.  Each filtered view depends
 // only on raw views v-1, v, v+1, so the same kernels serve the per-pitch slab
 // (P:l.250) and the filter-once long-scan path.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace kats {
@@ -113,6 +119,293 @@ __global__ void __launch_bounds__(256) k_hilbert(FilterParams p, int64_t n_lines
 }
 
 // ---------------------------------------------------------------------------
+// K3 on the tensor cores (default when the taps fit): split by
+// output parity the odd-tap convolution is a dense GEMM per parity,
+//   g4[line][2n + par] = Σ_k g3[line][2k + 1 - par] · K[2(n - k) + 2 par - 1],
+// M = κ-lines, N = K = ⌈n_α/2⌉ (padded to NH, a multiple of 32).  fp32
+// accuracy from 3xTF32: A = A_h + A_l, B = B_h + B_l (A_h, B_h: fp32 with the
+// low 13 mantissa bits cleared, exactly representable in TF32; the remainders
+// are exact in fp32), D = A_h B_h + A_h B_l + A_l B_h accumulated in fp32 in
+// TMEM (the dropped A_l B_l is ~2^-20 relative).  One CTA = 128 lines x one
+// parity; 4 warps stage each 32-wide K chunk of A (split on the fly) and of the
+// precomputed tap matrix (hi/lo, plan table) into shared memory in the
+// canonical no-swizzle K-major UMMA layout (8-row x 16-byte core matrices:
+// LBO = 128 B along K, SBO = 1024 B along M/N), one thread issues
+// tcgen05.mma.kind::tf32 (M = 128, N <= 256 per instruction, K = 8) and
+// commits to an mbarrier; the epilogue reads the accumulator with tcgen05.ld.
+// ---------------------------------------------------------------------------
+constexpr int TC_M = 128, TC_KC = 32;
+
+__host__ __device__ inline int hilbert_tc_nh(int nc) { return ((nc + 1) / 2 + 31) / 32 * 32; }
+
+// canonical K-major offset (bytes) of element (row, k) in a [rows][32] chunk
+__device__ __forceinline__ unsigned tc_off(int row, int k)
+{
+    return (unsigned)((row >> 3) * 1024 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ uint64_t tc_desc(unsigned saddr)
+{
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)(1024u >> 4) << 32) |
+           (1ull << 46);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n_lines)
+{
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC;
+    const int par = blockIdx.y;                                  // output parity
+    const int nin = (nc - (1 - par) + 1) / 2, nout = (nc - par + 1) / 2;
+    const int64_t line0 = (int64_t)blockIdx.x * TC_M;
+    unsigned char *Ah = tsm, *Al = tsm + TC_M * TC_KC * 4;
+    unsigned char *Bh = Al + TC_M * TC_KC * 4, *Bl = Bh + NH * TC_KC * 4;
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ unsigned s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+    if (warp == 0) {
+        unsigned cols = 32;
+        while (cols < (unsigned)NH) cols <<= 1;
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = s_tmem;
+    // instruction descriptor: D f32, A/B tf32, both K-major, M = 128
+    const unsigned idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_M >> 4) << 24);
+    const float4 *btab = reinterpret_cast<const float4 *>(p.hilbert_tc) + (size_t)par * NK * 2 * NH * TC_KC / 4;
+    const unsigned sAh = (unsigned)__cvta_generic_to_shared(Ah), sAl = (unsigned)__cvta_generic_to_shared(Al);
+    const unsigned sBh = (unsigned)__cvta_generic_to_shared(Bh), sBl = (unsigned)__cvta_generic_to_shared(Bl);
+
+    for (int kc = 0; kc < NK; ++kc) {
+        // A chunk: lane = (row within an 8-row group, k quad); a warp stores 512 contiguous bytes
+        const int rr = lane & 7, kq = lane >> 3;
+        for (int g = warp; g < TC_M / 8; g += 4) {
+            const int row = g * 8 + rr;
+            const int64_t line = line0 + row;
+            const float *src = p.g3 + line * nc + (1 - par);
+#pragma unroll
+            for (int qb = 0; qb < 2; ++qb) {
+                const int k0 = kc * TC_KC + (qb * 4 + kq) * 4;
+                float v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    v[i] = (line < n_lines && k0 + i < nin) ? __ldg(src + 2 * (k0 + i)) : 0.f;
+                const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
+                const unsigned o = tc_off(row, (qb * 4 + kq) * 4);
+                *reinterpret_cast<float4 *>(Ah + o) = h;
+                *reinterpret_cast<float4 *>(Al + o) = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
+            }
+        }
+        // B chunk (hi, lo): already in the canonical layout in the plan table
+        const float4 *bsrc = btab + (size_t)kc * 2 * NH * TC_KC / 4;
+        float4 *bdst = reinterpret_cast<float4 *>(Bh);
+        for (int i = tid; i < 2 * NH * TC_KC / 4; i += 128) bdst[i] = __ldg(bsrc + i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int n0 = 0; n0 < NH; n0 += 256) {
+                const int nn = NH - n0 < 256 ? NH - n0 : 256;
+                const unsigned idesc = idesc_base | ((unsigned)(nn >> 3) << 17);
+                const unsigned boff = (unsigned)(n0 / 8) * 1024u;
+#pragma unroll
+                for (int kk = 0; kk < TC_KC / 8; ++kk) {
+                    const unsigned ko = (unsigned)kk * 256u;
+                    const uint64_t a_h = tc_desc(sAh + ko), a_l = tc_desc(sAl + ko);
+                    const uint64_t b_h = tc_desc(sBh + boff + ko), b_l = tc_desc(sBl + boff + ko);
+                    const unsigned first = (kc == 0 && kk == 0) ? 0u : 1u;
+                    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n\t}"
+                                 ::"r"(tmem + (unsigned)n0), "l"(a_h), "l"(b_h), "r"(idesc), "r"(first));
+                    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;"
+                                 ::"r"(tmem + (unsigned)n0), "l"(a_h), "l"(b_l), "r"(idesc));
+                    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;"
+                                 ::"r"(tmem + (unsigned)n0), "l"(a_l), "l"(b_h), "r"(idesc));
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                         : "memory");
+        }
+        // the MMAs have read this chunk once the commit lands (phase kc & 1)
+        asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
+                     "@!d bra WAIT_%=;\n\t}" ::"r"(bar), "r"((unsigned)(kc & 1)) : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    // epilogue: warp w owns accumulator rows (lines) 32w .. 32w+31 = TMEM lanes
+    const int64_t line = line0 + warp * 32 + lane;
+    float *dst = p.g4 + line * nc + par;
+    for (int c = 0; c < NH; c += 16) {
+        float v[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+                       "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+                     : "r"(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (line < n_lines) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (c + i < nout) dst[2 * (c + i)] = v[i];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        unsigned cols = 32;
+        while (cols < (unsigned)NH) cols <<= 1;
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+    }
+}
+
+// Both parities per CTA (NH <= 256: two accumulators fit TMEM's 512 columns).
+// A K chunk covers inputs l in [64 kc, 64 kc + 64) of each line (coalesced
+// loads), de-interleaved into the even- and odd-input tiles; output parity 0
+// takes the odd inputs, parity 1 the even ones.  The epilogue stages 32 lines x
+// 32 outputs per warp in padded shared memory so every line is written as
+// contiguous 128-byte runs.
+__global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t n_lines)
+{
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC;
+    const int64_t line0 = (int64_t)blockIdx.x * TC_M;
+    constexpr int AT = TC_M * TC_KC * 4;                         // one A tile (16 KB)
+    unsigned char *Aeh = tsm, *Ael = tsm + AT, *Aoh = tsm + 2 * AT, *Aol = tsm + 3 * AT;
+    unsigned char *B = tsm + 4 * AT;                             // [par][hi, lo][NH x 32]
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ unsigned s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+    unsigned cols = 32;
+    while (cols < 2u * (unsigned)NH) cols <<= 1;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = s_tmem;
+    const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(NH >> 3) << 17) | ((unsigned)(TC_M >> 4) << 24);
+    const unsigned sA[4] = {(unsigned)__cvta_generic_to_shared(Aeh), (unsigned)__cvta_generic_to_shared(Ael),
+                            (unsigned)__cvta_generic_to_shared(Aoh), (unsigned)__cvta_generic_to_shared(Aol)};
+    const unsigned sB = (unsigned)__cvta_generic_to_shared(B);
+    const unsigned bt = (unsigned)NH * TC_KC * 4;                 // one B tile
+
+    for (int kc = 0; kc < NK; ++kc) {
+        // A: lane = (row in an 8-row group, k quad); 8 consecutive inputs per lane = 4 (even, odd) pairs
+        const int rr = lane & 7, kq = lane >> 3;
+        for (int g = warp; g < TC_M / 8; g += 4) {
+            const int row = g * 8 + rr;
+            const int64_t line = line0 + row;
+            const float *src = p.g3 + line * nc;
+            const bool ok = line < n_lines;
+#pragma unroll
+            for (int qb = 0; qb < 2; ++qb) {
+                const int kl = (qb * 4 + kq) * 4;                   // k within the chunk
+                const int l0 = 2 * (kc * TC_KC + kl);               // first input column
+                float e[4], o[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    e[i] = (ok && l0 + 2 * i < nc) ? __ldg(src + l0 + 2 * i) : 0.f;
+                    o[i] = (ok && l0 + 2 * i + 1 < nc) ? __ldg(src + l0 + 2 * i + 1) : 0.f;
+                }
+                const unsigned off = tc_off(row, kl);
+                const float4 eh = make_float4(tf32_hi(e[0]), tf32_hi(e[1]), tf32_hi(e[2]), tf32_hi(e[3]));
+                const float4 oh = make_float4(tf32_hi(o[0]), tf32_hi(o[1]), tf32_hi(o[2]), tf32_hi(o[3]));
+                *reinterpret_cast<float4 *>(Aeh + off) = eh;
+                *reinterpret_cast<float4 *>(Ael + off) = make_float4(e[0] - eh.x, e[1] - eh.y, e[2] - eh.z, e[3] - eh.w);
+                *reinterpret_cast<float4 *>(Aoh + off) = oh;
+                *reinterpret_cast<float4 *>(Aol + off) = make_float4(o[0] - oh.x, o[1] - oh.y, o[2] - oh.z, o[3] - oh.w);
+            }
+        }
+        // B chunk kc of both parities (hi, lo each), canonical layout in the plan table
+        const float4 *tab = reinterpret_cast<const float4 *>(p.hilbert_tc);
+        for (int par = 0; par < 2; ++par) {
+            const float4 *bsrc = tab + (((size_t)par * NK + kc) * 2) * NH * TC_KC / 4;
+            float4 *bdst = reinterpret_cast<float4 *>(B + (size_t)par * 2 * bt);
+            for (int i = tid; i < 2 * NH * TC_KC / 4; i += 128) bdst[i] = __ldg(bsrc + i);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int par = 0; par < 2; ++par) {
+                const unsigned ah = sA[par == 0 ? 2 : 0], al = sA[par == 0 ? 3 : 1];   // parity 0 <- odd inputs
+                const unsigned bh = sB + (unsigned)par * 2u * bt, bl = bh + bt;
+                const unsigned d = tmem + (unsigned)(par * NH);
+#pragma unroll
+                for (int kk = 0; kk < TC_KC / 8; ++kk) {
+                    const unsigned ko = (unsigned)kk * 256u;
+                    const uint64_t a_h = tc_desc(ah + ko), a_l = tc_desc(al + ko);
+                    const uint64_t b_h = tc_desc(bh + ko), b_l = tc_desc(bl + ko);
+                    const unsigned acc = (kc == 0 && kk == 0) ? 0u : 1u;
+                    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n\t}"
+                                 ::"r"(d), "l"(a_h), "l"(b_h), "r"(idesc), "r"(acc));
+                    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;" ::"r"(d), "l"(a_h),
+                                 "l"(b_l), "r"(idesc));
+                    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;" ::"r"(d), "l"(a_l),
+                                 "l"(b_h), "r"(idesc));
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                         : "memory");
+        }
+        asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
+                     "@!d bra WAIT_%=;\n\t}" ::"r"(bar), "r"((unsigned)(kc & 1)) : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    // epilogue: per warp, 32 lines (its TMEM lanes) x 32 output columns at a time through smem
+    float *stg = reinterpret_cast<float *>(tsm) + warp * 32 * 33;
+    const unsigned trow = tmem + ((unsigned)(warp * 32) << 16);
+    for (int c = 0; c < NH; c += 16) {
+        float v0[16], v1[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=f"(v0[0]), "=f"(v0[1]), "=f"(v0[2]), "=f"(v0[3]), "=f"(v0[4]), "=f"(v0[5]), "=f"(v0[6]), "=f"(v0[7]),
+                       "=f"(v0[8]), "=f"(v0[9]), "=f"(v0[10]), "=f"(v0[11]), "=f"(v0[12]), "=f"(v0[13]), "=f"(v0[14]), "=f"(v0[15])
+                     : "r"(trow + (unsigned)c));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=f"(v1[0]), "=f"(v1[1]), "=f"(v1[2]), "=f"(v1[3]), "=f"(v1[4]), "=f"(v1[5]), "=f"(v1[6]), "=f"(v1[7]),
+                       "=f"(v1[8]), "=f"(v1[9]), "=f"(v1[10]), "=f"(v1[11]), "=f"(v1[12]), "=f"(v1[13]), "=f"(v1[14]), "=f"(v1[15])
+                     : "r"(trow + (unsigned)(NH + c)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // lane = line; output columns 2c .. 2c+31 (parity 0 at even, parity 1 at odd)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            stg[lane * 33 + 2 * i] = v0[i];
+            stg[lane * 33 + 2 * i + 1] = v1[i];
+        }
+        __syncwarp();
+        const int l = 2 * c + lane;
+        for (int r = 0; r < 32; ++r) {
+            const int64_t line = line0 + warp * 32 + r;
+            if (line < n_lines && l < nc) p.g4[line * nc + l] = stg[r * 33 + lane];
+        }
+        __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
+// ---------------------------------------------------------------------------
 // K4: gF[v][m][l] = cos α_l · lerp_ψ(g4[v][·][l], ψ̂(α_l, w_m))   (Eqs. 13-15)
 //
 // Output for the backprojection: per view, column-major 2x2 tap quads in
@@ -169,8 +462,68 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     k_deriv_fwd_rebin<<<grid, 128, 0, s>>>(p);
 }
 
+size_t hilbert_tc_table_floats(int nc) { return 2 * 2 * (size_t)hilbert_tc_nh(nc) * hilbert_tc_nh(nc); }
+
+// [par][kc][hi, lo][NH x 32 canonical K-major] (see k_hilbert_tc)
+void hilbert_tc_table(int nc, const float *kd, std::vector<float> &out)
+{
+    const int NH = hilbert_tc_nh(nc), NK = NH / TC_KC;
+    out.assign(hilbert_tc_table_floats(nc), 0.f);
+    for (int par = 0; par < 2; ++par) {
+        const int nin = (nc - (1 - par) + 1) / 2, nout = (nc - par + 1) / 2;
+        for (int kc = 0; kc < NK; ++kc)
+            for (int n = 0; n < NH; ++n)
+                for (int kl = 0; kl < TC_KC; ++kl) {
+                    const int k = kc * TC_KC + kl;
+                    float b = 0.f;
+                    if (n < nout && k < nin) b = kd[2 * (n - k) + 2 * par - 1 + nc - 1];
+                    uint32_t u;
+                    std::memcpy(&u, &b, 4);
+                    u &= 0xFFFFE000u;
+                    float hi;
+                    std::memcpy(&hi, &u, 4);
+                    const size_t off = (size_t)((n >> 3) * 1024 + (kl >> 2) * 128 + (n & 7) * 16 + (kl & 3) * 4) / 4;
+                    const size_t blk = (((size_t)par * NK + kc) * 2) * NH * TC_KC;
+                    out[blk + off] = hi;
+                    out[blk + (size_t)NH * TC_KC + off] = b - hi;
+                }
+    }
+}
+
+bool hilbert_tc_usable(const FilterParams &p)
+{
+    const char *e = std::getenv("KATS_HILBERT");
+    if (e && std::string(e) == "fp32") return false;
+    return p.hilbert_tc != nullptr && hilbert_tc_nh(p.nc) <= 512;
+}
+
 void launch_hilbert(const FilterParams &p, cudaStream_t s)
 {
+    if (hilbert_tc_usable(p) && hilbert_tc_nh(p.nc) <= 256) {
+        const int NH = hilbert_tc_nh(p.nc);
+        const size_t smem = (size_t)4 * TC_M * TC_KC * 4 + (size_t)4 * NH * TC_KC * 4;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_hilbert_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            attr = true;
+        }
+        const int64_t n_lines = (int64_t)p.n_views * p.npsi;
+        k_hilbert_tc2<<<(unsigned)((n_lines + TC_M - 1) / TC_M), 128, smem, s>>>(p, n_lines);
+        return;
+    }
+    if (hilbert_tc_usable(p)) {
+        const int NH = hilbert_tc_nh(p.nc);
+        const size_t smem = (size_t)2 * TC_M * TC_KC * 4 + (size_t)2 * NH * TC_KC * 4;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_hilbert_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+        const int64_t n_lines = (int64_t)p.n_views * p.npsi;
+        dim3 grid((unsigned)((n_lines + TC_M - 1) / TC_M), 2);
+        k_hilbert_tc<<<grid, 128, smem, s>>>(p, n_lines);
+        return;
+    }
     const int tpl = 2 * (((p.nc + 1) / 2 + HR - 1) / HR);
     const int lpb = tpl >= 256 ? 1 : 256 / tpl;
     const int64_t n_lines = (int64_t)p.n_views * p.npsi;

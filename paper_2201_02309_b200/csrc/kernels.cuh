@@ -1,6 +1,7 @@
 // kernels.cuh — launch interfaces of the sm_100a kernels (internal).
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "plan.hpp"
@@ -18,6 +19,7 @@ struct FilterParams {
     const RebinEntry *br;     // [nr][nc]
     const float *cos_alpha;   // [nc]
     const float *hilbert;     // [2nc-1]
+    const float *hilbert_tc;  // tensor-core tap table (hilbert_tc_table), or null
     float *g3, *g4;           // κ-line intermediates [n_views][npsi][nc]
     float4 *gq;               // filtered views as column-major 2x2 sum/difference tap quads [n_views][nc][nr+2] (BP input)
     float *gF;                // optional plain filtered views [n_views][nr][nc] (debug), may be null
@@ -25,6 +27,8 @@ struct FilterParams {
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
 void launch_hilbert(const FilterParams &p, cudaStream_t s);           // K3:  Eq. 12
+size_t hilbert_tc_table_floats(int nc);
+void hilbert_tc_table(int nc, const float *kd, std::vector<float> &out);
 void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s);     // K4:  Eqs. 13-15
 
 // Step 7 backprojection over `n_items`

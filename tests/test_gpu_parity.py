@@ -59,10 +59,17 @@ def test_reconstruct_matches_oracle(name):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("name", ["T1", "T3"])
-def test_filter_stages_match_oracle(name):
+@pytest.mark.parametrize("hilbert", ["tc", "fp32"])
+@pytest.mark.parametrize("name", ["T1", "T3", "C1"])
+def test_filter_stages_match_oracle(name, hilbert, monkeypatch):
+    """Steps 1-6 per stage (g3, g4, gF) against the oracle; K3 both on the tensor
+    cores (3xTF32 GEMM, default) and as the fp32 direct convolution."""
     import torch
     from oracle import oracle
+    if hilbert == "fp32":
+        monkeypatch.setenv("KATS_HILBERT", "fp32")
+    else:
+        monkeypatch.delenv("KATS_HILBERT", raising=False)
     cfg, sino, _, _ = _case(name)
     p = _plan(cfg)
     v0, nv = p.pitch_views(0)
@@ -166,3 +173,19 @@ def test_every_bp_kernel_variant_matches_oracle(variant, kernel, monkeypatch):
     torch.cuda.synchronize()
     assert p.bp_kernel() == kernel
     _check(vol.cpu().numpy(), ref, contrast)
+
+
+@pytest.mark.parametrize("name", ["T2", "T3"])
+def test_pipelined_reconstruct_matches_oracle(name, monkeypatch):
+    """KATS_PIPELINE=1: per-pitch backprojections on two streams behind a
+    high-priority filter stream (forked from and joined to the caller's stream)
+    give the oracle's volume too."""
+    import torch
+    monkeypatch.setenv("KATS_PIPELINE", "1")
+    cfg, sino, ref, contrast = _case(name)
+    p = _plan(cfg)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"], stream=s)
+        host = vol.cpu()          # ordered after the join on the caller's stream
+    _check(host.numpy(), ref, contrast)
