@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __g
     __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
     __shared__ int s_k0, s_k1;
     __shared__ unsigned s_tmem;
+    __shared__ float4 s_vg[kMaxSlots];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = warp == kConsumerWarps;
@@ -723,6 +724,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __g
             for (int n = 0; n < NV; ++n) {
                 if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
                 const unsigned full = full0 + 8u * sl;
+                // the view's geometry record rides with its slot (released by the arrive below)
+                s_vg[sl] = __ldg(reinterpret_cast<const float4 *>(p.view) + (KC0 + n - p.view_lo));
                 mbar_expect_tx(full, box_bytes);
                 tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 0, boxc[n], vbase + n, full);
                 if (++sl == S) { sl = 0; phase ^= 1u; }
@@ -732,6 +735,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __g
     }
 
     // ---- consumer warps ----
+    const unsigned slot0 = stage_sa - kMagicBits * 16u;   // quad row r of slot s, column c: slot0 + s*slot_bytes + c*col_bytes + (kMagicBits + r)*16
     // slice t -> TMEM column t mod Wc of the warp's range (lane = TMEM lane)
     const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * Wc);
     {
@@ -784,9 +788,9 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __g
         const int hi_w = __reduce_max_sync(0xffffffffu, work ? t_hi : -1);
         if (hi_w >= lo_w) {
             float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f;
-            unsigned colbase = (stage_sa + (unsigned)(sl * vq) * 16u - kMagicBits * 16u) ^ p.zero;
+            int ci = 0;                                              // idle lanes read column 0 of the slot
             if (work) {
-                const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+                const float4 vg = s_vg[sl];
                 const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
                 const float u = fmaf(y, vg.x, -x * vg.y);
                 const float inv_v = rcp_approx(vstar);
@@ -808,9 +812,10 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __g
                 const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
                 step = sc * p.dz;
                 base = fmaf(sc, -vg.z, p.row_cc);                   // slice 0 (centred quad-row position)
-                const int ci = min(max(l - boxc[n], 0), BW - 1);
-                colbase = (stage_sa + (unsigned)(sl * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
+                ci = min(max(l - boxc[n], 0), BW - 1);
             }
+            // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
+            const unsigned colbase = (slot0 + (unsigned)sl * p.slot_bytes + (unsigned)ci * p.col_bytes) ^ p.zero;
             // slices open in every working lane: groups inside [lo_full, hi_full] need no mask
             const int lo_full = __reduce_max_sync(0xffffffffu, work ? t_lo : INT_MIN);
             const int hi_full = __reduce_min_sync(0xffffffffu, work ? t_hi : INT_MAX);
@@ -981,6 +986,8 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
         q.nbatch = kMaxSlots;
         while (q.nbatch > 2 && tmem_smem_bytes(q) > 74 * 1024) q.nbatch /= 2;
         q.lg_nbatch = __builtin_ctz((unsigned)q.nbatch);
+        q.slot_bytes = 16u * (unsigned)((p.fp_cols_column * (p.nr + 2) + 7) & ~7);
+        q.col_bytes = 16u * (unsigned)(p.nr + 2);
         const size_t sm = tmem_smem_bytes(q);
         CUtensorMap qmap;
         if (alloc <= 128 && sm <= 200 * 1024 && make_quad_map(p, p.gq_views, &qmap)) {

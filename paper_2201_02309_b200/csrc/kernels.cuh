@@ -65,7 +65,8 @@ struct BPParams {
     int warp_span;            // max live slices of a warp (host, TMEM-window kernel)
     int pad_quads;            // head/tail pad (quads) for the TMEM-window kernel: 7 slices of row travel
     int tmem_cols, tmem_alloc;
-    int lg_nbatch;            // log2(nbatch) (TMEM kernel: slot parity from the view counter)// TMEM columns per warp / allocated per CTA (set by the launcher)
+    int lg_nbatch;            // log2(nbatch) (TMEM kernel: slot parity from the view counter)
+    unsigned slot_bytes, col_bytes;   // TMEM kernel: bytes per ring slot / per quad column in a slot// TMEM columns per warp / allocated per CTA (set by the launcher)
     float *vol;               // [n_items][nz][ny][nx]
 };
 
