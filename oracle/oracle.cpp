@@ -336,6 +336,100 @@ double bp_voxel(const G &o, double x, double y, double z, const double *gF, int6
     return acc * o.dlam / (2.0 * PI);      /* +1/2π (step 7, P:l.157; reading A3) */
 }
 
+/* ---------- Adjoint (NEXT-1): the transpose of the linear map
+ * sinogram -> volume above, written step by step in reverse order.  Pinned by
+ * the dot-product identity <A x, y> = <x, A^T y> against the forward
+ * (tests/test_oracle_adjoint.py), per stage and for the whole layer. */
+
+/* Transpose of sample(): scatter `val` onto the four bilinear taps. */
+inline void sample_T(const G &o, double *gvT, double alpha, double w, double val)
+{
+    int l, m; double fa, fw;
+    if (!lin_index(alpha / o.g.d_alpha + 0.5 * (o.g.n_cols - 1) - o.g.alpha_offset, o.g.n_cols, &l, &fa)) return;
+    if (!lin_index(w / o.g.d_w + 0.5 * (o.g.n_rows - 1), o.g.n_rows, &m, &fw)) return;
+    const int nc = o.g.n_cols;
+    gvT[(size_t)m * nc + l] += (1.0 - fw) * (1.0 - fa) * val;
+    gvT[(size_t)m * nc + l + 1] += (1.0 - fw) * fa * val;
+    gvT[(size_t)(m + 1) * nc + l] += fw * (1.0 - fa) * val;
+    gvT[(size_t)(m + 1) * nc + l + 1] += fw * fa * val;
+}
+
+/* Transpose of bp_voxel() for one voxel: adds y * d f / d gF into gFT. */
+void bp_voxel_T(const G &o, double x, double y_, double z, double yv, double *gFT, int64_t gF0, int64_t gFn)
+{
+    if (!in_fov(o, x, y_)) return;
+    double li, lo;
+    pi_line(o, x, y_, z, &li, &lo);
+    int64_t kf, kl; double wf, wl;
+    bp_weights(o, li, lo, &kf, &kl, &wf, &wl);
+    if (kf < gF0 || kl >= gF0 + gFn) return;
+    const size_t vs = (size_t)o.g.n_rows * o.g.n_cols;
+    for (int64_t k = kf; k <= kl; ++k) {
+        double om = (k == kf) ? wf : (k == kl) ? wl : 1.0;
+        double lam = k * o.dlam;
+        double c = std::cos(lam + o.g.lambda0), s = std::sin(lam + o.g.lambda0);
+        double vstar = o.g.R - x * c - y_ * s;
+        double astar = std::atan((-x * s + y_ * c) / vstar);
+        double wstar = o.g.D * std::cos(astar) / vstar * (z - o.g.z0 - o.h * lam);
+        sample_T(o, gFT + (size_t)(k - gF0) * vs, astar, wstar, yv * om / vstar * o.dlam / (2.0 * PI));
+    }
+}
+
+/* Transpose of filter_view() steps 2-6 for one view: gFT (rows x cols) ->
+ * g1T (rows x cols) = (step 2..6)^T gFT; step 1's stencil is applied by the caller. */
+void filter_view_T(const G &o, const std::vector<double> &Kh, const Rebin &rb, const double *gFT, double *g1T)
+{
+    const int nr = o.g.n_rows, nc = o.g.n_cols, np = o.n_psi;
+    std::vector<double> g4T((size_t)np * nc, 0.0), g3T((size_t)np * nc, 0.0), g2T((size_t)nr * nc, 0.0);
+    /* steps 5-6^T: gF = cos(alpha) lerp_psi(g4) */
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            size_t t = (size_t)m * nc + l;
+            int i = rb.bi[t]; double f = rb.bf[t];
+            if (i < 0) continue;
+            double v = std::cos(alpha_l(o, l)) * gFT[t];
+            g4T[(size_t)i * nc + l] += (1.0 - f) * v;
+            g4T[(size_t)(i + 1) * nc + l] += f * v;
+        }
+    /* step 4^T: g4(l) = sum_l' K[l-l'] g3(l')  =>  g3T(l') = sum_l K[l-l'] g4T(l) */
+    for (int i = 0; i < np; ++i)
+        for (int lp = 0; lp < nc; ++lp) {
+            double acc = 0.0;
+            for (int l = 0; l < nc; ++l) acc += Kh[(size_t)(l - lp + nc - 1)] * g4T[(size_t)i * nc + l];
+            g3T[(size_t)i * nc + lp] = acc;
+        }
+    /* step 3^T: g3 = lerp_w(g2) */
+    for (int i = 0; i < np; ++i)
+        for (int l = 0; l < nc; ++l) {
+            size_t t = (size_t)i * nc + l;
+            int m = rb.fi[t]; double f = rb.ff[t];
+            if (m < 0) continue;
+            g2T[(size_t)m * nc + l] += (1.0 - f) * g3T[t];
+            g2T[(size_t)(m + 1) * nc + l] += f * g3T[t];
+        }
+    /* step 2^T: g2 = D/sqrt(D^2+w^2) g1 */
+    for (int m = 0; m < nr; ++m) {
+        double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + w_m(o, m) * w_m(o, m));
+        for (int l = 0; l < nc; ++l) g1T[(size_t)m * nc + l] = wgt * g2T[(size_t)m * nc + l];
+    }
+}
+
+/* Step 1^T: g1(v) = (g(v+1) - g(v-1))/(2 dlam) + D_alpha g(v)  =>  scatter g1T(v). */
+void deriv_T(const G &o, const double *g1T, int64_t v, double *outT, int64_t s0)
+{
+    const int nr = o.g.n_rows, nc = o.g.n_cols;
+    auto at = [&](int64_t vv, int m, int l) -> double & { return outT[((vv - s0) * nr + m) * (int64_t)nc + l]; };
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            double t = g1T[(size_t)m * nc + l];
+            at(v + 1, m, l) += t / (2.0 * o.dlam);
+            at(v - 1, m, l) -= t / (2.0 * o.dlam);
+            if (l == 0) { at(v, m, 1) += t / o.g.d_alpha; at(v, m, 0) -= t / o.g.d_alpha; }
+            else if (l == nc - 1) { at(v, m, nc - 1) += t / o.g.d_alpha; at(v, m, nc - 2) -= t / o.g.d_alpha; }
+            else { at(v, m, l + 1) += t / (2.0 * o.g.d_alpha); at(v, m, l - 1) -= t / (2.0 * o.g.d_alpha); }
+        }
+}
+
 }  // namespace
 
 extern "C" {
@@ -504,6 +598,65 @@ int ora_reconstruct(const ora_geom *g, const float *sino, int64_t s0, int64_t sn
         std::vector<double> gF((size_t)(nv - 2) * rs);
         ora_filter(g, sino, s0, sn, fv + 1, nv - 2, nullptr, nullptr, nullptr, gF.data());
         ora_backproject(g, k, gF.data(), fv + 1, nv - 2, vol + (size_t)(k - k0) * vs);
+    }
+    return 0;
+}
+
+/* Adjoint of ora_backproject for pitch `pitch`: gFT [gFn][rows][cols] (double)
+ * += BP^T vol.  (Separately pinned by <BP gF, y> = <gF, BP^T y>.) */
+void ora_backproject_T(const ora_geom *g, int32_t pitch, const double *vol, int64_t gF0, int64_t gFn, double *gFT)
+{
+    G o = make(g);
+    const int nx = g->nx, ny = g->ny, nz = g->nz;
+    const size_t vs = (size_t)g->n_rows * g->n_cols;
+    /* voxels scatter into overlapping views: one private copy per thread, summed at the end */
+    #pragma omp parallel
+    {
+        std::vector<double> loc((size_t)gFn * vs, 0.0);
+        #pragma omp for collapse(2) schedule(dynamic, 1)
+        for (int j = 0; j < nz; ++j)
+            for (int iy = 0; iy < ny; ++iy)
+                for (int ix = 0; ix < nx; ++ix)
+                    bp_voxel_T(o, x_i(o, ix), y_i(o, iy), z_j(o, j, pitch), vol[((size_t)j * ny + iy) * nx + ix],
+                               loc.data(), gF0, gFn);
+        #pragma omp critical
+        for (size_t i = 0; i < loc.size(); ++i) gFT[i] += loc[i];
+    }
+}
+
+/* Adjoint of ora_filter (gF output) for views [v_first, v_first + n_out):
+ * sinoT (double, views s0 .. s0+sn-1) += F^T gFT.  Needs v_first-1 >= s0 and
+ * v_first+n_out+1 <= s0+sn. */
+int ora_filter_T(const ora_geom *g, const double *gFT, int64_t v_first, int64_t n_out, int64_t s0, int64_t sn, double *sinoT)
+{
+    G o = make(g);
+    if (v_first - 1 < s0 || v_first + n_out + 1 > s0 + sn) return -1;
+    std::vector<double> K = hilbert_kernel(o);
+    Rebin rb = rebin_maps(o);
+    const size_t rs = (size_t)g->n_rows * g->n_cols;
+    std::vector<double> g1T((size_t)n_out * rs);
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n_out; ++i) filter_view_T(o, K, rb, gFT + i * rs, g1T.data() + i * rs);
+    for (int64_t i = 0; i < n_out; ++i) deriv_T(o, g1T.data() + i * rs, v_first + i, sinoT, s0);
+    return 0;
+}
+
+/* Adjoint of ora_reconstruct: vol [np*nz][ny][nx] (double) -> sinoT (double,
+ * views s0 .. s0+sn-1, overwritten).  For each pitch: BP^T into its slab's
+ * filtered views, then the filter's transpose onto the raw views (P:l.246-262
+ * reversed).  Returns -1 if a slab is not covered. */
+int ora_adjoint(const ora_geom *g, const double *vol, int32_t k0, int32_t np, int64_t s0, int64_t sn, double *sinoT)
+{
+    const size_t vs = (size_t)g->nx * g->ny * g->nz;
+    const size_t rs = (size_t)g->n_rows * g->n_cols;
+    std::memset(sinoT, 0, sizeof(double) * rs * (size_t)sn);
+    for (int32_t k = k0; k < k0 + np; ++k) {
+        int64_t fv, nv;
+        ora_pitch_slab(g, k, &fv, &nv);
+        if (fv < s0 || fv + nv > s0 + sn) return -1;
+        std::vector<double> gFT((size_t)(nv - 2) * rs, 0.0);
+        ora_backproject_T(g, k, vol + (size_t)(k - k0) * vs, fv + 1, nv - 2, gFT.data());
+        ora_filter_T(g, gFT.data(), fv + 1, nv - 2, s0, sn, sinoT);
     }
     return 0;
 }

@@ -68,6 +68,11 @@ def lib():
                                                       _I32, ctypes.c_int64, _D]),
             "ora_reconstruct": (ctypes.c_int, [_G, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                                ctypes.c_int32, _D]),
+            "ora_backproject_T": (None, [_G, ctypes.c_int32, _D, ctypes.c_int64, ctypes.c_int64, _D]),
+            "ora_filter_T": (ctypes.c_int, [_G, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_int64, _D]),
+            "ora_adjoint": (ctypes.c_int, [_G, _D, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                           ctypes.c_int64, _D]),
         }
         for name, (res, args) in sig.items():
             f = getattr(l, name)
@@ -217,3 +222,36 @@ def reconstruct(cfg, sino, s0, k0, n_pitches):
     if rc:
         raise ValueError("oracle reconstruct: sinogram does not cover a requested pitch slab")
     return vol
+
+
+# ---- adjoint (NEXT-1): transposes of the maps above, pinned by dot-product tests ----
+
+def backproject_T(cfg, pitch, vol, gF0, gFn):
+    """BP^T: volume of pitch `pitch` -> filtered-view adjoint [gFn][rows][cols] for views gF0.. ."""
+    vol = np.ascontiguousarray(vol, dtype=np.float64)
+    out = np.zeros((gFn, cfg["n_rows"], cfg["n_cols"]))
+    g = geom(cfg)
+    lib().ora_backproject_T(ctypes.byref(g), pitch, _p(vol, _D), gF0, gFn, _p(out, _D))
+    return out
+
+
+def filter_T(cfg, gFT, v_first, s0, sn):
+    """F^T: filtered-view adjoint for views v_first.. -> raw-view adjoint for views s0..s0+sn-1."""
+    gFT = np.ascontiguousarray(gFT, dtype=np.float64)
+    out = np.zeros((sn, cfg["n_rows"], cfg["n_cols"]))
+    g = geom(cfg)
+    rc = lib().ora_filter_T(ctypes.byref(g), _p(gFT, _D), v_first, gFT.shape[0], s0, sn, _p(out, _D))
+    if rc:
+        raise ValueError("oracle filter_T: output views do not hold the +-1 halo")
+    return out
+
+
+def adjoint(cfg, vol, k0, n_pitches, s0, sn):
+    """A^T of reconstruct(): volume [n_pitches*nz][ny][nx] -> sinogram adjoint [sn][rows][cols]."""
+    vol = np.ascontiguousarray(vol, dtype=np.float64)
+    out = np.empty((sn, cfg["n_rows"], cfg["n_cols"]))
+    g = geom(cfg)
+    rc = lib().ora_adjoint(ctypes.byref(g), _p(vol, _D), k0, n_pitches, s0, sn, _p(out, _D))
+    if rc:
+        raise ValueError("oracle adjoint: sinogram does not cover a requested pitch slab")
+    return out
