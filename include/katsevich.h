@@ -137,6 +137,27 @@ int katsevich_reconstruct_host(katsevich_plan *plan, const float *host_sino, int
                                int32_t first_pitch, int32_t n_pitches, float *host_vol,
                                void *workspace, size_t workspace_bytes, void *cuda_stream);
 
+/* ---- adjoint (NEXT-1: training through the layer) ---- */
+
+/* Workspace for katsevich_adjoint: katsevich_workspace_bytes plus one fp32
+ * detector image per filtered view of the union. */
+int katsevich_adjoint_workspace_bytes(const katsevich_plan *plan, int32_t n_pitches, size_t *bytes);
+
+/* Adjoint (transpose) of katsevich_reconstruct's linear map sinogram -> volume
+ * (the layer the paper trains through, P:l.303).
+ *   vol       [n_pitches*nz][ny][nx] fp32, device (input)
+ *   sino_out  [sn][rows][cols] fp32, device, first view s0 (output, overwritten;
+ *             0 outside the pitches' slabs); must cover views
+ *             k*views_per_turn + bp_lo - 1 .. k*views_per_turn + bp_hi + 1 for
+ *             every requested pitch k (KATS_ERR_COVERAGE otherwise)
+ * Steps in reverse: step 7^T (quad adjoints, per-CTA shared-memory
+ * accumulation + red.global.add), then per view the transposes of steps 6..1.
+ * fp32, summation order not fixed (atomics): results are reproducible to
+ * rounding, not bitwise.  Asynchronous on cuda_stream. */
+int katsevich_adjoint(katsevich_plan *plan, const float *vol, int32_t first_pitch, int32_t n_pitches,
+                      float *sino_out, int64_t s0, int64_t sn, void *workspace, size_t workspace_bytes,
+                      void *cuda_stream);
+
 /* ---- debug / parity entry points ---- */
 
 /* Steps 1-6 (Eqs. 8-15) for views [out_first_view, out_first_view + n_out):

@@ -3,5 +3,6 @@
 """
 from ._lib import LIB_PATH, KatsevichError, KatsevichGeometry, lib  # noqa: F401
 from .plan import STAGES, Plan, geometry_from_config  # noqa: F401
+from . import autograd  # noqa: F401
 
-__all__ = ["Plan", "geometry_from_config", "KatsevichError", "KatsevichGeometry", "lib", "LIB_PATH", "STAGES"]
+__all__ = ["Plan", "geometry_from_config", "KatsevichError", "KatsevichGeometry", "lib", "LIB_PATH", "STAGES", "autograd"]

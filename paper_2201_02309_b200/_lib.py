@@ -62,6 +62,8 @@ SIGNATURES = {
     "katsevich_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
     "katsevich_profile_read": (ctypes.c_int, [_P, ctypes.POINTER(KatsevichStats), ctypes.c_int]),
     "katsevich_bp_kernel": (ctypes.c_int, [_P]),
+    "katsevich_adjoint_workspace_bytes": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_SZ)]),
+    "katsevich_adjoint": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _I64, _I64, _P, _SZ, _P]),
     "katsevich_destroy": (None, [_P]),
     "katsevich_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "katsevich_last_error_detail": (ctypes.c_char_p, [_P]),

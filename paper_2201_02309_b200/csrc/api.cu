@@ -126,6 +126,7 @@ FilterParams filter_params(const katsevich_plan *p)
     f.inv_2dalpha = (float)(1.0 / (2.0 * p->g.d_alpha));
     f.wlen = p->d.wlen; f.fr = p->d.fr; f.br = p->d.br;
     f.cos_alpha = p->d.cos_alpha; f.hilbert = p->d.hilbert; f.hilbert_tc = p->d.hilbert_tc;
+    f.sign = 1.f;
     return f;
 }
 
@@ -346,6 +347,15 @@ int katsevich_workspace_bytes_host(const katsevich_plan *p, int32_t n_pitches, s
     return KATS_OK;
 }
 
+int katsevich_adjoint_workspace_bytes(const katsevich_plan *p, int32_t n_pitches, size_t *bytes)
+{
+    int rc = katsevich_workspace_bytes(p, n_pitches, bytes);
+    if (rc) return rc;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    *bytes += align_up(sizeof(float) * rs * (size_t)n_union_views(p, n_pitches));      // g1^T of every view
+    return KATS_OK;
+}
+
 // two low-priority streams for per-pitch backprojections and one highest-priority stream for
 // the filter chunks that must finish before the next pitch's backprojection can start
 static int ensure_bp_streams(katsevich_plan *p)
@@ -463,6 +473,76 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     }
     for (int k = std::max(0, n_pitches - 2); k < n_pitches; ++k)       // join
         KCHECK(p, cudaStreamWaitEvent(s, (cudaEvent_t)p->sync_events[k], 0));
+    return KATS_OK;
+}
+
+// Adjoint of katsevich_reconstruct (NEXT-1): vol [n_pitches*nz][ny][nx] -> sino_out [sn][rows][cols]
+// (overwritten; views outside the pitches' slabs are 0).  Step 7^T into quad adjoints over the
+// union of filtered views, then steps 6..1 transposed per 256-view chunk, then the view/α
+// difference stencils transposed onto the raw views.
+int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, int32_t n_pitches,
+                      float *sino_out, int64_t s0, int64_t sn, void *workspace, size_t workspace_bytes,
+                      void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!vol || !sino_out || !workspace) return KATS_ERR_NULL;
+    if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
+    size_t need;
+    katsevich_adjoint_workspace_bytes(p, n_pitches, &need);
+    if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
+    const int vt = p->g.views_per_turn;
+    const HostTables &t = p->t;
+    const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;
+    const int64_t nu = n_union_views(p, n_pitches);
+    if (u0 - 1 < s0 || u0 + nu + 1 > s0 + sn) {
+        p->detail = "output sinogram views do not cover the pitches' slabs";
+        return KATS_ERR_COVERAGE;
+    }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t qs = quad_view_elems(p);
+    float4 *qT = (float4 *)workspace;
+    const size_t qbytes = align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches));
+    float *scratch = (float *)((char *)workspace + qbytes);
+    float *g1T = (float *)((char *)workspace + qbytes + align_up(filter_chunk_bytes(p)));
+    KCHECK(p, cudaMemsetAsync(qT, 0, sizeof(float4) * qs * (size_t)nu, s));
+    KCHECK(p, cudaMemsetAsync(sino_out, 0, sizeof(float) * rs * (size_t)sn, s));
+    BPParams b = bp_params(p);
+    b.gqT = qT;
+    b.gq_views = nu;
+    b.off0 = (int64_t)first_pitch * vt - u0;
+    b.item_views = vt;
+    b.n_items = n_pitches;
+    b.vol = const_cast<float *>(vol);
+    {
+        LaunchScope ls(p, ST_K5, s);
+        if (launch_backproject_adjoint(b, s) != 0) {
+            p->detail = "adjoint backprojection: plan not supported (non-monotone PI windows)";
+            return KATS_ERR_ARGUMENT;
+        }
+    }
+    KCHECK(p, cudaGetLastError());
+    FilterParams f = filter_params(p);
+    const size_t ps = (size_t)t.n_psi * p->g.n_cols;
+    for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
+        const int nv = (int)std::min<int64_t>(kFilterChunk, nu - v0);
+        f.n_views = nv;
+        f.g4 = scratch + (size_t)kFilterChunk * ps;                // g4^T
+        f.g3 = scratch;                                            // g3^T
+        { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos_T(f, qT + v0 * qs, s); }
+        KCHECK(p, cudaGetLastError());
+        FilterParams h = f;                                        // K3^T = -K3: reads g4^T, writes g3^T
+        h.g3 = f.g4;
+        h.g4 = f.g3;
+        h.sign = -1.f;
+        { LaunchScope ls(p, ST_K3, s); launch_hilbert(h, s); }
+        KCHECK(p, cudaGetLastError());
+        { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
+        KCHECK(p, cudaGetLastError());
+    }
+    { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nu, sino_out + (u0 - 1 - s0) * rs, s); }
+    KCHECK(p, cudaGetLastError());
     return KATS_OK;
 }
 

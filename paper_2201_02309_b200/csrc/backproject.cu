@@ -377,7 +377,8 @@ __device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, floa
 // is shared by every active slice (~40 at C3/C4).
 // ---------------------------------------------------------------------------
 template <bool POLY, int W>
-__global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(BPParams p, const __grid_constant__ CUtensorMap qmap)
+// (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
+__global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch;
@@ -652,7 +653,8 @@ size_t tmem_smem_bytes(const BPParams &p)
 }
 
 template <bool POLY>
-__global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(BPParams p, const __grid_constant__ CUtensorMap qmap)
+// (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
+__global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant__ CUtensorMap qmap, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch, Wc = p.tmem_cols;
@@ -891,6 +893,205 @@ __global__ void k_make_quads(const float *gF, float4 *q, int64_t n, int nr, int 
     q[i] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0, c1 - a1);
 }
 
+// ---------------------------------------------------------------------------
+// Adjoint of step 7 (NEXT-1).  The forward reads, per interior
+// update, one quad Q = (s'0, s'1, d0, d1) of column l at quad row r and adds
+//   w0 (s'0 + P d0) + w1 (s'1 + P d1)         (times scale at the end),
+// so its transpose adds  y scale (w0, w1, w0 P, w1 P)  to that quad of the
+// quad-adjoint buffer gqT [views][nc][nr+2] (float4, same layout as gq).
+// Same tiles, PI windows, geometry, box planning and quad selection as the
+// forward kernels; per view, a CTA accumulates its box (the footprint the
+// forward TMA-loads) in shared memory with atomics and reduce-adds it into
+// gqT (red.global.add.v4.f32).  End views (fractional weights, checked
+// samples) are scattered per voxel by k_bp_adjoint_ends.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_add4(float4 *dst, float a, float b, float c, float d)
+{
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+template <bool POLY, bool CHECK>
+__global__ void __launch_bounds__(TX *TY) k_bp_adjoint(BPParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];   // one symbol per TU: keep the TMA kernels' alignment
+    const int BW = p.fp_cols_column, NQ = p.nr + 2, nbox = BW * NQ;
+    float4 *box = reinterpret_cast<float4 *>(smem);
+    int *boxc = reinterpret_cast<int *>(smem + (size_t)nbox * 16);
+    __shared__ int s_k0, s_k1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
+    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int item = blockIdx.z;
+    const bool inside = ix < p.nx && iy < p.ny;
+    const size_t plane = (size_t)p.nx * p.ny;
+    const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const int2 *pik = p.pi_k + col;
+    if (tid == 0) { s_k0 = INT_MAX; s_k1 = INT_MIN; }
+    for (int i = tid; i < nbox; i += TX * TY) box[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    int K0 = INT_MAX, K1 = INT_MIN;
+    if (inside) {
+        const int2 e0 = pik[0];
+        if (e0.x <= e0.y) { K0 = e0.x + 1; K1 = pik[(size_t)(p.nz - 1) * plane].y - 1; }
+    }
+    int wk0 = K0, wk1 = K1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wk0 = min(wk0, __shfl_xor_sync(0xffffffffu, wk0, o));
+        wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
+    }
+    if (lane == 0) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    __syncthreads();
+    const int KC0 = s_k0, NV = s_k1 - s_k0 + 1;
+    {
+        const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
+        for (int n = tid; n < NV; n += TX * TY) boxc[n] = plan_col<POLY>(p, KC0 + n, xa, ya);
+    }
+    __syncthreads();
+    const float *yv = p.vol + (size_t)item * p.nz * plane + col;
+    float4 *qT = p.gqT + (p.off0 + (int64_t)item * p.item_views) * (p.viewbytes / 16);
+    const bool active_col = inside && K0 <= K1;
+    int t_lo = 0, t_hi = -1;
+    int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
+    for (int n = 0; n < NV; ++n) {
+        const int k = KC0 + n;
+        if (active_col) {
+            while (k >= next_open) {
+                ++t_hi;
+                if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+                next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
+            }
+            while (k >= next_close) {
+                ++t_lo;
+                next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
+            }
+        }
+        if (active_col && t_hi >= t_lo && k <= K1) {
+            const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+            const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+            const float u = fmaf(y, vg.x, -x * vg.y);
+            const float inv_v = rcp_approx(vstar);
+            float colpos;
+            if (POLY) {
+                const float tt = u * inv_v, q = tt * tt;
+                float a = p.at[6];
+                a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+                a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+                colpos = fmaf(tt, a, p.col_c);
+            } else {
+                colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+            }
+            const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
+            const int l = __float2int_rz(cp);
+            const float fa = cp - __int2float_rn(l);
+            const float w1 = fa * inv_v, w0 = inv_v - w1;
+            const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+            const float step = sc * p.dz;
+            const float base = fmaf(sc, -vg.z, p.row_cc);
+            if (CHECK) {
+                // footprints may leave the detector: per-sample range tests (reading A9), direct scatter
+                if (colpos >= 0.f && colpos <= p.colmax) {
+                    float4 *qc = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)l * NQ;
+                    for (int t = t_lo; t <= t_hi; ++t) {
+                        const float P = fmaf((float)t, step, base);
+                        if (!(P >= p.pm_lo && P <= p.pm_hi)) continue;
+                        const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
+                        const float yy = yv[(size_t)t * plane] * p.scale;
+                        const float a0 = w0 * yy, a1 = w1 * yy;
+                        red_add4(qc + r, a0, a1, a0 * P, a1 * P);
+                    }
+                }
+            } else {
+                const int ci = min(max(l - boxc[n], 0), BW - 1);
+                float *bc = reinterpret_cast<float *>(box + ci * NQ);
+                for (int t = t_lo; t <= t_hi; ++t) {
+                    const float P = fmaf((float)t, step, base);
+                    const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
+                    const float yy = yv[(size_t)t * plane] * p.scale;
+                    const float a0 = w0 * yy, a1 = w1 * yy;
+                    float *d = bc + 4 * r;
+                    atomicAdd(d, a0);
+                    atomicAdd(d + 1, a1);
+                    atomicAdd(d + 2, a0 * P);
+                    atomicAdd(d + 3, a1 * P);
+                }
+            }
+        }
+        if (CHECK) continue;
+        __syncthreads();
+        float4 *dst = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)boxc[n] * NQ;
+        for (int i = tid; i < nbox; i += TX * TY) {
+            const float4 v = box[i];
+            if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) {
+                red_add4(dst + i, v.x, v.y, v.z, v.w);
+                box[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// end views of every voxel: checked samples with the fractional weights (reading A9)
+template <bool POLY>
+__global__ void k_bp_adjoint_ends(BPParams p)
+{
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x, iy = blockIdx.y, t = blockIdx.z % p.nz;
+    const int item = blockIdx.z / p.nz;
+    if (ix >= p.nx) return;
+    const size_t plane = (size_t)p.nx * p.ny;
+    const size_t col = (size_t)iy * p.nx + ix;
+    const int2 e0 = p.pi_k[col];
+    if (!(e0.x <= e0.y)) return;                                   // outside U: the forward writes 0
+    const int2 e = p.pi_k[(size_t)t * plane + col];
+    const float2 w = p.pi_w[(size_t)t * plane + col];
+    const float yy = p.vol[((size_t)item * p.nz + t) * plane + col] * p.scale;
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    const u64 qbase = reinterpret_cast<u64>(p.gqT) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
+#pragma unroll
+    for (int end = 0; end < 2; ++end) {
+        const int k = end ? e.y : e.x;
+        const float weight = end ? w.y : w.x;
+        const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+        const ViewSetup s = view_setup<POLY>(p, qbase + (u64)((int64_t)k * p.viewbytes), vg, x, y, 0.f);
+        if (!(s.colpos >= 0.f && s.colpos <= p.colmax)) continue;
+        const float pm = fmaf((float)t, s.step, s.base);
+        if (!(pm >= p.pm_lo && pm <= p.pm_hi)) continue;
+        float w0, w1;
+        upk(s.W, w0, w1);
+        const float g = yy * weight;
+        const float q = pm + s.qmagic;
+        float4 *dst = reinterpret_cast<float4 *>(s.colbase + ((u64)__float_as_uint(q) << 4));
+        red_add4(dst, w0 * g, w1 * g, w0 * g * pm, w1 * g * pm);
+    }
+}
+
+int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
+{
+    const size_t sm = (size_t)p.fp_cols_column * (p.nr + 2) * 16 + sizeof(int) * (size_t)p.max_cta_views;
+    if (!p.windows_monotone || sm > 200 * 1024) return -1;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bp_adjoint<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_adjoint<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_adjoint<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_adjoint<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
+    if (p.checked) {
+        if (p.poly) k_bp_adjoint<true, true><<<grid, TX * TY, sm, s>>>(p);
+        else k_bp_adjoint<false, true><<<grid, TX * TY, sm, s>>>(p);
+    } else {
+        if (p.poly) k_bp_adjoint<true, false><<<grid, TX * TY, sm, s>>>(p);
+        else k_bp_adjoint<false, false><<<grid, TX * TY, sm, s>>>(p);
+    }
+    dim3 ge((p.nx + 127) / 128, p.ny, p.nz * p.n_items);
+    if (p.poly) k_bp_adjoint_ends<true><<<ge, 128, 0, s>>>(p);
+    else k_bp_adjoint_ends<false><<<ge, 128, 0, s>>>(p);
+    return 0;
+}
+
 void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cudaStream_t s)
 {
     const int64_t total = n * (nr + 2) * nc;
@@ -912,7 +1113,7 @@ void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const CUtensorM
         cudaFuncSetAttribute(k_bp_tmem<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_bp_tmem<POLY><<<grid, kWsThreads, sm, s>>>(q, qmap);
+    k_bp_tmem<POLY><<<grid, kWsThreads, sm, s>>>(qmap, q);
 }
 
 template <int W>
@@ -924,8 +1125,8 @@ void launch_window(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &q
         cudaFuncSetAttribute(k_bp_window<false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    if (q.poly) k_bp_window<true, W><<<grid, kWsThreads, sm, s>>>(q, qmap);
-    else k_bp_window<false, W><<<grid, kWsThreads, sm, s>>>(q, qmap);
+    if (q.poly) k_bp_window<true, W><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    else k_bp_window<false, W><<<grid, kWsThreads, sm, s>>>(qmap, q);
 }
 
 namespace {

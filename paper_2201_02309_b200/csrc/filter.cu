@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_hilbert(FilterParams p, int64_t n_lines
     float *dst = p.g4 + (line0 + li) * nc;
 #pragma unroll
     for (int j = 0; j < HR; ++j)
-        if (l0 + 2 * j < nc) dst[l0 + 2 * j] = acc[j];
+        if (l0 + 2 * j < nc) dst[l0 + 2 * j] = p.sign * acc[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
         if (line < n_lines) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-                if (c + i < nout) dst[2 * (c + i)] = v[i];
+                if (c + i < nout) dst[2 * (c + i)] = p.sign * v[i];
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t 
         const int l = 2 * c + lane;
         for (int r = 0; r < 32; ++r) {
             const int64_t line = line0 + warp * 32 + r;
-            if (line < n_lines && l < nc) p.g4[line * nc + l] = stg[r * 33 + lane];
+            if (line < n_lines && l < nc) p.g4[line * nc + l] = p.sign * stg[r * 33 + lane];
         }
         __syncwarp();
     }
@@ -547,6 +547,97 @@ void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
         attr_set = true;
     }
     k_bwd_rebin_cos<<<grid, 256, smem, s>>>(p);
+}
+
+// ---------------------------------------------------------------------------
+// Adjoint of steps 1-6 (NEXT-1); DESIGN.md §5.  Per view:
+//   quad adjoint -> gF^T (transpose of the quad construction of K4, gathered)
+//   -> K4^T: g4^T = scatter over ψ of cos α · gF^T           (k_bwd_rebin_cos_T)
+//   -> K3^T = -K3 (the kernel is odd: K[-d] = -K[d])          (launch_hilbert, sign -1)
+//   -> K2^T with the length weight: g1^T = wlen · scatter over w of g3^T  (k_fwd_rebin_T)
+//   -> K1^T: transposed view/α difference stencils (gathered, k_deriv_T).
+// A thread owns one detector column of a view in the scatters, so no atomics.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_bwd_rebin_cos_T(FilterParams p, const float4 *__restrict__ qT)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
+    if (l >= p.nc) return;
+    const int nc = p.nc, nr = p.nr, nq = nr + 2, c = (nr + 2) / 2;
+    float *g4T = p.g4 + (size_t)v * p.npsi * nc + l;
+    for (int i = 0; i < p.npsi; ++i) g4T[(size_t)i * nc] = 0.f;
+    const float4 *qa = qT + ((size_t)v * nc + l) * nq;           // column l: its taps are quad x, z
+    const float4 *qb = l > 0 ? qa - nq : nullptr;                // column l-1: this column is its y, w
+    const float ca = __ldg(p.cos_alpha + l);
+    for (int m = 0; m < nr; ++m) {
+        // quad r = m + 2 has row m as its lower tap, quad r = m + 1 as its upper tap
+        const float rh = (float)(m + 2 - c), rl = (float)(m + 1 - c);
+        const float4 A = qa[m + 2], B = qa[m + 1];
+        float gt = 0.5f * A.x - (A.z - rh * A.x) + 0.5f * B.x + (B.z - rl * B.x);
+        if (qb) {
+            const float4 C = qb[m + 2], D = qb[m + 1];
+            gt += 0.5f * C.y - (C.w - rh * C.y) + 0.5f * D.y + (D.w - rl * D.y);
+        }
+        const RebinEntry e = p.br[m * nc + l];
+        if (e.idx < 0) continue;
+        const float val = ca * gt;
+        g4T[(size_t)e.idx * nc] += (1.f - e.frac) * val;
+        g4T[(size_t)(e.idx + 1) * nc] += e.frac * val;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_fwd_rebin_T(FilterParams p, float *__restrict__ g1T)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
+    if (l >= p.nc) return;
+    const int nc = p.nc;
+    float *o = g1T + (size_t)v * p.nr * nc + l;
+    for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] = 0.f;
+    const float *g3T = p.g3 + (size_t)v * p.npsi * nc + l;
+    for (int i = 0; i < p.npsi; ++i) {
+        const RebinEntry e = p.fr[i * nc + l];
+        if (e.idx < 0) continue;
+        const float t = g3T[(size_t)i * nc];
+        o[(size_t)e.idx * nc] += (1.f - e.frac) * t;
+        o[(size_t)(e.idx + 1) * nc] += e.frac * t;
+    }
+    for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] *= __ldg(p.wlen + m);
+}
+
+// raw view v (absolute u0 - 1 .. u0 + nu) <- g1^T of filtered views v-1, v, v+1 (those in [u0, u0+nu))
+__global__ void __launch_bounds__(128) k_deriv_T(FilterParams p, const float *__restrict__ g1T, int64_t nu,
+                                                 float *__restrict__ out)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x, m = blockIdx.y;
+    const int64_t vr = blockIdx.z;                                // raw view - (u0 - 1)
+    if (l >= p.nc) return;
+    const int nc = p.nc;
+    const size_t rs = (size_t)p.nr * nc;
+    auto g = [&](int64_t f, int ll) -> float {                    // g1^T of filtered view f (relative to u0)
+        return (f >= 0 && f < nu) ? g1T[(size_t)f * rs + (size_t)m * nc + ll] : 0.f;
+    };
+    const int64_t f = vr - 1;                                     // this raw view as a filtered view
+    float acc = (g(f - 1, l) - g(f + 1, l)) * p.inv_2dlam;        // view stencil (g(v+1) - g(v-1)) / 2Δλ
+    // α stencil of the same view: centred inside, one-sided at both edges
+    if (l == 0) acc -= g(f, 0) * p.inv_dalpha;
+    if (l == nc - 1) acc += g(f, nc - 1) * p.inv_dalpha;
+    if (l >= 1) acc += g(f, l - 1) * (l - 1 == 0 ? p.inv_dalpha : p.inv_2dalpha);
+    if (l + 1 <= nc - 1) acc -= g(f, l + 1) * (l + 1 == nc - 1 ? p.inv_dalpha : p.inv_2dalpha);
+    out[(size_t)vr * rs + (size_t)m * nc + l] = acc;
+}
+
+void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s)
+{
+    k_bwd_rebin_cos_T<<<dim3((p.nc + 127) / 128, p.n_views), 128, 0, s>>>(p, qT);
+}
+
+void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s)
+{
+    k_fwd_rebin_T<<<dim3((p.nc + 127) / 128, p.n_views), 128, 0, s>>>(p, g1T);
+}
+
+void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s)
+{
+    k_deriv_T<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)(nu + 2)), 128, 0, s>>>(p, g1T, nu, out);
 }
 
 }  // namespace kats

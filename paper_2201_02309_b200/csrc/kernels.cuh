@@ -23,6 +23,7 @@ struct FilterParams {
     float *g3, *g4;           // κ-line intermediates [n_views][npsi][nc]
     float4 *gq;               // filtered views as column-major 2x2 sum/difference tap quads [n_views][nc][nr+2] (BP input)
     float *gF;                // optional plain filtered views [n_views][nr][nc] (debug), may be null
+    float sign;               // K3 output sign: +1 forward, -1 for the adjoint (odd kernel)
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
@@ -30,6 +31,10 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s);           // K3:  Eq
 size_t hilbert_tc_table_floats(int nc);
 void hilbert_tc_table(int nc, const float *kd, std::vector<float> &out);
 void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s);     // K4:  Eqs. 13-15
+// adjoint (NEXT-1)
+void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s);   // quad^T + K4^T
+void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s);            // K2^T + length weight
+void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s);  // K1^T
 
 // Step 7 backprojection over `n_items`
 // independent pitches/slabs sharing the periodic tables.
@@ -67,10 +72,12 @@ struct BPParams {
     int tmem_cols, tmem_alloc;
     int lg_nbatch;            // log2(nbatch) (TMEM kernel: slot parity from the view counter)
     unsigned slot_bytes, col_bytes;   // TMEM kernel: bytes per ring slot / per quad column in a slot// TMEM columns per warp / allocated per CTA (set by the launcher)
-    float *vol;               // [n_items][nz][ny][nx]
+    float *vol;               // [n_items][nz][ny][nx] (adjoint: the input)
+    float4 *gqT;              // adjoint: quad-adjoint output, layout of gq (accumulated)
 };
 
 int launch_backproject(const BPParams &p, cudaStream_t s);            // K5; returns the KATS_BP_* variant
+int launch_backproject_adjoint(const BPParams &p, cudaStream_t s);    // K5^T into p.gqT (-1: plan unsupported)
 void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cudaStream_t s);
 
 }  // namespace kats

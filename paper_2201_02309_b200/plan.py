@@ -170,6 +170,26 @@ class Plan:
                                                      _stream_handle(stream)))
         return out_host
 
+    def adjoint_workspace_bytes(self, n_pitches: int = 1) -> int:
+        b = ctypes.c_size_t()
+        self._check(lib().katsevich_adjoint_workspace_bytes(self._h, n_pitches, ctypes.byref(b)))
+        return b.value
+
+    def adjoint(self, vol, sino_first_view: int, n_views: int, first_pitch: int = 0, n_pitches: int = 1,
+                out=None, stream=None):
+        """Transpose of reconstruct() (katsevich_adjoint): vol, a cuda float32 tensor
+        [n_pitches*nz][ny][nx] -> sinogram adjoint [n_views][rows][cols] for views
+        from sino_first_view (0 outside the pitches' slabs)."""
+        import torch
+        assert vol.is_cuda and vol.dtype == torch.float32 and vol.is_contiguous()
+        g = self.geometry
+        if out is None:
+            out = torch.empty((n_views, g.n_rows, g.n_cols), dtype=torch.float32, device=vol.device)
+        ws = self._workspace(self.adjoint_workspace_bytes(n_pitches))
+        self._check(lib().katsevich_adjoint(self._h, _ptr(vol), first_pitch, n_pitches, _ptr(out), sino_first_view,
+                                            n_views, _ptr(ws), ws.numel(), _stream_handle(stream)))
+        return out
+
     def filter(self, sino, sino_first_view: int, out_first_view: int, n_out: int, stages=("gF",), stream=None):
         import torch
         g = self.geometry
