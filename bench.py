@@ -263,6 +263,32 @@ def run_ours(args):
         iso = {"k5_ms_per_launch": st_iso["ms"][k] / max(1, st_iso["launches"][k]),
                "launches": st_iso["launches"][k] // n_iso}
 
+    # ---- adjoint (NEXT-1): the transpose of the same step, volume -> sinogram, device-resident ----
+    adj = None
+    if not batch and not args.no_adjoint:
+        vol_y = torch.randn(out.shape, device=dev, generator=torch.Generator(device=dev).manual_seed(11))
+        sino_t = torch.empty((host_in.shape[0],) + tuple(host_in.shape[1:]), dtype=torch.float32, device=dev)
+        for _ in range(args.warmup):
+            plan.adjoint(vol_y, v0, sino_t.shape[0], first_pitch, pitches, out=sino_t, stream=stream)
+        torch.cuda.synchronize()
+        plan.profile_read(reset=True)
+        plan.profile_enable(True)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            plan.adjoint(vol_y, v0, sino_t.shape[0], first_pitch, pitches, out=sino_t, stream=stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        st_adj = plan.profile_read(reset=True)
+        plan.profile_enable(False)
+        adj_ms = a0.elapsed_time(a1) / args.steps
+        if world > 1:
+            t = torch.tensor([adj_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            adj_ms = float(t.item())
+        adj = {"ms_per_step": adj_ms, "k5T_ms_per_step": st_adj["ms"]["K5_backproject"] / args.steps}
+        del vol_y, sino_t
+
     # ---- e2e: host (pinned) in -> host out through katsevich_reconstruct_host ----
     e2e = None
     if not batch:
@@ -352,6 +378,11 @@ def run_ours(args):
                          "frac": U_rank * bp_smem_bytes_per_update() / (iso["k5_ms_per_launch"] * 1e-3) / 1e9 / smem_peak}},
         "clocks": clk,
     }
+    if adj:
+        line["adjoint"] = {"metric": "voxel-view updates/s (transpose: volume -> sinogram)",
+                           "value": U_all / (adj["ms_per_step"] * 1e-3), "unit": "updates/s",
+                           "ms_per_step": adj["ms_per_step"], "k5T_ms_per_step": adj["k5T_ms_per_step"],
+                           "note": "katsevich_adjoint over the same pitches, inputs resident, CUDA events"}
     if e2e:
         line["e2e"] = {"value": U_all / (e2e["ms_per_step"] * 1e-3), "unit": "updates/s",
                        "ms_per_step": e2e["ms_per_step"],
@@ -450,6 +481,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-adjoint", action="store_true", help="skip the adjoint (NEXT-1) measurement")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -910,14 +910,34 @@ __device__ __forceinline__ void red_add4(float4 *dst, float a, float b, float c,
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
-template <bool POLY, bool CHECK>
-__global__ void __launch_bounds__(TX *TY) k_bp_adjoint(BPParams p)
+// Interior views, plans whose footprints stay on the detector.  Same lanes,
+// windows and geometry as the forward kernels; per view the CTA accumulates its
+// footprint box (the box the forward TMA-loads) in shared memory, then
+// reduce-adds it into gqT (red.global.add.v4.f32).
+//  * sm_100a has no native shared-memory float add (atomicAdd is a CAS loop, a
+//    chain of shared-memory round trips); 32-bit integer ATOMS.ADD is native
+//    and fire-and-forget.  So the box holds fixed-point int32 sums with one
+//    scale per CTA and view for the (w0, w1) components and one for the
+//    (w0 P, w1 P) components: S = 2^21 / B, B = the view's largest single
+//    contribution bound over the CTA (column max |y| x 1/v*, x max |P| of the
+//    window ends).  Float -> int is one FFMA against 1.5 * 2^23 (exact
+//    round-to-nearest for |v| < 2^22); sums of up to 2^10 contributions fit.
+//    Rounding error per contribution <= 2^-22 B.
+//  * Lanes of a warp that share a detector column would hit the same quad at
+//    the same step; a lane therefore walks its window in a rotated order
+//    (starting 3 x lane slices in), so ATOMS rarely serialize.
+//  * y (scaled) is staged once in shared memory, column-major with an odd
+//    stride, so the rotated slice reads are conflict-free.
+template <bool POLY>
+__global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];   // one symbol per TU: keep the TMA kernels' alignment
-    const int BW = p.fp_cols_column, NQ = p.nr + 2, nbox = BW * NQ;
-    float4 *box = reinterpret_cast<float4 *>(smem);
-    int *boxc = reinterpret_cast<int *>(smem + (size_t)nbox * 16);
+    const int BW = p.fp_cols_column, NQ = p.nr + 2, nbox = BW * NQ, nzp = p.nz | 1;
+    int *pl = reinterpret_cast<int *>(smem);                           // [4][nbox] fixed-point quad components
+    float *ys = reinterpret_cast<float *>(pl + 4 * nbox);              // [TX*TY][nzp] scale * y
+    int *boxc = reinterpret_cast<int *>(ys + TX * TY * nzp);
     __shared__ int s_k0, s_k1;
+    __shared__ unsigned s_b[2];                                        // view bounds (float bits, >= 0)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
     const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
@@ -926,8 +946,18 @@ __global__ void __launch_bounds__(TX *TY) k_bp_adjoint(BPParams p)
     const size_t plane = (size_t)p.nx * p.ny;
     const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
     const int2 *pik = p.pi_k + col;
-    if (tid == 0) { s_k0 = INT_MAX; s_k1 = INT_MIN; }
-    for (int i = tid; i < nbox; i += TX * TY) box[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid == 0) { s_k0 = INT_MAX; s_k1 = INT_MIN; s_b[0] = 0u; s_b[1] = 0u; }
+    for (int i = tid; i < 4 * nbox; i += TX * TY) pl[i] = 0;
+    float ycmax = 0.f;                                                 // this column's max |scale * y|
+    {
+        const float *yv = p.vol + (size_t)item * p.nz * plane + col;
+        float *yc = ys + tid * nzp;
+        for (int t = 0; t < p.nz; ++t) {
+            const float v = inside ? yv[(size_t)t * plane] * p.scale : 0.f;
+            yc[t] = v;
+            ycmax = fmaxf(ycmax, fabsf(v));
+        }
+    }
     __syncthreads();
     int K0 = INT_MAX, K1 = INT_MIN;
     if (inside) {
@@ -949,11 +979,11 @@ __global__ void __launch_bounds__(TX *TY) k_bp_adjoint(BPParams p)
         for (int n = tid; n < NV; n += TX * TY) boxc[n] = plan_col<POLY>(p, KC0 + n, xa, ya);
     }
     __syncthreads();
-    const float *yv = p.vol + (size_t)item * p.nz * plane + col;
     float4 *qT = p.gqT + (p.off0 + (int64_t)item * p.item_views) * (p.viewbytes / 16);
     const bool active_col = inside && K0 <= K1;
     int t_lo = 0, t_hi = -1;
     int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
+    const float *yc = ys + tid * nzp;
     for (int n = 0; n < NV; ++n) {
         const int k = KC0 + n;
         if (active_col) {
@@ -967,7 +997,10 @@ __global__ void __launch_bounds__(TX *TY) k_bp_adjoint(BPParams p)
                 next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
             }
         }
-        if (active_col && t_hi >= t_lo && k <= K1) {
+        const bool work = active_col && t_hi >= t_lo && k <= K1;
+        float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f, b01 = 0.f, b23 = 0.f;
+        int ci = 0;
+        if (work) {
             const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
             const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
             const float u = fmaf(y, vg.x, -x * vg.y);
@@ -985,50 +1018,113 @@ __global__ void __launch_bounds__(TX *TY) k_bp_adjoint(BPParams p)
             const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
             const int l = __float2int_rz(cp);
             const float fa = cp - __int2float_rn(l);
-            const float w1 = fa * inv_v, w0 = inv_v - w1;
+            w1 = fa * inv_v;
+            w0 = inv_v - w1;
             const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
-            const float step = sc * p.dz;
-            const float base = fmaf(sc, -vg.z, p.row_cc);
-            if (CHECK) {
-                // footprints may leave the detector: per-sample range tests (reading A9), direct scatter
-                if (colpos >= 0.f && colpos <= p.colmax) {
-                    float4 *qc = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)l * NQ;
-                    for (int t = t_lo; t <= t_hi; ++t) {
-                        const float P = fmaf((float)t, step, base);
-                        if (!(P >= p.pm_lo && P <= p.pm_hi)) continue;
-                        const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
-                        const float yy = yv[(size_t)t * plane] * p.scale;
-                        const float a0 = w0 * yy, a1 = w1 * yy;
-                        red_add4(qc + r, a0, a1, a0 * P, a1 * P);
-                    }
-                }
-            } else {
-                const int ci = min(max(l - boxc[n], 0), BW - 1);
-                float *bc = reinterpret_cast<float *>(box + ci * NQ);
-                for (int t = t_lo; t <= t_hi; ++t) {
-                    const float P = fmaf((float)t, step, base);
-                    const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
-                    const float yy = yv[(size_t)t * plane] * p.scale;
-                    const float a0 = w0 * yy, a1 = w1 * yy;
-                    float *d = bc + 4 * r;
-                    atomicAdd(d, a0);
-                    atomicAdd(d + 1, a1);
-                    atomicAdd(d + 2, a0 * P);
-                    atomicAdd(d + 3, a1 * P);
-                }
+            step = sc * p.dz;
+            base = fmaf(sc, -vg.z, p.row_cc);
+            ci = min(max(l - boxc[n], 0), BW - 1);
+            b01 = ycmax * inv_v * 1.0001f;
+            const float pm = fmaxf(fabsf(fmaf((float)t_lo, step, base)), fabsf(fmaf((float)t_hi, step, base)));
+            b23 = b01 * pm * 1.0001f;
+        }
+        const unsigned r01 = __reduce_max_sync(0xffffffffu, __float_as_uint(b01));
+        const unsigned r23 = __reduce_max_sync(0xffffffffu, __float_as_uint(b23));
+        if (lane == 0) { atomicMax(&s_b[0], r01); atomicMax(&s_b[1], r23); }
+        __syncthreads();
+        const float B01 = __uint_as_float(s_b[0]), B23 = __uint_as_float(s_b[1]);
+        const float S01 = B01 > 0.f ? 2097152.f / B01 : 0.f, S23 = B23 > 0.f ? 2097152.f / B23 : 0.f;
+        if (work) {
+            int *c0 = pl + ci * NQ;
+            const float e0 = w0 * S01, e1 = w1 * S01, f0 = w0 * S23, f1 = w1 * S23;
+            const int nt = t_hi - t_lo + 1;
+            int t = t_lo + (3 * lane) % nt;                             // rotated start
+            for (int i = 0; i < nt; ++i) {
+                const float P = fmaf((float)t, step, base);
+                const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
+                const float yy = yc[t], yP = yy * P;
+                atomicAdd(c0 + r, (int)(__float_as_uint(fmaf(e0, yy, kMagic)) - kMagicBits));
+                atomicAdd(c0 + nbox + r, (int)(__float_as_uint(fmaf(e1, yy, kMagic)) - kMagicBits));
+                atomicAdd(c0 + 2 * nbox + r, (int)(__float_as_uint(fmaf(f0, yP, kMagic)) - kMagicBits));
+                atomicAdd(c0 + 3 * nbox + r, (int)(__float_as_uint(fmaf(f1, yP, kMagic)) - kMagicBits));
+                t = t == t_hi ? t_lo : t + 1;
             }
         }
-        if (CHECK) continue;
         __syncthreads();
+        if (tid == 0) { s_b[0] = 0u; s_b[1] = 0u; }                      // bounds of the next view
+        const float i01 = B01 * (1.f / 2097152.f), i23 = B23 * (1.f / 2097152.f);
         float4 *dst = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)boxc[n] * NQ;
         for (int i = tid; i < nbox; i += TX * TY) {
-            const float4 v = box[i];
-            if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) {
-                red_add4(dst + i, v.x, v.y, v.z, v.w);
-                box[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int a = pl[i], b = pl[nbox + i], c = pl[2 * nbox + i], d = pl[3 * nbox + i];
+            if (a | b | c | d) {
+                red_add4(dst + i, (float)a * i01, (float)b * i01, (float)c * i23, (float)d * i23);
+                pl[i] = 0; pl[nbox + i] = 0; pl[2 * nbox + i] = 0; pl[3 * nbox + i] = 0;
             }
         }
         __syncthreads();
+    }
+}
+
+// Interior views, plans whose footprints may leave the detector: per-sample range
+// tests (reading A9) and a direct global scatter (the chunked L1 forward's transpose).
+template <bool POLY>
+__global__ void __launch_bounds__(TX *TY) k_bp_adjoint_checked(BPParams p)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
+    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int item = blockIdx.z;
+    if (ix >= p.nx || iy >= p.ny) return;
+    const size_t plane = (size_t)p.nx * p.ny;
+    const size_t col = (size_t)iy * p.nx + ix;
+    const int2 *pik = p.pi_k + col;
+    const int2 e0 = pik[0];
+    if (!(e0.x <= e0.y)) return;
+    const int K0 = e0.x + 1, K1 = pik[(size_t)(p.nz - 1) * plane].y - 1;
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    const float *yv = p.vol + (size_t)item * p.nz * plane + col;
+    float4 *qT = p.gqT + (p.off0 + (int64_t)item * p.item_views) * (p.viewbytes / 16);
+    const int NQ = p.nr + 2;
+    int t_lo = 0, t_hi = -1, next_open = K0, next_close = INT_MAX;
+    for (int k = K0; k <= K1; ++k) {
+        while (k >= next_open) {
+            ++t_hi;
+            if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+            next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
+        }
+        while (k >= next_close) {
+            ++t_lo;
+            next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
+        }
+        if (t_hi < t_lo) continue;
+        const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+        const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+        const float u = fmaf(y, vg.x, -x * vg.y);
+        const float inv_v = rcp_approx(vstar);
+        float colpos;
+        if (POLY) {
+            const float tt = u * inv_v, q = tt * tt;
+            float a = p.at[6];
+            a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+            a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+            colpos = fmaf(tt, a, p.col_c);
+        } else {
+            colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+        }
+        if (!(colpos >= 0.f && colpos <= p.colmax)) continue;
+        const int l = __float2int_rz(colpos);
+        const float fa = colpos - __int2float_rn(l);
+        const float w1 = fa * inv_v, w0 = inv_v - w1;
+        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+        const float step = sc * p.dz, base = fmaf(sc, -vg.z, p.row_cc);
+        float4 *qc = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)l * NQ;
+        for (int t = t_lo; t <= t_hi; ++t) {
+            const float P = fmaf((float)t, step, base);
+            if (!(P >= p.pm_lo && P <= p.pm_hi)) continue;
+            const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
+            const float yy = yv[(size_t)t * plane] * p.scale;
+            red_add4(qc + r, w0 * yy, w1 * yy, w0 * yy * P, w1 * yy * P);
+        }
     }
 }
 
@@ -1068,23 +1164,22 @@ __global__ void k_bp_adjoint_ends(BPParams p)
 
 int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
 {
-    const size_t sm = (size_t)p.fp_cols_column * (p.nr + 2) * 16 + sizeof(int) * (size_t)p.max_cta_views;
-    if (!p.windows_monotone || sm > 200 * 1024) return -1;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bp_adjoint<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_adjoint<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_adjoint<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_adjoint<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    if (!p.windows_monotone) return -1;
+    const size_t sm = 4 * sizeof(int) * (size_t)p.fp_cols_column * (p.nr + 2) +
+                      sizeof(float) * (size_t)TX * TY * (p.nz | 1) + sizeof(int) * (size_t)p.max_cta_views;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
-    if (p.checked) {
-        if (p.poly) k_bp_adjoint<true, true><<<grid, TX * TY, sm, s>>>(p);
-        else k_bp_adjoint<false, true><<<grid, TX * TY, sm, s>>>(p);
+    if (!p.checked && p.staged && sm <= 200 * 1024) {        // KATS_BP_KERNEL=l1: the checked kernel (A/B)
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_bp_adjoint<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_bp_adjoint<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = true;
+        }
+        if (p.poly) k_bp_adjoint<true><<<grid, TX * TY, sm, s>>>(p);
+        else k_bp_adjoint<false><<<grid, TX * TY, sm, s>>>(p);
     } else {
-        if (p.poly) k_bp_adjoint<true, false><<<grid, TX * TY, sm, s>>>(p);
-        else k_bp_adjoint<false, false><<<grid, TX * TY, sm, s>>>(p);
+        if (p.poly) k_bp_adjoint_checked<true><<<grid, TX * TY, 0, s>>>(p);
+        else k_bp_adjoint_checked<false><<<grid, TX * TY, 0, s>>>(p);
     }
     dim3 ge((p.nx + 127) / 128, p.ny, p.nz * p.n_items);
     if (p.poly) k_bp_adjoint_ends<true><<<ge, 128, 0, s>>>(p);
