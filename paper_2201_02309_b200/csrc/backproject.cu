@@ -932,9 +932,11 @@ template <bool POLY>
 __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];   // one symbol per TU: keep the TMA kernels' alignment
-    const int BW = p.fp_cols_column, NQ = p.nr + 2, nbox = BW * NQ, nzp = p.nz | 1;
-    int *pl = reinterpret_cast<int *>(smem);                           // [4][nbox] fixed-point quad components
-    float *ys = reinterpret_cast<float *>(pl + 4 * nbox);              // [TX*TY][nzp] scale * y
+    const int BW = p.fp_cols_column, NQ = p.nr + 2, nzp = p.nz | 1;
+    const int NQP = (NQ + 31) & ~31, nbox = BW * NQP;                 // column stride = 0 mod 32 banks
+    const int cpy = 4 * nbox + 16;                                     // second copy: 16 banks further
+    int *pl = reinterpret_cast<int *>(smem);                           // [2 copies][4][BW][NQP] fixed-point components
+    float *ys = reinterpret_cast<float *>(pl + 2 * cpy);               // [TX*TY][nzp] scale * y
     int *boxc = reinterpret_cast<int *>(ys + TX * TY * nzp);
     __shared__ int s_k0, s_k1;
     __shared__ unsigned s_b[2];                                        // view bounds (float bits, >= 0)
@@ -947,7 +949,7 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
     const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
     const int2 *pik = p.pi_k + col;
     if (tid == 0) { s_k0 = INT_MAX; s_k1 = INT_MIN; s_b[0] = 0u; s_b[1] = 0u; }
-    for (int i = tid; i < 4 * nbox; i += TX * TY) pl[i] = 0;
+    for (int i = tid; i < 2 * cpy; i += TX * TY) pl[i] = 0;
     float ycmax = 0.f;                                                 // this column's max |scale * y|
     {
         const float *yv = p.vol + (size_t)item * p.nz * plane + col;
@@ -1035,10 +1037,11 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
         const float B01 = __uint_as_float(s_b[0]), B23 = __uint_as_float(s_b[1]);
         const float S01 = B01 > 0.f ? 2097152.f / B01 : 0.f, S23 = B23 > 0.f ? 2097152.f / B23 : 0.f;
         if (work) {
-            int *c0 = pl + ci * NQ;
+            int *c0 = pl + (lane & 1) * cpy + ci * NQP;                  // odd lanes: the shifted copy
             const float e0 = w0 * S01, e1 = w1 * S01, f0 = w0 * S23, f1 = w1 * S23;
             const int nt = t_hi - t_lo + 1;
-            int t = t_lo + (3 * lane) % nt;                             // rotated start
+            // rotated start: lane L begins ~L rows below lane 0 (consecutive banks for a shared column)
+            int t = t_lo + (int)((float)lane * __frcp_rn(step)) % nt;
             for (int i = 0; i < nt; ++i) {
                 const float P = fmaf((float)t, step, base);
                 const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
@@ -1054,11 +1057,15 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
         if (tid == 0) { s_b[0] = 0u; s_b[1] = 0u; }                      // bounds of the next view
         const float i01 = B01 * (1.f / 2097152.f), i23 = B23 * (1.f / 2097152.f);
         float4 *dst = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)boxc[n] * NQ;
-        for (int i = tid; i < nbox; i += TX * TY) {
-            const int a = pl[i], b = pl[nbox + i], c = pl[2 * nbox + i], d = pl[3 * nbox + i];
+        for (int i = tid; i < BW * NQ; i += TX * TY) {
+            const int cc = i / NQ, j = cc * NQP + (i - cc * NQ);
+            int *q0 = pl + j, *q1 = pl + cpy + j;
+            const int a = q0[0] + q1[0], b = q0[nbox] + q1[nbox], c = q0[2 * nbox] + q1[2 * nbox],
+                      d = q0[3 * nbox] + q1[3 * nbox];
             if (a | b | c | d) {
                 red_add4(dst + i, (float)a * i01, (float)b * i01, (float)c * i23, (float)d * i23);
-                pl[i] = 0; pl[nbox + i] = 0; pl[2 * nbox + i] = 0; pl[3 * nbox + i] = 0;
+                q0[0] = 0; q0[nbox] = 0; q0[2 * nbox] = 0; q0[3 * nbox] = 0;
+                q1[0] = 0; q1[nbox] = 0; q1[2 * nbox] = 0; q1[3 * nbox] = 0;
             }
         }
         __syncthreads();
@@ -1165,7 +1172,7 @@ __global__ void k_bp_adjoint_ends(BPParams p)
 int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
 {
     if (!p.windows_monotone) return -1;
-    const size_t sm = 4 * sizeof(int) * (size_t)p.fp_cols_column * (p.nr + 2) +
+    const size_t sm = sizeof(int) * 2 * (4 * (size_t)p.fp_cols_column * ((p.nr + 2 + 31) & ~31) + 16) +
                       sizeof(float) * (size_t)TX * TY * (p.nz | 1) + sizeof(int) * (size_t)p.max_cta_views;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
     if (!p.checked && p.staged && sm <= 200 * 1024) {        // KATS_BP_KERNEL=l1: the checked kernel (A/B)
