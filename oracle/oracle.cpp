@@ -430,6 +430,96 @@ void deriv_T(const G &o, const double *g1T, int64_t v, double *outT, int64_t s0)
         }
 }
 
+/* ---------- NEXT-3: data generation (P:l.353-404; SPEC "simulate") ----------
+ * Scan ray of detector sample (v, m, l) (P:l.87-94 helix, curved detector
+ * P:l.117, l.311-349): source a(λ) = (R cos(λ+λ0), R sin(λ+λ0), z0 + hλ),
+ * direction ∝ D sinα e_t − D cosα e_r + w e_z, e_r = (cos, sin, 0),
+ * e_t = (−sin, cos, 0) at angle λ+λ0 — the geometry bp_voxel inverts
+ * (α* = atan(u/v*), w* = D cosα* (z − z_src)/v*). */
+void scan_ray(const G &o, int64_t v, int m, int l, double src[3], double dir[3])
+{
+    const double lam = v * o.dlam;
+    const double c = std::cos(lam + o.g.lambda0), sn = std::sin(lam + o.g.lambda0);
+    src[0] = o.g.R * c; src[1] = o.g.R * sn; src[2] = o.g.z0 + o.h * lam;
+    const double a = alpha_l(o, l), w = w_m(o, m);
+    const double sa = std::sin(a), ca = std::cos(a);
+    double d[3] = {o.g.D * (-sa * sn - ca * c), o.g.D * (sa * c - ca * sn), w};
+    const double n = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    dir[0] = d[0] / n; dir[1] = d[1] / n; dir[2] = d[2] / n;
+}
+
+/* Length of a unit-speed line inside an ellipsoid {c, semi-axes a,b,c (c <= 0:
+ * infinite cylinder along z), rotation φ about z}: the roots of a quadratic. */
+double ellipsoid_chord(const double *e, const double o[3], const double d[3])
+{
+    const double cp = std::cos(e[6]), sp = std::sin(e[6]);
+    const double ox = o[0] - e[0], oy = o[1] - e[1], oz = o[2] - e[2];
+    const double px = (cp * ox + sp * oy) / e[3], py = (-sp * ox + cp * oy) / e[4];
+    const double qx = (cp * d[0] + sp * d[1]) / e[3], qy = (-sp * d[0] + cp * d[1]) / e[4];
+    double A = qx * qx + qy * qy, B = 2.0 * (px * qx + py * qy), C = px * px + py * py - 1.0;
+    if (e[5] > 0.0) {
+        const double pz = oz / e[5], qz = d[2] / e[5];
+        A += qz * qz; B += 2.0 * pz * qz; C += pz * pz;
+    }
+    if (A <= 0.0) return 0.0;
+    const double disc = B * B - 4.0 * A * C;
+    return disc > 0.0 ? std::sqrt(disc) / A : 0.0;
+}
+
+/* Philox4x32-10 (Salmon et al., SC'11): counter-based stream, identical on the GPU side. */
+void philox(uint32_t ctr[4], const uint32_t key[2])
+{
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * ctr[0], p1 = (uint64_t)0xCD9E8D57u * ctr[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ ctr[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ ctr[3] ^ k1;
+        ctr[1] = (uint32_t)p1; ctr[3] = (uint32_t)p0; ctr[0] = n0; ctr[2] = n2;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+}
+
+/* Stream of one sample: counter (index lo, index hi, draw, 0), key = seed; two
+ * uniforms in (0, 1) with 53 bits per Philox call. */
+struct Stream {
+    uint32_t key[2]; uint64_t idx; uint32_t draw = 0; double buf[2]; int left = 0;
+    double uniform()
+    {
+        if (!left) {
+            uint32_t c[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), draw++, 0u};
+            philox(c, key);
+            buf[0] = ((double)((((uint64_t)(c[0] >> 5)) << 26) | (c[1] >> 6)) + 0.5) * 0x1p-53;
+            buf[1] = ((double)((((uint64_t)(c[2] >> 5)) << 26) | (c[3] >> 6)) + 0.5) * 0x1p-53;
+            left = 2;
+        }
+        return buf[2 - left--];
+    }
+};
+
+/* Poisson(lam) for lam >= 10: PTRS, transformed rejection with squeeze
+ * (W. Hörmann, Insurance: Math. Econ. 12, 1993). */
+int64_t poisson_ptrs(double lam, Stream &st)
+{
+    const double slam = std::sqrt(lam), loglam = std::log(lam);
+    const double b = 0.931 + 2.53 * slam, a = -0.059 + 0.02483 * b;
+    const double invalpha = 1.1239 + 1.1328 / (b - 3.4), vr = 0.9277 - 3.6224 / (b - 2.0);
+    for (;;) {
+        const double U = st.uniform() - 0.5, V = st.uniform();
+        const double us = 0.5 - std::fabs(U);
+        const double k = std::floor((2.0 * a / us + b) * U + lam + 0.43);
+        if (us >= 0.07 && V <= vr) return (int64_t)k;
+        if (k < 0.0 || (us < 0.013 && V > us)) continue;
+        if (std::log(V) + std::log(invalpha) - std::log(a / (us * us) + b) <= -lam + k * loglam - std::lgamma(k + 1.0))
+            return (int64_t)k;
+    }
+}
+
+/* Standard normal by Box-Muller (one uniform pair per draw). */
+double normal(Stream &st)
+{
+    const double u1 = st.uniform(), u2 = st.uniform();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * PI * u2);
+}
+
 }  // namespace
 
 extern "C" {
@@ -659,6 +749,153 @@ int ora_adjoint(const ora_geom *g, const double *vol, int32_t k0, int32_t np, in
         ora_filter_T(g, gFT.data(), fv + 1, nv - 2, s0, sn, sinoT);
     }
     return 0;
+}
+
+/* ---- NEXT-3: data generation ---- */
+
+/* Exact line integrals of an ellipsoid phantom ell[n][8] = {cx,cy,cz,a,b,c,φ,ρ}
+ * for views v0 .. v0+nv-1: out[nv][rows][cols] (double). */
+void ora_project_ellipsoids(const ora_geom *g, const double *ell, int32_t n, int64_t v0, int32_t nv, double *out)
+{
+    G o = make(g);
+    const int nr = g->n_rows, nc = g->n_cols;
+    #pragma omp parallel for collapse(2) schedule(static)
+    for (int32_t iv = 0; iv < nv; ++iv)
+        for (int m = 0; m < nr; ++m)
+            for (int l = 0; l < nc; ++l) {
+                double src[3], dir[3];
+                scan_ray(o, v0 + iv, m, l, src, dir);
+                double acc = 0.0;
+                for (int k = 0; k < n; ++k) acc += ell[8 * k + 7] * ellipsoid_chord(ell + 8 * k, src, dir);
+                out[((size_t)iv * nr + m) * nc + l] = acc;
+            }
+}
+
+/* Sampled line integrals of a voxel volume vol[nzv][ny][nx] (the plan's x/y
+ * grid x_i = (i - nx/2) dx, slices z_j = zv0 + j dzv), trilinear interpolation
+ * with zeros outside the grid, along the segment of the ray inside the box
+ * where the interpolant can be nonzero (one voxel beyond the outer centres),
+ * split into N = ceil(len / (0.5 min(dx, dy, dzv))) equal steps sampled at
+ * their midpoints (SPEC project_numeric).  *n_trunc counts rays whose segment
+ * inside the x/y box leaves the volume's z extent (that part counts 0). */
+void ora_project_volume(const ora_geom *g, const float *vol, int32_t nzv, double zv0, double dzv,
+                        int64_t v0, int32_t nv, double *out, int64_t *n_trunc)
+{
+    G o = make(g);
+    const int nr = g->n_rows, nc = g->n_cols, nx = g->nx, ny = g->ny;
+    const double lo[3] = {x_i(o, 0) - g->dx, y_i(o, 0) - g->dy, zv0 - dzv};
+    const double hi[3] = {x_i(o, nx - 1) + g->dx, y_i(o, ny - 1) + g->dy, zv0 + (nzv - 1) * dzv + dzv};
+    const double ds = 0.5 * std::min(std::min(g->dx, g->dy), dzv);
+    int64_t trunc = 0;
+    auto at = [&](int i, int j, int k) -> double {
+        if (i < 0 || i >= nx || j < 0 || j >= ny || k < 0 || k >= nzv) return 0.0;
+        return vol[((size_t)k * ny + j) * nx + i];
+    };
+    #pragma omp parallel for collapse(2) schedule(static) reduction(+:trunc)
+    for (int32_t iv = 0; iv < nv; ++iv)
+        for (int m = 0; m < nr; ++m)
+            for (int l = 0; l < nc; ++l) {
+                double src[3], dir[3];
+                scan_ray(o, v0 + iv, m, l, src, dir);
+                double t0 = -1e300, t1 = 1e300, t0xy = -1e300, t1xy = 1e300;
+                for (int a = 0; a < 3; ++a) {
+                    if (dir[a] == 0.0) {
+                        if (src[a] < lo[a] || src[a] > hi[a]) { t0 = 1.0; t1 = 0.0; }
+                        continue;
+                    }
+                    double ta = (lo[a] - src[a]) / dir[a], tb = (hi[a] - src[a]) / dir[a];
+                    if (ta > tb) std::swap(ta, tb);
+                    t0 = std::max(t0, ta); t1 = std::min(t1, tb);
+                    if (a < 2) { t0xy = std::max(t0xy, ta); t1xy = std::min(t1xy, tb); }
+                }
+                double acc = 0.0;
+                if (t1xy > t0xy && (t0 > t0xy + 1e-9 || t1 < t1xy - 1e-9)) ++trunc;
+                if (t1 > t0) {
+                    const int64_t N = (int64_t)std::ceil((t1 - t0) / ds);
+                    const double h = (t1 - t0) / N;
+                    for (int64_t i = 0; i < N; ++i) {
+                        const double t = t0 + (i + 0.5) * h;
+                        const double fx = (src[0] + t * dir[0] - x_i(o, 0)) / g->dx;
+                        const double fy = (src[1] + t * dir[1] - y_i(o, 0)) / g->dy;
+                        const double fz = (src[2] + t * dir[2] - zv0) / dzv;
+                        const int ix = (int)std::floor(fx), iy = (int)std::floor(fy), iz = (int)std::floor(fz);
+                        const double ax = fx - ix, ay = fy - iy, az = fz - iz;
+                        double v = 0.0;
+                        for (int c = 0; c < 8; ++c) {
+                            const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+                            const double w = (dx ? ax : 1.0 - ax) * (dy ? ay : 1.0 - ay) * (dz ? az : 1.0 - az);
+                            v += w * at(ix + dx, iy + dy, iz + dz);
+                        }
+                        acc += v * h;
+                    }
+                }
+                out[((size_t)iv * nr + m) * nc + l] = acc;
+            }
+    if (n_trunc) *n_trunc = trunc;
+}
+
+/* α down/upsampling (P:l.394-397: α_sp = α_cor[0:stride:end], "upsample by
+ * interpolation"): keeps columns 0, stride, ...; linear interpolation between
+ * kept columns, the last kept value held beyond it.  sino/out [nv][rows][cols]. */
+void ora_resample_alpha(const ora_geom *g, const double *sino, int64_t nv, int32_t stride, double *out)
+{
+    const int nr = g->n_rows, nc = g->n_cols;
+    const int last = stride * ((nc - 1) / stride);
+    for (int64_t r = 0; r < nv * nr; ++r) {
+        const double *s = sino + r * nc;
+        double *d = out + r * nc;
+        for (int l = 0; l < nc; ++l) {
+            if (l >= last) { d[l] = s[last]; continue; }
+            const int l0 = stride * (l / stride);
+            const double f = (double)(l - l0) / stride;
+            d[l] = (1.0 - f) * s[l0] + f * s[l0 + stride];
+        }
+    }
+}
+
+/* 'Gaussian+Poisson' noise of P:l.398-404 on an (upsampled) sinogram of views
+ * v_first .. v_first+nv-1 (absolute indices: the random stream of a sample is
+ * keyed by (seed, (v * rows + m) * cols + l), so chunking does not change it):
+ *   t = I0 exp(-g/M), s = Poisson(t) + Normal(0, var) (reading: a Poisson draw of
+ *   mean t, not t + Poisson(t)), s = max(s, 1), out = log(I0/s) M.
+ * M = max of g over the call (> 0).  counts (optional) receives the Poisson draws.
+ * mode 1 = noiseless check: Poisson replaced by its mean and var = 0. */
+int ora_add_noise(const ora_geom *g, const double *sino, int64_t v_first, int64_t nv, double I0, double var,
+                  uint64_t seed, int mode, double *out, int64_t *counts, double *M_out)
+{
+    const int nr = g->n_rows, nc = g->n_cols;
+    const int64_t n = nv * nr * nc;
+    double M = 0.0;
+    for (int64_t i = 0; i < n; ++i) M = std::max(M, sino[i]);
+    if (!(M > 0.0)) return -1;
+    if (M_out) *M_out = M;
+    const double sd = std::sqrt(var);
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        const double t = I0 * std::exp(-sino[i] / M);
+        double s;
+        if (mode == 1) {
+            s = t;
+        } else {
+            Stream st;
+            st.key[0] = (uint32_t)seed; st.key[1] = (uint32_t)(seed >> 32);
+            st.idx = (uint64_t)(v_first * nr * nc) + (uint64_t)i;
+            const int64_t k = poisson_ptrs(t, st);
+            if (counts) counts[i] = k;
+            s = (double)k + sd * normal(st);
+        }
+        s = std::max(s, 1.0);
+        out[i] = std::log(I0 / s) * M;
+    }
+    return 0;
+}
+
+/* Philox4x32-10 of one counter (for the known-answer pin). */
+void ora_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    philox(c, key);
+    std::memcpy(out, c, sizeof(c));
 }
 
 }  // extern "C"

@@ -73,6 +73,14 @@ def lib():
                                             ctypes.c_int64, _D]),
             "ora_adjoint": (ctypes.c_int, [_G, _D, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
                                            ctypes.c_int64, _D]),
+            "ora_project_ellipsoids": (None, [_G, _D, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, _D]),
+            "ora_project_volume": (None, [_G, _F, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_int64, ctypes.c_int32, _D, _I64]),
+            "ora_resample_alpha": (None, [_G, _D, ctypes.c_int64, ctypes.c_int32, _D]),
+            "ora_add_noise": (ctypes.c_int, [_G, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_uint64, ctypes.c_int, _D, _I64, _D]),
+            "ora_philox": (None, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
+                                  ctypes.POINTER(ctypes.c_uint32)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(l, name)
@@ -255,3 +263,57 @@ def adjoint(cfg, vol, k0, n_pitches, s0, sn):
     if rc:
         raise ValueError("oracle adjoint: sinogram does not cover a requested pitch slab")
     return out
+
+
+# ---- NEXT-3: data generation (P:l.353-404) ----
+
+def project_ellipsoids(cfg, ellipsoids, v0, n_views):
+    """Exact line integrals [n_views][rows][cols] (float64) of an ellipsoid phantom."""
+    e = np.ascontiguousarray(np.asarray(ellipsoids, dtype=np.float64).reshape(-1, 8))
+    out = np.empty((n_views, cfg["n_rows"], cfg["n_cols"]))
+    g = geom(cfg)
+    lib().ora_project_ellipsoids(ctypes.byref(g), _p(e, _D), e.shape[0], v0, n_views, _p(out, _D))
+    return out
+
+
+def project_volume(cfg, vol, zv0, dzv, v0, n_views):
+    """Trilinear ray-marched line integrals of vol [nzv][ny][nx] (slices at zv0 + j dzv).
+    Returns (sino float64, number of rays truncated by the volume's z extent)."""
+    vol = np.ascontiguousarray(vol, dtype=np.float32)
+    out = np.empty((n_views, cfg["n_rows"], cfg["n_cols"]))
+    nt = ctypes.c_int64()
+    g = geom(cfg)
+    lib().ora_project_volume(ctypes.byref(g), _p(vol, _F), vol.shape[0], zv0, dzv, v0, n_views, _p(out, _D),
+                             ctypes.byref(nt))
+    return out, nt.value
+
+
+def resample_alpha(cfg, sino, stride):
+    """alpha_sp = alpha[0:stride:end], then linear interpolation back (edge hold)."""
+    sino = np.ascontiguousarray(sino, dtype=np.float64)
+    out = np.empty_like(sino)
+    g = geom(cfg)
+    lib().ora_resample_alpha(ctypes.byref(g), _p(sino, _D), sino.shape[0], stride, _p(out, _D))
+    return out
+
+
+def add_noise(cfg, sino, v_first, I0=1e5, var=0.5, seed=0, mode=0):
+    """'Gaussian+Poisson' noise; returns (noisy float64, Poisson counts int64, M)."""
+    sino = np.ascontiguousarray(sino, dtype=np.float64)
+    out = np.empty_like(sino)
+    counts = np.zeros(sino.shape, dtype=np.int64)
+    M = ctypes.c_double()
+    g = geom(cfg)
+    rc = lib().ora_add_noise(ctypes.byref(g), _p(sino, _D), v_first, sino.shape[0], I0, var, seed, mode,
+                             _p(out, _D), _p(counts, _I64), ctypes.byref(M))
+    if rc:
+        raise ValueError("oracle add_noise: max of the sinogram must be > 0")
+    return out, counts, M.value
+
+
+def philox(ctr, key):
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    lib().ora_philox(c, k, o)
+    return list(o)
