@@ -5,7 +5,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp,-O3 -Xpt
 PKG       := paper_2201_02309_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libkatsevich.so
-OBJS      := $(CSRC)/precompute.o $(CSRC)/api.o $(CSRC)/filter.o $(CSRC)/backproject.o
+OBJS      := $(CSRC)/precompute.o $(CSRC)/api.o $(CSRC)/filter.o $(CSRC)/backproject.o $(CSRC)/datagen.o
 HDRS      := include/katsevich.h $(CSRC)/plan.hpp $(CSRC)/kernels.cuh
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so

@@ -263,6 +263,28 @@ def run_ours(args):
         iso = {"k5_ms_per_launch": st_iso["ms"][k] / max(1, st_iso["launches"][k]),
                "launches": st_iso["launches"][k] // n_iso}
 
+    # ---- e2e: host (pinned) in -> host out through katsevich_reconstruct_host ----
+    e2e = None
+    if not batch:
+        pin_in = torch.from_numpy(host_in).pin_memory()
+        pin_out = torch.empty(vol_shape, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t1 = time.perf_counter()
+        ne = max(3, min(args.steps, 10))
+        for _ in range(ne):
+            plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t1) * 1e3 / ne
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"ms_per_step": e2e_ms, "h2d": pin_in.numel() * 4, "d2h": pin_out.numel() * 4}
+
     # ---- adjoint (NEXT-1): the transpose of the same step, volume -> sinogram, device-resident ----
     adj = None
     if not batch and not args.no_adjoint:
@@ -289,27 +311,41 @@ def run_ours(args):
         adj = {"ms_per_step": adj_ms, "k5T_ms_per_step": st_adj["ms"]["K5_backproject"] / args.steps}
         del vol_y, sino_t
 
-    # ---- e2e: host (pinned) in -> host out through katsevich_reconstruct_host ----
-    e2e = None
-    if not batch:
-        pin_in = torch.from_numpy(host_in).pin_memory()
-        pin_out = torch.empty(vol_shape, dtype=torch.float32).pin_memory()
-        for _ in range(2):
-            plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t1 = time.perf_counter()
-        ne = max(3, min(args.steps, 10))
-        for _ in range(ne):
-            plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
-        torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t1) * 1e3 / ne
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"ms_per_step": e2e_ms, "h2d": pin_in.numel() * 4, "d2h": pin_out.numel() * 4}
+    # ---- data generation (NEXT-3): projection of the workload's phantom over the rank's scan,
+    # ray marching through the reconstructed volume (a view subset), sparse-view + noise degradation ----
+    dg = None
+    if not batch and not args.no_datagen:
+        nvs = host_in.shape[0]
+        sino_g = torch.empty(tuple(host_in.shape), dtype=torch.float32, device=dev)
+        nvv = min(64, nvs)
+        sino_v = torch.empty((nvv,) + tuple(host_in.shape[1:]), dtype=torch.float32, device=dev)
+        zf, dzv = float(first_pitch * cfg["P"]), cfg["P"] / cfg["nz"]
+
+        def timed(fn, reps):
+            for _ in range(max(1, args.warmup)):
+                fn()
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(reps):
+                fn()
+            b1.record(stream)
+            torch.cuda.synchronize()
+            return b0.elapsed_time(b1) / reps
+
+        ph = cfg["phantom"]
+        ms_pe = timed(lambda: plan.project_ellipsoids(ph, v0, nvs, out=sino_g, stream=stream), args.steps)
+        ms_pv = timed(lambda: plan.project_volume(out, zf, dzv, v0 + nvs // 2, nvv, out=sino_v, stream=stream), 3)
+        ms_dg = timed(lambda: plan.degrade(sino_g, v0, 4, 1e5, 0.5, 1234, stream=stream), args.steps)
+        rays = nvs * cfg["n_rows"] * cfg["n_cols"]
+        dg = {"project_ellipsoids": {"value": rays / (ms_pe * 1e-3), "unit": "rays/s", "ms": ms_pe, "rays": rays,
+                                     "ellipsoids": len(ph), "precision": "f64"},
+              "project_volume": {"value": nvv * cfg["n_rows"] * cfg["n_cols"] / (ms_pv * 1e-3), "unit": "rays/s",
+                                 "ms": ms_pv, "views": nvv,
+                                 "volume_xyz": [cfg["nx"], cfg["ny"], int(out.shape[0])], "precision": "f32"},
+              "degrade": {"value": rays / (ms_dg * 1e-3), "unit": "samples/s", "ms": ms_dg,
+                          "what": "alpha stride 4 + 'Gaussian+Poisson' (I0 1e5, var 0.5), Philox4x32-10"}}
+        del sino_g, sino_v
 
     if rank != 0:
         if world > 1:
@@ -378,6 +414,8 @@ def run_ours(args):
                          "frac": U_rank * bp_smem_bytes_per_update() / (iso["k5_ms_per_launch"] * 1e-3) / 1e9 / smem_peak}},
         "clocks": clk,
     }
+    if dg:
+        line["datagen"] = dg
     if adj:
         line["adjoint"] = {"metric": "voxel-view updates/s (transpose: volume -> sinogram)",
                            "value": U_all / (adj["ms_per_step"] * 1e-3), "unit": "updates/s",
@@ -482,6 +520,7 @@ def main():
     ap.add_argument("--gather", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-adjoint", action="store_true", help="skip the adjoint (NEXT-1) measurement")
+    ap.add_argument("--no-datagen", action="store_true", help="skip the data-generation (NEXT-3) measurement")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:

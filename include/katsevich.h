@@ -158,6 +158,43 @@ int katsevich_adjoint(katsevich_plan *plan, const float *vol, int32_t first_pitc
                       float *sino_out, int64_t s0, int64_t sn, void *workspace, size_t workspace_bytes,
                       void *cuda_stream);
 
+/* ---- data generation (NEXT-3: training-shaped inputs) ---- */
+
+/* Exact line integrals of an ellipsoid phantom along the plan's helical scan
+ * rays (helix P:l.87-94, curved detector P:l.117, l.311-349) for views
+ * first_view .. first_view+n_views-1.
+ *   ell   [n_ell][8] double, HOST: {cx, cy, cz, a, b, c, phi, rho} (mm, rad,
+ *         density; c <= 0: infinite elliptic cylinder along z; densities add)
+ *   sino  [n_views][rows][cols] fp32, device (output)
+ * fp64 chords (closed-form quadratic); asynchronous on cuda_stream. */
+int katsevich_project_ellipsoids(katsevich_plan *plan, const double *ell, int32_t n_ell, int64_t first_view,
+                                 int64_t n_views, float *sino, void *cuda_stream);
+
+/* Sampled line integrals of a voxel volume (P:l.354, "simulate scanning the CT
+ * image labels"): vol [nz_vol][ny][nx] fp32, device, on the plan's x/y grid
+ * (x_i = (i - nx/2) dx) with slices z_j = z_first + j dz_vol; trilinear
+ * interpolation (0 outside the grid), N = ceil(length / (0.5 min voxel)) equal
+ * steps sampled at their midpoints.  n_truncated (host, optional: synchronises)
+ * receives the number of rays whose x/y segment leaves the volume's z extent. */
+int katsevich_project_volume(katsevich_plan *plan, const float *vol, int32_t nz_vol, double z_first, double dz_vol,
+                             int64_t first_view, int64_t n_views, float *sino, int64_t *n_truncated,
+                             void *cuda_stream);
+
+/* Sparse-view degradation of P:l.394-404 on a sinogram of views first_view ..
+ * (device fp32 in / out [n_views][rows][cols]): keep the α columns 0,
+ * alpha_stride, ... and interpolate linearly back (last kept value held
+ * beyond it); then the 'Gaussian+Poisson' noise with M = max of the upsampled
+ * data (computed on the device): t = I0 exp(-g/M), s = Poisson(t) +
+ * Normal(0, gauss_var), s = max(s, 1), out = log(I0/s) M.  Random numbers:
+ * Philox4x32-10 keyed by (seed, absolute sample index) — deterministic and
+ * independent of chunking.  mode 1: noiseless check (Poisson -> its mean,
+ * var 0).  counts (device int64, optional) receives the Poisson draws; M_out
+ * (device fp32, optional) the M used.  Input must be >= 0 (KATS_ERR_ARGUMENT
+ * for bad parameters). */
+int katsevich_degrade(katsevich_plan *plan, const float *sino, int64_t first_view, int64_t n_views,
+                      int32_t alpha_stride, double I0, double gauss_var, uint64_t seed, int32_t mode, float *out,
+                      int64_t *counts, float *M_out, void *cuda_stream);
+
 /* ---- debug / parity entry points ---- */
 
 /* Steps 1-6 (Eqs. 8-15) for views [out_first_view, out_first_view + n_out):

@@ -64,6 +64,11 @@ SIGNATURES = {
     "katsevich_bp_kernel": (ctypes.c_int, [_P]),
     "katsevich_adjoint_workspace_bytes": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_SZ)]),
     "katsevich_adjoint": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _I64, _I64, _P, _SZ, _P]),
+    "katsevich_project_ellipsoids": (ctypes.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),
+    "katsevich_project_volume": (ctypes.c_int, [_P, _P, _I32, ctypes.c_double, ctypes.c_double, _I64, _I64, _P,
+                                                _PI64, _P]),
+    "katsevich_degrade": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_uint64, _I32, _P, _P, _P, _P]),
     "katsevich_destroy": (None, [_P]),
     "katsevich_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "katsevich_last_error_detail": (ctypes.c_char_p, [_P]),

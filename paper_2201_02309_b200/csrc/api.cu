@@ -94,6 +94,7 @@ void free_device(katsevich_plan *p)
     p->event_pool.clear();
     for (void *e : p->sync_events) cudaEventDestroy((cudaEvent_t)e);
     p->sync_events.clear();
+    if (p->dg_scratch) { cudaFree(p->dg_scratch); p->dg_scratch = nullptr; p->dg_scratch_bytes = 0; }
     if (p->copy_stream) { cudaStreamDestroy((cudaStream_t)p->copy_stream); p->copy_stream = nullptr; }
     if (p->copy_stream2) { cudaStreamDestroy((cudaStream_t)p->copy_stream2); p->copy_stream2 = nullptr; }
     for (void *&b : p->bp_streams)
@@ -133,9 +134,12 @@ FilterParams filter_params(const katsevich_plan *p)
 // Filter n_out views whose raw data (with ±1 halo) is at sino_v0 - rows*cols
 // .. ; writes gF (and optionally full g3/g4 when dbg3/dbg4 are given).
 int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float4 *gq,
-               float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s)
+               float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s, bool overlapped = false)
 {
     FilterParams f = filter_params(p);
+    // concurrently with the TMEM backprojection (3 CTAs x 128 TMEM columns per SM) the tensor-core
+    // Hilbert's 256-column allocation would wait for TMEM: use the fp32 direct convolution there
+    if (overlapped) f.hilbert_tc = nullptr;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     const size_t qs = quad_view_elems(p);
     const size_t ps = (size_t)p->t.n_psi * p->g.n_cols;
@@ -654,7 +658,7 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
         while (c_next < nchunks && u0 + c_next * kFilterChunk < filt_end) {
             const int64_t a = u0 + c_next * kFilterChunk, n = std::min<int64_t>(kFilterChunk, nu - c_next * kFilterChunk);
             KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[c_next], 0));
-            rc = run_filter(p, dsino + (a - fv) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs);
+            rc = run_filter(p, dsino + (a - fv) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs, true);
             if (rc) return rc;
             ++c_next;
         }
@@ -684,6 +688,96 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
     KCHECK(p, cudaStreamSynchronize((cudaStream_t)p->bp_streams[1]));
     KCHECK(p, cudaStreamSynchronize(fs));
     KCHECK(p, cudaStreamSynchronize(s));
+    return KATS_OK;
+}
+
+// ---- data generation (NEXT-3) ----
+static DataGenParams datagen_params(const katsevich_plan *p)
+{
+    const katsevich_geometry &g = p->g;
+    DataGenParams d{};
+    d.R = g.R; d.D = g.D; d.h = g.pitch / (2.0 * kPi); d.lambda0 = g.lambda0; d.z0 = g.z0;
+    d.dlam = 2.0 * kPi / g.views_per_turn; d.d_w = g.d_w; d.d_alpha = g.d_alpha; d.alpha_offset = g.alpha_offset;
+    d.dx = g.dx; d.dy = g.dy; d.nr = g.n_rows; d.nc = g.n_cols; d.nx = g.nx; d.ny = g.ny;
+    return d;
+}
+
+static int plan_scratch(katsevich_plan *p, size_t bytes)
+{
+    if (p->dg_scratch_bytes >= bytes) return KATS_OK;
+    if (p->dg_scratch) cudaFree(p->dg_scratch);
+    p->dg_scratch = nullptr;
+    p->dg_scratch_bytes = 0;
+    KCHECK(p, cudaMalloc(&p->dg_scratch, bytes));
+    p->dg_scratch_bytes = bytes;
+    return KATS_OK;
+}
+
+int katsevich_project_ellipsoids(katsevich_plan *p, const double *ell, int32_t n_ell, int64_t first_view,
+                                 int64_t n_views, float *sino, void *cuda_stream)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (p->device < 0) return KATS_ERR_NO_DEVICE;
+    if (!sino || (n_ell > 0 && !ell)) return KATS_ERR_NULL;
+    if (n_views < 1 || n_ell < 0 || n_ell > 2048) return KATS_ERR_ARGUMENT;
+    cudaSetDevice(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    int rc = plan_scratch(p, sizeof(double) * 8 * (size_t)std::max(n_ell, 1));
+    if (rc) return rc;
+    if (n_ell > 0)
+        KCHECK(p, cudaMemcpyAsync(p->dg_scratch, ell, sizeof(double) * 8 * (size_t)n_ell, cudaMemcpyHostToDevice, s));
+    { LaunchScope ls(p, ST_OTHER, s);
+      launch_project_ellipsoids(datagen_params(p), (const double *)p->dg_scratch, n_ell, first_view, n_views, sino, s); }
+    KCHECK(p, cudaGetLastError());
+    return KATS_OK;
+}
+
+int katsevich_project_volume(katsevich_plan *p, const float *vol, int32_t nz_vol, double z_first, double dz_vol,
+                             int64_t first_view, int64_t n_views, float *sino, int64_t *n_truncated, void *cuda_stream)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (p->device < 0) return KATS_ERR_NO_DEVICE;
+    if (!vol || !sino) return KATS_ERR_NULL;
+    if (n_views < 1 || nz_vol < 1 || !(dz_vol > 0.0)) return KATS_ERR_ARGUMENT;
+    cudaSetDevice(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    int rc = plan_scratch(p, 64);
+    if (rc) return rc;
+    unsigned long long *cnt = (unsigned long long *)p->dg_scratch;
+    KCHECK(p, cudaMemsetAsync(cnt, 0, sizeof(*cnt), s));
+    { LaunchScope ls(p, ST_OTHER, s);
+      launch_project_volume(datagen_params(p), vol, nz_vol, (float)z_first, (float)dz_vol, first_view, n_views, sino,
+                            cnt, s); }
+    KCHECK(p, cudaGetLastError());
+    if (n_truncated) {
+        unsigned long long h = 0;
+        KCHECK(p, cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+        KCHECK(p, cudaStreamSynchronize(s));
+        *n_truncated = (int64_t)h;
+    }
+    return KATS_OK;
+}
+
+int katsevich_degrade(katsevich_plan *p, const float *sino, int64_t first_view, int64_t n_views, int32_t alpha_stride,
+                      double I0, double gauss_var, uint64_t seed, int32_t mode, float *out, int64_t *counts,
+                      float *M_out, void *cuda_stream)
+{
+    if (!p) return KATS_ERR_NULL;
+    if (p->device < 0) return KATS_ERR_NO_DEVICE;
+    if (!sino || !out) return KATS_ERR_NULL;
+    if (n_views < 1 || alpha_stride < 1 || !(I0 > 0.0) || gauss_var < 0.0 || (mode != 0 && mode != 1))
+        return KATS_ERR_ARGUMENT;
+    cudaSetDevice(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const size_t n = (size_t)n_views * p->g.n_rows * p->g.n_cols;
+    int rc = plan_scratch(p, 256 + sizeof(float) * n);
+    if (rc) return rc;
+    unsigned *maxbits = (unsigned *)p->dg_scratch;
+    float *up = (float *)((char *)p->dg_scratch + 256);
+    { LaunchScope ls(p, ST_OTHER, s);
+      launch_degrade(datagen_params(p), sino, first_view, n_views, alpha_stride, I0, gauss_var, seed, mode, up, maxbits,
+                     out, (long long *)counts, M_out, s); }
+    KCHECK(p, cudaGetLastError());
     return KATS_OK;
 }
 

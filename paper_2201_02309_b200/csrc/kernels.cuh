@@ -81,4 +81,17 @@ int launch_backproject(const BPParams &p, cudaStream_t s);            // K5; ret
 int launch_backproject_adjoint(const BPParams &p, cudaStream_t s);    // K5^T into p.gqT (-1: plan unsupported)
 void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cudaStream_t s);
 
+// ---- data generation (NEXT-3, datagen.cu) ----
+struct DataGenParams {
+    double R, D, h, lambda0, z0, dlam, d_w, d_alpha, alpha_offset, dx, dy;
+    int nr, nc, nx, ny;
+};
+void launch_project_ellipsoids(const DataGenParams &p, const double *ell, int n, int64_t v0, int64_t nv, float *out,
+                               cudaStream_t s);
+void launch_project_volume(const DataGenParams &p, const float *vol, int nzv, float zv0, float dzv, int64_t v0,
+                           int64_t nv, float *out, unsigned long long *n_trunc, cudaStream_t s);
+void launch_degrade(const DataGenParams &p, const float *in, int64_t v0, int64_t nv, int stride, double I0, double var,
+                    uint64_t seed, int mode, float *up, unsigned *maxbits, float *out, long long *counts, float *M_out,
+                    cudaStream_t s);
+
 }  // namespace kats

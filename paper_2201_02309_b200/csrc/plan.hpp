@@ -80,6 +80,8 @@ struct katsevich_plan {
     void *copy_stream2 = nullptr;           // device->host
     void *bp_streams[2] = {nullptr, nullptr};  // alternating per-pitch backprojection streams (low priority)
     void *filter_stream = nullptr;          // filter chunks (highest priority)
+    void *dg_scratch = nullptr;             // data generation: phantom / counter / upsampled scratch
+    size_t dg_scratch_bytes = 0;
     std::vector<void *> sync_events;
 };
 

@@ -190,6 +190,46 @@ class Plan:
                                             n_views, _ptr(ws), ws.numel(), _stream_handle(stream)))
         return out
 
+    # -- data generation (NEXT-3) -------------------------------------------
+    def project_ellipsoids(self, ellipsoids, first_view: int, n_views: int, out=None, stream=None):
+        """Exact line integrals of an ellipsoid phantom [n][8] (host) -> cuda float32 [n_views][rows][cols]."""
+        import torch
+        e = np.ascontiguousarray(np.asarray(ellipsoids, dtype=np.float64).reshape(-1, 8))
+        g = self.geometry
+        if out is None:
+            out = torch.empty((n_views, g.n_rows, g.n_cols), dtype=torch.float32, device=f"cuda:{self.device}")
+        self._check(lib().katsevich_project_ellipsoids(self._h, e.ctypes.data_as(ctypes.c_void_p), e.shape[0],
+                                                       first_view, n_views, _ptr(out), _stream_handle(stream)))
+        return out
+
+    def project_volume(self, vol, z_first: float, dz: float, first_view: int, n_views: int, out=None, stream=None):
+        """Trilinear ray-marched line integrals of vol (cuda float32 [nz][ny][nx]); returns
+        (sinogram, number of rays truncated by the volume's z extent)."""
+        import torch
+        assert vol.is_cuda and vol.dtype == torch.float32 and vol.is_contiguous()
+        g = self.geometry
+        if out is None:
+            out = torch.empty((n_views, g.n_rows, g.n_cols), dtype=torch.float32, device=vol.device)
+        nt = ctypes.c_int64()
+        self._check(lib().katsevich_project_volume(self._h, _ptr(vol), vol.shape[0], z_first, dz, first_view, n_views,
+                                                   _ptr(out), ctypes.byref(nt), _stream_handle(stream)))
+        return out, nt.value
+
+    def degrade(self, sino, first_view: int, alpha_stride: int = 4, I0: float = 1e5, gauss_var: float = 0.5,
+                seed: int = 0, mode: int = 0, return_counts: bool = False, stream=None):
+        """Sparse-view + 'Gaussian+Poisson' degradation (katsevich_degrade) of a cuda float32
+        sinogram whose first view is first_view.  Returns out (and counts, M when return_counts)."""
+        import torch
+        assert sino.is_cuda and sino.dtype == torch.float32 and sino.is_contiguous()
+        out = torch.empty_like(sino)
+        counts = torch.zeros(sino.shape, dtype=torch.int64, device=sino.device) if return_counts else None
+        M = torch.zeros(1, dtype=torch.float32, device=sino.device)
+        self._check(lib().katsevich_degrade(self._h, _ptr(sino), first_view, sino.shape[0], alpha_stride, I0,
+                                            gauss_var, seed, mode, _ptr(out),
+                                            _ptr(counts) if counts is not None else None, _ptr(M),
+                                            _stream_handle(stream)))
+        return (out, counts, M) if return_counts else out
+
     def filter(self, sino, sino_first_view: int, out_first_view: int, n_out: int, stages=("gF",), stream=None):
         import torch
         g = self.geometry
