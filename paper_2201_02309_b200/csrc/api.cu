@@ -137,9 +137,10 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
                float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s, bool overlapped = false)
 {
     FilterParams f = filter_params(p);
-    // concurrently with the TMEM backprojection (3 CTAs x 128 TMEM columns per SM) the tensor-core
-    // Hilbert's 256-column allocation would wait for TMEM: use the fp32 direct convolution there
-    if (overlapped) f.hilbert_tc = nullptr;
+    // concurrently with the TMEM backprojection (3 CTAs x 128 TMEM columns per SM) the two-parity
+    // tensor-core Hilbert's 256-column allocation would wait for TMEM: use the per-parity kernel
+    // (128 columns; the same MMA sequence per accumulator, so bitwise the same result)
+    f.hilbert_overlap = overlapped ? 1 : 0;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     const size_t qs = quad_view_elems(p);
     const size_t ps = (size_t)p->t.n_psi * p->g.n_cols;

@@ -499,7 +499,13 @@ bool hilbert_tc_usable(const FilterParams &p)
 
 void launch_hilbert(const FilterParams &p, cudaStream_t s)
 {
-    if (hilbert_tc_usable(p) && hilbert_tc_nh(p.nc) <= 256) {
+    if (hilbert_tc_usable(p) && p.hilbert_overlap && hilbert_tc_nh(p.nc) > 128) {
+        FilterParams q = p;                                       // a >128-column TMEM allocation would wait
+        q.hilbert_tc = nullptr;
+        launch_hilbert(q, s);
+        return;
+    }
+    if (hilbert_tc_usable(p) && hilbert_tc_nh(p.nc) <= 256 && !p.hilbert_overlap) {
         const int NH = hilbert_tc_nh(p.nc);
         const size_t smem = (size_t)4 * TC_M * TC_KC * 4 + (size_t)4 * NH * TC_KC * 4;
         static bool attr = false;

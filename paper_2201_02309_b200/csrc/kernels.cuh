@@ -24,6 +24,7 @@ struct FilterParams {
     float4 *gq;               // filtered views as column-major 2x2 sum/difference tap quads [n_views][nc][nr+2] (BP input)
     float *gF;                // optional plain filtered views [n_views][nr][nc] (debug), may be null
     float sign;               // K3 output sign: +1 forward, -1 for the adjoint (odd kernel)
+    int hilbert_overlap;      // K3 runs next to the TMEM backprojection: keep its TMEM allocation <= 128 columns
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
