@@ -5,7 +5,10 @@ Pitches are independent given their slab and share every periodic table
 rank r reconstructs a contiguous block of pitches from the views that block
 needs (its pitches plus the PI-window overlap).  The only collective is the
 optional gather of the volume slabs (NCCL over NVLink on B200; gloo in the
-CPU tests).  Nothing here computes: reconstruction runs in libkatsevich.so.
+CPU tests).  Training through the layer (the adjoint, NEXT-1) has one real
+exchange: neighbouring ranks' view ranges overlap by the PI-window halo, so
+their sinogram adjoints must be summed there (reduce_view_halos).  Nothing
+here computes the method: reconstruction and adjoint run in libkatsevich.so.
 """
 from __future__ import annotations
 
@@ -76,3 +79,59 @@ def gather_volumes(local, shards, nz: int, dst: int = 0, group=None):
         return torch.cat([parts[s.rank][: s.n_pitches * nz] for s in shards], dim=0)
     dist.gather(buf, None, dst=dst, group=group)
     return None
+
+
+def check_view_ranges(view_ranges):
+    """reduce_view_halos' precondition: increasing starts, overlaps only between neighbours."""
+    starts = [v for v, n in view_ranges if n]
+    if starts != sorted(starts):
+        raise ValueError("view ranges must be in increasing order of their first view")
+    for a in range(len(view_ranges)):
+        for b in range(a + 2, len(view_ranges)):
+            va, na = view_ranges[a]
+            vb, nb = view_ranges[b]
+            if na and nb and vb < va + na:
+                raise ValueError(f"ranks {a} and {b} are not neighbours but their view ranges overlap")
+
+
+def reduce_view_halos(local, view_ranges, group=None):
+    """Sum the overlapping parts of per-rank view arrays in place (owner computes).
+
+    local        this rank's array [nv_r][rows][cols] for views [v0_r, v0_r + nv_r)
+    view_ranges  [(v0_r, nv_r)] for every rank, increasing v0_r; only neighbouring
+                 ranges may overlap (the PI-window halo of a pitch block).
+    After the call every rank holds, over its whole range, the sum of all ranks'
+    contributions — e.g. the sinogram gradient of a pitch-sharded reconstruction,
+    whose per-rank adjoints overlap where the slabs do.  One batched point-to-point
+    exchange with each neighbour (NCCL on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    assert len(view_ranges) == world
+    check_view_ranges(view_ranges)
+    v0, nv = view_ranges[rank]
+
+    def overlap(r):
+        va, na = view_ranges[r]
+        lo, hi = max(v0, va), min(v0 + nv, va + na)
+        return (lo, hi) if na and nv and lo < hi else None
+
+    ops, recv = [], []
+    for nb in (rank - 1, rank + 1):
+        if 0 <= nb < world:
+            o = overlap(nb)
+            if o is None:
+                continue
+            lo, hi = o
+            send = local[lo - v0:hi - v0].contiguous()
+            buf = torch.empty_like(send)
+            ops.append(dist.P2POp(dist.isend, send, nb, group))
+            ops.append(dist.P2POp(dist.irecv, buf, nb, group))
+            recv.append((lo, hi, buf))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for lo, hi, buf in recv:
+        local[lo - v0:hi - v0] += buf
+    return local

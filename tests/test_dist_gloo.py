@@ -70,3 +70,50 @@ def test_gloo_sharded_reconstruction_equals_single_process(world):
     mp.start_processes(_worker, args=(world, _free_port(), "T3", ret), nprocs=world, start_method="spawn")
     assert ret["equal"], "gathered sharded volume differs from the single-process volume"
     assert ret["shape"][0] == 3 * 19
+
+
+def _adj_worker(rank, world, port, cfg_name, ret):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from synth import configs
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = configs.get(cfg_name)
+    s0, sn = cfg["scan_v0"], cfg["scan_nv"]
+    rng = np.random.default_rng(12)
+    y = rng.standard_normal((cfg["n_pitches"] * cfg["nz"], cfg["ny"], cfg["nx"]))   # d loss / d volume
+    shards = kd.pitch_shards(cfg["n_pitches"], world)
+    pv = lambda k: oracle.pitch_slab(cfg, k)
+    ranges = [kd.shard_views(pv, s) for s in shards]
+    me = shards[rank]
+    v0, nv = ranges[rank]
+    ylocal = y[me.first_pitch * cfg["nz"]:(me.first_pitch + me.n_pitches) * cfg["nz"]]
+    # this rank's part of the layer's adjoint over its own views (the GPU would run katsevich_adjoint)
+    g = torch.from_numpy(oracle.adjoint(cfg, ylocal, me.first_pitch, me.n_pitches, v0, nv))
+    kd.reduce_view_halos(g, ranges)
+    ref = oracle.adjoint(cfg, y, 0, cfg["n_pitches"], s0, sn)[v0 - s0:v0 - s0 + nv]
+    ret[rank] = float(np.abs(g.numpy() - ref).max() / np.abs(ref).max())
+    dist.destroy_process_group()
+
+
+def test_sharded_adjoint_with_halo_reduction_equals_single_process():
+    """Training a pitch-sharded layer: the per-rank adjoints summed over the
+    overlapping view halos equal the single-process adjoint on every rank's range."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_adj_worker, args=(world, port, "T2", ret), nprocs=world, join=True)
+    assert set(ret.keys()) == {0, 1}
+    for r in range(world):
+        assert ret[r] <= 1e-12, ret[r]
+
+
+def test_view_range_precondition():
+    kd.check_view_ranges([(0, 10), (6, 10), (14, 10)])            # neighbours overlap: fine
+    with pytest.raises(ValueError):
+        kd.check_view_ranges([(0, 10), (5, 10), (8, 10)])          # ranks 0 and 2 overlap
+    with pytest.raises(ValueError):
+        kd.check_view_ranges([(10, 5), (0, 5)])                     # not increasing
