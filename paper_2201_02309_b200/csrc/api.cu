@@ -520,11 +520,6 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
     b.item_views = vt;
     b.n_items = n_pitches;
     b.vol = const_cast<float *>(vol);
-    {   // bound on one contribution per unit |y|: w <= 1/v*_min, |P| <= max centred quad row (+ step margin)
-        const double vmin = p->g.R - p->t.r_fov;
-        const double pmax = std::max(1.0, 0.5 * (p->g.n_rows + 2) + 2.0);
-        b.adj_bound = (float)(p->t.dlam / (2.0 * kPi) / vmin * pmax * 1.01);
-    }
     {
         LaunchScope ls(p, ST_K5, s);
         if (launch_backproject_adjoint(b, s) != 0) {

@@ -63,16 +63,8 @@ __device__ __forceinline__ float rsqrt_approx(float x)
 __device__ __forceinline__ u64 pk(float a, float b) { u64 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
 __device__ __forceinline__ void upk(u64 v, float &a, float &b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 __device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
-// acc += a * b where (mask & bit) != 0, in place (one predicated FFMA2)
-__device__ __forceinline__ void fma2_if(u64 &acc, u64 a, u64 b, unsigned mask, unsigned bit)
-{
-    asm("{\n\t.reg .pred q;\n\t.reg .b32 m;\n\tand.b32 m, %3, %4;\n\tsetp.ne.b32 q, m, 0;\n\t"
-        "@q fma.rn.f32x2 %0, %1, %2, %0;\n\t}"
-        : "+l"(acc) : "l"(a), "l"(b), "r"(mask), "r"(bit));
-}
 __device__ __forceinline__ void fma2_acc(u64 &acc, u64 a, u64 b) { asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b)); }
 
 __device__ __forceinline__ float4 ldq(u64 addr) { return __ldg(reinterpret_cast<const float4 *>(addr)); }
@@ -569,13 +561,6 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(const __grid_consta
 // (end views, write, column zeroed) warp-uniformly once every lane has closed
 // it.  Without the ~48 accumulator registers three CTAs share an SM.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void tm_ld8(unsigned ta, float (&v)[8])
-{
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-                 : "r"(ta));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void tm_ld8_nowait(unsigned ta, float (&v)[8])
 {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -594,38 +579,6 @@ __device__ __forceinline__ void tm_st8(unsigned ta, const float (&v)[8])
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                  ::"r"(ta), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                  : "memory");
-}
-__device__ __forceinline__ void tm_ld16(unsigned ta, u64 (&v)[8])
-{
-    float a[16];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=f"(a[0]), "=f"(a[1]), "=f"(a[2]), "=f"(a[3]), "=f"(a[4]), "=f"(a[5]), "=f"(a[6]), "=f"(a[7]),
-                   "=f"(a[8]), "=f"(a[9]), "=f"(a[10]), "=f"(a[11]), "=f"(a[12]), "=f"(a[13]), "=f"(a[14]), "=f"(a[15])
-                 : "r"(ta));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = pk(a[2 * j], a[2 * j + 1]);
-}
-__device__ __forceinline__ void tm_st16(unsigned ta, const u64 (&v)[8])
-{
-    float a[16];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) upk(v[j], a[2 * j], a[2 * j + 1]);
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-                 ::"r"(ta), "f"(a[0]), "f"(a[1]), "f"(a[2]), "f"(a[3]), "f"(a[4]), "f"(a[5]), "f"(a[6]), "f"(a[7]),
-                   "f"(a[8]), "f"(a[9]), "f"(a[10]), "f"(a[11]), "f"(a[12]), "f"(a[13]), "f"(a[14]), "f"(a[15])
-                 : "memory");
-}
-__device__ __forceinline__ float tm_ld2sum(unsigned ta)
-{
-    float a, b;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=f"(a), "=f"(b) : "r"(ta));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    return a + b;
-}
-__device__ __forceinline__ void tm_st2zero(unsigned ta)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%1};" ::"r"(ta), "f"(0.f) : "memory");
 }
 __device__ __forceinline__ float tm_ld1(unsigned ta)
 {

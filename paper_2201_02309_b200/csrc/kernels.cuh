@@ -75,7 +75,6 @@ struct BPParams {
     unsigned slot_bytes, col_bytes;   // TMEM kernel: bytes per ring slot / per quad column in a slot// TMEM columns per warp / allocated per CTA (set by the launcher)
     float *vol;               // [n_items][nz][ny][nx] (adjoint: the input)
     float4 *gqT;              // adjoint: quad-adjoint output, layout of gq (accumulated)
-    float adj_bound;          // adjoint: scale x max 1/v* x max(1, max |P|), bound per unit |y| of one contribution
 };
 
 int launch_backproject(const BPParams &p, cudaStream_t s);            // K5; returns the KATS_BP_* variant
