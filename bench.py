@@ -135,6 +135,40 @@ def smem_peak_gbs(sm_mhz):
     return 148 * 128 * sm_mhz * 1e6 / 1e9
 
 
+PAPER_CONTEXT = {
+    "reported": "no reconstruction time or throughput for the Katsevich layer (BASELINE.md section 1)",
+    "closest": "full network training step (sinogram CNN + Katsevich layer + image CNN, fwd+bwd) about 5-6 s, "
+               "batch 1, one 581-view x 16 x 627 slab -> 512x512x10, NVIDIA RTX A6000, TensorFlow 2.5 (P:l.302-304)",
+    "derived_bound": ">= ~9e7 voxel-view updates/s on the A6000 if the whole step were the layer (BASELINE.md)",
+}
+
+
+def n_filtered_views(plan, cfg, n_items, batch):
+    ti = plan.table_info()
+    per_slab = ti["bp_hi"] - ti["bp_lo"] + 1
+    if batch:
+        return per_slab * batch
+    return (n_items - 1) * cfg["views_per_turn"] + per_slab          # filter-once over the union
+
+
+def filter_stage_rooflines(plan, cfg, stats, steps, nu, hbm_peak):
+    """Achieved GB/s of each filter stage's ALGORITHMIC HBM bytes (each input read once, each output
+    written once; g3/g4 of a 256-view chunk may in fact stay in L2) against the HBM peak."""
+    npsi = plan.table_info()["n_psi"]
+    nr, nc = cfg["n_rows"], cfg["n_cols"]
+    by = {"K12_deriv_fwd_rebin": 4.0 * (nu + 2) * nr * nc + 4.0 * nu * npsi * nc,
+          "K3_hilbert": 8.0 * nu * npsi * nc,
+          "K4_bwd_rebin_cos": 4.0 * nu * npsi * nc + 16.0 * nu * nc * (nr + 2)}
+    out = {}
+    for k, b in by.items():
+        ms = stats["busy_ms"].get(k, 0.0) / steps
+        if ms > 0:
+            gbs = b / (ms * 1e-3) / 1e9
+            out[k] = {"ms_per_step": ms, "algorithmic_bytes": b, "achieved_gbs": gbs, "hbm_peak_gbs": hbm_peak,
+                      "frac": gbs / hbm_peak}
+    return out
+
+
 def ncu_traffic(config_name):
     """dram bytes per K5 launch from the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "ncu_k5_traffic.json")
@@ -393,6 +427,9 @@ def run_ours(args):
         "updates_per_step": U_all,
         "gpu_launches": stats["total_launches"],
         "stage_busy_share_of_step": share,
+        "filter_stages": filter_stage_rooflines(plan, cfg, stats, args.steps, n_filtered_views(plan, cfg, n_items, batch),
+                                                peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])),
+        "paper_context": PAPER_CONTEXT,
         "precompute_s": t_pre,
         "roofline": {"bound": "smem", "kernel": bp_kernel, "achieved": achieved_smem, "peak": smem_peak,
                      "unit": "GB/s", "frac": achieved_smem / smem_peak,
@@ -402,6 +439,11 @@ def run_ours(args):
                      "k5_ms_per_launch": k5_ms_launch, "k5_updates_per_s": U_rank / (k5_busy * 1e-3),
                      "peak_source": f"148 SMs x 128 B/clk shared-memory pipe x {peaks.get('sm_max_mhz', 1965.0)} MHz "
                                     f"({src} sm_max); DESIGN.md §5",
+                     "secondary_hbm": None if not ncu_traffic(cfg["name"]) else {
+                         "achieved": ncu_traffic(cfg["name"]) / (iso["k5_ms_per_launch"] * 1e-3) / 1e9
+                         if iso else None,
+                         "peak": peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]), "unit": "GB/s",
+                         "note": "ncu DRAM bytes of one 8-pitch K5 launch / its isolated time: far from bound"},
                      "secondary_alu": {"achieved": achieved_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
                                        "frac": achieved_tflops / fp32_peak,
                                        "flops_per_update": bp_flops_per_update()},

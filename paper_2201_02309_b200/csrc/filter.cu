@@ -242,21 +242,31 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
                      "@!d bra WAIT_%=;\n\t}" ::"r"(bar), "r"((unsigned)(kc & 1)) : "memory");
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    // epilogue: warp w owns accumulator rows (lines) 32w .. 32w+31 = TMEM lanes
-    const int64_t line = line0 + warp * 32 + lane;
-    float *dst = p.g4 + line * nc + par;
-    for (int c = 0; c < NH; c += 16) {
-        float v[16];
+    // epilogue: warp w owns accumulator rows (lines) 32w .. 32w+31 = TMEM lanes.  32 lines x 32
+    // outputs at a time go through padded shared memory (the A tiles are free now), so each line's
+    // outputs leave as one store spanning 256 bytes instead of 32 lines' scattered words.
+    float *stg = reinterpret_cast<float *>(tsm) + warp * 32 * 33;
+    const unsigned trow = tmem + ((unsigned)(warp * 32) << 16);
+    for (int c = 0; c < NH; c += 32) {
+        float v[32];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
                        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
-                     : "r"(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)c));
+                     : "r"(trow + (unsigned)c));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]),
+                       "=f"(v[24]), "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+                     : "r"(trow + (unsigned)(c + 16)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (line < n_lines) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-                if (c + i < nout) dst[2 * (c + i)] = p.sign * v[i];
+        for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+        __syncwarp();
+        const int n = c + lane;                                   // output n of this parity: column 2n + par
+        for (int r = 0; r < 32; ++r) {
+            const int64_t line = line0 + warp * 32 + r;
+            if (line < n_lines && n < nout) p.g4[line * nc + 2 * n + par] = p.sign * stg[r * 33 + lane];
         }
+        __syncwarp();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

@@ -159,9 +159,9 @@ def test_coverage_error_names_pitches():
 
 @pytest.mark.parametrize("variant,kernel", [(None, "k_bp_tmem"), ("window", "k_bp_window"), ("l1", "k_backproject")])
 def test_every_bp_kernel_variant_matches_oracle(variant, kernel, monkeypatch):
-    """Each step-7 kernel (TMEM window = default, register window, chunked L1
-    path) on C1 against the oracle, and the plan reports that
-    the forced variant is the one that ran (katsevich_bp_kernel)."""
+    """Each step-7 kernel (TMEM window = default for C1's 44-slice windows, register
+    window, chunked L1 path) on C1 against the oracle, and the plan
+    reports that the forced variant is the one that ran (katsevich_bp_kernel)."""
     import torch
     if variant is None:
         monkeypatch.delenv("KATS_BP_KERNEL", raising=False)
