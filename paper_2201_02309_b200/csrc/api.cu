@@ -17,7 +17,9 @@ using namespace kats;
 
 namespace {
 
-constexpr int kFilterChunk = 256;   // views per filter chunk (g3/g4 stay L2-resident)
+// Views per filter chunk: 256 keeps a wide-κ chunk's g3/g4 L2-resident (C4: 2 x 24 MB); with few
+// κ-lines a chunk grows so the tensor-core Hilbert launch has enough CTAs to hide its per-CTA latency.
+static int filter_chunk_views(const katsevich_plan *p) { return 256 * std::max(1, 128 / std::max(1, p->t.n_psi)); }
 
 enum Stage { ST_K12 = 0, ST_K3 = 1, ST_K4 = 2, ST_K5 = 3, ST_FIX = 4, ST_OTHER = 5 };
 
@@ -110,7 +112,7 @@ int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
 
 size_t filter_chunk_bytes(const katsevich_plan *p)
 {
-    return 2 * sizeof(float) * (size_t)kFilterChunk * p->t.n_psi * p->g.n_cols;
+    return 2 * sizeof(float) * (size_t)filter_chunk_views(p) * p->t.n_psi * p->g.n_cols;
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -134,7 +136,8 @@ FilterParams filter_params(const katsevich_plan *p)
 // Filter n_out views whose raw data (with ±1 halo) is at sino_v0 - rows*cols
 // .. ; writes gF (and optionally full g3/g4 when dbg3/dbg4 are given).
 int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float4 *gq,
-               float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s, bool overlapped = false)
+               float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s, bool overlapped = false,
+               int64_t slab_views = 0)
 {
     FilterParams f = filter_params(p);
     // concurrently with the TMEM backprojection (3 CTAs x 128 TMEM columns per SM) the two-parity
@@ -144,9 +147,12 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     const size_t qs = quad_view_elems(p);
     const size_t ps = (size_t)p->t.n_psi * p->g.n_cols;
+    const int kFilterChunk = filter_chunk_views(p);
     for (int64_t v0 = 0; v0 < n_out; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, n_out - v0);
-        f.sino = raw_first_out + v0 * rs;
+        f.sino = raw_first_out;                                    // K12 maps view0 + v to its raw view
+        f.view0 = v0;
+        f.slab_views = slab_views;
         f.n_views = nv;
         f.g3 = dbg3 ? dbg3 + v0 * ps : scratch;
         f.g4 = dbg4 ? dbg4 + v0 * ps : scratch + (size_t)kFilterChunk * ps;
@@ -397,6 +403,7 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
 {
     int rc = check_device_plan(p);
     if (rc) return rc;
+    const int kFilterChunk = filter_chunk_views(p);
     if (!sino || !vol || !workspace) return KATS_ERR_NULL;
     if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
     size_t need;
@@ -491,6 +498,7 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
 {
     int rc = check_device_plan(p);
     if (rc) return rc;
+    const int kFilterChunk = filter_chunk_views(p);
     if (!vol || !sino_out || !workspace) return KATS_ERR_NULL;
     if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
     size_t need;
@@ -569,10 +577,11 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     float4 *gq = (float4 *)workspace;
     const size_t qs = quad_view_elems(p);
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
-    for (int b = 0; b < B; ++b) {
-        rc = run_filter(p, slabs + ((size_t)b * nslab + 1) * rs, nbp, gq + (size_t)b * nbp * qs, scratch, nullptr, nullptr, nullptr, s);
-        if (rc) return rc;
-    }
+    // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
+    // keeps its own +-1 halo)
+    rc = run_filter(p, slabs + rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp);
+    if (rc) return rc;
+    (void)nslab;
     BPParams bp = bp_params(p);
     bp.gq = gq;
     bp.gq_views = nbp * B;
@@ -591,6 +600,7 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
 {
     int rc = check_device_plan(p);
     if (rc) return rc;
+    const int kFilterChunk = filter_chunk_views(p);
     if (!host_sino || !host_vol || !workspace) return KATS_ERR_NULL;
     if (n_pitches < 1) return KATS_ERR_ARGUMENT;
     size_t need, base;

@@ -40,7 +40,9 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin(FilterParams p)
     const RebinEntry e = p.fr[i * p.nc + l];
     float out = 0.f;
     if (e.idx >= 0) {
-        const float *gv = p.sino + (size_t)v * p.nr * p.nc;
+        const int64_t g = p.view0 + v;
+        const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+        const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
         float a = g2_at(p, gv, e.idx, l);
         float b = g2_at(p, gv, e.idx + 1, l);
         out = fmaf(e.frac, b - a, a);

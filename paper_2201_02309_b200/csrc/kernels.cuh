@@ -10,7 +10,8 @@ namespace kats {
 
 // Filter steps 1-6 over `n_views` consecutive views.
 struct FilterParams {
-    const float *sino;        // raw view v at sino + v * rows*cols (v relative to the output range; halo at v = -1 and n_views)
+    const float *sino;        // raw data of filtered view g = view0 + v at sino + raw(g) * rows*cols, raw(g) = g (+ 2 per
+                              // preceding slab), halo at raw(g) -+ 1
     int n_views;
     int nr, nc, npsi;
     float inv_2dlam, inv_dalpha, inv_2dalpha;
@@ -25,6 +26,8 @@ struct FilterParams {
     float *gF;                // optional plain filtered views [n_views][nr][nc] (debug), may be null
     float sign;               // K3 output sign: +1 forward, -1 for the adjoint (odd kernel)
     int hilbert_overlap;      // K3 runs next to the TMEM backprojection: keep its TMEM allocation <= 128 columns
+    int64_t view0;            // K12: first filtered view of this launch in the run_filter sequence
+    int64_t slab_views;       // K12: filtered views per slab of a batch (each slab carries its own +-1 halo); 0 = one scan
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
