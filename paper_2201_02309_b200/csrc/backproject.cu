@@ -370,7 +370,7 @@ __device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, floa
 // ---------------------------------------------------------------------------
 template <bool POLY, int W>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, 2) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch;
@@ -1256,11 +1256,13 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
         }
     }
     BPParams q = p;
-    // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 2 CTAs share an SM
-    q.nbatch = kMaxSlots;
-    while (q.nbatch > 2 && backproject_smem_bytes(q) > 100 * 1024) q.nbatch /= 2;
-    const size_t sm = backproject_smem_bytes(q);
     const int W = p.max_active <= 8 ? 8 : p.max_active <= 16 ? 16 : p.max_active <= 32 ? 32 : p.max_active <= 48 ? 48 : 0;
+    // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 3 CTAs (W <= 16, <= 72
+    // registers) or 2 CTAs share an SM
+    const size_t budget = (W > 0 && W <= 16 ? 74 : 100) * 1024;
+    q.nbatch = kMaxSlots;
+    while (q.nbatch > 2 && backproject_smem_bytes(q) > budget) q.nbatch /= 2;
+    const size_t sm = backproject_smem_bytes(q);
     CUtensorMap qmap;
     if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * (p.nr + 2) <= 256 &&
         p.tail_quads <= 4096 &&
