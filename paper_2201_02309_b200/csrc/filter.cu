@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(256) k_hilbert(FilterParams p, int64_t n_lines
 // tcgen05.mma.kind::tf32 (M = 128, N <= 256 per instruction, K = 8) and
 // commits to an mbarrier; the epilogue reads the accumulator with tcgen05.ld.
 // ---------------------------------------------------------------------------
-constexpr int TC_M = 128, TC_KC = 32;
+// operand staging is latency-bound: the per-parity kernel (one CTA per SM, TMEM-limited) stages with
+// 16 warps, the two-parity kernel (two CTAs per SM) with 8; warps w, w+4, ... share a TMEM lane quarter
+constexpr int TC_M = 128, TC_KC = 32, TC_THREADS = 512, TC2_THREADS = 256;
 
 __host__ __device__ inline int hilbert_tc_nh(int nc) { return ((nc + 1) / 2 + 31) / 32 * 32; }
 
@@ -154,19 +156,19 @@ __device__ __forceinline__ uint64_t tc_desc(unsigned saddr)
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-__global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n_lines)
+__global__ void __launch_bounds__(TC_THREADS, 1) k_hilbert_tc(FilterParams p, int64_t n_lines, int nstage)
 {
     extern __shared__ __align__(1024) unsigned char tsm[];
     const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC;
     const int par = blockIdx.y;                                  // output parity
     const int nin = (nc - (1 - par) + 1) / 2, nout = (nc - par + 1) / 2;
     const int64_t line0 = (int64_t)blockIdx.x * TC_M;
-    unsigned char *Ah = tsm, *Al = tsm + TC_M * TC_KC * 4;
-    unsigned char *Bh = Al + TC_M * TC_KC * 4, *Bl = Bh + NH * TC_KC * 4;
-    __shared__ __align__(8) unsigned long long s_bar;
+    // nstage = 2: chunk kc+1 is staged while the tensor core works on chunk kc (one mbarrier per stage)
+    const unsigned stage_bytes = (unsigned)(2 * TC_M * TC_KC * 4 + 2 * NH * TC_KC * 4);
+    __shared__ __align__(8) unsigned long long s_bar[2];
     __shared__ unsigned s_tmem;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+    const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_bar[0]);
     if (warp == 0) {
         unsigned cols = 32;
         while (cols < (unsigned)NH) cols <<= 1;
@@ -175,7 +177,8 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -185,13 +188,22 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
     // instruction descriptor: D f32, A/B tf32, both K-major, M = 128
     const unsigned idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_M >> 4) << 24);
     const float4 *btab = reinterpret_cast<const float4 *>(p.hilbert_tc) + (size_t)par * NK * 2 * NH * TC_KC / 4;
-    const unsigned sAh = (unsigned)__cvta_generic_to_shared(Ah), sAl = (unsigned)__cvta_generic_to_shared(Al);
-    const unsigned sBh = (unsigned)__cvta_generic_to_shared(Bh), sBl = (unsigned)__cvta_generic_to_shared(Bl);
-
     for (int kc = 0; kc < NK; ++kc) {
+        const int st = kc % nstage;
+        if (kc >= nstage) {                                       // the MMAs of chunk kc - nstage read this stage
+            asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
+                         "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
+                         "@!d bra WAIT_%=;\n\t}" ::"r"(bar0 + 8u * st), "r"((unsigned)(((kc - nstage) / nstage) & 1))
+                         : "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        unsigned char *Ah = tsm + st * stage_bytes, *Al = Ah + TC_M * TC_KC * 4;
+        unsigned char *Bh = Al + TC_M * TC_KC * 4, *Bl = Bh + NH * TC_KC * 4;
+        const unsigned sAh = (unsigned)__cvta_generic_to_shared(Ah), sAl = (unsigned)__cvta_generic_to_shared(Al);
+        const unsigned sBh = (unsigned)__cvta_generic_to_shared(Bh), sBl = (unsigned)__cvta_generic_to_shared(Bl);
         // A chunk: lane = (row within an 8-row group, k quad); a warp stores 512 contiguous bytes
         const int rr = lane & 7, kq = lane >> 3;
-        for (int g = warp; g < TC_M / 8; g += 4) {
+        for (int g = warp; g < TC_M / 8; g += TC_THREADS / 32) {
             const int row = g * 8 + rr;
             const int64_t line = line0 + row;
             const float *src = p.g3 + line * nc + (1 - par);
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
         // B chunk (hi, lo): already in the canonical layout in the plan table
         const float4 *bsrc = btab + (size_t)kc * 2 * NH * TC_KC / 4;
         float4 *bdst = reinterpret_cast<float4 *>(Bh);
-        for (int i = tid; i < 2 * NH * TC_KC / 4; i += 128) bdst[i] = __ldg(bsrc + i);
+        for (int i = tid; i < 2 * NH * TC_KC / 4; i += TC_THREADS) bdst[i] = __ldg(bsrc + i);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
         __syncthreads();
         if (tid == 0) {
@@ -235,21 +247,25 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
                                  ::"r"(tmem + (unsigned)n0), "l"(a_l), "l"(b_h), "r"(idesc));
                 }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                         : "memory");
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                         ::"r"(bar0 + 8u * st) : "memory");
         }
-        // the MMAs have read this chunk once the commit lands (phase kc & 1)
+    }
+    {   // the last commit covers every MMA issued before it
+        const int kl = NK - 1;
         asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
                      "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
-                     "@!d bra WAIT_%=;\n\t}" ::"r"(bar), "r"((unsigned)(kc & 1)) : "memory");
+                     "@!d bra WAIT_%=;\n\t}" ::"r"(bar0 + 8u * (kl % nstage)), "r"((unsigned)((kl / nstage) & 1))
+                     : "memory");
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     // epilogue: warp w owns accumulator rows (lines) 32w .. 32w+31 = TMEM lanes.  32 lines x 32
     // outputs at a time go through padded shared memory (the A tiles are free now), so each line's
     // outputs leave as one store spanning 256 bytes instead of 32 lines' scattered words.
+    const int q4 = warp & 3;                                      // TMEM lane quarter = lines 32 q4 ..
     float *stg = reinterpret_cast<float *>(tsm) + warp * 32 * 33;
-    const unsigned trow = tmem + ((unsigned)(warp * 32) << 16);
-    for (int c = 0; c < NH; c += 32) {
+    const unsigned trow = tmem + ((unsigned)(q4 * 32) << 16);
+    for (int c = 32 * (warp >> 2); c < NH; c += 32 * (TC_THREADS / 128)) {
         float v[32];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
@@ -265,7 +281,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
         __syncwarp();
         const int n = c + lane;                                   // output n of this parity: column 2n + par
         for (int r = 0; r < 32; ++r) {
-            const int64_t line = line0 + warp * 32 + r;
+            const int64_t line = line0 + q4 * 32 + r;
             if (line < n_lines && n < nout) p.g4[line * nc + 2 * n + par] = p.sign * stg[r * 33 + lane];
         }
         __syncwarp();
@@ -285,7 +301,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc(FilterParams p, int64_t n
 // takes the odd inputs, parity 1 the even ones.  The epilogue stages 32 lines x
 // 32 outputs per warp in padded shared memory so every line is written as
 // contiguous 128-byte runs.
-__global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t n_lines)
+__global__ void __launch_bounds__(TC2_THREADS, 1) k_hilbert_tc2(FilterParams p, int64_t n_lines)
 {
     extern __shared__ __align__(1024) unsigned char tsm[];
     const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC;
@@ -321,7 +337,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t 
     for (int kc = 0; kc < NK; ++kc) {
         // A: lane = (row in an 8-row group, k quad); 8 consecutive inputs per lane = 4 (even, odd) pairs
         const int rr = lane & 7, kq = lane >> 3;
-        for (int g = warp; g < TC_M / 8; g += 4) {
+        for (int g = warp; g < TC_M / 8; g += TC2_THREADS / 32) {
             const int row = g * 8 + rr;
             const int64_t line = line0 + row;
             const float *src = p.g3 + line * nc;
@@ -350,7 +366,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t 
         for (int par = 0; par < 2; ++par) {
             const float4 *bsrc = tab + (((size_t)par * NK + kc) * 2) * NH * TC_KC / 4;
             float4 *bdst = reinterpret_cast<float4 *>(B + (size_t)par * 2 * bt);
-            for (int i = tid; i < 2 * NH * TC_KC / 4; i += 128) bdst[i] = __ldg(bsrc + i);
+            for (int i = tid; i < 2 * NH * TC_KC / 4; i += TC2_THREADS) bdst[i] = __ldg(bsrc + i);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
@@ -385,9 +401,10 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t 
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     // epilogue: per warp, 32 lines (its TMEM lanes) x 32 output columns at a time through smem
+    const int q4 = warp & 3;                                      // TMEM lane quarter = lines 32 q4 ..
     float *stg = reinterpret_cast<float *>(tsm) + warp * 32 * 33;
-    const unsigned trow = tmem + ((unsigned)(warp * 32) << 16);
-    for (int c = 0; c < NH; c += 16) {
+    const unsigned trow = tmem + ((unsigned)(q4 * 32) << 16);
+    for (int c = 16 * (warp >> 2); c < NH; c += 16 * (TC2_THREADS / 128)) {
         float v0[16], v1[16];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                      : "=f"(v0[0]), "=f"(v0[1]), "=f"(v0[2]), "=f"(v0[3]), "=f"(v0[4]), "=f"(v0[5]), "=f"(v0[6]), "=f"(v0[7]),
@@ -407,7 +424,7 @@ __global__ void __launch_bounds__(128, 1) k_hilbert_tc2(FilterParams p, int64_t 
         __syncwarp();
         const int l = 2 * c + lane;
         for (int r = 0; r < 32; ++r) {
-            const int64_t line = line0 + warp * 32 + r;
+            const int64_t line = line0 + q4 * 32 + r;
             if (line < n_lines && l < nc) p.g4[line * nc + l] = p.sign * stg[r * 33 + lane];
         }
         __syncwarp();
@@ -526,20 +543,23 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
             attr = true;
         }
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
-        k_hilbert_tc2<<<(unsigned)((n_lines + TC_M - 1) / TC_M), 128, smem, s>>>(p, n_lines);
+        k_hilbert_tc2<<<(unsigned)((n_lines + TC_M - 1) / TC_M), TC2_THREADS, smem, s>>>(p, n_lines);
         return;
     }
     if (hilbert_tc_usable(p)) {
         const int NH = hilbert_tc_nh(p.nc);
-        const size_t smem = (size_t)2 * TC_M * TC_KC * 4 + (size_t)2 * NH * TC_KC * 4;
+        const size_t stage = (size_t)2 * TC_M * TC_KC * 4 + (size_t)2 * NH * TC_KC * 4;
+        // double-buffer when two stages fit, except next to the backprojection (keep its footprint small)
+        const int nstage = (!p.hilbert_overlap && 2 * stage <= 220 * 1024) ? 2 : 1;
+        const size_t smem = nstage * stage;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(k_hilbert_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_hilbert_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
             attr = true;
         }
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
         dim3 grid((unsigned)((n_lines + TC_M - 1) / TC_M), 2);
-        k_hilbert_tc<<<grid, 128, smem, s>>>(p, n_lines);
+        k_hilbert_tc<<<grid, TC_THREADS, smem, s>>>(p, n_lines, nstage);
         return;
     }
     const int tpl = 2 * (((p.nc + 1) / 2 + HR - 1) / HR);
