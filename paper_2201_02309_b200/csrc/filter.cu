@@ -50,6 +50,38 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin(FilterParams p)
     p.g3[((size_t)v * p.npsi + i) * p.nc + l] = out;
 }
 
+// Same computation, one thread per (view, column, <= 32 κ-lines) walking the κ-lines in ψ
+// order: neighbouring κ-lines cross the same or adjacent detector rows, so the
+// two g2 rows a sample needs are mostly already in hand (two-row cache);
+// identical arithmetic to g2_at, coalesced along α for the table reads and the
+// g3 stores.
+__global__ void __launch_bounds__(128) k_deriv_fwd_rebin_col(FilterParams p, int seg)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
+    const int i0 = blockIdx.z * seg, i1 = min(i0 + seg, p.npsi);   // this thread's κ-lines
+    if (l >= p.nc) return;
+    const int64_t g = p.view0 + v;
+    const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+    const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
+    float *out = p.g3 + (size_t)v * p.npsi * p.nc + l;
+    int r0 = -2, r1 = -2;                                          // cached rows and their g2
+    float c0 = 0.f, c1 = 0.f;
+    for (int i = i0; i < i1; ++i) {
+        const RebinEntry e = p.fr[i * p.nc + l];
+        float o = 0.f;
+        if (e.idx >= 0) {
+            const int m = e.idx;
+            float a, b;
+            if (m == r0) { a = c0; b = (m + 1 == r1) ? c1 : g2_at(p, gv, m + 1, l); }
+            else if (m == r1) { a = c1; b = g2_at(p, gv, m + 1, l); }
+            else { a = g2_at(p, gv, m, l); b = g2_at(p, gv, m + 1, l); }
+            r0 = m; c0 = a; r1 = m + 1; c1 = b;
+            o = fmaf(e.frac, b - a, a);
+        }
+        out[(size_t)i * p.nc] = o;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: g4 = Σ_l' K[l-l'] g3[l'] along each κ-line (Eq. 12, h_H = 1/(πs) of
 //     Eq. e4, band-limited kernel of DESIGN.md reading A10: only odd
@@ -487,8 +519,12 @@ __global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
 {
-    dim3 grid((p.nc + 127) / 128, p.npsi, p.n_views);
-    k_deriv_fwd_rebin<<<grid, 128, 0, s>>>(p);
+    if (p.nc >= 256) {       // wide detectors (C2, C3, C5 measured); C4's 184 columns: per-sample kernel
+        const int nseg = (p.npsi + 31) / 32, seg = (p.npsi + nseg - 1) / nseg;   // <= 32 κ-lines per thread
+        k_deriv_fwd_rebin_col<<<dim3((p.nc + 127) / 128, p.n_views, nseg), 128, 0, s>>>(p, seg);
+        return;
+    }
+    k_deriv_fwd_rebin<<<dim3((p.nc + 127) / 128, p.npsi, p.n_views), 128, 0, s>>>(p);
 }
 
 size_t hilbert_tc_table_floats(int nc) { return 2 * 2 * (size_t)hilbert_tc_nh(nc) * hilbert_tc_nh(nc); }
