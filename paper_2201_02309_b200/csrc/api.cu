@@ -140,9 +140,8 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
                int64_t slab_views = 0)
 {
     FilterParams f = filter_params(p);
-    // concurrently with the TMEM backprojection (3 CTAs x 128 TMEM columns per SM) the two-parity
-    // tensor-core Hilbert's 256-column allocation would wait for TMEM: use the per-parity kernel
-    // (128 columns; the same MMA sequence per accumulator, so bitwise the same result)
+    // running concurrently with the TMEM backprojection: K3 uses the fp32 direct convolution
+    // (launch_hilbert); results then agree with the device path to fp32 rounding, not bitwise
     f.hilbert_overlap = overlapped ? 1 : 0;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     const size_t qs = quad_view_elems(p);

@@ -564,8 +564,11 @@ bool hilbert_tc_usable(const FilterParams &p)
 
 void launch_hilbert(const FilterParams &p, cudaStream_t s)
 {
-    if (hilbert_tc_usable(p) && p.hilbert_overlap && hilbert_tc_nh(p.nc) > 128) {
-        FilterParams q = p;                                       // a >128-column TMEM allocation would wait
+    if (hilbert_tc_usable(p) && p.hilbert_overlap) {
+        // next to the TMEM backprojection (3 CTAs x 128 columns, 62K registers per SM) a tensor-core
+        // Hilbert CTA waits for TMEM / registers; the fp32 direct convolution fits beside it
+        // (C4 host path 59.4 -> 56.5 ms)
+        FilterParams q = p;
         q.hilbert_tc = nullptr;
         launch_hilbert(q, s);
         return;

@@ -121,13 +121,16 @@ def test_batch_matches_oracle():
 
 
 def test_host_entry_point_matches_device():
+    """The host entry point (copies overlapped; its K3 runs beside the backprojection as the
+    fp32 direct convolution) agrees with the device path to fp32 rounding, and with the oracle."""
     import torch
     cfg, sino, ref, contrast = _case("T3")
     p = _plan(cfg)
     h = p.reconstruct_host(sino, cfg["scan_v0"], 0, cfg["n_pitches"])
     d = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
     torch.cuda.synchronize()
-    assert np.array_equal(h.numpy(), d.cpu().numpy())
+    hh, dd = h.numpy().astype(np.float64), d.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(hh - dd) <= 1e-6 * np.linalg.norm(dd)
     _check(h.numpy(), ref, contrast)
 
 
