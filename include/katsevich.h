@@ -158,6 +158,18 @@ int katsevich_adjoint(katsevich_plan *plan, const float *vol, int32_t first_pitc
                       float *sino_out, int64_t s0, int64_t sn, void *workspace, size_t workspace_bytes,
                       void *cuda_stream);
 
+/* Workspace for katsevich_adjoint_batch. */
+int katsevich_adjoint_batch_workspace_bytes(const katsevich_plan *plan, int32_t B, size_t *bytes);
+
+/* Adjoint of katsevich_reconstruct_batch (the training-shaped workload: B
+ * independent one-pitch slabs, the layer the paper trains through):
+ *   vols       [B][nz][ny][nx] fp32, device (input)
+ *   slabs_out  [B][n_slab][rows][cols] fp32, device (output, overwritten), n_slab
+ *              as katsevich_pitch_views reports for pitch 0 (each slab with its
+ *              own +-1 halo).  Asynchronous; reproducible to rounding. */
+int katsevich_adjoint_batch(katsevich_plan *plan, const float *vols, int32_t B, float *slabs_out, void *workspace,
+                            size_t workspace_bytes, void *cuda_stream);
+
 /* ---- data generation (NEXT-3: training-shaped inputs) ---- */
 
 /* Exact line integrals of an ellipsoid phantom along the plan's helical scan

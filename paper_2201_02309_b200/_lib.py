@@ -64,6 +64,8 @@ SIGNATURES = {
     "katsevich_bp_kernel": (ctypes.c_int, [_P]),
     "katsevich_adjoint_workspace_bytes": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_SZ)]),
     "katsevich_adjoint": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _I64, _I64, _P, _SZ, _P]),
+    "katsevich_adjoint_batch_workspace_bytes": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_SZ)]),
+    "katsevich_adjoint_batch": (ctypes.c_int, [_P, _P, _I32, _P, _P, _SZ, _P]),
     "katsevich_project_ellipsoids": (ctypes.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),
     "katsevich_project_volume": (ctypes.c_int, [_P, _P, _I32, ctypes.c_double, ctypes.c_double, _I64, _I64, _P,
                                                 _PI64, _P]),

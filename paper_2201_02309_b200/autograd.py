@@ -31,3 +31,22 @@ def reconstruct(plan: Plan, sino: torch.Tensor, sino_first_view: int, first_pitc
                 n_pitches: int = 1) -> torch.Tensor:
     """Differentiable reconstruction: gradients flow to `sino` through the adjoint."""
     return KatsevichReconstruct.apply(sino, plan, sino_first_view, first_pitch, n_pitches)
+
+
+class KatsevichReconstructBatch(torch.autograd.Function):
+    """vols = A(slabs) for B independent one-pitch slabs (the paper's training workload);
+    d loss / d slabs = A^T (d loss / d vols) (katsevich_adjoint_batch)."""
+
+    @staticmethod
+    def forward(ctx, slabs: torch.Tensor, plan: Plan):
+        ctx.plan = plan
+        return plan.reconstruct_batch(slabs.detach().contiguous(), stream=torch.cuda.current_stream())
+
+    @staticmethod
+    def backward(ctx, grad_vols: torch.Tensor):
+        return ctx.plan.adjoint_batch(grad_vols.detach().contiguous(), stream=torch.cuda.current_stream()), None
+
+
+def reconstruct_batch(plan: Plan, slabs: torch.Tensor) -> torch.Tensor:
+    """Differentiable batch reconstruction [B][n_slab][rows][cols] -> [B][nz][ny][nx]."""
+    return KatsevichReconstructBatch.apply(slabs, plan)

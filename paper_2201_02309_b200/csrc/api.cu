@@ -366,6 +366,15 @@ int katsevich_adjoint_workspace_bytes(const katsevich_plan *p, int32_t n_pitches
     return KATS_OK;
 }
 
+int katsevich_adjoint_batch_workspace_bytes(const katsevich_plan *p, int32_t B, size_t *bytes)
+{
+    int rc = katsevich_workspace_bytes(p, B, bytes);
+    if (rc) return rc;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    *bytes += align_up(sizeof(float) * rs * (size_t)(p->t.bp_hi - p->t.bp_lo + 1) * B);   // g1^T of every view
+    return KATS_OK;
+}
+
 // two low-priority streams for per-pitch backprojections and one highest-priority stream for
 // the filter chunks that must finish before the next pitch's backprojection can start
 static int ensure_bp_streams(katsevich_plan *p)
@@ -554,6 +563,69 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
         KCHECK(p, cudaGetLastError());
     }
     { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nu, sino_out + (u0 - 1 - s0) * rs, s); }
+    KCHECK(p, cudaGetLastError());
+    return KATS_OK;
+}
+
+// Adjoint of katsevich_reconstruct_batch: vols [B][nz][ny][nx] -> slabs_out [B][n_slab][rows][cols]
+// (overwritten).  Step 7^T over the B slabs as items, the filter transposes over all slabs' views
+// in one chunked pass, the difference stencils transposed inside each slab.
+int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, float *slabs_out, void *workspace,
+                            size_t workspace_bytes, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!vols || !slabs_out || !workspace) return KATS_ERR_NULL;
+    if (B < 1) return KATS_ERR_ARGUMENT;
+    size_t need;
+    katsevich_adjoint_batch_workspace_bytes(p, B, &need);
+    if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
+    const int kFilterChunk = filter_chunk_views(p);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const HostTables &t = p->t;
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t qs = quad_view_elems(p);
+    const int64_t nbp = t.bp_hi - t.bp_lo + 1, nu = nbp * B;
+    float4 *qT = (float4 *)workspace;
+    const size_t qbytes = align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nu));
+    float *scratch = (float *)((char *)workspace + qbytes);
+    float *g1T = (float *)((char *)workspace + qbytes + align_up(filter_chunk_bytes(p)));
+    KCHECK(p, cudaMemsetAsync(qT, 0, sizeof(float4) * qs * (size_t)nu, s));
+    KCHECK(p, cudaMemsetAsync(slabs_out, 0, sizeof(float) * rs * (size_t)(nbp + 2) * B, s));
+    BPParams b = bp_params(p);
+    b.gqT = qT;
+    b.gq_views = nu;
+    b.off0 = -t.bp_lo;
+    b.item_views = nbp;
+    b.n_items = B;
+    b.vol = const_cast<float *>(vols);
+    {
+        LaunchScope ls(p, ST_K5, s);
+        if (launch_backproject_adjoint(b, s) != 0) {
+            p->detail = "adjoint backprojection: plan not supported (non-monotone PI windows)";
+            return KATS_ERR_ARGUMENT;
+        }
+    }
+    KCHECK(p, cudaGetLastError());
+    FilterParams f = filter_params(p);
+    const size_t ps = (size_t)t.n_psi * p->g.n_cols;
+    for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
+        const int nv = (int)std::min<int64_t>(kFilterChunk, nu - v0);
+        f.n_views = nv;
+        f.g4 = scratch + (size_t)kFilterChunk * ps;
+        f.g3 = scratch;
+        { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos_T(f, qT + v0 * qs, s); }
+        KCHECK(p, cudaGetLastError());
+        FilterParams h = f;
+        h.g3 = f.g4;
+        h.g4 = f.g3;
+        h.sign = -1.f;
+        { LaunchScope ls(p, ST_K3, s); launch_hilbert(h, s); }
+        KCHECK(p, cudaGetLastError());
+        { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
+        KCHECK(p, cudaGetLastError());
+    }
+    { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nbp, slabs_out, s, B); }
     KCHECK(p, cudaGetLastError());
     return KATS_OK;
 }

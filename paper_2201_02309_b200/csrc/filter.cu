@@ -685,10 +685,13 @@ __global__ void __launch_bounds__(128) k_deriv_T(FilterParams p, const float *__
                                                  float *__restrict__ out)
 {
     const int l = blockIdx.x * blockDim.x + threadIdx.x, m = blockIdx.y;
-    const int64_t vr = blockIdx.z;                                // raw view - (u0 - 1)
+    const int64_t per = nu + 2;                                   // raw views of an item (slab of a batch)
+    const int64_t item = blockIdx.z / per, vr = blockIdx.z - item * per;   // raw view - (u0 - 1)
     if (l >= p.nc) return;
     const int nc = p.nc;
     const size_t rs = (size_t)p.nr * nc;
+    g1T += (size_t)item * nu * rs;                                // the stencils stay inside the item
+    out += (size_t)item * per * rs;
     auto g = [&](int64_t f, int ll) -> float {                    // g1^T of filtered view f (relative to u0)
         return (f >= 0 && f < nu) ? g1T[(size_t)f * rs + (size_t)m * nc + ll] : 0.f;
     };
@@ -712,9 +715,9 @@ void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s)
     k_fwd_rebin_T<<<dim3((p.nc + 127) / 128, p.n_views), 128, 0, s>>>(p, g1T);
 }
 
-void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s)
+void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s, int items)
 {
-    k_deriv_T<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)(nu + 2)), 128, 0, s>>>(p, g1T, nu, out);
+    k_deriv_T<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)((nu + 2) * items)), 128, 0, s>>>(p, g1T, nu, out);
 }
 
 }  // namespace kats

@@ -38,7 +38,8 @@ void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s);     // K4:  Eq
 // adjoint (NEXT-1)
 void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s);   // quad^T + K4^T
 void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s);            // K2^T + length weight
-void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s);  // K1^T
+void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s,
+                    int items = 1);  // K1^T (items: slabs of a batch, nu filtered views each)
 
 // Step 7 backprojection over `n_items`
 // independent pitches/slabs sharing the periodic tables.

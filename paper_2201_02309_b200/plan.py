@@ -230,6 +230,23 @@ class Plan:
                                             _stream_handle(stream)))
         return (out, counts, M) if return_counts else out
 
+    def adjoint_batch(self, vols, out=None, stream=None):
+        """Transpose of reconstruct_batch (katsevich_adjoint_batch): vols cuda float32
+        [B][nz][ny][nx] -> slab adjoints [B][n_slab][rows][cols]."""
+        import torch
+        assert vols.is_cuda and vols.dtype == torch.float32 and vols.is_contiguous()
+        B = vols.shape[0]
+        g = self.geometry
+        nv = self.pitch_views(0)[1]
+        if out is None:
+            out = torch.empty((B, nv, g.n_rows, g.n_cols), dtype=torch.float32, device=vols.device)
+        b = ctypes.c_size_t()
+        self._check(lib().katsevich_adjoint_batch_workspace_bytes(self._h, B, ctypes.byref(b)))
+        ws = self._workspace(b.value)
+        self._check(lib().katsevich_adjoint_batch(self._h, _ptr(vols), B, _ptr(out), _ptr(ws), ws.numel(),
+                                                  _stream_handle(stream)))
+        return out
+
     def filter(self, sino, sino_first_view: int, out_first_view: int, n_out: int, stages=("gF",), stream=None):
         import torch
         g = self.geometry

@@ -90,3 +90,35 @@ def test_autograd_gradient_is_the_adjoint():
     assert torch.allclose(x.grad, ref, rtol=0, atol=1e-6 * float(ref.abs().max()))
     # and the forward value is the plain reconstruction
     assert torch.equal(vol.detach(), p.reconstruct(x.detach(), s0, 0, npit))
+
+
+def test_adjoint_batch_matches_oracle_and_autograd():
+    """katsevich_adjoint_batch (training-shaped batches of one-pitch slabs) against the
+    oracle adjoint of each slab, the batch dot-product identity, and autograd."""
+    import torch
+    import paper_2201_02309_b200 as k
+    from oracle import oracle
+    from synth import configs
+    cfg = configs.get("T2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    B = 3
+    rng = np.random.default_rng(21)
+    y = rng.standard_normal((B, cfg["nz"], cfg["ny"], cfg["nx"])).astype(np.float32)
+    got = p.adjoint_batch(torch.from_numpy(y).cuda()).cpu().numpy().astype(np.float64)
+    for b in range(B):
+        ref = oracle.adjoint(cfg, y[b].astype(np.float64), 0, 1, v0, nv)
+        e = np.linalg.norm(got[b] - ref) / np.linalg.norm(ref)
+        assert e <= 1e-4, f"slab {b}: rel L2 {e:.3e}"
+    x = torch.from_numpy(rng.standard_normal((B, nv, cfg["n_rows"], cfg["n_cols"])).astype(np.float32)).cuda()
+    yy = torch.from_numpy(y).cuda()
+    ax = p.reconstruct_batch(x)
+    aty = p.adjoint_batch(yy)
+    lhs = float((ax.double() * yy.double()).sum())
+    rhs = float((x.double() * aty.double()).sum())
+    scale = float(ax.double().norm() * yy.double().norm())
+    assert abs(lhs - rhs) <= 1e-5 * scale
+    x.requires_grad_(True)
+    loss = (k.autograd.reconstruct_batch(p, x) * yy).sum()
+    loss.backward()
+    assert torch.allclose(x.grad, aty, rtol=0, atol=1e-6 * float(aty.abs().max()))
