@@ -893,6 +893,7 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
     int *boxc = reinterpret_cast<int *>(ys + TX * TY * nzp);
     __shared__ int s_k0, s_k1;
     __shared__ unsigned s_b[2];                                        // view bounds (float bits, >= 0)
+    __shared__ int s_rect[4];                                          // box columns / quad rows touched in the view
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
     const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
@@ -901,7 +902,10 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
     const size_t plane = (size_t)p.nx * p.ny;
     const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
     const int2 *pik = p.pi_k + col;
-    if (tid == 0) { s_k0 = INT_MAX; s_k1 = INT_MIN; s_b[0] = 0u; s_b[1] = 0u; }
+    if (tid == 0) {
+        s_k0 = INT_MAX; s_k1 = INT_MIN; s_b[0] = 0u; s_b[1] = 0u;
+        s_rect[0] = INT_MAX; s_rect[1] = -1; s_rect[2] = INT_MAX; s_rect[3] = -1;
+    }
     for (int i = tid; i < 2 * cpy; i += TX * TY) pl[i] = 0;
     float ycmax = 0.f;                                                 // this column's max |scale * y|
     {
@@ -954,7 +958,7 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
         }
         const bool work = active_col && t_hi >= t_lo && k <= K1;
         float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f, b01 = 0.f, b23 = 0.f;
-        int ci = 0;
+        int ci = 0, rlo = 0, rhi = -1;
         if (work) {
             const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
             const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
@@ -980,14 +984,25 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             base = fmaf(sc, -vg.z, p.row_cc);
             ci = min(max(l - boxc[n], 0), BW - 1);
             b01 = ycmax * inv_v * 1.0001f;
-            const float pm = fmaxf(fabsf(fmaf((float)t_lo, step, base)), fabsf(fmaf((float)t_hi, step, base)));
-            b23 = b01 * pm * 1.0001f;
+            const float plo = fmaf((float)t_lo, step, base), phi = fmaf((float)t_hi, step, base);
+            b23 = b01 * fmaxf(fabsf(plo), fabsf(phi)) * 1.0001f;
+            rlo = (int)(__float_as_uint(plo + p.qmagic) - kMagicBits);    // rows grow with t
+            rhi = (int)(__float_as_uint(phi + p.qmagic) - kMagicBits);
         }
         const unsigned r01 = __reduce_max_sync(0xffffffffu, __float_as_uint(b01));
         const unsigned r23 = __reduce_max_sync(0xffffffffu, __float_as_uint(b23));
-        if (lane == 0) { atomicMax(&s_b[0], r01); atomicMax(&s_b[1], r23); }
+        const int c_lo = __reduce_min_sync(0xffffffffu, work ? ci : INT_MAX);
+        const int c_hi = __reduce_max_sync(0xffffffffu, work ? ci : -1);
+        const int q_lo = __reduce_min_sync(0xffffffffu, work ? rlo : INT_MAX);
+        const int q_hi = __reduce_max_sync(0xffffffffu, work ? rhi : -1);
+        if (lane == 0) {
+            atomicMax(&s_b[0], r01); atomicMax(&s_b[1], r23);
+            atomicMin(&s_rect[0], c_lo); atomicMax(&s_rect[1], c_hi);
+            atomicMin(&s_rect[2], q_lo); atomicMax(&s_rect[3], q_hi);
+        }
         __syncthreads();
         const float B01 = __uint_as_float(s_b[0]), B23 = __uint_as_float(s_b[1]);
+        const int rc0 = s_rect[0], rc1 = s_rect[1], rq0 = max(s_rect[2], 0), rq1 = min(s_rect[3], NQ - 1);
         const float S01 = B01 > 0.f ? 2097152.f / B01 : 0.f, S23 = B23 > 0.f ? 2097152.f / B23 : 0.f;
         if (work) {
             int *c0 = pl + (lane & 1) * cpy + ci * NQP;                  // odd lanes: the shifted copy
@@ -1007,16 +1022,22 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             }
         }
         __syncthreads();
-        if (tid == 0) { s_b[0] = 0u; s_b[1] = 0u; }                      // bounds of the next view
+        if (tid == 0) {                                                // bounds of the next view
+            s_b[0] = 0u; s_b[1] = 0u;
+            s_rect[0] = INT_MAX; s_rect[1] = -1; s_rect[2] = INT_MAX; s_rect[3] = -1;
+        }
         const float i01 = B01 * (1.f / 2097152.f), i23 = B23 * (1.f / 2097152.f);
         float4 *dst = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)boxc[n] * NQ;
-        for (int i = tid; i < BW * NQ; i += TX * TY) {
-            const int cc = i / NQ, j = cc * NQP + (i - cc * NQ);
+        // only the rectangle of box columns x quad rows the view touched
+        const int nqr = rq1 - rq0 + 1, ntouch = rc1 >= rc0 && nqr > 0 ? (rc1 - rc0 + 1) * nqr : 0;
+        for (int i = tid; i < ntouch; i += TX * TY) {
+            const int cc = rc0 + i / nqr, rr = rq0 + (i - (i / nqr) * nqr);
+            const int j = cc * NQP + rr;
             int *q0 = pl + j, *q1 = pl + cpy + j;
             const int a = q0[0] + q1[0], b = q0[nbox] + q1[nbox], c = q0[2 * nbox] + q1[2 * nbox],
                       d = q0[3 * nbox] + q1[3 * nbox];
             if (a | b | c | d) {
-                red_add4(dst + i, (float)a * i01, (float)b * i01, (float)c * i23, (float)d * i23);
+                red_add4(dst + cc * NQ + rr, (float)a * i01, (float)b * i01, (float)c * i23, (float)d * i23);
                 q0[0] = 0; q0[nbox] = 0; q0[2 * nbox] = 0; q0[3 * nbox] = 0;
                 q1[0] = 0; q1[nbox] = 0; q1[2 * nbox] = 0; q1[3 * nbox] = 0;
             }
