@@ -635,6 +635,11 @@ void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
 //   -> K1^T: transposed view/α difference stencils (gathered, k_deriv_T).
 // A thread owns one detector column of a view in the scatters, so no atomics.
 // ---------------------------------------------------------------------------
+// k_fwd_rebin_T: the scatter target (one column of g1^T) is private to the thread; it is accumulated
+// in shared memory ([entry][thread]: conflict-free) and written out once, coalesced across α.
+// (K4^T keeps its global read-modify-write: its npsi-deep column would cost occupancy.)
+constexpr int KT_THREADS = 64;
+
 __global__ void __launch_bounds__(128) k_bwd_rebin_cos_T(FilterParams p, const float4 *__restrict__ qT)
 {
     const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
@@ -662,22 +667,25 @@ __global__ void __launch_bounds__(128) k_bwd_rebin_cos_T(FilterParams p, const f
     }
 }
 
-__global__ void __launch_bounds__(128) k_fwd_rebin_T(FilterParams p, float *__restrict__ g1T)
+__global__ void __launch_bounds__(KT_THREADS) k_fwd_rebin_T(FilterParams p, float *__restrict__ g1T)
 {
+    extern __shared__ float acc_s[];                               // [nr][KT_THREADS]
     const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
-    if (l >= p.nc) return;
     const int nc = p.nc;
-    float *o = g1T + (size_t)v * p.nr * nc + l;
-    for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] = 0.f;
-    const float *g3T = p.g3 + (size_t)v * p.npsi * nc + l;
-    for (int i = 0; i < p.npsi; ++i) {
-        const RebinEntry e = p.fr[i * nc + l];
-        if (e.idx < 0) continue;
-        const float t = g3T[(size_t)i * nc];
-        o[(size_t)e.idx * nc] += (1.f - e.frac) * t;
-        o[(size_t)(e.idx + 1) * nc] += e.frac * t;
+    float *acc = acc_s + threadIdx.x;
+    for (int m = 0; m < p.nr; ++m) acc[m * KT_THREADS] = 0.f;
+    if (l < nc) {
+        const float *g3T = p.g3 + (size_t)v * p.npsi * nc + l;
+        for (int i = 0; i < p.npsi; ++i) {
+            const RebinEntry e = p.fr[i * nc + l];
+            if (e.idx < 0) continue;
+            const float t = g3T[(size_t)i * nc];
+            acc[e.idx * KT_THREADS] += (1.f - e.frac) * t;
+            acc[(e.idx + 1) * KT_THREADS] += e.frac * t;
+        }
+        float *o = g1T + (size_t)v * p.nr * nc + l;
+        for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] = acc[m * KT_THREADS] * __ldg(p.wlen + m);
     }
-    for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] *= __ldg(p.wlen + m);
 }
 
 // raw view v (absolute u0 - 1 .. u0 + nu) <- g1^T of filtered views v-1, v, v+1 (those in [u0, u0+nu))
@@ -712,7 +720,8 @@ void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_
 
 void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s)
 {
-    k_fwd_rebin_T<<<dim3((p.nc + 127) / 128, p.n_views), 128, 0, s>>>(p, g1T);
+    k_fwd_rebin_T<<<dim3((p.nc + KT_THREADS - 1) / KT_THREADS, p.n_views), KT_THREADS,
+                    sizeof(float) * p.nr * KT_THREADS, s>>>(p, g1T);
 }
 
 void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s, int items)
