@@ -206,10 +206,19 @@ BPParams bp_params(const katsevich_plan *p)
         const double r_near = g.R - p->t.r_fov;
         const double step_max = g.D / (r_near * g.d_w) * (g.pitch / g.nz_per_pitch);
         b.tail_quads = 8 + (int)std::ceil(3.0 * step_max) + 2;
-        b.pad_quads = 12 + (int)std::ceil((p->t.warp_span + 8) * step_max);   // TMEM kernel: warp-union groups
+        // TMEM kernel: warp-union groups of one view / of two views
+        b.pad_quads = 12 + (int)std::ceil((p->t.warp_span + 8) * step_max);
+        b.pad_quads2 = 12 + (int)std::ceil((std::max(p->t.warp_span, p->t.warp_span2) + 8) * step_max);
+    }
+    {   // staged column pitch: 3 or 5 (mod 8) quads, so lanes on neighbouring detector columns
+        // (C3: ~1 column per voxel) read different 16-B bank groups; the extra rows are TMA zero fill
+        int nq = g.n_rows + 2;
+        while ((nq & 7) != 3 && (nq & 7) != 5) ++nq;
+        b.nq_s = 2 * nq <= 256 ? nq : g.n_rows + 2;
     }
     b.zero = 0u;
     b.warp_span = p->t.warp_span;
+    b.warp_span2 = p->t.warp_span2;
     b.fp_rows = p->t.fp_rows;
     const char *ev = std::getenv("KATS_BP_KERNEL");          // "l1" forces the L1-path kernel (A/B tests)
     b.staged = !(ev && std::string(ev) == "l1");
@@ -307,10 +316,10 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
     p->precomputed = true;
     if (const char *v = std::getenv("KATS_VERBOSE"); v && *v == '1')
         std::fprintf(stderr, "[katsevich] n_psi %d, bp views [%lld, %lld], w_L %.6f, interior_in_detector %d, "
-                             "footprint box %d cols x %d quad rows, column box %d cols, max active slices %d, monotone %d, warp span %d\n",
+                             "footprint box %d cols x %d quad rows, column box %d cols, max active slices %d, monotone %d, warp span %d (pairs %d)\n",
                      p->t.n_psi, (long long)p->t.bp_lo, (long long)p->t.bp_hi, p->t.w_L,
                      (int)p->t.interior_in_detector, p->t.fp_cols, p->t.fp_rows, p->t.fp_cols_column,
-                     p->t.max_active, (int)p->t.windows_monotone, p->t.warp_span);
+                     p->t.max_active, (int)p->t.windows_monotone, p->t.warp_span, p->t.warp_span2);
     return p->t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }
 

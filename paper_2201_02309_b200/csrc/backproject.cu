@@ -373,7 +373,7 @@ template <bool POLY, int W>
 __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch;
+    const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch;          // NQ: staged column pitch (quads)
     const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged view (128-B aligned)
     const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
     float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
@@ -600,17 +600,17 @@ __host__ __device__ inline size_t tmem_head_bytes(const BPParams &p)
 
 size_t tmem_smem_bytes(const BPParams &p)
 {
-    const int vq = (p.fp_cols_column * (p.nr + 2) + 7) & ~7;
+    const int vq = (p.fp_cols_column * p.nq_s + 7) & ~7;
     return tmem_head_bytes(p) + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
            16 * (size_t)p.pad_quads;
 }
 
-template <bool POLY>
+template <bool POLY, int VP>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
 __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant__ CUtensorMap qmap, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int BW = p.fp_cols_column, NQ = p.nr + 2, S = p.nbatch, Wc = p.tmem_cols;
+    const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch, Wc = p.tmem_cols;   // NQ: staged column pitch
     const int vq = (BW * NQ + 7) & ~7;
     const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
     const size_t head = tmem_head_bytes(p);                   // pad for reads below the first column
@@ -721,21 +721,83 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
         tm_st1(tc, 0.f);
     };
 
+    // advance the lane's window [t_lo, t_hi] to view k (opens at k_first + 1, closes at k_last)
+    auto advance = [&](int k) {
+        if (!active_col) return;
+        while (k >= next_open) {
+            ++t_hi;
+            if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+            next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
+        }
+        while (k >= next_close) {
+            ++t_lo;
+            next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
+        }
+    };
+    // the lane's sample geometry for a view: column weights (1/v* folded in), centred row position
+    // of slice 0 and its per-slice step, box column
+    auto geom = [&](const float4 vg, int n, float &w0, float &w1, float &base, float &step, int &ci) {
+        const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+        const float u = fmaf(y, vg.x, -x * vg.y);
+        const float inv_v = rcp_approx(vstar);
+        float colpos;
+        if (POLY) {
+            const float tt = u * inv_v, q = tt * tt;
+            float a = p.at[6];
+            a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+            a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+            colpos = fmaf(tt, a, p.col_c);
+        } else {
+            colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+        }
+        const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
+        const int l = __float2int_rz(cp);
+        const float fa = cp - __int2float_rn(l);
+        w1 = fa * inv_v;
+        w0 = inv_v - w1;
+        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+        step = sc * p.dz;
+        base = fmaf(sc, -vg.z, p.row_cc);                       // slice 0 (centred quad-row position)
+        ci = min(max(l - boxc[n], 0), BW - 1);
+    };
+    const unsigned wmask = (unsigned)Wc - 1u;                    // Wc is a power of two
+    // 8 samples of one view for the group's slices (PM: packed positions of slices j, j+1)
+    auto sample8 = [&](unsigned colbase, u64 PM, u64 S2, float (&v)[8][2]) {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+            const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
+            float q0, q1, p0, p1;
+            upk(Q, q0, q1);
+            upk(PM, p0, p1);
+            const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+            const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+            upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), v[j][0], v[j][1]);
+            upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), v[j + 1][0], v[j + 1][1]);
+            PM = add2(PM, S2);
+        }
+    };
+    // a8 += w0 v0 + w1 v1 for the slices of the group inside the lane's window (fast: every slice)
+    auto accum8 = [&](float (&a8)[8], const float (&v)[8][2], float w0, float w1, bool fast, int tb, int lo, int hi,
+                      bool work) {
+        if (fast) {
+            // all 8 slices open in every working lane; idle lanes add exactly 0 (w = 0, finite reads)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
+        } else {
+            const int jl = min(max(lo - tb, 0), 8), jh = min(max(hi - tb + 1, 0), 8);
+            const unsigned mask = work ? ((0xffu << jl) & ((1u << jh) - 1u)) : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (mask & (1u << j)) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
+        }
+    };
+
+    if constexpr (VP == 1) {
     for (int n = 0; n < NV; ++n) {
         const int k = KC0 + n;
         const int sl = n & (S - 1);                   // ring size is a power of two
         mbar_wait(full0 + 8u * sl, (unsigned)(n >> p.lg_nbatch) & 1u);
-        if (active_col) {
-            while (k >= next_open) {
-                ++t_hi;
-                if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
-                next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
-            }
-            while (k >= next_close) {                                // closes at k_last (end view)
-                ++t_lo;
-                next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
-            }
-        }
+        advance(k);
         const int lo_all = __reduce_min_sync(0xffffffffu, active_col ? t_lo : INT_MAX);
         while (t_f < lo_all && t_f < p.nz) flush_slice(t_f++);
         const bool work = active_col && t_hi >= t_lo && k <= K1;
@@ -744,39 +806,14 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
         if (hi_w >= lo_w) {
             float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f;
             int ci = 0;                                              // idle lanes read column 0 of the slot
-            if (work) {
-                const float4 vg = s_vg[sl];
-                const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
-                const float u = fmaf(y, vg.x, -x * vg.y);
-                const float inv_v = rcp_approx(vstar);
-                float colpos;
-                if (POLY) {
-                    const float tt = u * inv_v, q = tt * tt;
-                    float a = p.at[6];
-                    a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
-                    a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
-                    colpos = fmaf(tt, a, p.col_c);
-                } else {
-                    colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
-                }
-                const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
-                const int l = __float2int_rz(cp);
-                const float fa = cp - __int2float_rn(l);
-                w1 = fa * inv_v;
-                w0 = inv_v - w1;
-                const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
-                step = sc * p.dz;
-                base = fmaf(sc, -vg.z, p.row_cc);                   // slice 0 (centred quad-row position)
-                ci = min(max(l - boxc[n], 0), BW - 1);
-            }
+            if (work) geom(s_vg[sl], n, w0, w1, base, step, ci);
             // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
             const unsigned colbase = (slot0 + (unsigned)sl * p.slot_bytes + (unsigned)ci * p.col_bytes) ^ p.zero;
             // slices open in every working lane: groups inside [lo_full, hi_full] need no mask
             const int lo_full = __reduce_max_sync(0xffffffffu, work ? t_lo : INT_MIN);
             const int hi_full = __reduce_min_sync(0xffffffffu, work ? t_hi : INT_MAX);
-            const u64 S2 = pk(2.f * step, 2.f * step);
+            const u64 S2 = pk(2.f * step, 2.f * step), S8 = pk(8.f * step, 8.f * step);
             const int m0 = lo_w & ~7;
-            const unsigned wmask = (unsigned)Wc - 1u;                // Wc is a power of two
             unsigned cc = (unsigned)m0 & wmask;                      // column of the group's first slice
             // every read stays within (warp span + 7) slices of an open slice: the pads cover that
             u64 PM = pk(fmaf((float)m0, step, base), fmaf((float)(m0 + 1), step, base));
@@ -784,36 +821,76 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
                 float a8[8];
                 tm_ld8_nowait(tw + cc, a8);
                 float v[8][2];
-#pragma unroll
-                for (int j = 0; j < 8; j += 2) {
-                    const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
-                    float q0, q1, p0, p1;
-                    upk(Q, q0, q1);
-                    upk(PM, p0, p1);
-                    const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
-                    const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                    upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), v[j][0], v[j][1]);
-                    upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), v[j + 1][0], v[j + 1][1]);
-                    PM = add2(PM, S2);
-                }
+                sample8(colbase, PM, S2, v);
+                PM = add2(PM, S8);
                 tm_wait_ld8(a8);
-                if (tb >= lo_full && tb + 7 <= hi_full) {
-                    // all 8 slices open in every working lane; idle lanes add exactly 0 (w = 0, finite reads)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
-                } else {
-                    const int jl = min(max(t_lo - tb, 0), 8), jh = min(max(t_hi - tb + 1, 0), 8);
-                    const unsigned mask = work ? ((0xffu << jl) & ((1u << jh) - 1u)) : 0u;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (mask & (1u << j)) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
-                }
+                accum8(a8, v, w0, w1, tb >= lo_full && tb + 7 <= hi_full, tb, t_lo, t_hi, work);
                 tm_st8(tw + cc, a8);
                 cc = (cc + 8u) & wmask;
             }
             tm_wait_st();
         }
         mbar_arrive(empty0 + 8u * sl);
+    }
+    } else {
+    // two consecutive views (A = k, B = k + 1) per pass: one window walk, flush, group setup and
+    // TMEM load/store per group for both (the host sized Wc and the pads with the pair span)
+    for (int n = 0; n < NV; n += 2) {
+        const int k = KC0 + n;
+        const bool hasB = n + 1 < NV;                                // warp-uniform
+        const int slA = n & (S - 1), slB = (n + 1) & (S - 1);
+        mbar_wait(full0 + 8u * slA, (unsigned)(n >> p.lg_nbatch) & 1u);
+        if (hasB) mbar_wait(full0 + 8u * slB, (unsigned)((n + 1) >> p.lg_nbatch) & 1u);
+        advance(k);
+        const int loA = t_lo, hiA = t_hi;
+        const bool workA = active_col && t_hi >= t_lo && k <= K1;
+        const int lo_all = __reduce_min_sync(0xffffffffu, active_col ? t_lo : INT_MAX);
+        while (t_f < lo_all && t_f < p.nz) flush_slice(t_f++);
+        bool workB = false;
+        if (hasB) {
+            advance(k + 1);
+            workB = active_col && t_hi >= t_lo && k + 1 <= K1;
+        }
+        const int loB = t_lo, hiB = t_hi;
+        const int lo_w = __reduce_min_sync(0xffffffffu, min(workA ? loA : INT_MAX, workB ? loB : INT_MAX));
+        const int hi_w = __reduce_max_sync(0xffffffffu, max(workA ? hiA : -1, workB ? hiB : -1));
+        if (hi_w >= lo_w) {
+            float w0A = 0.f, w1A = 0.f, baseA = 0.f, stepA = 0.f, w0B = 0.f, w1B = 0.f, baseB = 0.f, stepB = 0.f;
+            int ciA = 0, ciB = 0;
+            if (workA) geom(s_vg[slA], n, w0A, w1A, baseA, stepA, ciA);
+            if (workB) geom(s_vg[slB], n + 1, w0B, w1B, baseB, stepB, ciB);
+            const unsigned colA = (slot0 + (unsigned)slA * p.slot_bytes + (unsigned)ciA * p.col_bytes) ^ p.zero;
+            // without a view B its (zero-weight) reads go to slot A, which holds finite data
+            const unsigned colB = (slot0 + (unsigned)(hasB ? slB : slA) * p.slot_bytes + (unsigned)ciB * p.col_bytes) ^ p.zero;
+            const int lo_fA = __reduce_max_sync(0xffffffffu, workA ? loA : INT_MIN);
+            const int hi_fA = __reduce_min_sync(0xffffffffu, workA ? hiA : INT_MAX);
+            const int lo_fB = __reduce_max_sync(0xffffffffu, workB ? loB : INT_MIN);
+            const int hi_fB = __reduce_min_sync(0xffffffffu, workB ? hiB : INT_MAX);
+            const int m0 = lo_w & ~7;
+            unsigned cc = (unsigned)m0 & wmask;
+            u64 PMA = pk(fmaf((float)m0, stepA, baseA), fmaf((float)(m0 + 1), stepA, baseA));
+            u64 PMB = pk(fmaf((float)m0, stepB, baseB), fmaf((float)(m0 + 1), stepB, baseB));
+            const u64 S2A = pk(2.f * stepA, 2.f * stepA), S2B = pk(2.f * stepB, 2.f * stepB);
+            const u64 S8A = pk(8.f * stepA, 8.f * stepA), S8B = pk(8.f * stepB, 8.f * stepB);
+            for (int tb = m0; tb <= hi_w; tb += 8) {
+                float a8[8];
+                tm_ld8_nowait(tw + cc, a8);
+                float v[8][2];
+                sample8(colA, PMA, S2A, v);
+                tm_wait_ld8(a8);
+                accum8(a8, v, w0A, w1A, tb >= lo_fA && tb + 7 <= hi_fA, tb, loA, hiA, workA);
+                sample8(colB, PMB, S2B, v);
+                accum8(a8, v, w0B, w1B, tb >= lo_fB && tb + 7 <= hi_fB, tb, loB, hiB, workB);
+                tm_st8(tw + cc, a8);
+                PMA = add2(PMA, S8A);
+                PMB = add2(PMB, S8B);
+                cc = (cc + 8u) & wmask;
+            }
+            tm_wait_st();
+        }
+        mbar_arrive(empty0 + 8u * slA);
+        if (hasB) mbar_arrive(empty0 + 8u * slB);
+    }
     }
     // every window has closed by K1 + 1: flush the rest
     const int hi_all = __reduce_max_sync(0xffffffffu, active_col ? p.nz - 1 : -1);
@@ -1176,20 +1253,20 @@ void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cu
 
 size_t backproject_smem_bytes(const BPParams &p)
 {
-    const size_t vq = ((size_t)p.fp_cols_column * (p.nr + 2) + 7) & ~(size_t)7;
+    const size_t vq = ((size_t)p.fp_cols_column * p.nq_s + 7) & ~(size_t)7;
     return kBoxesBytes + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
            16 * (size_t)p.tail_quads;
 }
 
-template <bool POLY>
+template <bool POLY, int VP>
 void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &qmap, cudaStream_t s)
 {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_bp_tmem<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_tmem<POLY, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_bp_tmem<POLY><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    k_bp_tmem<POLY, VP><<<grid, kWsThreads, sm, s>>>(qmap, q);
 }
 
 template <int W>
@@ -1233,7 +1310,9 @@ bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
     if (!fn) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)2 * (p.nr + 2), (cuuint64_t)p.nc, (cuuint64_t)n_views};
     const cuuint64_t strides[2] = {(cuuint64_t)(p.nr + 2) * 16, (cuuint64_t)p.viewbytes};
-    const cuuint32_t box[3] = {(cuuint32_t)(2 * (p.nr + 2)), (cuuint32_t)p.fp_cols_column, 1};
+    // the box's column is p.nq_s >= nr + 2 quads: the rows past the detector are zero-filled (out of
+    // bounds) and make the staged column pitch an odd number of 16-B bank groups
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * p.nq_s), (cuuint32_t)p.fp_cols_column, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1253,26 +1332,44 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     // TMEM-window kernel for wide windows (accumulators in tensor memory, 3 CTAs per SM); for
     // windows of <= 32 slices the register window is lighter and faster (C2, C5 measured)
     if (!want_window && p.max_active > 32 && p.staged && !p.checked && p.windows_monotone && p.warp_span > 0 &&
-        2 * (p.nr + 2) <= 256 &&
+        2 * p.nq_s <= 256 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
-        BPParams q = p;
-        q.tmem_cols = 16;                                         // power of two >= span + 2 alias-free groups
-        while (q.tmem_cols < ((p.warp_span + 7) & ~7) + 16) q.tmem_cols *= 2;
-        int alloc = 32;
-        while (alloc < 2 * q.tmem_cols) alloc *= 2;               // 2 warps per TMEM lane quarter
-        q.tmem_alloc = alloc;
-        // deepest power-of-two ring such that 3 CTAs fit in shared memory (and TMEM: 3 x alloc <= 512)
-        q.nbatch = kMaxSlots;
-        while (q.nbatch > 2 && tmem_smem_bytes(q) > 74 * 1024) q.nbatch /= 2;
+        // TMEM columns, allocation and ring depth for one view (vp 1) or two views (vp 2) per pass
+        auto size_tmem = [&](int vp) {
+            BPParams q = p;
+            const int span = vp == 2 ? std::max(p.warp_span, p.warp_span2) : p.warp_span;
+            if (vp == 2) q.pad_quads = p.pad_quads2;
+            q.tmem_cols = 16;                                     // power of two >= span + 2 alias-free groups
+            while (q.tmem_cols < ((span + 7) & ~7) + 16) q.tmem_cols *= 2;
+            int alloc = 32;
+            while (alloc < 2 * q.tmem_cols) alloc *= 2;           // 2 warps per TMEM lane quarter
+            q.tmem_alloc = alloc;
+            // deepest power-of-two ring such that 3 CTAs fit in shared memory (and TMEM: 3 x alloc <= 512)
+            q.nbatch = kMaxSlots;
+            while (q.nbatch > 2 && tmem_smem_bytes(q) > 74 * 1024) q.nbatch /= 2;
+            return q;
+        };
+        // view pairs halve the per-view overhead, but not at the price of TMEM (CTAs per SM) or ring
+        // depth, and only with two pairs in flight (a 2-slot ring would stall the producer; C3 measured)
+        const BPParams q1 = size_tmem(1), q2 = size_tmem(2);
+        int vp = q2.tmem_alloc == q1.tmem_alloc && q2.nbatch == q1.nbatch && q2.nbatch >= 4 ? 2 : 1;
+        if (const char *ve = std::getenv("KATS_BP_VP")) vp = std::string(ve) == "1" ? 1 : 2;   // A/B tests
+        BPParams q = vp == 2 ? q2 : q1;
+        const int alloc = q.tmem_alloc;
         q.lg_nbatch = __builtin_ctz((unsigned)q.nbatch);
-        q.slot_bytes = 16u * (unsigned)((p.fp_cols_column * (p.nr + 2) + 7) & ~7);
-        q.col_bytes = 16u * (unsigned)(p.nr + 2);
+        q.slot_bytes = 16u * (unsigned)((p.fp_cols_column * p.nq_s + 7) & ~7);
+        q.col_bytes = 16u * (unsigned)p.nq_s;
         const size_t sm = tmem_smem_bytes(q);
         CUtensorMap qmap;
         if (alloc <= 128 && sm <= 200 * 1024 && make_quad_map(p, p.gq_views, &qmap)) {
             dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
-            if (p.poly) launch_tmem_kernel<true>(q, gw, sm, qmap, s);
-            else launch_tmem_kernel<false>(q, gw, sm, qmap, s);
+            if (vp == 2) {
+                if (p.poly) launch_tmem_kernel<true, 2>(q, gw, sm, qmap, s);
+                else launch_tmem_kernel<false, 2>(q, gw, sm, qmap, s);
+            } else {
+                if (p.poly) launch_tmem_kernel<true, 1>(q, gw, sm, qmap, s);
+                else launch_tmem_kernel<false, 1>(q, gw, sm, qmap, s);
+            }
             return KATS_BP_TMEM;
         }
     }
@@ -1285,7 +1382,7 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     while (q.nbatch > 2 && backproject_smem_bytes(q) > budget) q.nbatch /= 2;
     const size_t sm = backproject_smem_bytes(q);
     CUtensorMap qmap;
-    if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * (p.nr + 2) <= 256 &&
+    if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
         p.tail_quads <= 4096 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_map(p, p.gq_views, &qmap)) {
         dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);

@@ -73,10 +73,13 @@ struct BPParams {
     int tail_quads;           // shared-memory pad after the ring for reads of not-yet-open window entries
     unsigned zero;            // runtime 0 (opaque to ptxas)
     int warp_span;            // max live slices of a warp (host, TMEM-window kernel)
-    int pad_quads;            // head/tail pad (quads) for the TMEM-window kernel: 7 slices of row travel
-    int tmem_cols, tmem_alloc;
+    int warp_span2;           // the same over two consecutive views (TMEM kernel, view pairs)
+    int pad_quads;            // head/tail pad (quads) for the TMEM-window kernel: span + 8 slices of row travel
+    int pad_quads2;           // the same for view pairs (span2)
+    int nq_s;                 // staged-kernel column pitch in quads: nr + 2 rounded up to 3 or 5 mod 8
+    int tmem_cols, tmem_alloc;   // TMEM columns per warp / allocated per CTA (set by the launcher)
     int lg_nbatch;            // log2(nbatch) (TMEM kernel: slot parity from the view counter)
-    unsigned slot_bytes, col_bytes;   // TMEM kernel: bytes per ring slot / per quad column in a slot// TMEM columns per warp / allocated per CTA (set by the launcher)
+    unsigned slot_bytes, col_bytes;   // TMEM kernel: bytes per ring slot / per quad column in a slot
     float *vol;               // [n_items][nz][ny][nx] (adjoint: the input)
     float4 *gqT;              // adjoint: quad-adjoint output, layout of gq (accumulated)
 };

@@ -36,6 +36,7 @@ struct HostTables {
     bool windows_monotone = false;          // per column: k_first, k_last nondecreasing in z, interior windows non-empty
     int32_t fp_cols_column = 0;             // quad columns covering a tile's full-column samples of one view
     int32_t warp_span = 0;                  // max live slices of one warp (8x4 columns): newest open .. oldest unflushed
+    int32_t warp_span2 = 0;                 // same for two consecutive views done together: open at k+1 .. unflushed at k
 };
 
 // Per-view geometry for the backprojection (pitch-relative view k in [bp_lo, bp_hi]).

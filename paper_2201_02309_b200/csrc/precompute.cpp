@@ -388,10 +388,10 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
 
         // TMEM-window kernel: per warp (8x4 columns), the span of slices between the oldest slice
         // not closed by every lane (warp-uniform flush point) and the newest slice open in any lane
-        int span = 0;
+        int span = 0, span2 = 0;
         if (t.windows_monotone) {
             const int nwx = (o.nx + 7) / 8, nwy = (o.ny + 3) / 4;
-            #pragma omp parallel for collapse(2) schedule(dynamic, 4) reduction(max:span)
+            #pragma omp parallel for collapse(2) schedule(dynamic, 4) reduction(max:span, span2)
             for (int wy = 0; wy < nwy; ++wy)
                 for (int wx = 0; wx < nwx; ++wx) {
                     std::vector<size_t> cols;
@@ -410,6 +410,7 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
                         kmax = std::max<int64_t>(kmax, t.pi_last[c + (o.nz - 1) * plane]);
                     }
                     std::vector<int> lo(cols.size(), 0), hi(cols.size(), -1);
+                    int tf_prev = INT32_MAX;
                     for (int64_t k = kmin; k <= kmax; ++k) {
                         int tf = INT32_MAX, th = -1;
                         for (size_t q = 0; q < cols.size(); ++q) {
@@ -420,10 +421,15 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
                             th = std::max(th, hi[q]);
                         }
                         if (th >= tf) span = std::max(span, th - tf + 1);
+                        // views k-1, k in one pass: flushed up to the k-1 point, open up to k
+                        const int tf2 = std::min(tf, tf_prev);
+                        if (th >= tf2) span2 = std::max(span2, th - tf2 + 1);
+                        tf_prev = tf;
                     }
                 }
         }
         t.warp_span = span;
+        t.warp_span2 = std::max(span, span2);
     }
     return t.td_covered ? KATS_OK : KATS_WARN_TD_NOT_COVERED;
 }

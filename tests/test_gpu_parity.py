@@ -160,16 +160,20 @@ def test_coverage_error_names_pitches():
     assert ei.value.code == -4 and "reconstructible" in str(ei.value)
 
 
-@pytest.mark.parametrize("variant,kernel", [(None, "k_bp_tmem"), ("window", "k_bp_window"), ("l1", "k_backproject")])
-def test_every_bp_kernel_variant_matches_oracle(variant, kernel, monkeypatch):
-    """Each step-7 kernel (TMEM window = default for C1's 44-slice windows, register
-    window, chunked L1 path) on C1 against the oracle, and the plan
-    reports that the forced variant is the one that ran (katsevich_bp_kernel)."""
+@pytest.mark.parametrize("variant,vp,kernel", [(None, None, "k_bp_tmem"), (None, "1", "k_bp_tmem"),
+                                               (None, "2", "k_bp_tmem"), ("window", None, "k_bp_window"),
+                                               ("l1", None, "k_backproject")])
+def test_every_bp_kernel_variant_matches_oracle(variant, vp, kernel, monkeypatch):
+    """Each step-7 kernel (TMEM window = default for C1's 44-slice windows, with one
+    or two views per pass; register window; chunked L1 path) on C1
+    against the oracle, and the plan reports that the forced variant is the one
+    that ran (katsevich_bp_kernel)."""
     import torch
-    if variant is None:
-        monkeypatch.delenv("KATS_BP_KERNEL", raising=False)
-    else:
-        monkeypatch.setenv("KATS_BP_KERNEL", variant)
+    for env, val in (("KATS_BP_KERNEL", variant), ("KATS_BP_VP", vp)):
+        if val is None:
+            monkeypatch.delenv(env, raising=False)
+        else:
+            monkeypatch.setenv(env, val)
     cfg, sino, ref, contrast = _case("C1")
     p = _plan(cfg)
     vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
