@@ -215,6 +215,7 @@ BPParams bp_params(const katsevich_plan *p)
         int nq = g.n_rows + 2;
         while ((nq & 7) != 3 && (nq & 7) != 5) ++nq;
         b.nq_s = 2 * nq <= 256 ? nq : g.n_rows + 2;
+        b.bp_items = 1;
     }
     b.zero = 0u;
     b.warp_span = p->t.warp_span;

@@ -368,24 +368,35 @@ __device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, floa
 // when it closes, so no view does partial work and the per-(x, y, view) setup
 // is shared by every active slice (~40 at C3/C4).
 // ---------------------------------------------------------------------------
-template <bool POLY, int W>
+// Variants V (compile time, so the plain kernel's code is untouched by the others):
+//   V = 0  plain;
+//   V = 1  + warp-uniform sample tail: entries past every lane's last open slice are not sampled;
+//   V = 2  + two batch items per CTA (C5: one-pitch slabs share the geometry, so each view's
+//          per-lane setup serves both boxes) + 4 x 2 column blocks per quarter-warp (fewer
+//          detector columns, hence bank groups, per LDS.128 wavefront).
+template <bool POLY, int W, int V>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
 {
+    constexpr int NI = V == 2 ? 2 : 1;
+    constexpr bool TAIL = V >= 1, QMAP42 = V == 2;
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch;          // NQ: staged column pitch (quads)
-    const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged view (128-B aligned)
+    const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged box (128-B aligned)
+    const int vs = NI * vq;                                              // quads per slot (NI items' boxes)
     const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
     float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
-    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vq * 16);   // first column per view
+    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vs * 16);   // first column per view
     __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
     __shared__ int s_k0, s_k1;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = warp == kConsumerWarps;
-    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
-    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
-    const int item = blockIdx.z;
+    // a warp owns 8 x 4 columns; each quarter-warp (the lanes one LDS.128 wavefront serves) a 4 x 2
+    // block of them, so its samples spread over fewer detector columns (bank groups)
+    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (QMAP42 ? (lane & 3) + 4 * ((lane >> 3) & 1) : lane & 7);
+    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (QMAP42 ? ((lane >> 2) & 1) + 2 * (lane >> 4) : lane >> 3);
+    const int item0 = blockIdx.z * NI;
     const bool inside = !producer && ix < p.nx && iy < p.ny;
     const size_t plane = (size_t)p.nx * p.ny;
     const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
@@ -412,7 +423,8 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
     }
     if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
     const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
-    const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
+    const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item0 * p.item_views) * p.viewbytes);
+    const u64 qitem = (u64)(p.item_views * p.viewbytes);                // bytes between items' views
     __syncthreads();
     const int KC0 = s_k0, KC1 = s_k1;
     const int NV = KC1 - KC0 + 1;
@@ -425,8 +437,8 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
 
     if (producer) {
         if (NV <= 0) return;
-        // ---- producer warp: lanes 0..3 stream one view's full-height column box each per round ----
-        const int vbase = (int)(p.off0 + (int64_t)item * p.item_views) + KC0;
+        // ---- producer warp: lanes 0..3 stream one view's full-height column boxes (NI items) each per round ----
+        const int vbase = (int)(p.off0 + (int64_t)item0 * p.item_views) + KC0;
         const int G = min(4, S);                              // lanes in flight; divides S (powers of 2)
         if (lane < G) {
             int sl = lane;
@@ -434,8 +446,11 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
             for (int n = lane; n < NV; n += G) {
                 if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
                 const unsigned full = full0 + 8u * sl;
-                mbar_expect_tx(full, box_bytes);
-                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 0, boxc[n], vbase + n, full);
+                mbar_expect_tx(full, NI * box_bytes);
+#pragma unroll
+                for (int i = 0; i < NI; ++i)
+                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qmap, 0, boxc[n],
+                            vbase + (int)(i * p.item_views) + n, full);
                 sl += G;
                 if (sl >= S) { sl -= S; phase ^= 1u; }
             }
@@ -444,11 +459,13 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
     }
 
     // ---- consumer warps ----
-    float acc[W];
+    float acc[NI][W];
 #pragma unroll
-    for (int i = 0; i < W; ++i) acc[i] = 0.f;
+    for (int b = 0; b < NI; ++b)
+#pragma unroll
+        for (int i = 0; i < W; ++i) acc[b][i] = 0.f;
     const float2 *piw = p.pi_w + col;
-    float *out = p.vol + (size_t)item * p.nz * plane + col;
+    float *out = p.vol + (size_t)item0 * p.nz * plane + col;
     const bool active_col = inside && K0 <= K1;
     int t_lo = 0, t_hi = -1;
     int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
@@ -457,15 +474,18 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
     auto flush = [&]() {
         const int2 e = pik[(size_t)t_lo * plane];
         const float2 w = piw[(size_t)t_lo * plane];
-        u64 ends = 0ull;
-        tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t_lo, w.x, ends);
-        tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t_lo, w.y, ends);
-        float ea, eb;
-        upk(ends, ea, eb);
-        out[(size_t)t_lo * plane] = (acc[0] + ea + eb) * p.scale;
 #pragma unroll
-        for (int i = 0; i < W - 1; ++i) acc[i] = acc[i + 1];
-        acc[W - 1] = 0.f;
+        for (int b = 0; b < NI; ++b) {
+            u64 ends = 0ull;
+            tap_checked<POLY>(p, qbase + b * qitem, e.x, x, y, 0.f, t_lo, w.x, ends);
+            tap_checked<POLY>(p, qbase + b * qitem, e.y, x, y, 0.f, t_lo, w.y, ends);
+            float ea, eb;
+            upk(ends, ea, eb);
+            out[(size_t)b * p.nz * plane + (size_t)t_lo * plane] = (acc[b][0] + ea + eb) * p.scale;
+#pragma unroll
+            for (int i = 0; i < W - 1; ++i) acc[b][i] = acc[b][i + 1];
+            acc[b][W - 1] = 0.f;
+        }
         ++t_lo;
         next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;   // b + 1 = k_last
     };
@@ -506,35 +526,45 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
                 const float step = sc * p.dz;
                 const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));    // entry 0 = slice t_lo
                 const int ci = min(max(l - boxc[n], 0), BW - 1);
-                // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
-                const unsigned colbase = (stage_sa + (unsigned)(sl * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
                 const u64 S2 = pk(2.f * step, 2.f * step);
-                u64 PM = pk(base, base + step);
+                // (V >= 1) entries past every working lane's last open slice are not sampled at all
+                int n_w = W;
+                if constexpr (TAIL) n_w = __reduce_max_sync(__activemask(), n_act);
 #pragma unroll
-                for (int g = 0; g < W; g += kGroup) {
-                    if (g < n_act) {
+                for (int b = 0; b < NI; ++b) {
+                    // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
+                    const unsigned colbase =
+                        (stage_sa + (unsigned)(sl * vs + b * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
+                    u64 PM = pk(base, base + step);
 #pragma unroll
-                        for (int j = 0; j < kGroup; j += 2) {
-                            const int i = g + j;
-                            // entries >= n_act (not yet open) read at most a few quad rows past the
-                            // column (a tail pad keeps them inside the allocation); their sums are dropped
-                            const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
-                            float q0, q1, p0, p1;
-                            upk(Q, q0, q1);
-                            upk(PM, p0, p1);
-                            const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
-                            const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                            // the two columns' row samples s' + p d, then their α weights
-                            float a0, b0, a1, b1;
-                            upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), a0, b0);
-                            upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), a1, b1);
-                            if (i < n_act) acc[i] = fmaf(a0, w0, fmaf(b0, w1, acc[i]));
-                            if (i + 1 < n_act) acc[i + 1] = fmaf(a1, w0, fmaf(b1, w1, acc[i + 1]));
-                            PM = add2(PM, S2);
+                    for (int g = 0; g < W; g += kGroup) {
+                        if (g < n_act) {
+#pragma unroll
+                            for (int j = 0; j < kGroup; j += 2) {
+                                const int i = g + j;
+                                // entries >= n_act (not yet open) read at most a few quad rows past the
+                                // column (a tail pad keeps them inside the allocation); their sums are dropped
+                                const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
+                                float q0, q1, p0, p1;
+                                upk(Q, q0, q1);
+                                upk(PM, p0, p1);
+                                if constexpr (TAIL) {
+                                    if (i >= n_w) break;
+                                }
+                                const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
+                                const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
+                                // the two columns' row samples s' + p d, then their α weights
+                                float a0, b0, a1, b1;
+                                upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), a0, b0);
+                                upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), a1, b1);
+                                if (i < n_act) acc[b][i] = fmaf(a0, w0, fmaf(b0, w1, acc[b][i]));
+                                if (i + 1 < n_act) acc[b][i + 1] = fmaf(a1, w0, fmaf(b1, w1, acc[b][i + 1]));
+                                PM = add2(PM, S2);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < kGroup; j += 2) PM = add2(PM, S2);
                         }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < kGroup; j += 2) PM = add2(PM, S2);
                     }
                 }
             }
@@ -543,7 +573,8 @@ __global__ void __launch_bounds__(kWsThreads, (W <= 16 ? 3 : 2)) k_bp_window(con
     }
     if (!inside) return;
     if (!active_col) {                                            // outside U: the column is 0
-        for (int t = 0; t < p.nz; ++t) out[(size_t)t * plane] = 0.f;
+        for (int b = 0; b < NI; ++b)
+            for (int t = 0; t < p.nz; ++t) out[(size_t)b * p.nz * plane + (size_t)t * plane] = 0.f;
         return;
     }
     while (t_hi + 1 < p.nz) ++t_hi;                               // (all windows opened by K1)
@@ -1254,7 +1285,7 @@ void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cu
 size_t backproject_smem_bytes(const BPParams &p)
 {
     const size_t vq = ((size_t)p.fp_cols_column * p.nq_s + 7) & ~(size_t)7;
-    return kBoxesBytes + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
+    return kBoxesBytes + (size_t)p.nbatch * p.bp_items * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
            16 * (size_t)p.tail_quads;
 }
 
@@ -1274,12 +1305,31 @@ void launch_window(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &q
 {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_bp_window<true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_window<false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_window<true, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_window<false, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_window<true, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_window<false, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if constexpr (W <= 16) {
+            cudaFuncSetAttribute(k_bp_window<true, W, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(k_bp_window<false, W, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }
         attr = true;
     }
-    if (q.poly) k_bp_window<true, W><<<grid, kWsThreads, sm, s>>>(qmap, q);
-    else k_bp_window<false, W><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    const int v = q.win_variant;
+    if constexpr (W <= 16) {
+        if (v == 2) {
+            if (q.poly) k_bp_window<true, W, 2><<<grid, kWsThreads, sm, s>>>(qmap, q);
+            else k_bp_window<false, W, 2><<<grid, kWsThreads, sm, s>>>(qmap, q);
+            return;
+        }
+    }
+    if (v == 1) {
+        if (q.poly) k_bp_window<true, W, 1><<<grid, kWsThreads, sm, s>>>(qmap, q);
+        else k_bp_window<false, W, 1><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    } else {
+        if (q.poly) k_bp_window<true, W, 0><<<grid, kWsThreads, sm, s>>>(qmap, q);
+        else k_bp_window<false, W, 0><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    }
 }
 
 namespace {
@@ -1375,9 +1425,15 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     }
     BPParams q = p;
     const int W = p.max_active <= 8 ? 8 : p.max_active <= 16 ? 16 : p.max_active <= 32 ? 32 : p.max_active <= 48 ? 48 : 0;
-    // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 3 CTAs (W <= 16, <= 72
-    // registers) or 2 CTAs share an SM
-    const size_t budget = (W > 0 && W <= 16 ? 74 : 100) * 1024;
+    // batches of an even number of items with small windows: variant 2 (two items per CTA share
+    // each view's per-lane geometry); otherwise the plain kernel (KATS_BP_WINV=0|1|2: A/B tests)
+    q.win_variant = W > 0 && W <= 16 && p.n_items >= 2 && p.n_items % 2 == 0 ? 2 : 0;
+    if (const char *wv = std::getenv("KATS_BP_WINV")) q.win_variant = std::atoi(wv);
+    if (q.win_variant == 2 && !(W > 0 && W <= 16 && p.n_items % 2 == 0)) q.win_variant = 1;
+    q.bp_items = q.win_variant == 2 ? 2 : 1;
+    // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 3 CTAs (W * items <= 16,
+    // <= 72 registers) or 2 CTAs share an SM
+    const size_t budget = (W > 0 && W * q.bp_items <= 16 ? 74 : 100) * 1024;
     q.nbatch = kMaxSlots;
     while (q.nbatch > 2 && backproject_smem_bytes(q) > budget) q.nbatch /= 2;
     const size_t sm = backproject_smem_bytes(q);
@@ -1385,7 +1441,7 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
         p.tail_quads <= 4096 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_map(p, p.gq_views, &qmap)) {
-        dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
+        dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
         switch (W) {
         case 8: launch_window<8>(q, gw, sm, qmap, s); break;
         case 16: launch_window<16>(q, gw, sm, qmap, s); break;

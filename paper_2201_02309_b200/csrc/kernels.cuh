@@ -77,6 +77,8 @@ struct BPParams {
     int pad_quads;            // head/tail pad (quads) for the TMEM-window kernel: span + 8 slices of row travel
     int pad_quads2;           // the same for view pairs (span2)
     int nq_s;                 // staged-kernel column pitch in quads: nr + 2 rounded up to 3 or 5 mod 8
+    int bp_items;             // window kernel: batch items per CTA (1 or 2; set by the launcher)
+    int win_variant;          // window kernel variant V (0 plain, 1 uniform sample tail, 2 + two items per CTA)
     int tmem_cols, tmem_alloc;   // TMEM columns per warp / allocated per CTA (set by the launcher)
     int lg_nbatch;            // log2(nbatch) (TMEM kernel: slot parity from the view counter)
     unsigned slot_bytes, col_bytes;   // TMEM kernel: bytes per ring slot / per quad column in a slot

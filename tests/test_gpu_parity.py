@@ -98,16 +98,23 @@ def test_backproject_only_matches_oracle(name):
     _check(got.cpu().numpy(), ref, contrast)
 
 
-def test_batch_matches_oracle():
-    """Independent one-pitch slabs (C5-shaped, small): reconstruct_batch."""
+@pytest.mark.parametrize("n_slabs,winv", [(3, None), (4, None), (4, "0")])
+def test_batch_matches_oracle(n_slabs, winv, monkeypatch):
+    """Independent one-pitch slabs (C5-shaped, small): reconstruct_batch, odd and
+    even batches (even batches may pair items per CTA in the window kernel), and
+    the plain window kernel forced (KATS_BP_WINV=0)."""
     import torch
     from oracle import oracle
     from synth import configs, synth
+    if winv is None:
+        monkeypatch.delenv("KATS_BP_WINV", raising=False)
+    else:
+        monkeypatch.setenv("KATS_BP_WINV", winv)
     cfg = configs.get("T2")
     p = _plan(cfg)
     v0, nv = p.pitch_views(0)
     slabs, refs, contrasts = [], [], []
-    for s in range(3):
+    for s in range(n_slabs):
         ph = configs.random_ellipsoids(s, 6, 180.0, -5.0, cfg["P"] + 5.0)
         sino = synth.project(cfg, ph, v0, nv)
         slabs.append(sino)
@@ -116,7 +123,7 @@ def test_batch_matches_oracle():
         contrasts.append(t.max() - t.min())
     got = p.reconstruct_batch(torch.from_numpy(np.stack(slabs)).cuda())
     torch.cuda.synchronize()
-    for b in range(3):
+    for b in range(n_slabs):
         _check(got[b].cpu().numpy(), refs[b], contrasts[b])
 
 
@@ -162,14 +169,16 @@ def test_coverage_error_names_pitches():
 
 @pytest.mark.parametrize("variant,vp,kernel", [(None, None, "k_bp_tmem"), (None, "1", "k_bp_tmem"),
                                                (None, "2", "k_bp_tmem"), ("window", None, "k_bp_window"),
-                                               ("l1", None, "k_backproject")])
+                                               ("window", "winv1", "k_bp_window"), ("l1", None, "k_backproject")])
 def test_every_bp_kernel_variant_matches_oracle(variant, vp, kernel, monkeypatch):
     """Each step-7 kernel (TMEM window = default for C1's 44-slice windows, with one
     or two views per pass; register window; chunked L1 path) on C1
     against the oracle, and the plan reports that the forced variant is the one
     that ran (katsevich_bp_kernel)."""
     import torch
-    for env, val in (("KATS_BP_KERNEL", variant), ("KATS_BP_VP", vp)):
+    winv = "1" if vp == "winv1" else None
+    vp = None if vp == "winv1" else vp
+    for env, val in (("KATS_BP_KERNEL", variant), ("KATS_BP_VP", vp), ("KATS_BP_WINV", winv)):
         if val is None:
             monkeypatch.delenv(env, raising=False)
         else:
