@@ -86,7 +86,7 @@ void free_device(katsevich_plan *p)
     if (p->device < 0) return;
     cudaSetDevice(p->device);
     void *ptrs[] = {p->d.pi_k, p->d.pi_w, p->d.view, p->d.fr, p->d.br, p->d.cos_alpha, p->d.wlen, p->d.hilbert,
-                    p->d.hilbert_tc};
+                    p->d.hilbert_tc, p->d.hilbert_hk};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     p->d = DeviceTables{};
@@ -129,6 +129,7 @@ FilterParams filter_params(const katsevich_plan *p)
     f.inv_2dalpha = (float)(1.0 / (2.0 * p->g.d_alpha));
     f.wlen = p->d.wlen; f.fr = p->d.fr; f.br = p->d.br;
     f.cos_alpha = p->d.cos_alpha; f.hilbert = p->d.hilbert; f.hilbert_tc = p->d.hilbert_tc;
+    f.hilbert_hk = p->d.hilbert_hk;
     f.sign = 1.f;
     return f;
 }
@@ -312,6 +313,9 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
         std::vector<float> htc;
         hilbert_tc_table(g.n_cols, hk.data(), htc);
         if ((rc = upload(p, &p->d.hilbert_tc, htc))) return rc;
+        std::vector<float> hhk;
+        hilbert_hk_table(g.n_cols, hk.data(), hhk);
+        if ((rc = upload(p, &p->d.hilbert_hk, hhk))) return rc;
         KCHECK(p, cudaDeviceSynchronize());
     }
     p->precomputed = true;

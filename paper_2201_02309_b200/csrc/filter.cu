@@ -327,6 +327,185 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_hilbert_tc(FilterParams p, in
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3 on the tensor cores with the tap matrix held as Hankel core matrices (default for wide
+// detectors).  Per parity the tap matrix is Toeplitz, B[n][k] = T(n - k).  With the K index
+// reversed in both operands (k' = NH - 1 - k) it is Hankel, B'[n][k'] = T(n + k' - NH + 1), so
+// the canonical K-major core matrix (8 rows n x 4 columns k') at row group ng and K quad kq'
+// depends only on s = 2 ng + kq'.  The NH/2 distinct cores are stored consecutively (128 B
+// each) and the UMMA descriptor walks them with LBO = 128 B (next K quad = next core) and
+// SBO = 256 B (next row group = two cores on): the whole B operand of one parity is 64 NH
+// bytes per TF32 half, loaded once per CTA instead of streamed per K chunk.  The A chunks
+// (κ-line samples of the parity's inputs, K reversed, split hi/lo) go through an
+// nstage-deep ring; one thread issues the 3xTF32 MMAs of a chunk and commits them to the
+// stage's mbarrier, so staging chunk kc+1.. overlaps the tensor core on chunk kc.
+// ---------------------------------------------------------------------------
+// Persistent: 2 CTAs per SM, each fixed to one parity (its taps loaded once), loop over work items
+// (128-line block, output half).  nsplit = 2 (NH > 256): an item covers one half of the outputs
+// (N = NH/2) so the accumulator fits 256 TMEM columns and two CTAs share an SM (one's staging and
+// epilogue overlap the other's MMAs).
+constexpr int HK_THREADS = 512;
+
+__device__ __forceinline__ uint64_t hk_desc(unsigned saddr)
+{
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)(256u >> 4) << 32) |
+           (1ull << 46);
+}
+
+__global__ void __launch_bounds__(HK_THREADS, 2) k_hilbert_hk(FilterParams p, int64_t n_lines, int nstage, int nsplit)
+{
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC, NS = NH / 2;
+    const int NN = NH / nsplit;                                  // outputs of an item: [n_lo, n_lo + NN)
+    const int par = blockIdx.x & 1, cta = blockIdx.x >> 1, ncta = gridDim.x >> 1;
+    const int nin = (nc - (1 - par) + 1) / 2, nout = (nc - par + 1) / 2;
+    const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
+    unsigned char *Bh = tsm, *Bl = tsm + NS * 128;               // Hankel cores, hi / lo
+    unsigned char *A0 = tsm + 2 * NS * 128;
+    const unsigned stage_bytes = (unsigned)(2 * TC_M * TC_KC * 4);   // A hi + lo of one K chunk
+    // epilogue staging: the A ring (idle between an item's last MMA and the next item's first chunk)
+    float *stg_all = reinterpret_cast<float *>(A0);
+    __shared__ __align__(8) unsigned long long s_bar[4];
+    __shared__ unsigned s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned bar0 = (unsigned)__cvta_generic_to_shared(&s_bar[0]);
+    unsigned cols = 32;
+    while (cols < (unsigned)NN) cols <<= 1;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < nstage; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * i));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {   // the parity's tap cores (hi then lo, 8 float4 per core)
+        const float4 *src = reinterpret_cast<const float4 *>(p.hilbert_hk) + (size_t)par * 2 * NS * 8;
+        float4 *dst = reinterpret_cast<float4 *>(Bh);
+        for (int i = tid; i < 2 * NS * 8; i += HK_THREADS) dst[i] = __ldg(src + i);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = s_tmem;
+    const unsigned idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_M >> 4) << 24);
+    const unsigned sBh = (unsigned)__cvta_generic_to_shared(Bh), sBl = (unsigned)__cvta_generic_to_shared(Bl);
+    const int rr = lane & 7, kq = lane >> 3;
+    // a thread's samples of one A chunk: row warp * 8 + rr, K quads kq and 4 + kq; element (row, j)
+    // is input k = NH - 1 - (32 kc + j) of the line
+    static_assert(HK_THREADS / 32 == TC_M / 8, "one 8-row group per warp");
+    const int row = warp * 8 + rr;
+    const int q4 = warp & 3;                                     // epilogue: TMEM lane quarter
+    const unsigned trow = tmem + ((unsigned)(q4 * 32) << 16);
+    float *stg = stg_all + warp * 32 * 17;
+    int g = 0;                                                   // chunks issued by this CTA (ring phase)
+    for (int64_t item = cta; item < n_items; item += ncta) {
+        const int64_t line0 = item / nsplit * TC_M;
+        const int n_lo = (int)(item % nsplit) * NN;
+        const int64_t line = line0 + row;
+        const float *src = p.g3 + line * nc + (1 - par);
+        auto load_chunk = [&](int kc, float (&v)[2][4]) {
+#pragma unroll
+            for (int qb = 0; qb < 2; ++qb)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int k = NH - 1 - (kc * TC_KC + (qb * 4 + kq) * 4 + i);
+                    v[qb][i] = (line < n_lines && k < nin) ? __ldg(src + 2 * k) : 0.f;
+                }
+        };
+        float cur[2][4];
+        load_chunk(0, cur);
+        for (int kc = 0; kc < NK; ++kc, ++g) {
+            const int st = g % nstage;
+            float nxt[2][4];                                      // next chunk's loads fly over this one
+            if (kc + 1 < NK) load_chunk(kc + 1, nxt);
+            if (g >= nstage) {                                    // the MMAs of chunk g - nstage read this stage
+                asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
+                             "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
+                             "@!d bra WAIT_%=;\n\t}" ::"r"(bar0 + 8u * st), "r"((unsigned)(((g - nstage) / nstage) & 1))
+                             : "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            unsigned char *Ah = A0 + st * stage_bytes, *Al = Ah + TC_M * TC_KC * 4;
+#pragma unroll
+            for (int qb = 0; qb < 2; ++qb) {
+                const float *v = cur[qb];
+                const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
+                const unsigned o = tc_off(row, (qb * 4 + kq) * 4);
+                *reinterpret_cast<float4 *>(Ah + o) = h;
+                *reinterpret_cast<float4 *>(Al + o) = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
+            }
+#pragma unroll
+            for (int qb = 0; qb < 2; ++qb)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cur[qb][i] = nxt[qb][i];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned sAh = (unsigned)__cvta_generic_to_shared(Ah), sAl = (unsigned)__cvta_generic_to_shared(Al);
+                for (int n0 = n_lo; n0 < n_lo + NN; n0 += 256) {
+                    const int nn = n_lo + NN - n0 < 256 ? n_lo + NN - n0 : 256;
+                    const unsigned idesc = idesc_base | ((unsigned)(nn >> 3) << 17);
+                    const unsigned tcol = tmem + (unsigned)(n0 - n_lo);
+#pragma unroll
+                    for (int kk = 0; kk < TC_KC / 8; ++kk) {
+                        const unsigned core = (unsigned)(2 * (n0 >> 3) + kc * 8 + kk * 2) * 128u;   // s of (n0, k' = 32 kc + 8 kk)
+                        const uint64_t a_h = tc_desc(sAh + (unsigned)kk * 256u), a_l = tc_desc(sAl + (unsigned)kk * 256u);
+                        const uint64_t b_h = hk_desc(sBh + core), b_l = hk_desc(sBl + core);
+                        const unsigned first = (kc == 0 && kk == 0) ? 0u : 1u;
+                        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n\t}"
+                                     ::"r"(tcol), "l"(a_h), "l"(b_h), "r"(idesc), "r"(first));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;"
+                                     ::"r"(tcol), "l"(a_h), "l"(b_l), "r"(idesc));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;"
+                                     ::"r"(tcol), "l"(a_l), "l"(b_h), "r"(idesc));
+                    }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                             ::"r"(bar0 + 8u * st) : "memory");
+            }
+        }
+        {   // the item's last commit covers every MMA issued before it
+            const int gl = g - 1;
+            asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
+                         "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
+                         "@!d bra WAIT_%=;\n\t}" ::"r"(bar0 + 8u * (gl % nstage)), "r"((unsigned)((gl / nstage) & 1))
+                         : "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        // epilogue: warp w owns accumulator rows (lines) 32 (w & 3) .. = TMEM lane quarter; 32 lines x 16
+        // outputs at a time go through padded shared memory
+        for (int c = 16 * (warp >> 2); c < NN; c += 16 * (HK_THREADS / 128)) {
+            float v[16];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+                           "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+                         : "r"(trow + (unsigned)c));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) stg[lane * 17 + i] = v[i];
+            __syncwarp();
+            const int cl = lane & 15, rh = lane >> 4;               // half-warps take alternate lines
+            const int n = n_lo + c + cl;                            // output n of this parity: column 2n + par
+            for (int r = rh; r < 32; r += 2) {
+                const int64_t ln = line0 + q4 * 32 + r;
+                if (ln < n_lines && n < nout && c + cl < NN) p.g4[ln * nc + 2 * n + par] = p.sign * stg[r * 17 + cl];
+            }
+            __syncwarp();
+        }
+        // the next item's first MMA overwrites the accumulator: every warp's reads must be done
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
 // Both parities per CTA (NH <= 256: two accumulators fit TMEM's 512 columns).
 // A K chunk covers inputs l in [64 kc, 64 kc + 64) of each line (coalesced
 // loads), de-interleaved into the even- and odd-input tiles; output parity 0
@@ -555,6 +734,32 @@ void hilbert_tc_table(int nc, const float *kd, std::vector<float> &out)
     }
 }
 
+size_t hilbert_hk_table_floats(int nc) { return 2 * 2 * (size_t)(hilbert_tc_nh(nc) / 2) * 32; }
+
+// [par][hi, lo][NH/2 Hankel cores][8 rows x 4] (see k_hilbert_hk): core s, row r, column c holds
+// the tap of n - k = 4 s + r + c - (NH - 1), i.e. K[2 (n - k) + 2 par - 1] (0 outside the kernel)
+void hilbert_hk_table(int nc, const float *kd, std::vector<float> &out)
+{
+    const int NH = hilbert_tc_nh(nc), NS = NH / 2;
+    out.assign(hilbert_hk_table_floats(nc), 0.f);
+    for (int par = 0; par < 2; ++par)
+        for (int sc = 0; sc < NS; ++sc)
+            for (int r = 0; r < 8; ++r)
+                for (int c = 0; c < 4; ++c) {
+                    const int d = 4 * sc + r + c - (NH - 1);
+                    const int t = 2 * d + 2 * par - 1;
+                    const float b = (t >= -(nc - 1) && t <= nc - 1) ? kd[t + nc - 1] : 0.f;
+                    uint32_t u;
+                    std::memcpy(&u, &b, 4);
+                    u &= 0xFFFFE000u;
+                    float hi;
+                    std::memcpy(&hi, &u, 4);
+                    const size_t o = (size_t)sc * 32 + r * 4 + c;
+                    out[((size_t)par * 2 + 0) * NS * 32 + o] = hi;
+                    out[((size_t)par * 2 + 1) * NS * 32 + o] = b - hi;
+                }
+}
+
 bool hilbert_tc_usable(const FilterParams &p)
 {
     const char *e = std::getenv("KATS_HILBERT");
@@ -571,6 +776,34 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
         FilterParams q = p;
         q.hilbert_tc = nullptr;
         launch_hilbert(q, s);
+        return;
+    }
+    // KATS_HILBERT=tc: the per-chunk tap-streaming kernels (A/B tests); =hk: Hankel cores for every width
+    const char *he = std::getenv("KATS_HILBERT");
+    const bool force_tc = he && std::string(he) == "tc", force_hk = he && std::string(he) == "hk";
+    if (hilbert_tc_usable(p) && p.hilbert_hk && !force_tc && (hilbert_tc_nh(p.nc) > 128 || force_hk)) {
+        const int NH = hilbert_tc_nh(p.nc);
+        // halves only where 2 CTAs per SM pay for reading A twice (C3 NH 384: 1.20 -> 1.13 ms;
+        // C5 NH 320: 1.32 -> 1.59 ms, measured)
+        int nsplit = NH > 352 ? 2 : 1;
+        if (const char *e = std::getenv("KATS_HILBERT_SPLIT")) nsplit = std::atoi(e) == 1 || NH % 64 ? 1 : 2;
+        const size_t taps = (size_t)128 * NH, stage = (size_t)2 * TC_M * TC_KC * 4;
+        // as many A stages (2..4) as leave room for two CTAs per SM (the epilogue reuses the ring:
+        // 16 warps x 32 x 17 floats <= 2 stages)
+        int nstage = 4;
+        while (nstage > 2 && taps + nstage * stage > 110 * 1024) --nstage;
+        const size_t smem = taps + nstage * stage;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_hilbert_hk, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+            attr = true;
+        }
+        const int64_t n_lines = (int64_t)p.n_views * p.npsi;
+        const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+        const int per_par = (int)std::min<int64_t>(n_items, nsm);      // persistent: 2 CTAs per SM, one per parity
+        k_hilbert_hk<<<(unsigned)(2 * per_par), HK_THREADS, smem, s>>>(p, n_lines, nstage, nsplit);
         return;
     }
     if (hilbert_tc_usable(p) && hilbert_tc_nh(p.nc) <= 256 && !p.hilbert_overlap) {

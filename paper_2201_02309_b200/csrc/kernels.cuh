@@ -21,6 +21,7 @@ struct FilterParams {
     const float *cos_alpha;   // [nc]
     const float *hilbert;     // [2nc-1]
     const float *hilbert_tc;  // tensor-core tap table (hilbert_tc_table), or null
+    const float *hilbert_hk;  // tensor-core Hankel-core tap table (hilbert_hk_table), or null
     float *g3, *g4;           // κ-line intermediates [n_views][npsi][nc]
     float4 *gq;               // filtered views as column-major 2x2 sum/difference tap quads [n_views][nc][nr+2] (BP input)
     float *gF;                // optional plain filtered views [n_views][nr][nc] (debug), may be null
@@ -34,6 +35,8 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eq
 void launch_hilbert(const FilterParams &p, cudaStream_t s);           // K3:  Eq. 12
 size_t hilbert_tc_table_floats(int nc);
 void hilbert_tc_table(int nc, const float *kd, std::vector<float> &out);
+size_t hilbert_hk_table_floats(int nc);
+void hilbert_hk_table(int nc, const float *kd, std::vector<float> &out);
 void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s);     // K4:  Eqs. 13-15
 // adjoint (NEXT-1)
 void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s);   // quad^T + K4^T

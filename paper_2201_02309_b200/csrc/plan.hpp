@@ -54,6 +54,7 @@ struct DeviceTables {
     float *wlen = nullptr;         // [n_rows]  D / sqrt(D² + w²)
     float *hilbert = nullptr;      // [2 n_cols - 1]  K[d], d = -(nc-1)..nc-1
     float *hilbert_tc = nullptr;   // K3 tensor-core tap matrices (hi/lo TF32 split, UMMA layout)
+    float *hilbert_hk = nullptr;   // K3 tensor-core Hankel tap cores (hi/lo TF32 split)
 };
 
 struct ProfRecord { int stage; void *ev0; void *ev1; };

@@ -59,17 +59,18 @@ def test_reconstruct_matches_oracle(name):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("hilbert", ["tc", "fp32"])
+@pytest.mark.parametrize("hilbert", ["default", "tc", "hk", "fp32"])
 @pytest.mark.parametrize("name", ["T1", "T3", "C1"])
 def test_filter_stages_match_oracle(name, hilbert, monkeypatch):
-    """Steps 1-6 per stage (g3, g4, gF) against the oracle; K3 both on the tensor
-    cores (3xTF32 GEMM, default) and as the fp32 direct convolution."""
+    """Steps 1-6 per stage (g3, g4, gF) against the oracle; K3 on the tensor cores
+    (3xTF32 GEMM: default choice, tap-streaming kernels, Hankel-core kernel) and as
+    the fp32 direct convolution."""
     import torch
     from oracle import oracle
-    if hilbert == "fp32":
-        monkeypatch.setenv("KATS_HILBERT", "fp32")
-    else:
+    if hilbert == "default":
         monkeypatch.delenv("KATS_HILBERT", raising=False)
+    else:
+        monkeypatch.setenv("KATS_HILBERT", hilbert)
     cfg, sino, _, _ = _case(name)
     p = _plan(cfg)
     v0, nv = p.pitch_views(0)
