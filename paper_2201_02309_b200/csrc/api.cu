@@ -749,7 +749,10 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
         while (c_next < nchunks && u0 + c_next * kFilterChunk < filt_end) {
             const int64_t a = u0 + c_next * kFilterChunk, n = std::min<int64_t>(kFilterChunk, nu - c_next * kFilterChunk);
             KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[c_next], 0));
-            rc = run_filter(p, dsino + (a - fv) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs, true);
+            // before the first pitch's BP nothing runs beside the filter: tensor-core Hilbert; after
+            // it the filter shares SMs with TMEM backprojection CTAs: fp32 Hilbert (launch_hilbert)
+            rc = run_filter(p, dsino + (a - fv) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs,
+                            k > 0);
             if (rc) return rc;
             ++c_next;
         }

@@ -1,0 +1,8 @@
+# x4 head/tail groups in the TMEM kernel: parity + C4, C3, C1 bench
+cd $GRAFT_REPO_ROOT
+make -s all > gpurun_out/build.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for cfg in C4 C3 C1; do
+  timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --no-adjoint --no-datagen > gpurun_out/x4_$cfg.json 2>/dev/null
+done
+echo done
