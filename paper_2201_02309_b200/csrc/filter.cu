@@ -2,6 +2,7 @@
 // PAPER.md §II (l.117-154) as sm_100a kernels.  Each filtered view depends
 // only on raw views v-1, v, v+1, so the same kernels serve the per-pitch slab
 // (P:l.250) and the filter-once long-scan path.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -31,23 +32,33 @@ __device__ __forceinline__ float g2_at(const FilterParams &p, const float *__res
     return __ldg(p.wlen + m) * (dq + da);
 }
 
-__global__ void __launch_bounds__(128) k_deriv_fwd_rebin(FilterParams p)
+// A CTA spans a whole detector row (narrow detectors) and kPsiPer κ-lines of one view: each
+// thread computes kPsiPer independent samples (loads in flight together); few, fat CTAs instead
+// of one per (view, κ-line) (C4: 66K CTAs of 128 threads per chunk were launch-rate bound).
+constexpr int kPsiPer = 8;
+
+__global__ void __launch_bounds__(256) k_deriv_fwd_rebin(FilterParams p)
 {
     const int l = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i = blockIdx.y;
+    const int i0 = blockIdx.y * kPsiPer;
     const int v = blockIdx.z;
     if (l >= p.nc) return;
-    const RebinEntry e = p.fr[i * p.nc + l];
-    float out = 0.f;
-    if (e.idx >= 0) {
-        const int64_t g = p.view0 + v;
-        const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
-        const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
-        float a = g2_at(p, gv, e.idx, l);
-        float b = g2_at(p, gv, e.idx + 1, l);
-        out = fmaf(e.frac, b - a, a);
+    const int64_t g = p.view0 + v;
+    const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+    const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
+    float *out = p.g3 + ((size_t)v * p.npsi + i0) * p.nc + l;
+#pragma unroll
+    for (int j = 0; j < kPsiPer; ++j) {
+        if (i0 + j >= p.npsi) break;
+        const RebinEntry e = p.fr[(i0 + j) * p.nc + l];
+        float o = 0.f;
+        if (e.idx >= 0) {
+            const float a = g2_at(p, gv, e.idx, l);
+            const float b = g2_at(p, gv, e.idx + 1, l);
+            o = fmaf(e.frac, b - a, a);
+        }
+        out[(size_t)j * p.nc] = o;
     }
-    p.g3[((size_t)v * p.npsi + i) * p.nc + l] = out;
 }
 
 // Same computation, one thread per (view, column, <= 32 κ-lines) walking the κ-lines in ψ
@@ -703,7 +714,8 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
         k_deriv_fwd_rebin_col<<<dim3((p.nc + 127) / 128, p.n_views, nseg), 128, 0, s>>>(p, seg);
         return;
     }
-    k_deriv_fwd_rebin<<<dim3((p.nc + 127) / 128, p.npsi, p.n_views), 128, 0, s>>>(p);
+    const int bx = std::min(256, (p.nc + 31) / 32 * 32);
+    k_deriv_fwd_rebin<<<dim3((p.nc + bx - 1) / bx, (p.npsi + kPsiPer - 1) / kPsiPer, p.n_views), bx, 0, s>>>(p);
 }
 
 size_t hilbert_tc_table_floats(int nc) { return 2 * 2 * (size_t)hilbert_tc_nh(nc) * hilbert_tc_nh(nc); }

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+make -s all > gpurun_out/build.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "filter_stages or reconstruct_matches" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for cfg in C4 C1; do
+  timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --no-adjoint --no-datagen > gpurun_out/k12_$cfg.json 2>/dev/null
+done
+echo done
