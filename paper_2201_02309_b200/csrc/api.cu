@@ -211,11 +211,21 @@ BPParams bp_params(const katsevich_plan *p)
         b.pad_quads = 12 + (int)std::ceil((p->t.warp_span + 8) * step_max);
         b.pad_quads2 = 12 + (int)std::ceil((std::max(p->t.warp_span, p->t.warp_span2) + 8) * step_max);
     }
-    {   // staged column pitch: 3 or 5 (mod 8) quads, so lanes on neighbouring detector columns
-        // (C3: ~1 column per voxel) read different 16-B bank groups; the extra rows are TMA zero fill
-        int nq = g.n_rows + 2;
+    {   // staged quad rows: interior samples have |w| <= w_L (the plan's margin check), i.e. quad rows
+        // round(w/dw + (nr-1)/2 + 1.5); one row of slack either side for fp32 rounding (C3: 51 of 66)
+        int q0 = 0, q1 = g.n_rows + 1;
+        if (p->t.interior_in_detector) {
+            const double cr = 0.5 * (g.n_rows - 1) + 1.5, hw = p->t.w_L / g.d_w;
+            q0 = std::max(0, (int)std::floor(cr - hw) - 1);
+            q1 = std::min(g.n_rows + 1, (int)std::ceil(cr + hw) + 1);
+        }
+        // staged column pitch: 3 or 5 (mod 8) quads, so lanes on neighbouring detector columns
+        // (C3: ~1 column per voxel) read different 16-B bank groups; rows past the detector are TMA zero fill
+        int nq = q1 - q0 + 1;
         while ((nq & 7) != 3 && (nq & 7) != 5) ++nq;
-        b.nq_s = 2 * nq <= 256 ? nq : g.n_rows + 2;
+        if (2 * nq > 256) { q0 = 0; nq = g.n_rows + 2; }
+        b.q_lo = q0;
+        b.nq_s = nq;
         b.bp_items = 1;
     }
     b.zero = 0u;

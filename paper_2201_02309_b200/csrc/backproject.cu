@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
                 mbar_expect_tx(full, NI * box_bytes);
 #pragma unroll
                 for (int i = 0; i < NI; ++i)
-                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qmap, 0, boxc[n],
+                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qmap, 2 * p.q_lo, boxc[n],
                             vbase + (int)(i * p.item_views) + n, full);
                 sl += G;
                 if (sl >= S) { sl -= S; phase ^= 1u; }
@@ -534,7 +534,8 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
                 for (int b = 0; b < NI; ++b) {
                     // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
                     const unsigned colbase =
-                        (stage_sa + (unsigned)(sl * vs + b * vq + ci * NQ) * 16u - kMagicBits * 16u) ^ p.zero;
+                        (stage_sa + (unsigned)(sl * vs + b * vq + ci * NQ) * 16u - (kMagicBits + (unsigned)p.q_lo) * 16u) ^
+                        p.zero;
                     u64 PM = pk(base, base + step);
 #pragma unroll
                     for (int g = 0; g < W; g += kGroup) {
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
                 // the view's geometry record rides with its slot (released by the arrive below)
                 s_vg[sl] = __ldg(reinterpret_cast<const float4 *>(p.view) + (KC0 + n - p.view_lo));
                 mbar_expect_tx(full, box_bytes);
-                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 0, boxc[n], vbase + n, full);
+                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 2 * p.q_lo, boxc[n], vbase + n, full);
                 if (++sl == S) { sl = 0; phase ^= 1u; }
             }
         }
@@ -721,7 +722,9 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     }
 
     // ---- consumer warps ----
-    const unsigned slot0 = stage_sa - kMagicBits * 16u;   // quad row r of slot s, column c: slot0 + s*slot_bytes + c*col_bytes + (kMagicBits + r)*16
+    // quad row r of slot s, column c: slot0 + s*slot_bytes + c*col_bytes + (kMagicBits + r)*16 (the box's
+    // first staged quad row is q_lo)
+    const unsigned slot0 = stage_sa - (kMagicBits + (unsigned)p.q_lo) * 16u;
     // slice t -> TMEM column t mod Wc of the warp's range (lane = TMEM lane)
     const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * Wc);
     {
@@ -1360,8 +1363,9 @@ bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
     if (!fn) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)2 * (p.nr + 2), (cuuint64_t)p.nc, (cuuint64_t)n_views};
     const cuuint64_t strides[2] = {(cuuint64_t)(p.nr + 2) * 16, (cuuint64_t)p.viewbytes};
-    // the box's column is p.nq_s >= nr + 2 quads: the rows past the detector are zero-filled (out of
-    // bounds) and make the staged column pitch an odd number of 16-B bank groups
+    // the box's column is p.nq_s quads from quad row p.q_lo (the rows interior samples can reach, |w| <=
+    // w_L); rows past the detector are zero-filled (out of bounds); the pitch is an odd number of
+    // 16-B bank groups
     const cuuint32_t box[3] = {(cuuint32_t)(2 * p.nq_s), (cuuint32_t)p.fp_cols_column, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
