@@ -517,6 +517,200 @@ __global__ void __launch_bounds__(HK_THREADS, 2) k_hilbert_hk(FilterParams p, in
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized Hankel-core K3 (default for wide detectors).  One persistent CTA per SM, fixed
+// to one parity, walks work items (128-line block, output half with N = NN <= 256):
+//   warps 0-7   producers: load an A chunk (128 lines x 32 inputs, K reversed), split hi/lo, store
+//               it in the canonical layout into a 4-deep ring, one mbarrier arrive per warp;
+//   warp 8      MMA: one thread issues the chunk's 3xTF32 MMAs (B = the resident Hankel cores)
+//               into one of two TMEM accumulators and commits the ring slot back to the producers;
+//               after an item's last chunk it commits the accumulator to the epilogue;
+//   warps 9-12  epilogue: one TMEM lane quarter each, accumulator -> padded smem -> g4, then free
+//               the accumulator, while the tensor core already works on the next item.
+// ---------------------------------------------------------------------------
+constexpr int WS_PROD = 8, WS_EPI = 4, WS_THREADS = 32 * (WS_PROD + 1 + WS_EPI), WS_NST = 4;
+
+__device__ __forceinline__ void ws_wait(unsigned bar, unsigned parity)
+{
+    asm volatile("{\n\t.reg .pred d;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 d, [%0], %1;\n\t"
+                 "@!d bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void ws_arrive(unsigned bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, int64_t n_lines, int nsplit)
+{
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC, NS = NH / 2;
+    const int NN = NH / nsplit;
+    const int par = blockIdx.x & 1, cta = blockIdx.x >> 1, ncta = gridDim.x >> 1;
+    const int nin = (nc - (1 - par) + 1) / 2, nout = (nc - par + 1) / 2;
+    const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
+    unsigned char *Bh = tsm, *Bl = tsm + NS * 128;
+    unsigned char *A0 = tsm + 2 * NS * 128;
+    constexpr unsigned kStage = 2 * TC_M * TC_KC * 4;
+    float *stg_all = reinterpret_cast<float *>(A0 + WS_NST * kStage);   // epilogue: 4 warps x 32 x 17
+    __shared__ __align__(8) unsigned long long s_full[WS_NST], s_empty[WS_NST], s_afull[2], s_aempty[2];
+    __shared__ unsigned s_tmem;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
+    const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
+    const unsigned afull0 = (unsigned)__cvta_generic_to_shared(&s_afull[0]);
+    const unsigned aempty0 = (unsigned)__cvta_generic_to_shared(&s_aempty[0]);
+    if (warp == WS_PROD) {                                       // two accumulators of 256 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < WS_NST; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(full0 + 8u * i), "r"(WS_PROD));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8u * i));
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(afull0 + 8u * i));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(aempty0 + 8u * i), "r"(WS_EPI));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {   // the parity's tap cores (hi then lo)
+        const float4 *src = reinterpret_cast<const float4 *>(p.hilbert_hk) + (size_t)par * 2 * NS * 8;
+        float4 *dst = reinterpret_cast<float4 *>(Bh);
+        for (int i = tid; i < 2 * NS * 8; i += WS_THREADS) dst[i] = __ldg(src + i);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = s_tmem;
+
+    if (warp < WS_PROD) {
+        // ---- producers: thread -> rows 32 rg + 8 gq + rr (gq = 0..3), inputs j in [4 kq, 4 kq + 4) of a
+        //      chunk; a load instruction covers 8 lines x 4 K quads (128 contiguous bytes per line) ----
+        const int rr = tid & 7, kq = (tid >> 3) & 7, rg = tid >> 6;
+        int g = 0;
+        for (int64_t item = cta; item < n_items; item += ncta) {
+            const int64_t line0 = item / nsplit * TC_M + rg * 32 + rr;
+            auto load = [&](int kc, float (&v)[16]) {
+#pragma unroll
+                for (int gq = 0; gq < 4; ++gq) {
+                    const int64_t line = line0 + gq * 8;
+                    const float *src = p.g3 + line * nc + (1 - par);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int k = NH - 1 - (kc * TC_KC + 4 * kq + i);
+                        v[4 * gq + i] = (line < n_lines && k < nin) ? __ldg(src + 2 * k) : 0.f;
+                    }
+                }
+            };
+            float cur[16];
+            load(0, cur);
+            for (int kc = 0; kc < NK; ++kc, ++g) {
+                const int st = g % WS_NST;
+                float nxt[16];
+                if (kc + 1 < NK) load(kc + 1, nxt);
+                if (g >= WS_NST) ws_wait(empty0 + 8u * st, (unsigned)((g / WS_NST) - 1) & 1u);
+                unsigned char *Ah = A0 + st * kStage, *Al = Ah + TC_M * TC_KC * 4;
+#pragma unroll
+                for (int gq = 0; gq < 4; ++gq) {
+                    const float *v = cur + 4 * gq;
+                    const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
+                    const unsigned o = tc_off(rg * 32 + gq * 8 + rr, 4 * kq);
+                    *reinterpret_cast<float4 *>(Ah + o) = h;
+                    *reinterpret_cast<float4 *>(Al + o) = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+                __syncwarp();
+                if (lane == 0) ws_arrive(full0 + 8u * st);
+            }
+        }
+    } else if (warp == WS_PROD) {
+        // ---- MMA issuer ----
+        if (lane == 0) {
+            const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_M >> 4) << 24) |
+                                   ((unsigned)(NN >> 3) << 17);
+            const unsigned sBh = (unsigned)__cvta_generic_to_shared(Bh), sBl = (unsigned)__cvta_generic_to_shared(Bl);
+            int g = 0, it = 0;
+            for (int64_t item = cta; item < n_items; item += ncta, ++it) {
+                const int acc = it & 1;
+                const int n_lo = (int)(item % nsplit) * NN;
+                if (it >= 2) ws_wait(aempty0 + 8u * acc, (unsigned)((it >> 1) - 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const unsigned tcol = tmem + (unsigned)(acc * 256);
+                for (int kc = 0; kc < NK; ++kc, ++g) {
+                    const int st = g % WS_NST;
+                    ws_wait(full0 + 8u * st, (unsigned)(g / WS_NST) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned sAh = (unsigned)__cvta_generic_to_shared(A0 + st * kStage);
+                    const unsigned sAl = sAh + TC_M * TC_KC * 4;
+#pragma unroll
+                    for (int kk = 0; kk < TC_KC / 8; ++kk) {
+                        const unsigned core = (unsigned)(2 * (n_lo >> 3) + kc * 8 + kk * 2) * 128u;
+                        const uint64_t a_h = tc_desc(sAh + (unsigned)kk * 256u), a_l = tc_desc(sAl + (unsigned)kk * 256u);
+                        const uint64_t b_h = hk_desc(sBh + core), b_l = hk_desc(sBl + core);
+                        const unsigned first = (kc == 0 && kk == 0) ? 0u : 1u;
+                        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, q;\n\t}"
+                                     ::"r"(tcol), "l"(a_h), "l"(b_h), "r"(idesc), "r"(first));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;"
+                                     ::"r"(tcol), "l"(a_h), "l"(b_l), "r"(idesc));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;"
+                                     ::"r"(tcol), "l"(a_l), "l"(b_h), "r"(idesc));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                 ::"r"(empty0 + 8u * st) : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                             ::"r"(afull0 + 8u * acc) : "memory");
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- epilogue: TMEM lane quarter q4 = lines 32 q4 .. of the item ----
+        const int ew = warp - WS_PROD - 1, q4 = warp & 3;
+        float *stg = stg_all + ew * 32 * 17;
+        int it = 0;
+        for (int64_t item = cta; item < n_items; item += ncta, ++it) {
+            const int acc = it & 1;
+            const int64_t line0 = item / nsplit * TC_M;
+            const int n_lo = (int)(item % nsplit) * NN;
+            ws_wait(afull0 + 8u * acc, (unsigned)(it >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const unsigned trow = tmem + ((unsigned)(q4 * 32) << 16) + (unsigned)(acc * 256);
+            for (int c = 0; c < NN; c += 16) {
+                float v[16];
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                             : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+                               "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+                             : "r"(trow + (unsigned)c));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int i = 0; i < 16; ++i) stg[lane * 17 + i] = v[i];
+                __syncwarp();
+                const int cl = lane & 15, rh = lane >> 4;
+                const int n = n_lo + c + cl;
+                for (int r = rh; r < 32; r += 2) {
+                    const int64_t ln = line0 + q4 * 32 + r;
+                    if (ln < n_lines && n < nout && c + cl < NN) p.g4[ln * nc + 2 * n + par] = p.sign * stg[r * 17 + cl];
+                }
+                __syncwarp();
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) ws_arrive(aempty0 + 8u * acc);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == WS_PROD) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
 // Both parities per CTA (NH <= 256: two accumulators fit TMEM's 512 columns).
 // A K chunk covers inputs l in [64 kc, 64 kc + 64) of each line (coalesced
 // loads), de-interleaved into the even- and odd-input tiles; output parity 0
@@ -792,7 +986,8 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
     }
     // KATS_HILBERT=tc: the per-chunk tap-streaming kernels (A/B tests); =hk: Hankel cores for every width
     const char *he = std::getenv("KATS_HILBERT");
-    const bool force_tc = he && std::string(he) == "tc", force_hk = he && std::string(he) == "hk";
+    const bool force_tc = he && std::string(he) == "tc",
+               force_hk = he && (std::string(he) == "hk" || std::string(he) == "hk1" || std::string(he) == "ws");
     if (hilbert_tc_usable(p) && p.hilbert_hk && !force_tc && (hilbert_tc_nh(p.nc) > 128 || force_hk)) {
         const int NH = hilbert_tc_nh(p.nc);
         // halves only where 2 CTAs per SM pay for reading A twice (C3 NH 384: 1.20 -> 1.13 ms;
@@ -811,6 +1006,24 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
             attr = true;
         }
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
+        // warp-specialized for wide detectors (C3 1.13 -> 1.00 ms, C5 1.33 -> 1.07 ms); at NH <= 256 the
+        // two-CTA persistent kernel is faster (C2 0.18 vs 0.21 ms). KATS_HILBERT=hk1: never specialized
+        const bool ws = (NH > 256 || (he && std::string(he) == "ws")) && !(he && std::string(he) == "hk1");
+        if (ws) {
+            const int ns = NH > 256 ? 2 : 1;                          // accumulators of <= 256 columns, two of them
+            const size_t wsm = taps + (size_t)WS_NST * stage + (size_t)WS_EPI * 32 * 17 * 4;
+            static bool wattr = false;
+            if (!wattr) {
+                cudaFuncSetAttribute(k_hilbert_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+                wattr = true;
+            }
+            int nsm2 = 148;
+            cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, 0);
+            const int64_t items = (n_lines + TC_M - 1) / TC_M * ns;
+            const int per = (int)std::min<int64_t>(items, std::max(1, nsm2 / 2));   // one CTA per SM, half per parity
+            k_hilbert_ws<<<(unsigned)(2 * per), WS_THREADS, wsm, s>>>(p, n_lines, ns);
+            return;
+        }
         const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);

@@ -59,7 +59,7 @@ def test_reconstruct_matches_oracle(name):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("hilbert", ["default", "tc", "hk", "fp32"])
+@pytest.mark.parametrize("hilbert", ["default", "tc", "hk", "hk1", "ws", "fp32"])
 @pytest.mark.parametrize("name", ["T1", "T3", "C1"])
 def test_filter_stages_match_oracle(name, hilbert, monkeypatch):
     """Steps 1-6 per stage (g3, g4, gF) against the oracle; K3 on the tensor cores
