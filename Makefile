@@ -17,7 +17,7 @@ $(CSRC)/precompute.o: $(CSRC)/precompute.cpp $(HDRS)
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC,-fopenmp,-O3 -x c++ -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp -Xlinker -z,defs
 
 oracle/liboracle.so: oracle/oracle.cpp
 	g++ -O2 -std=c++17 -fopenmp -fPIC -shared -o $@ $<

@@ -25,6 +25,7 @@
 //    out-of-detector test (A9, A11);
 //  * which slices of the chunk see view k is a bitmask recomputed only at the
 //    2·JZ events where a slice's interior window opens or closes.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -358,6 +359,42 @@ __device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, floa
     return max(0, min(c0, p.nc - p.fp_cols_column));
 }
 
+// Tensor maps of the staged kernels: box widths p.box_w[0] (= the largest box) >= [1] >= [2] columns.
+struct QMaps { CUtensorMap m[3]; };
+bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width);
+// the three box widths of a plan: the full column box, 4/5 and 16/25 of it (C5: 56, 45, 36 columns;
+// the tile widths of its views average 35.5)
+inline void set_box_widths(BPParams &p)
+{
+    const int w = p.fp_cols_column;
+    p.box_w[0] = w;
+    p.box_w[1] = std::min(w, (4 * w + 4) / 5);
+    p.box_w[2] = std::min(p.box_w[1], (16 * w + 24) / 25);
+}
+bool make_quad_maps(BPParams &p, QMaps *m)
+{
+    set_box_widths(p);
+    for (int i = 0; i < 3; ++i)
+        if (!make_quad_map(p, p.gq_views, &m->m[i], p.box_w[i])) return false;
+    return true;
+}
+
+// staged box of view k for a CTA tile: first column c0 (clamped like plan_col) and the narrowest
+// width class covering the tile's corner-ray columns + 1 column of fp32 slack: c0 | class << 16
+template <bool POLY>
+__device__ __forceinline__ int plan_col_cls(const BPParams &p, int k, float xa, float ya)
+{
+    const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+    const float xb = xa + (TX - 1) * p.dx, yb = ya + (TY - 1) * p.dy;
+    const float ca = col_of<POLY>(p, xa, ya, vg.x, vg.y), cb = col_of<POLY>(p, xb, ya, vg.x, vg.y);
+    const float cc = col_of<POLY>(p, xa, yb, vg.x, vg.y), cd = col_of<POLY>(p, xb, yb, vg.x, vg.y);
+    const float cmin = fminf(fminf(ca, cb), fminf(cc, cd)), cmax = fmaxf(fmaxf(ca, cb), fmaxf(cc, cd));
+    const int c0 = max(0, min((int)floorf(cmin) - 1, p.nc - p.fp_cols_column));
+    const int need = (int)floorf(cmax) + 2 - c0;
+    const int cls = need <= p.box_w[2] ? 2 : need <= p.box_w[1] ? 1 : 0;
+    return c0 | (cls << 16);
+}
+
 // ---------------------------------------------------------------------------
 // Sliding-window kernel.  A thread owns a whole (x, y) column of the pitch and
 // keeps W scalar accumulators for exactly the slices whose interior PI windows
@@ -376,7 +413,7 @@ __device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, floa
 //          detector columns, hence bank groups, per LDS.128 wavefront).
 template <bool POLY, int W, int V>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ CUtensorMap qmap, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ QMaps qm, BPParams p)
 {
     constexpr int NI = V == 2 ? 2 : 1;
     constexpr bool TAIL = V >= 1, QMAP42 = V == 2;
@@ -384,7 +421,6 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
     const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch;          // NQ: staged column pitch (quads)
     const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged box (128-B aligned)
     const int vs = NI * vq;                                              // quads per slot (NI items' boxes)
-    const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
     float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
     int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vs * 16);   // first column per view
     __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
@@ -431,13 +467,13 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
     const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
     {
         const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
-        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col<POLY>(p, KC0 + n, xa, ya);
+        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya);
     }
     __syncthreads();
 
     if (producer) {
         if (NV <= 0) return;
-        // ---- producer warp: lanes 0..3 stream one view's full-height column boxes (NI items) each per round ----
+        // ---- producer warp: lanes 0..3 stream one view's column boxes (NI items) each per round ----
         const int vbase = (int)(p.off0 + (int64_t)item0 * p.item_views) + KC0;
         const int G = min(4, S);                              // lanes in flight; divides S (powers of 2)
         if (lane < G) {
@@ -446,10 +482,11 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
             for (int n = lane; n < NV; n += G) {
                 if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
                 const unsigned full = full0 + 8u * sl;
-                mbar_expect_tx(full, NI * box_bytes);
+                const int bc = boxc[n], cls = bc >> 16;
+                mbar_expect_tx(full, NI * (unsigned)(p.box_w[cls] * NQ) * 16u);
 #pragma unroll
                 for (int i = 0; i < NI; ++i)
-                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qmap, 2 * p.q_lo, boxc[n],
+                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qm.m[cls], 2 * p.q_lo, bc & 0xFFFF,
                             vbase + (int)(i * p.item_views) + n, full);
                 sl += G;
                 if (sl >= S) { sl -= S; phase ^= 1u; }
@@ -525,7 +562,7 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
                 const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
                 const float step = sc * p.dz;
                 const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));    // entry 0 = slice t_lo
-                const int ci = min(max(l - boxc[n], 0), BW - 1);
+                const int ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
                 const u64 S2 = pk(2.f * step, 2.f * step);
                 // (V >= 1) entries past every working lane's last open slice are not sampled at all
                 int n_w = W;
@@ -639,12 +676,11 @@ size_t tmem_smem_bytes(const BPParams &p)
 
 template <bool POLY, int VP>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant__ CUtensorMap qmap, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant__ QMaps qm, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch, Wc = p.tmem_cols;   // NQ: staged column pitch
     const int vq = (BW * NQ + 7) & ~7;
-    const unsigned box_bytes = (unsigned)(BW * NQ) * 16u;
     const size_t head = tmem_head_bytes(p);                   // pad for reads below the first column
     float4 *stage = reinterpret_cast<float4 *>(smem + head);
     int *boxc = reinterpret_cast<int *>(smem + head + (size_t)S * vq * 16);
@@ -698,7 +734,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
     {
         const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
-        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col<POLY>(p, KC0 + n, xa, ya);
+        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya);
     }
     __syncthreads();
 
@@ -713,8 +749,9 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
                 const unsigned full = full0 + 8u * sl;
                 // the view's geometry record rides with its slot (released by the arrive below)
                 s_vg[sl] = __ldg(reinterpret_cast<const float4 *>(p.view) + (KC0 + n - p.view_lo));
-                mbar_expect_tx(full, box_bytes);
-                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qmap, 2 * p.q_lo, boxc[n], vbase + n, full);
+                const int bc = boxc[n], cls = bc >> 16;
+                mbar_expect_tx(full, (unsigned)(p.box_w[cls] * NQ) * 16u);
+                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qm.m[cls], 2 * p.q_lo, bc & 0xFFFF, vbase + n, full);
                 if (++sl == S) { sl = 0; phase ^= 1u; }
             }
         }
@@ -792,7 +829,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
         const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
         step = sc * p.dz;
         base = fmaf(sc, -vg.z, p.row_cc);                       // slice 0 (centred quad-row position)
-        ci = min(max(l - boxc[n], 0), BW - 1);
+        ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
     };
     const unsigned wmask = (unsigned)Wc - 1u;                    // Wc is a power of two
     // 8 samples of one view for the group's slices (PM: packed positions of slices j, j+1)
@@ -1293,7 +1330,7 @@ size_t backproject_smem_bytes(const BPParams &p)
 }
 
 template <bool POLY, int VP>
-void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &qmap, cudaStream_t s)
+void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
     static bool attr = false;
     if (!attr) {
@@ -1304,7 +1341,7 @@ void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const CUtensorM
 }
 
 template <int W>
-void launch_window(const BPParams &q, dim3 grid, size_t sm, const CUtensorMap &qmap, cudaStream_t s)
+void launch_window(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
     static bool attr = false;
     if (!attr) {
@@ -1355,9 +1392,11 @@ EncodeTiledFn encode_tiled()
     return fn;
 }
 
+}  // namespace
+
 // the quad array as a 3-D tensor of 8-byte elements: (2 * (nr+2) per column, nc columns, n_views);
 // box = full column height x fp_cols_column columns x 1 view
-bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
+bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width)
 {
     EncodeTiledFn fn = encode_tiled();
     if (!fn) return false;
@@ -1366,13 +1405,12 @@ bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map)
     // the box's column is p.nq_s quads from quad row p.q_lo (the rows interior samples can reach, |w| <=
     // w_L); rows past the detector are zero-filled (out of bounds); the pitch is an odd number of
     // 16-B bank groups
-    const cuuint32_t box[3] = {(cuuint32_t)(2 * p.nq_s), (cuuint32_t)p.fp_cols_column, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * p.nq_s), (cuuint32_t)width, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-}  // namespace
 
 int launch_backproject(const BPParams &p, cudaStream_t s)
 {
@@ -1414,8 +1452,8 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
         q.slot_bytes = 16u * (unsigned)((p.fp_cols_column * p.nq_s + 7) & ~7);
         q.col_bytes = 16u * (unsigned)p.nq_s;
         const size_t sm = tmem_smem_bytes(q);
-        CUtensorMap qmap;
-        if (alloc <= 128 && sm <= 200 * 1024 && make_quad_map(p, p.gq_views, &qmap)) {
+        QMaps qmap;
+        if (alloc <= 128 && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
             dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
             if (vp == 2) {
                 if (p.poly) launch_tmem_kernel<true, 2>(q, gw, sm, qmap, s);
@@ -1441,10 +1479,10 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     q.nbatch = kMaxSlots;
     while (q.nbatch > 2 && backproject_smem_bytes(q) > budget) q.nbatch /= 2;
     const size_t sm = backproject_smem_bytes(q);
-    CUtensorMap qmap;
+    QMaps qmap;
     if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
         p.tail_quads <= 4096 &&
-        p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_map(p, p.gq_views, &qmap)) {
+        p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_maps(q, &qmap)) {
         dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
         switch (W) {
         case 8: launch_window<8>(q, gw, sm, qmap, s); break;
