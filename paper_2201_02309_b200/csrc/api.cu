@@ -112,7 +112,7 @@ int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
 
 size_t filter_chunk_bytes(const katsevich_plan *p)
 {
-    return 2 * sizeof(float) * (size_t)filter_chunk_views(p) * p->t.n_psi * p->g.n_cols;
+    return 2 * sizeof(float) * (size_t)filter_chunk_views(p) * p->t.n_psi * g3_line_pitch(p->g.n_cols);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -144,9 +144,12 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
     // running concurrently with the TMEM backprojection: K3 uses the fp32 direct convolution
     // (launch_hilbert); results then agree with the device path to fp32 rounding, not bitwise
     f.hilbert_overlap = overlapped ? 1 : 0;
+    f.hp = g3_half_pitch(p->g.n_cols);
+    f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K12 writes the lines the chosen K3 reads
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
     const size_t qs = quad_view_elems(p);
-    const size_t ps = (size_t)p->t.n_psi * p->g.n_cols;
+    const size_t ps_dbg = (size_t)p->t.n_psi * p->g.n_cols;              // debug stage arrays: plain lines
+    const size_t ps = (size_t)p->t.n_psi * g3_line_pitch(p->g.n_cols);  // scratch lines
     const int kFilterChunk = filter_chunk_views(p);
     for (int64_t v0 = 0; v0 < n_out; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, n_out - v0);
@@ -154,11 +157,22 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
         f.view0 = v0;
         f.slab_views = slab_views;
         f.n_views = nv;
-        f.g3 = dbg3 ? dbg3 + v0 * ps : scratch;
-        f.g4 = dbg4 ? dbg4 + v0 * ps : scratch + (size_t)kFilterChunk * ps;
+        f.g3 = scratch;
+        f.g4 = dbg4 ? dbg4 + v0 * ps_dbg : scratch + (size_t)kFilterChunk * ps;
         f.gq = gq + v0 * qs;
         f.gF = dbgF ? dbgF + v0 * rs : nullptr;
-        { LaunchScope ls(p, ST_K12, s); launch_deriv_fwd_rebin(f, s); }
+        if (dbg3) {                                                // debug: g3 as plain lines too
+            FilterParams d = f;
+            d.k3_in_split = 0;
+            d.g3 = dbg3 + v0 * ps_dbg;
+            { LaunchScope ls(p, ST_K12, s); launch_deriv_fwd_rebin(d, s); }
+            KCHECK(p, cudaGetLastError());
+            if (!f.k3_in_split) f.g3 = d.g3;
+        }
+        if (!dbg3 || f.k3_in_split) {
+            LaunchScope ls(p, ST_K12, s);
+            launch_deriv_fwd_rebin(f, s);
+        }
         KCHECK(p, cudaGetLastError());
         { LaunchScope ls(p, ST_K3, s); launch_hilbert(f, s); }
         KCHECK(p, cudaGetLastError());
@@ -569,7 +583,9 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
     }
     KCHECK(p, cudaGetLastError());
     FilterParams f = filter_params(p);
-    const size_t ps = (size_t)t.n_psi * p->g.n_cols;
+    f.hp = g3_half_pitch(p->g.n_cols);
+    f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K4^T writes the lines K3^T reads
+    const size_t ps = (size_t)t.n_psi * g3_line_pitch(p->g.n_cols);
     for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, nu - v0);
         f.n_views = nv;
@@ -632,7 +648,9 @@ int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, flo
     }
     KCHECK(p, cudaGetLastError());
     FilterParams f = filter_params(p);
-    const size_t ps = (size_t)t.n_psi * p->g.n_cols;
+    f.hp = g3_half_pitch(p->g.n_cols);
+    f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K4^T writes the lines K3^T reads
+    const size_t ps = (size_t)t.n_psi * g3_line_pitch(p->g.n_cols);
     for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, nu - v0);
         f.n_views = nv;
@@ -900,10 +918,10 @@ int katsevich_filter(katsevich_plan *p, const float *sino, int64_t s0, int64_t s
     cudaStream_t s = (cudaStream_t)cuda_stream;
     float *scratch = nullptr;
     float4 *gq = nullptr;
-    if (!g3 || !g4) KCHECK(p, cudaMallocAsync((void **)&scratch, filter_chunk_bytes(p), s));
+    KCHECK(p, cudaMallocAsync((void **)&scratch, filter_chunk_bytes(p), s));   // (split K3 input lines)
     KCHECK(p, cudaMallocAsync((void **)&gq, sizeof(float4) * quad_view_elems(p) * (size_t)n_out, s));
     rc = run_filter(p, sino + (out_first_view - s0) * rs, n_out, gq, scratch, g3, g4, gF, s);
-    if (scratch) cudaFreeAsync(scratch, s);
+    cudaFreeAsync(scratch, s);
     cudaFreeAsync(gq, s);
     return rc;
 }

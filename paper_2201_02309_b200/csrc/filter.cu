@@ -20,6 +20,12 @@ namespace kats {
 //      differences, one-sided at the α edges; reading A5).
 // Grid: x over α (coalesced), y over ψ, z over views.
 // ---------------------------------------------------------------------------
+// K3 input element (line, column l): plain lines of nc floats, or parity-split lines (p.k3_in_split)
+__device__ __forceinline__ size_t k3in_off(const FilterParams &p, size_t line, int l)
+{
+    return p.k3_in_split ? line * (size_t)(2 * p.hp) + (size_t)((l & 1) * p.hp + (l >> 1)) : line * (size_t)p.nc + l;
+}
+
 __device__ __forceinline__ float g2_at(const FilterParams &p, const float *__restrict__ gv, int m, int l)
 {
     const int rs = p.nr * p.nc, vs = rs;
@@ -46,7 +52,7 @@ __global__ void __launch_bounds__(256) k_deriv_fwd_rebin(FilterParams p)
     const int64_t g = p.view0 + v;
     const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
     const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
-    float *out = p.g3 + ((size_t)v * p.npsi + i0) * p.nc + l;
+    const size_t line0 = (size_t)v * p.npsi + i0;
 #pragma unroll
     for (int j = 0; j < kPsiPer; ++j) {
         if (i0 + j >= p.npsi) break;
@@ -57,7 +63,7 @@ __global__ void __launch_bounds__(256) k_deriv_fwd_rebin(FilterParams p)
             const float b = g2_at(p, gv, e.idx + 1, l);
             o = fmaf(e.frac, b - a, a);
         }
-        out[(size_t)j * p.nc] = o;
+        p.g3[k3in_off(p, line0 + j, l)] = o;
     }
 }
 
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin_col(FilterParams p, int
     const int64_t g = p.view0 + v;
     const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
     const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
-    float *out = p.g3 + (size_t)v * p.npsi * p.nc + l;
+    const size_t line0 = (size_t)v * p.npsi;
     int r0 = -2, r1 = -2;                                          // cached rows and their g2
     float c0 = 0.f, c1 = 0.f;
     for (int i = i0; i < i1; ++i) {
@@ -89,7 +95,7 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin_col(FilterParams p, int
             r0 = m; c0 = a; r1 = m + 1; c1 = b;
             o = fmaf(e.frac, b - a, a);
         }
-        out[(size_t)i * p.nc] = o;
+        p.g3[k3in_off(p, line0 + i, l)] = o;
     }
 }
 
@@ -529,6 +535,18 @@ __global__ void __launch_bounds__(HK_THREADS, 2) k_hilbert_hk(FilterParams p, in
 //               the accumulator, while the tensor core already works on the next item.
 // ---------------------------------------------------------------------------
 constexpr int WS_PROD = 8, WS_EPI = 4, WS_THREADS = 32 * (WS_PROD + 1 + WS_EPI), WS_NST = 4;
+// A tiles of this kernel: K-major core matrices with LBO = 144 B (K quads 9 bank groups apart) and
+// SBO = 1152 B, so the 8 K quads of one line a quarter-warp stores hit 8 different 16-B bank groups
+constexpr unsigned WS_LBO = 144, WS_SBO = 1152, WS_ATILE = (TC_M / 8) * WS_SBO;
+__device__ __forceinline__ unsigned ws_off(int row, int k)
+{
+    return (unsigned)((row >> 3) * WS_SBO + (k >> 2) * WS_LBO + (row & 7) * 16 + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t ws_desc(unsigned saddr)
+{
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(WS_LBO >> 4) << 16) | ((uint64_t)(WS_SBO >> 4) << 32) |
+           (1ull << 46);
+}
 
 __device__ __forceinline__ void ws_wait(unsigned bar, unsigned parity)
 {
@@ -551,7 +569,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
     const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
     unsigned char *Bh = tsm, *Bl = tsm + NS * 128;
     unsigned char *A0 = tsm + 2 * NS * 128;
-    constexpr unsigned kStage = 2 * TC_M * TC_KC * 4;
+    constexpr unsigned kStage = 2 * WS_ATILE;
     float *stg_all = reinterpret_cast<float *>(A0 + WS_NST * kStage);   // epilogue: 4 warps x 32 x 17
     __shared__ __align__(8) unsigned long long s_full[WS_NST], s_empty[WS_NST], s_afull[2], s_aempty[2];
     __shared__ unsigned s_tmem;
@@ -588,22 +606,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
     const unsigned tmem = s_tmem;
 
     if (warp < WS_PROD) {
-        // ---- producers: thread -> rows 32 rg + 8 gq + rr (gq = 0..3), inputs j in [4 kq, 4 kq + 4) of a
-        //      chunk; a load instruction covers 8 lines x 4 K quads (128 contiguous bytes per line) ----
-        const int rr = tid & 7, kq = (tid >> 3) & 7, rg = tid >> 6;
+        // ---- producers (parity-split input lines): thread -> K quad kq of the chunk, rows rs + 32 j; a quad
+        //      is one aligned float4 of the parity's inputs k = 4m .. 4m+3 (m = NH/4 - 1 - 8 kc - kq), stored
+        //      reversed (K is reversed); a load instruction covers 4 lines x 128 contiguous bytes ----
+        const int kq = tid & 7, rs = tid >> 3;
+        const int hp = p.hp;
         int g = 0;
         for (int64_t item = cta; item < n_items; item += ncta) {
-            const int64_t line0 = item / nsplit * TC_M + rg * 32 + rr;
+            const int64_t line0 = item / nsplit * TC_M + rs;
             auto load = [&](int kc, float (&v)[16]) {
+                const int k0 = 4 * (NH / 4 - 1 - 8 * kc - kq);
 #pragma unroll
-                for (int gq = 0; gq < 4; ++gq) {
-                    const int64_t line = line0 + gq * 8;
-                    const float *src = p.g3 + line * nc + (1 - par);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int k = NH - 1 - (kc * TC_KC + 4 * kq + i);
-                        v[4 * gq + i] = (line < n_lines && k < nin) ? __ldg(src + 2 * k) : 0.f;
-                    }
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t line = line0 + 32 * j;
+                    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (line < n_lines && k0 < nin)
+                        q = __ldg(reinterpret_cast<const float4 *>(p.g3 + line * (2 * hp) + (1 - par) * hp + k0));
+                    v[4 * j + 0] = k0 + 3 < nin ? q.w : 0.f;               // k' order: k0+3, .., k0
+                    v[4 * j + 1] = k0 + 2 < nin ? q.z : 0.f;
+                    v[4 * j + 2] = k0 + 1 < nin ? q.y : 0.f;
+                    v[4 * j + 3] = q.x;
                 }
             };
             float cur[16];
@@ -613,12 +635,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
                 float nxt[16];
                 if (kc + 1 < NK) load(kc + 1, nxt);
                 if (g >= WS_NST) ws_wait(empty0 + 8u * st, (unsigned)((g / WS_NST) - 1) & 1u);
-                unsigned char *Ah = A0 + st * kStage, *Al = Ah + TC_M * TC_KC * 4;
+                unsigned char *Ah = A0 + st * kStage, *Al = Ah + WS_ATILE;
 #pragma unroll
-                for (int gq = 0; gq < 4; ++gq) {
-                    const float *v = cur + 4 * gq;
+                for (int j = 0; j < 4; ++j) {
+                    const float *v = cur + 4 * j;
                     const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
-                    const unsigned o = tc_off(rg * 32 + gq * 8 + rr, 4 * kq);
+                    const unsigned o = ws_off(rs + 32 * j, 4 * kq);
                     *reinterpret_cast<float4 *>(Ah + o) = h;
                     *reinterpret_cast<float4 *>(Al + o) = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
                 }
@@ -647,11 +669,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
                     ws_wait(full0 + 8u * st, (unsigned)(g / WS_NST) & 1u);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const unsigned sAh = (unsigned)__cvta_generic_to_shared(A0 + st * kStage);
-                    const unsigned sAl = sAh + TC_M * TC_KC * 4;
+                    const unsigned sAl = sAh + WS_ATILE;
 #pragma unroll
                     for (int kk = 0; kk < TC_KC / 8; ++kk) {
                         const unsigned core = (unsigned)(2 * (n_lo >> 3) + kc * 8 + kk * 2) * 128u;
-                        const uint64_t a_h = tc_desc(sAh + (unsigned)kk * 256u), a_l = tc_desc(sAl + (unsigned)kk * 256u);
+                        const uint64_t a_h = ws_desc(sAh + (unsigned)kk * 2u * WS_LBO), a_l = ws_desc(sAl + (unsigned)kk * 2u * WS_LBO);
                         const uint64_t b_h = hk_desc(sBh + core), b_l = hk_desc(sBl + core);
                         const unsigned first = (kc == 0 && kk == 0) ? 0u : 1u;
                         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
@@ -973,6 +995,18 @@ bool hilbert_tc_usable(const FilterParams &p)
     return p.hilbert_tc != nullptr && hilbert_tc_nh(p.nc) <= 512;
 }
 
+// The warp-specialized Hankel kernel (wide detectors, or KATS_HILBERT=ws) reads parity-split input
+// lines; the filter drivers ask here before the input's writer (K12 / K4^T) runs and set
+// k3_in_split, which launch_hilbert then follows.
+bool hilbert_split_input(const FilterParams &p)
+{
+    if (!hilbert_tc_usable(p) || p.hilbert_overlap || !p.hilbert_hk) return false;
+    const char *he = std::getenv("KATS_HILBERT");
+    const std::string h = he ? he : "";
+    if (h == "tc" || h == "hk" || h == "hk1") return false;
+    return hilbert_tc_nh(p.nc) > 256 || h == "ws";
+}
+
 void launch_hilbert(const FilterParams &p, cudaStream_t s)
 {
     if (hilbert_tc_usable(p) && p.hilbert_overlap) {
@@ -988,7 +1022,7 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
     const char *he = std::getenv("KATS_HILBERT");
     const bool force_tc = he && std::string(he) == "tc",
                force_hk = he && (std::string(he) == "hk" || std::string(he) == "hk1" || std::string(he) == "ws");
-    if (hilbert_tc_usable(p) && p.hilbert_hk && !force_tc && (hilbert_tc_nh(p.nc) > 128 || force_hk)) {
+    if (p.k3_in_split || (hilbert_tc_usable(p) && p.hilbert_hk && !force_tc && (hilbert_tc_nh(p.nc) > 128 || force_hk))) {
         const int NH = hilbert_tc_nh(p.nc);
         // halves only where 2 CTAs per SM pay for reading A twice (C3 NH 384: 1.20 -> 1.13 ms;
         // C5 NH 320: 1.32 -> 1.59 ms, measured)
@@ -1006,12 +1040,12 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
             attr = true;
         }
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
-        // warp-specialized for wide detectors (C3 1.13 -> 1.00 ms, C5 1.33 -> 1.07 ms); at NH <= 256 the
-        // two-CTA persistent kernel is faster (C2 0.18 vs 0.21 ms). KATS_HILBERT=hk1: never specialized
-        const bool ws = (NH > 256 || (he && std::string(he) == "ws")) && !(he && std::string(he) == "hk1");
+        // warp-specialized for wide detectors (hilbert_split_input: its input lines are parity-split);
+        // at NH <= 256 the two-CTA persistent kernel is faster (C2 0.18 vs 0.21 ms)
+        const bool ws = p.k3_in_split != 0;
         if (ws) {
             const int ns = NH > 256 ? 2 : 1;                          // accumulators of <= 256 columns, two of them
-            const size_t wsm = taps + (size_t)WS_NST * stage + (size_t)WS_EPI * 32 * 17 * 4;
+            const size_t wsm = taps + (size_t)WS_NST * 2 * WS_ATILE + (size_t)WS_EPI * 32 * 17 * 4;
             static bool wattr = false;
             if (!wattr) {
                 cudaFuncSetAttribute(k_hilbert_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
@@ -1103,8 +1137,8 @@ __global__ void __launch_bounds__(128) k_bwd_rebin_cos_T(FilterParams p, const f
     const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
     if (l >= p.nc) return;
     const int nc = p.nc, nr = p.nr, nq = nr + 2, c = (nr + 2) / 2;
-    float *g4T = p.g4 + (size_t)v * p.npsi * nc + l;
-    for (int i = 0; i < p.npsi; ++i) g4T[(size_t)i * nc] = 0.f;
+    const size_t line0 = (size_t)v * p.npsi;                    // output: K3^T's input lines
+    for (int i = 0; i < p.npsi; ++i) p.g4[k3in_off(p, line0 + i, l)] = 0.f;
     const float4 *qa = qT + ((size_t)v * nc + l) * nq;           // column l: its taps are quad x, z
     const float4 *qb = l > 0 ? qa - nq : nullptr;                // column l-1: this column is its y, w
     const float ca = __ldg(p.cos_alpha + l);
@@ -1120,8 +1154,8 @@ __global__ void __launch_bounds__(128) k_bwd_rebin_cos_T(FilterParams p, const f
         const RebinEntry e = p.br[m * nc + l];
         if (e.idx < 0) continue;
         const float val = ca * gt;
-        g4T[(size_t)e.idx * nc] += (1.f - e.frac) * val;
-        g4T[(size_t)(e.idx + 1) * nc] += e.frac * val;
+        p.g4[k3in_off(p, line0 + e.idx, l)] += (1.f - e.frac) * val;
+        p.g4[k3in_off(p, line0 + e.idx + 1, l)] += e.frac * val;
     }
 }
 

@@ -29,10 +29,16 @@ struct FilterParams {
     int hilbert_overlap;      // K3 runs next to the TMEM backprojection: keep its TMEM allocation <= 128 columns
     int64_t view0;            // K12: first filtered view of this launch in the run_filter sequence
     int64_t slab_views;       // K12: filtered views per slab of a batch (each slab carries its own +-1 halo); 0 = one scan
+    int k3_in_split;          // K3's input lines are parity-split (even columns, then odd, each hp floats): written
+                              // by K12 (forward) / K4^T (adjoint) when the warp-specialized K3 reads them
+    int hp;                   // half pitch of a parity-split line (floats, multiple of 4)
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
 void launch_hilbert(const FilterParams &p, cudaStream_t s);           // K3:  Eq. 12
+bool hilbert_split_input(const FilterParams &p);                      // the K3 launch_hilbert picks reads split lines
+inline int g3_half_pitch(int nc) { return ((nc + 1) / 2 + 3) & ~3; }
+inline int g3_line_pitch(int nc) { return 2 * g3_half_pitch(nc); }   // >= nc; scratch line pitch
 size_t hilbert_tc_table_floats(int nc);
 void hilbert_tc_table(int nc, const float *kd, std::vector<float> &out);
 size_t hilbert_hk_table_floats(int nc);
