@@ -233,6 +233,15 @@ int katsevich_export_tables(const katsevich_plan *plan, int32_t *pi_first, int32
                             double *w_first, double *w_last, int32_t *fr_idx, double *fr_frac,
                             int32_t *br_idx, double *br_frac);
 
+/* Tensor-core Hilbert taps (Eq. 12 on the tcgen05 tensor cores, DESIGN.md §5 "Hankel tap cores"):
+ * fill out[] (host memory, out_floats >= 64 * NH with NH = 32 * ceil(ceil(n_cols / 2) / 32)) with
+ * the layout k_hilbert_hk / k_hilbert_ws load into shared memory: [parity 2][hi, lo][NH/2 cores]
+ * [8 rows][4], core s row r column c = the TF32 hi part / fp32 remainder of the tap
+ * taps[2 (n - k) + 2 parity - 1 + n_cols - 1] with n + k' = 4 s + r + c, k = NH - 1 - k' (0 where
+ * that offset is outside the 2 n_cols - 1 taps).  taps: host, [2 n_cols - 1], K[d] at d + n_cols - 1.
+ * Pure host function (no plan, no device).  KATS_ERR_ARGUMENT if out_floats is too small. */
+int katsevich_hilbert_hk_table(int32_t n_cols, const float *taps, float *out, size_t out_floats);
+
 /* ---- in-run kernel timing (CUDA events on the launching stream) ---- */
 
 /* Per-stage statistics accumulated while profiling is enabled. */

@@ -58,6 +58,7 @@ SIGNATURES = {
     "katsevich_filter": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I32, _P, _P, _P, _P]),
     "katsevich_backproject": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _P, _P]),
     "katsevich_table_info": (ctypes.c_int, [_P, _PI32, _PI64, _PI64]),
+    "katsevich_hilbert_hk_table": (ctypes.c_int, [_I32, _P, _P, _SZ]),
     "katsevich_export_tables": (ctypes.c_int, [_P, _PI32, _PI32, _PD, _PD, _PI32, _PD, _PI32, _PD]),
     "katsevich_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
     "katsevich_profile_read": (ctypes.c_int, [_P, ctypes.POINTER(KatsevichStats), ctypes.c_int]),

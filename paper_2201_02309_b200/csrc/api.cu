@@ -954,6 +954,16 @@ int katsevich_backproject(katsevich_plan *p, const float *gF, int64_t gF0, int64
     return KATS_OK;
 }
 
+int katsevich_hilbert_hk_table(int32_t n_cols, const float *taps, float *out, size_t out_floats)
+{
+    if (n_cols < 1 || !taps || !out) return KATS_ERR_ARGUMENT;
+    if (out_floats < hilbert_hk_table_floats(n_cols)) return KATS_ERR_ARGUMENT;
+    std::vector<float> t;
+    hilbert_hk_table(n_cols, taps, t);
+    std::copy(t.begin(), t.end(), out);
+    return KATS_OK;
+}
+
 int katsevich_table_info(const katsevich_plan *p, int32_t *n_psi, int64_t *lo, int64_t *hi)
 {
     if (!p) return KATS_ERR_NULL;

@@ -19,8 +19,13 @@ timeout 120 python scripts/stage_times.py --config C4 > gpurun_out/stages_$R.log
 ncu --set full --clock-control none --import-source on -k regex:"k_hilbert_tc2" -s 5 -c 1 \
     -o gpurun_out/k3_full_$R -f python scripts/stage_times.py --config C4 --reps 1 > gpurun_out/ncu_k3_$R.log 2>&1
 timeout 120 python scripts/prof_step.py --config C3 > gpurun_out/prof_c3_$R.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_hilbert_hk" -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"k_hilbert_ws|k_hilbert_hk" -s 2 -c 1 \
     -o gpurun_out/k3hk_full_$R -f python scripts/prof_step.py --config C3 > gpurun_out/ncu_k3hk_$R.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_bp_tmem|k_bp_window" -s 1 -c 1 \
+    -o gpurun_out/k5c3_full_$R -f python scripts/prof_step.py --config C3 > gpurun_out/ncu_k5c3_$R.log 2>&1
+timeout 120 python scripts/prof_step.py --config C5 > gpurun_out/prof_c5_$R.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_bp_tmem|k_bp_window" -s 1 -c 1 \
+    -o gpurun_out/k5c5_full_$R -f python scripts/prof_step.py --config C5 > gpurun_out/ncu_k5c5_$R.log 2>&1
 timeout 120 python scripts/adj_prof.py C4 > gpurun_out/adjp_$R.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_bp_adjoint" -s 2 -c 1 \
     -o gpurun_out/k5T_full_$R -f python scripts/adj_prof.py C4 > gpurun_out/ncu_k5T_$R.log 2>&1

@@ -124,3 +124,30 @@ def test_workspace_and_scan_views():
     b1, b3 = p.workspace_bytes(1), p.workspace_bytes(3)
     assert 0 < b1 < b3
     assert p.workspace_bytes(3, host=True) > b3
+
+
+@pytest.mark.parametrize("nc", [96, 184, 368, 627, 736])
+def test_hilbert_hankel_core_table(nc):
+    """The tensor-core Hilbert's B operand (Hankel tap cores), read the way the
+    UMMA descriptor walks it (core s = 2 (n >> 3) + (k' >> 2), row n & 7, column k' & 3), is the
+    per-parity Toeplitz tap matrix K[2 (n - k) + 2 p - 1] (Eq. 12 split by output parity) with the
+    K index reversed (k = NH - 1 - k'), split exactly into a TF32 hi part and an fp32 remainder."""
+    rng = np.random.default_rng(nc)
+    taps = rng.standard_normal(2 * nc - 1).astype(np.float32)
+    NH = 32 * math.ceil(math.ceil(nc / 2) / 32)
+    NS = NH // 2
+    out = np.full(64 * NH, np.nan, np.float32)
+    assert _lib.lib().katsevich_hilbert_hk_table(nc, taps.ctypes.data, out.ctypes.data, out.size - 1) != 0
+    assert _lib.lib().katsevich_hilbert_hk_table(nc, taps.ctypes.data, out.ctypes.data, out.size) == 0
+    t = out.reshape(2, 2, NS, 8, 4)
+    n = np.arange(NH)[:, None]
+    kp = np.arange(NH)[None, :]
+    s = 2 * (n >> 3) + (kp >> 2)
+    k = NH - 1 - kp
+    for par in (0, 1):
+        hi = t[par, 0][s, n & 7, kp & 3]
+        lo = t[par, 1][s, n & 7, kp & 3]
+        d = 2 * (n - k) + 2 * par - 1
+        ref = np.where(np.abs(d) <= nc - 1, taps[np.clip(d + nc - 1, 0, 2 * nc - 2)], np.float32(0))
+        assert np.array_equal(hi + lo, ref)
+        assert not np.any(hi.view(np.uint32) & 0x1FFF)          # exactly representable in TF32
