@@ -1421,9 +1421,11 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     const int block = TX * TY;
     const char *kv = std::getenv("KATS_BP_KERNEL");
     const bool want_window = kv && std::string(kv) == "window";
+    const bool want_tmem = kv && std::string(kv) == "tmem";      // A/B: the TMEM kernel for narrow windows too
     // TMEM-window kernel for wide windows (accumulators in tensor memory, 3 CTAs per SM); for
     // windows of <= 32 slices the register window is lighter and faster (C2, C5 measured)
-    if (!want_window && p.max_active > 32 && p.staged && !p.checked && p.windows_monotone && p.warp_span > 0 &&
+    if (!want_window && (p.max_active > 32 || want_tmem) && p.staged && !p.checked && p.windows_monotone &&
+        p.warp_span > 0 &&
         2 * p.nq_s <= 256 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
         // TMEM columns, allocation and ring depth for one view (vp 1) or two views (vp 2) per pass
