@@ -1034,7 +1034,7 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];   // one symbol per TU: keep the TMA kernels' alignment
     const int BW = p.fp_cols_column, NQ = p.nr + 2, nzp = p.nz | 1;
-    const int NQP = (NQ + 31) & ~31, nbox = BW * NQP;                 // column stride = 0 mod 32 banks
+    const int NQP = p.adj_nqp, nbox = BW * NQP;                      // box column stride (launcher: 0 mod 32 or odd)
     const int cpy = 4 * nbox + 16;                                     // second copy: 16 banks further
     int *pl = reinterpret_cast<int *>(smem);                           // [2 copies][4][BW][NQP] fixed-point components
     float *ys = reinterpret_cast<float *>(pl + 2 * cpy);               // [TX*TY][nzp] scale * y
@@ -1294,7 +1294,14 @@ __global__ void k_bp_adjoint_ends(BPParams p)
 int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
 {
     if (!p.windows_monotone) return -1;
-    const size_t sm = sizeof(int) * 2 * (4 * (size_t)p.fp_cols_column * ((p.nr + 2 + 31) & ~31) + 16) +
+    // box column stride: 0 mod 32 banks when a warp's lanes share detector columns (rows, spread by
+    // the rotated start, pick the bank: C3, C4); odd when they spread over many columns (C5: ~1.7
+    // columns per voxel, 56-column boxes; 0 mod 32 made every lane of a row hit one bank)
+    BPParams q = p;
+    q.adj_nqp = p.fp_cols_column >= 48 ? ((p.nr + 2) | 1) : ((p.nr + 2 + 31) & ~31);
+    if (const char *e = std::getenv("KATS_ADJ_PITCH"))
+        q.adj_nqp = std::string(e) == "odd" ? ((p.nr + 2) | 1) : ((p.nr + 2 + 31) & ~31);
+    const size_t sm = sizeof(int) * 2 * (4 * (size_t)p.fp_cols_column * q.adj_nqp + 16) +
                       sizeof(float) * (size_t)TX * TY * (p.nz | 1) + sizeof(int) * (size_t)p.max_cta_views;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
     if (!p.checked && p.staged && sm <= 200 * 1024) {        // KATS_BP_KERNEL=l1: the checked kernel (A/B)
@@ -1304,8 +1311,8 @@ int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
             cudaFuncSetAttribute(k_bp_adjoint<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             attr = true;
         }
-        if (p.poly) k_bp_adjoint<true><<<grid, TX * TY, sm, s>>>(p);
-        else k_bp_adjoint<false><<<grid, TX * TY, sm, s>>>(p);
+        if (p.poly) k_bp_adjoint<true><<<grid, TX * TY, sm, s>>>(q);
+        else k_bp_adjoint<false><<<grid, TX * TY, sm, s>>>(q);
     } else {
         if (p.poly) k_bp_adjoint_checked<true><<<grid, TX * TY, 0, s>>>(p);
         else k_bp_adjoint_checked<false><<<grid, TX * TY, 0, s>>>(p);
