@@ -359,6 +359,32 @@ __device__ __forceinline__ int plan_col(const BPParams &p, int k, float xa, floa
     return max(0, min(c0, p.nc - p.fp_cols_column));
 }
 
+// End views of the staged kernels' slices, ahead of them: vol = the two fractional end-view taps
+// (reading A9, full range tests) of every voxel, unscaled; the staged kernels finish a slice with
+// vol = (interior sum + vol) * scale, so their warp-uniform flush has no dependent gathers.
+template <bool POLY>
+__global__ void __launch_bounds__(128) k_bp_ends(BPParams p)
+{
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x, iy = blockIdx.y;
+    const int t = blockIdx.z % p.nz, item = blockIdx.z / p.nz;
+    if (ix >= p.nx) return;
+    const size_t plane = (size_t)p.nx * p.ny, col = (size_t)iy * p.nx + ix;
+    const int2 e = p.pi_k[(size_t)t * plane + col];
+    float v = 0.f;
+    if (e.x <= e.y) {
+        const float2 w = p.pi_w[(size_t)t * plane + col];
+        const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
+        const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+        u64 ends = 0ull;
+        tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t, w.x, ends);
+        tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t, w.y, ends);
+        float ea, eb;
+        upk(ends, ea, eb);
+        v = ea + eb;
+    }
+    p.vol[(size_t)item * p.nz * plane + (size_t)t * plane + col] = v;
+}
+
 // Tensor maps of the staged kernels: box widths p.box_w[0] (= the largest box) >= [1] >= [2] columns.
 struct QMaps { CUtensorMap m[3]; };
 bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width);
@@ -508,17 +534,11 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
     int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
 
     // slice t_lo's window is closed: add its two end views, write it, shift the register window
-    auto flush = [&]() {
-        const int2 e = pik[(size_t)t_lo * plane];
-        const float2 w = piw[(size_t)t_lo * plane];
+    auto flush = [&]() {                                          // (end views: k_bp_ends wrote them to out)
 #pragma unroll
         for (int b = 0; b < NI; ++b) {
-            u64 ends = 0ull;
-            tap_checked<POLY>(p, qbase + b * qitem, e.x, x, y, 0.f, t_lo, w.x, ends);
-            tap_checked<POLY>(p, qbase + b * qitem, e.y, x, y, 0.f, t_lo, w.y, ends);
-            float ea, eb;
-            upk(ends, ea, eb);
-            out[(size_t)b * p.nz * plane + (size_t)t_lo * plane] = (acc[b][0] + ea + eb) * p.scale;
+            float *o = out + (size_t)b * p.nz * plane + (size_t)t_lo * plane;
+            *o = (acc[b][0] + *o) * p.scale;
 #pragma unroll
             for (int i = 0; i < W - 1; ++i) acc[b][i] = acc[b][i + 1];
             acc[b][W - 1] = 0.f;
@@ -776,18 +796,28 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
 
     // warp-uniform: slice t is closed in every lane -> finish and write it, zero its column
+    // end views: either written ahead by k_bp_ends (p.ends_pre; the next slice's value is loaded one
+    // flush ahead) or sampled here (the kernel is LSU-bound and other warps hide the gathers: C4)
+    float end_next = active_col && p.ends_pre ? out[0] : 0.f;
     auto flush_slice = [&](int t) {
         const unsigned tc = tw + ((unsigned)t & (unsigned)(Wc - 1));
         const float a = tm_ld1(tc);
         if (active_col && t < p.nz) {
-            const int2 e = pik[(size_t)t * plane];
-            const float2 w = piw[(size_t)t * plane];
-            u64 ends = 0ull;
-            tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t, w.x, ends);
-            tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t, w.y, ends);
-            float ea, eb;
-            upk(ends, ea, eb);
-            out[(size_t)t * plane] = (a + ea + eb) * p.scale;
+            float ev;
+            if (p.ends_pre) {
+                ev = end_next;
+                if (t + 1 < p.nz) end_next = out[(size_t)(t + 1) * plane];
+            } else {
+                const int2 e = pik[(size_t)t * plane];
+                const float2 w = piw[(size_t)t * plane];
+                u64 ends = 0ull;
+                tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t, w.x, ends);
+                tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t, w.y, ends);
+                float ea, eb;
+                upk(ends, ea, eb);
+                ev = ea + eb;
+            }
+            out[(size_t)t * plane] = (a + ev) * p.scale;
         }
         tm_st1(tc, 0.f);
     };
@@ -1336,6 +1366,13 @@ size_t backproject_smem_bytes(const BPParams &p)
            16 * (size_t)p.tail_quads;
 }
 
+void launch_bp_ends(const BPParams &p, cudaStream_t s)
+{
+    dim3 g((p.nx + 127) / 128, p.ny, p.nz * p.n_items);
+    if (p.poly) k_bp_ends<true><<<g, 128, 0, s>>>(p);
+    else k_bp_ends<false><<<g, 128, 0, s>>>(p);
+}
+
 template <bool POLY, int VP>
 void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
@@ -1464,6 +1501,11 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
         QMaps qmap;
         if (alloc <= 128 && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
             dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
+            // end views ahead (k_bp_ends) except for the LSU-bound view-pair kernel, where the inline
+            // gathers are hidden by other warps (C4: 48.5 inline vs 48.9 ms; C3 7.69 -> 7.49 ms ahead)
+            q.ends_pre = vp == 2 ? 0 : 1;
+            if (const char *e = std::getenv("KATS_BP_ENDS")) q.ends_pre = std::string(e) == "pre";
+            if (q.ends_pre) launch_bp_ends(q, s);
             if (vp == 2) {
                 if (p.poly) launch_tmem_kernel<true, 2>(q, gw, sm, qmap, s);
                 else launch_tmem_kernel<false, 2>(q, gw, sm, qmap, s);
@@ -1493,6 +1535,10 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
         p.tail_quads <= 4096 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_maps(q, &qmap)) {
         dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
+        // the window kernel always finishes slices from end views written ahead (C5 2.55 -> 2.35 ms,
+        // C2 1.43 -> 1.38 ms)
+        q.ends_pre = 1;
+        launch_bp_ends(q, s);
         switch (W) {
         case 8: launch_window<8>(q, gw, sm, qmap, s); break;
         case 16: launch_window<16>(q, gw, sm, qmap, s); break;

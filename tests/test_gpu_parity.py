@@ -206,3 +206,24 @@ def test_pipelined_reconstruct_matches_oracle(name, monkeypatch):
         vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"], stream=s)
         host = vol.cpu()          # ordered after the join on the caller's stream
     _check(host.numpy(), ref, contrast)
+
+
+@pytest.mark.parametrize("kernel,ends", [(None, "pre"), (None, "inline"), ("window", None)])
+def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
+    """The staged step-7 kernels finish a slice with its two fractional end views either
+    written ahead by k_bp_ends (window kernel always; TMEM kernel with KATS_BP_ENDS=pre) or
+    sampled in the flush (TMEM kernel, inline): against the oracle on C1."""
+    import torch
+    if ends is None:
+        monkeypatch.delenv("KATS_BP_ENDS", raising=False)
+    else:
+        monkeypatch.setenv("KATS_BP_ENDS", ends)
+    if kernel is None:
+        monkeypatch.delenv("KATS_BP_KERNEL", raising=False)
+    else:
+        monkeypatch.setenv("KATS_BP_KERNEL", kernel)
+    cfg, sino, ref, contrast = _case("C1")
+    p = _plan(cfg)
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    _check(vol.cpu().numpy(), ref, contrast)
