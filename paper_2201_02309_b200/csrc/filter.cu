@@ -925,13 +925,18 @@ __global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
 {
-    if (p.nc >= 256) {       // wide detectors (C2, C3, C5 measured); C4's 184 columns: per-sample kernel
-        const int nseg = (p.npsi + 31) / 32, seg = (p.npsi + nseg - 1) / nseg;   // <= 32 κ-lines per thread
-        k_deriv_fwd_rebin_col<<<dim3((p.nc + 127) / 128, p.n_views, nseg), 128, 0, s>>>(p, seg);
+    // column walk, 8 κ-lines per thread (two-row g2 cache; measured best on every config: C4 1.69 ->
+    // 1.42 ms vs the per-sample kernel, C3 0.67 -> 0.65, C5 0.72 -> 0.71 vs 32-line segments);
+    // KATS_K12=sample: one thread per sample (8 κ-lines unrolled); colN: N κ-lines per thread
+    const char *ke = std::getenv("KATS_K12");
+    const std::string k12 = ke ? ke : "";
+    if (k12 == "sample") {
+        const int bx = std::min(256, (p.nc + 31) / 32 * 32);
+        k_deriv_fwd_rebin<<<dim3((p.nc + bx - 1) / bx, (p.npsi + kPsiPer - 1) / kPsiPer, p.n_views), bx, 0, s>>>(p);
         return;
     }
-    const int bx = std::min(256, (p.nc + 31) / 32 * 32);
-    k_deriv_fwd_rebin<<<dim3((p.nc + bx - 1) / bx, (p.npsi + kPsiPer - 1) / kPsiPer, p.n_views), bx, 0, s>>>(p);
+    const int seg = k12.rfind("col", 0) == 0 && std::atoi(k12.c_str() + 3) > 0 ? std::atoi(k12.c_str() + 3) : 8;
+    k_deriv_fwd_rebin_col<<<dim3((p.nc + 127) / 128, p.n_views, (p.npsi + seg - 1) / seg), 128, 0, s>>>(p, seg);
 }
 
 size_t hilbert_tc_table_floats(int nc) { return 2 * 2 * (size_t)hilbert_tc_nh(nc) * hilbert_tc_nh(nc); }

@@ -227,3 +227,24 @@ def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
     vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
     torch.cuda.synchronize()
     _check(vol.cpu().numpy(), ref, contrast)
+
+
+@pytest.mark.parametrize("k12", ["sample", "col3"])
+@pytest.mark.parametrize("name", ["T1", "C1"])
+def test_k12_variants_match_oracle(name, k12, monkeypatch):
+    """Steps 1-3 (g3) by the alternate K12 kernels: one thread per sample, and the column walk
+    with a ragged κ-line segment (3 lines per thread; the default walks 8)."""
+    import torch
+    from oracle import oracle
+    monkeypatch.setenv("KATS_K12", k12)
+    monkeypatch.delenv("KATS_HILBERT", raising=False)
+    cfg, sino, _, _ = _case(name)
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    out = p.filter(torch.from_numpy(sino).cuda(), cfg["scan_v0"], v0 + 1, nv - 2, stages=("g3", "gF"))
+    torch.cuda.synchronize()
+    ref = oracle.filter_views(cfg, sino, cfg["scan_v0"], v0 + 1, nv - 2, stages=("g3", "gF"))
+    for s in ("g3", "gF"):
+        got = out[s].cpu().numpy().astype(np.float64)
+        e = np.linalg.norm(got - ref[s]) / np.linalg.norm(ref[s])
+        assert e <= STAGE_REL, f"{s}: rel L2 {e:.3e}"
