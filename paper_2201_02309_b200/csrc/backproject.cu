@@ -1466,9 +1466,15 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     const char *kv = std::getenv("KATS_BP_KERNEL");
     const bool want_window = kv && std::string(kv) == "window";
     const bool want_tmem = kv && std::string(kv) == "tmem";      // A/B: the TMEM kernel for narrow windows too
+    // small grids: the staged kernels run one CTA per 16x16 column tile (and item); under one CTA per
+    // SM the z-chunked L1 kernel's parallelism wins (C1, 16 tiles: K5 0.262 -> 0.074 ms)
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t staged_ctas = (int64_t)((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY) * p.n_items;
+    const bool small_grid = staged_ctas < nsm && !want_tmem && !want_window;
     // TMEM-window kernel for wide windows (accumulators in tensor memory, 3 CTAs per SM); for
     // windows of <= 32 slices the register window is lighter and faster (C2, C5 measured)
-    if (!want_window && (p.max_active > 32 || want_tmem) && p.staged && !p.checked && p.windows_monotone &&
+    if (!small_grid && !want_window && (p.max_active > 32 || want_tmem) && p.staged && !p.checked && p.windows_monotone &&
         p.warp_span > 0 &&
         2 * p.nq_s <= 256 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
@@ -1531,7 +1537,7 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     while (q.nbatch > 2 && backproject_smem_bytes(q) > budget) q.nbatch /= 2;
     const size_t sm = backproject_smem_bytes(q);
     QMaps qmap;
-    if (p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
+    if (!small_grid && p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
         p.tail_quads <= 4096 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_maps(q, &qmap)) {
         dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);

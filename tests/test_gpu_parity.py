@@ -168,14 +168,15 @@ def test_coverage_error_names_pitches():
     assert ei.value.code == -4 and "reconstructible" in str(ei.value)
 
 
-@pytest.mark.parametrize("variant,vp,kernel", [(None, None, "k_bp_tmem"), (None, "1", "k_bp_tmem"),
-                                               (None, "2", "k_bp_tmem"), ("window", None, "k_bp_window"),
-                                               ("window", "winv1", "k_bp_window"), ("l1", None, "k_backproject")])
+@pytest.mark.parametrize("variant,vp,kernel", [(None, None, "k_backproject"), ("tmem", None, "k_bp_tmem"),
+                                               ("tmem", "1", "k_bp_tmem"), ("tmem", "2", "k_bp_tmem"),
+                                               ("window", None, "k_bp_window"), ("window", "winv1", "k_bp_window"),
+                                               ("l1", None, "k_backproject")])
 def test_every_bp_kernel_variant_matches_oracle(variant, vp, kernel, monkeypatch):
-    """Each step-7 kernel (TMEM window = default for C1's 44-slice windows, with one
-    or two views per pass; register window; chunked L1 path) on C1
-    against the oracle, and the plan reports that the forced variant is the one
-    that ran (katsevich_bp_kernel)."""
+    """Each step-7 kernel on C1 against the oracle: the default (C1's 16 column tiles are under
+    one CTA per SM, so the z-chunked L1 kernel), the TMEM window (forced; one or two views per
+    pass), the register window and the L1 path; the plan reports that the
+    expected variant is the one that ran (katsevich_bp_kernel)."""
     import torch
     winv = "1" if vp == "winv1" else None
     vp = None if vp == "winv1" else vp
@@ -208,7 +209,7 @@ def test_pipelined_reconstruct_matches_oracle(name, monkeypatch):
     _check(host.numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("kernel,ends", [(None, "pre"), (None, "inline"), ("window", None)])
+@pytest.mark.parametrize("kernel,ends", [("tmem", "pre"), ("tmem", "inline"), ("window", None)])
 def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
     """The staged step-7 kernels finish a slice with its two fractional end views either
     written ahead by k_bp_ends (window kernel always; TMEM kernel with KATS_BP_ENDS=pre) or
