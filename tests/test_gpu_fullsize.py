@@ -134,3 +134,51 @@ def test_c3_one_slice_sampled():
     ref = _oracle_voxels(cfg, sino, v0, 0, idx)
     g = vol.cpu().numpy()
     _check(g[idx[:, 2], idx[:, 1], idx[:, 0]].astype(np.float64), ref, _truth_contrast(cfg, cfg["phantom"], [0]))
+
+
+def _dot_check(ax, y, x, aty):
+    lhs = float((ax.double() * y.double()).sum())
+    rhs = float((x.double() * aty.double()).sum())
+    # Cauchy-Schwarz scale: |<Ax,y>| <= |Ax||y|, the scale of the rounding of either side
+    scale = max(float(ax.double().norm() * y.double().norm()), float(x.double().norm() * aty.double().norm()))
+    assert abs(lhs - rhs) <= 1e-5 * scale, (lhs, rhs, scale)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_dot_product(name):
+    """<A x, y> = <x, A^T y> at the full BASELINE size, forward and adjoint in the launch
+    configuration bench.py times (C4: all 8 pitches in one call; C3: the paper's 64 x 736 detector)."""
+    import torch
+    import paper_2201_02309_b200 as k
+    from synth import configs
+    cfg = configs.get(name)
+    npit = cfg["n_pitches"]
+    p = k.Plan(cfg, device=0)
+    p.precompute()
+    s0, sn = p.scan_views(0, npit)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn((sn, cfg["n_rows"], cfg["n_cols"]), device="cuda", generator=g)
+    y = torch.randn((npit * cfg["nz"], cfg["ny"], cfg["nx"]), device="cuda", generator=g)
+    ax = p.reconstruct(x, s0, 0, npit)
+    aty = p.adjoint(y, s0, sn, 0, npit)
+    torch.cuda.synchronize()
+    _dot_check(ax, y, x, aty)
+
+
+def test_full_size_batch_dot_product():
+    """The same identity for the C5 16-slab batch (reconstruct_batch / adjoint_batch)."""
+    import torch
+    import paper_2201_02309_b200 as k
+    from synth import configs
+    cfg = configs.get("C5")
+    p = k.Plan(cfg, device=0)
+    p.precompute()
+    v0, nv = p.pitch_views(0)
+    B = cfg["batch"]
+    g = torch.Generator(device="cuda").manual_seed(12)
+    x = torch.randn((B, nv, cfg["n_rows"], cfg["n_cols"]), device="cuda", generator=g)
+    y = torch.randn((B, cfg["nz"], cfg["ny"], cfg["nx"]), device="cuda", generator=g)
+    ax = p.reconstruct_batch(x)
+    aty = p.adjoint_batch(y)
+    torch.cuda.synchronize()
+    _dot_check(ax, y, x, aty)
