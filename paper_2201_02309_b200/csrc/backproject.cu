@@ -1438,6 +1438,22 @@ EncodeTiledFn encode_tiled()
 
 }  // namespace
 
+// 2-D fp32 tensor [dim1][dim0] (row stride stride1_bytes, a multiple of 16) with a box of box1 rows x
+// box0 columns, no swizzle, zero fill out of bounds (used by the filter's warp-specialized Hilbert)
+bool make_tensor_map_2d_f32(CUtensorMap *map, const float *base, uint64_t dim0, uint64_t dim1,
+                            uint64_t stride1_bytes, uint32_t box0, uint32_t box1)
+{
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)dim0, (cuuint64_t)dim1};
+    const cuuint64_t strides[1] = {(cuuint64_t)stride1_bytes};
+    const cuuint32_t box[2] = {box0, box1};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // the quad array as a 3-D tensor of 8-byte elements: (2 * (nr+2) per column, nc columns, n_views);
 // box = full column height x fp_cols_column columns x 1 view
 bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width)

@@ -9,9 +9,14 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "kernels.cuh"
 
 namespace kats {
+
+bool make_tensor_map_2d_f32(CUtensorMap *map, const float *base, uint64_t dim0, uint64_t dim1,
+                            uint64_t stride1_bytes, uint32_t box0, uint32_t box1);   // backproject.cu
 
 // ---------------------------------------------------------------------------
 // K12: g3[v][i][l] = lerp_w(g2[v][·][l], w_κ(α_l, ψ_i)),  g2 = D/sqrt(D²+w²)·g1,
@@ -534,7 +539,9 @@ __global__ void __launch_bounds__(HK_THREADS, 2) k_hilbert_hk(FilterParams p, in
 //   warps 9-12  epilogue: one TMEM lane quarter each, accumulator -> padded smem -> g4, then free
 //               the accumulator, while the tensor core already works on the next item.
 // ---------------------------------------------------------------------------
-constexpr int WS_PROD = 8, WS_EPI = 4, WS_THREADS = 32 * (WS_PROD + 1 + WS_EPI), WS_NST = 4;
+// warps 0-7 convert, 8 issues MMAs, 9-12 epilogue, 13 issues the A chunk TMAs
+constexpr int WS_PROD = 8, WS_EPI = 4, WS_THREADS = 32 * (WS_PROD + 1 + WS_EPI + 1), WS_NST = 2, WS_RAW = 4;
+constexpr unsigned WS_RAWB = TC_M * TC_KC * 4;                    // one raw A chunk: 128 lines x 32 inputs
 // A tiles of this kernel: K-major core matrices with LBO = 144 B (K quads 9 bank groups apart) and
 // SBO = 1152 B, so the 8 K quads of one line a quarter-warp stores hit 8 different 16-B bank groups
 constexpr unsigned WS_LBO = 144, WS_SBO = 1152, WS_ATILE = (TC_M / 8) * WS_SBO;
@@ -559,7 +566,9 @@ __device__ __forceinline__ void ws_arrive(unsigned bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-__global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, int64_t n_lines, int nsplit)
+// (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
+__global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(const __grid_constant__ CUtensorMap amap, FilterParams p,
+                                                              int64_t n_lines, int nsplit)
 {
     extern __shared__ __align__(1024) unsigned char tsm[];
     const int nc = p.nc, NH = hilbert_tc_nh(nc), NK = NH / TC_KC, NS = NH / 2;
@@ -570,14 +579,18 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
     unsigned char *Bh = tsm, *Bl = tsm + NS * 128;
     unsigned char *A0 = tsm + 2 * NS * 128;
     constexpr unsigned kStage = 2 * WS_ATILE;
-    float *stg_all = reinterpret_cast<float *>(A0 + WS_NST * kStage);   // epilogue: 4 warps x 32 x 17
+    unsigned char *R0 = A0 + WS_NST * kStage;                    // raw chunks (TMA): [WS_RAW][128][32] floats
+    float *stg_all = reinterpret_cast<float *>(R0 + WS_RAW * WS_RAWB);   // epilogue: 4 warps x 32 x 17
     __shared__ __align__(8) unsigned long long s_full[WS_NST], s_empty[WS_NST], s_afull[2], s_aempty[2];
+    __shared__ __align__(8) unsigned long long s_rfull[WS_RAW], s_rempty[WS_RAW];
     __shared__ unsigned s_tmem;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
     const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
     const unsigned afull0 = (unsigned)__cvta_generic_to_shared(&s_afull[0]);
     const unsigned aempty0 = (unsigned)__cvta_generic_to_shared(&s_aempty[0]);
+    const unsigned rfull0 = (unsigned)__cvta_generic_to_shared(&s_rfull[0]);
+    const unsigned rempty0 = (unsigned)__cvta_generic_to_shared(&s_rempty[0]);
     if (warp == WS_PROD) {                                       // two accumulators of 256 columns
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"(512u));
@@ -591,6 +604,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
         for (int i = 0; i < 2; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(afull0 + 8u * i));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(aempty0 + 8u * i), "r"(WS_EPI));
+        }
+        for (int i = 0; i < WS_RAW; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rfull0 + 8u * i));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(rempty0 + 8u * i), "r"(WS_PROD));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -606,49 +623,33 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
     const unsigned tmem = s_tmem;
 
     if (warp < WS_PROD) {
-        // ---- producers (parity-split input lines): thread -> K quad kq of the chunk, rows rs + 32 j; a quad
-        //      is one aligned float4 of the parity's inputs k = 4m .. 4m+3 (m = NH/4 - 1 - 8 kc - kq), stored
-        //      reversed (K is reversed); a load instruction covers 4 lines x 128 contiguous bytes ----
-        const int kq = tid & 7, rs = tid >> 3;
-        const int hp = p.hp;
+        // ---- converters: raw chunk (TMA, inputs k = NH - 32 - 32 kc + j ascending in j) -> reversed,
+        //      hi/lo-split canonical A tile; thread -> K quad q of the raw row, rows rs + 32 j ----
+        const int q = tid & 7, rs = tid >> 3;
         int g = 0;
         for (int64_t item = cta; item < n_items; item += ncta) {
-            const int64_t line0 = item / nsplit * TC_M + rs;
-            auto load = [&](int kc, float (&v)[16]) {
-                const int k0 = 4 * (NH / 4 - 1 - 8 * kc - kq);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int64_t line = line0 + 32 * j;
-                    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (line < n_lines && k0 < nin)
-                        q = __ldg(reinterpret_cast<const float4 *>(p.g3 + line * (2 * hp) + (1 - par) * hp + k0));
-                    v[4 * j + 0] = k0 + 3 < nin ? q.w : 0.f;               // k' order: k0+3, .., k0
-                    v[4 * j + 1] = k0 + 2 < nin ? q.z : 0.f;
-                    v[4 * j + 2] = k0 + 1 < nin ? q.y : 0.f;
-                    v[4 * j + 3] = q.x;
-                }
-            };
-            float cur[16];
-            load(0, cur);
             for (int kc = 0; kc < NK; ++kc, ++g) {
-                const int st = g % WS_NST;
-                float nxt[16];
-                if (kc + 1 < NK) load(kc + 1, nxt);
+                const int rst = g % WS_RAW, st = g % WS_NST;
+                ws_wait(rfull0 + 8u * rst, (unsigned)(g / WS_RAW) & 1u);
                 if (g >= WS_NST) ws_wait(empty0 + 8u * st, (unsigned)((g / WS_NST) - 1) & 1u);
+                const float *raw = reinterpret_cast<const float *>(R0 + rst * WS_RAWB);
                 unsigned char *Ah = A0 + st * kStage, *Al = Ah + WS_ATILE;
+                const int k0 = NH - 32 - 32 * kc + 4 * q;            // inputs k0 .. k0 + 3 of this quad
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const float *v = cur + 4 * j;
-                    const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
-                    const unsigned o = ws_off(rs + 32 * j, 4 * kq);
+                    const int row = rs + 32 * j;
+                    const float4 r4 = *reinterpret_cast<const float4 *>(raw + row * 32 + 4 * q);
+                    // k' order (K reversed): k0 + 3, k0 + 2, k0 + 1, k0; inputs k >= nin are not this parity's
+                    const float v0 = k0 + 3 < nin ? r4.w : 0.f, v1 = k0 + 2 < nin ? r4.z : 0.f;
+                    const float v2 = k0 + 1 < nin ? r4.y : 0.f, v3 = k0 < nin ? r4.x : 0.f;
+                    const float4 h = make_float4(tf32_hi(v0), tf32_hi(v1), tf32_hi(v2), tf32_hi(v3));
+                    const unsigned o = ws_off(row, 4 * (7 - q));
                     *reinterpret_cast<float4 *>(Ah + o) = h;
-                    *reinterpret_cast<float4 *>(Al + o) = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
+                    *reinterpret_cast<float4 *>(Al + o) = make_float4(v0 - h.x, v1 - h.y, v2 - h.z, v3 - h.w);
                 }
-#pragma unroll
-                for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
                 __syncwarp();
-                if (lane == 0) ws_arrive(full0 + 8u * st);
+                if (lane == 0) { ws_arrive(rempty0 + 8u * rst); ws_arrive(full0 + 8u * st); }
             }
         }
     } else if (warp == WS_PROD) {
@@ -689,6 +690,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(FilterParams p, in
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                              ::"r"(afull0 + 8u * acc) : "memory");
+            }
+        }
+        __syncwarp();
+    } else if (warp == WS_PROD + 1 + WS_EPI) {
+        // ---- A chunk TMA issuer: box of 32 inputs x 128 lines of the parity's half-lines ----
+        if (lane == 0) {
+            const int colbase = (1 - par) * p.hp + NH - 32;
+            int g = 0;
+            for (int64_t item = cta; item < n_items; item += ncta) {
+                const int line0 = (int)(item / nsplit * TC_M);
+                for (int kc = 0; kc < NK; ++kc, ++g) {
+                    const int rst = g % WS_RAW;
+                    if (g >= WS_RAW) ws_wait(rempty0 + 8u * rst, (unsigned)((g / WS_RAW) - 1) & 1u);
+                    const unsigned full = rfull0 + 8u * rst;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"(WS_RAWB) : "memory");
+                    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                                 ::"r"((unsigned)__cvta_generic_to_shared(R0 + rst * WS_RAWB)),
+                                   "l"(reinterpret_cast<uint64_t>(&amap)), "r"(colbase - 32 * kc), "r"(line0), "r"(full)
+                                 : "memory");
+                }
             }
         }
         __syncwarp();
@@ -1050,7 +1071,10 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
         const bool ws = p.k3_in_split != 0;
         if (ws) {
             const int ns = NH > 256 ? 2 : 1;                          // accumulators of <= 256 columns, two of them
-            const size_t wsm = taps + (size_t)WS_NST * 2 * WS_ATILE + (size_t)WS_EPI * 32 * 17 * 4;
+            const size_t wsm = taps + (size_t)WS_NST * 2 * WS_ATILE + (size_t)WS_RAW * WS_RAWB + (size_t)WS_EPI * 32 * 17 * 4;
+            CUtensorMap amap;                                         // the K3 input: [n_lines][2 hp] fp32
+            if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M))
+                return;
             static bool wattr = false;
             if (!wattr) {
                 cudaFuncSetAttribute(k_hilbert_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
@@ -1060,7 +1084,7 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
             cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, 0);
             const int64_t items = (n_lines + TC_M - 1) / TC_M * ns;
             const int per = (int)std::min<int64_t>(items, std::max(1, nsm2 / 2));   // one CTA per SM, half per parity
-            k_hilbert_ws<<<(unsigned)(2 * per), WS_THREADS, wsm, s>>>(p, n_lines, ns);
+            k_hilbert_ws<<<(unsigned)(2 * per), WS_THREADS, wsm, s>>>(amap, p, n_lines, ns);
             return;
         }
         const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
