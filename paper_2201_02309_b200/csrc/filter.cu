@@ -1070,7 +1070,11 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
         // at NH <= 256 the two-CTA persistent kernel is faster (C2 0.18 vs 0.21 ms)
         const bool ws = p.k3_in_split != 0;
         if (ws) {
-            const int ns = NH > 256 ? 2 : 1;                          // accumulators of <= 256 columns, two of them
+            int ns = NH > 256 ? 2 : 1;                                // accumulators of <= 256 columns, two of them
+            if (const char *e = std::getenv("KATS_HILBERT_WSSPLIT")) {   // A/B: output parts per item
+                const int v = std::atoi(e);
+                if (v >= 1 && NH % (16 * v) == 0 && NH / v <= 256) ns = v;
+            }
             const size_t wsm = taps + (size_t)WS_NST * 2 * WS_ATILE + (size_t)WS_RAW * WS_RAWB + (size_t)WS_EPI * 32 * 17 * 4;
             CUtensorMap amap;                                         // the K3 input: [n_lines][2 hp] fp32
             if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M))
