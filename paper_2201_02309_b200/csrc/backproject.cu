@@ -1070,8 +1070,8 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
     float *ys = reinterpret_cast<float *>(pl + 2 * cpy);               // [TX*TY][nzp] scale * y
     int *boxc = reinterpret_cast<int *>(ys + TX * TY * nzp);
     __shared__ int s_k0, s_k1;
-    __shared__ unsigned s_b[2];                                        // view bounds (float bits, >= 0)
-    __shared__ int s_rect[4];                                          // box columns / quad rows touched in the view
+    __shared__ unsigned s_ymax;                                        // CTA max |scale * y| (float bits, >= 0)
+    __shared__ int s_rect[2][4];                                       // box columns / quad rows touched (view parity)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
     const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
@@ -1081,8 +1081,8 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
     const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
     const int2 *pik = p.pi_k + col;
     if (tid == 0) {
-        s_k0 = INT_MAX; s_k1 = INT_MIN; s_b[0] = 0u; s_b[1] = 0u;
-        s_rect[0] = INT_MAX; s_rect[1] = -1; s_rect[2] = INT_MAX; s_rect[3] = -1;
+        s_k0 = INT_MAX; s_k1 = INT_MIN; s_ymax = 0u;
+        for (int i = 0; i < 2; ++i) { s_rect[i][0] = INT_MAX; s_rect[i][1] = -1; s_rect[i][2] = INT_MAX; s_rect[i][3] = -1; }
     }
     for (int i = tid; i < 2 * cpy; i += TX * TY) pl[i] = 0;
     float ycmax = 0.f;                                                 // this column's max |scale * y|
@@ -1107,9 +1107,24 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
         wk0 = min(wk0, __shfl_xor_sync(0xffffffffu, wk0, o));
         wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
     }
-    if (lane == 0) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+    const unsigned wy = __reduce_max_sync(0xffffffffu, __float_as_uint(ycmax));
+    if (lane == 0) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); atomicMax(&s_ymax, wy); }
     const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
     __syncthreads();
+    // fixed-point scales for every view of the CTA: a contribution is at most max|scale*y| / v*
+    // (w0 + w1 = 1/v*, v* >= R - the tile's farthest corner radius) for (w0, w1), times
+    // |P| <= (n_rows - 1)/2 + 1 (interior samples lie in the detector rows) for (w0 P, w1 P)
+    float B01, B23;
+    {
+        const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
+        const float xb = xa + (TX - 1) * p.dx, yb = ya + (TY - 1) * p.dy;
+        const float rx = fmaxf(fabsf(xa), fabsf(xb)), ry = fmaxf(fabsf(ya), fabsf(yb));
+        const float vmin = p.R - sqrtf(rx * rx + ry * ry);
+        B01 = __uint_as_float(s_ymax) / fmaxf(vmin, 1e-3f * p.R) * 1.001f;
+        B23 = B01 * (0.5f * (float)p.nr + 1.5f);
+    }
+    const float S01 = B01 > 0.f ? 2097152.f / B01 : 0.f, S23 = B23 > 0.f ? 2097152.f / B23 : 0.f;
+    const float i01 = B01 * (1.f / 2097152.f), i23 = B23 * (1.f / 2097152.f);
     const int KC0 = s_k0, NV = s_k1 - s_k0 + 1;
     {
         const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
@@ -1135,7 +1150,7 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             }
         }
         const bool work = active_col && t_hi >= t_lo && k <= K1;
-        float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f, b01 = 0.f, b23 = 0.f;
+        float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f;
         int ci = 0, rlo = 0, rhi = -1;
         if (work) {
             const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
@@ -1161,27 +1176,19 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             step = sc * p.dz;
             base = fmaf(sc, -vg.z, p.row_cc);
             ci = min(max(l - boxc[n], 0), BW - 1);
-            b01 = ycmax * inv_v * 1.0001f;
             const float plo = fmaf((float)t_lo, step, base), phi = fmaf((float)t_hi, step, base);
-            b23 = b01 * fmaxf(fabsf(plo), fabsf(phi)) * 1.0001f;
             rlo = (int)(__float_as_uint(plo + p.qmagic) - kMagicBits);    // rows grow with t
             rhi = (int)(__float_as_uint(phi + p.qmagic) - kMagicBits);
         }
-        const unsigned r01 = __reduce_max_sync(0xffffffffu, __float_as_uint(b01));
-        const unsigned r23 = __reduce_max_sync(0xffffffffu, __float_as_uint(b23));
         const int c_lo = __reduce_min_sync(0xffffffffu, work ? ci : INT_MAX);
         const int c_hi = __reduce_max_sync(0xffffffffu, work ? ci : -1);
         const int q_lo = __reduce_min_sync(0xffffffffu, work ? rlo : INT_MAX);
         const int q_hi = __reduce_max_sync(0xffffffffu, work ? rhi : -1);
+        int *rect = s_rect[n & 1];
         if (lane == 0) {
-            atomicMax(&s_b[0], r01); atomicMax(&s_b[1], r23);
-            atomicMin(&s_rect[0], c_lo); atomicMax(&s_rect[1], c_hi);
-            atomicMin(&s_rect[2], q_lo); atomicMax(&s_rect[3], q_hi);
+            atomicMin(&rect[0], c_lo); atomicMax(&rect[1], c_hi);
+            atomicMin(&rect[2], q_lo); atomicMax(&rect[3], q_hi);
         }
-        __syncthreads();
-        const float B01 = __uint_as_float(s_b[0]), B23 = __uint_as_float(s_b[1]);
-        const int rc0 = s_rect[0], rc1 = s_rect[1], rq0 = max(s_rect[2], 0), rq1 = min(s_rect[3], NQ - 1);
-        const float S01 = B01 > 0.f ? 2097152.f / B01 : 0.f, S23 = B23 > 0.f ? 2097152.f / B23 : 0.f;
         if (work) {
             int *c0 = pl + (lane & 1) * cpy + ci * NQP;                  // odd lanes: the shifted copy
             const float e0 = w0 * S01, e1 = w1 * S01, f0 = w0 * S23, f1 = w1 * S23;
@@ -1199,12 +1206,12 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
                 t = t == t_hi ? t_lo : t + 1;
             }
         }
-        __syncthreads();
-        if (tid == 0) {                                                // bounds of the next view
-            s_b[0] = 0u; s_b[1] = 0u;
-            s_rect[0] = INT_MAX; s_rect[1] = -1; s_rect[2] = INT_MAX; s_rect[3] = -1;
+        __syncthreads();                                               // the view's scatter and bounds are done
+        const int rc0 = rect[0], rc1 = rect[1], rq0 = max(rect[2], 0), rq1 = min(rect[3], NQ - 1);
+        if (tid == 0) {                                                // the next view's bounds (its readers,
+            int *nr = s_rect[(n + 1) & 1];                             // view n - 1, passed the last barrier)
+            nr[0] = INT_MAX; nr[1] = -1; nr[2] = INT_MAX; nr[3] = -1;
         }
-        const float i01 = B01 * (1.f / 2097152.f), i23 = B23 * (1.f / 2097152.f);
         float4 *dst = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)boxc[n] * NQ;
         // only the rectangle of box columns x quad rows the view touched
         const int nqr = rq1 - rq0 + 1, ntouch = rc1 >= rc0 && nqr > 0 ? (rc1 - rc0 + 1) * nqr : 0;
