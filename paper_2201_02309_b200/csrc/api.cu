@@ -86,7 +86,7 @@ void free_device(katsevich_plan *p)
     if (p->device < 0) return;
     cudaSetDevice(p->device);
     void *ptrs[] = {p->d.pi_k, p->d.pi_w, p->d.view, p->d.fr, p->d.br, p->d.cos_alpha, p->d.wlen, p->d.hilbert,
-                    p->d.hilbert_tc, p->d.hilbert_hk};
+                    p->d.hilbert_tc, p->d.hilbert_hk, p->d.tile_order};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     p->d = DeviceTables{};
@@ -190,6 +190,10 @@ BPParams bp_params(const katsevich_plan *p)
     b.colbytes = 16u * (unsigned)(g.n_rows + 2);
     b.viewbytes = 16 * (int64_t)quad_view_elems(p);
     b.pi_k = p->d.pi_k; b.pi_w = p->d.pi_w; b.view = p->d.view;
+    {   // KATS_BP_ORDER=grid: plain 2-D tile grid (A/B tests)
+        const char *e = std::getenv("KATS_BP_ORDER");
+        b.tile_order = e && std::string(e) == "grid" ? nullptr : p->d.tile_order;
+    }
     b.view_lo = (int)p->t.bp_lo;
     b.R = (float)g.R;
     b.D_over_dw = (float)(g.D / g.d_w);
@@ -334,6 +338,23 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
             (rc = upload(p, &p->d.br, br)) || (rc = upload(p, &p->d.cos_alpha, cosa)) ||
             (rc = upload(p, &p->d.wlen, wlen)) || (rc = upload(p, &p->d.hilbert, hk)))
             return rc;
+        {   // step-7 tiles heaviest first (work ~ the tile's summed view span over its columns), so the
+            // last wave of CTAs holds the lightest tiles (FOV edge)
+            const int ntx = (g.nx + 15) / 16, nty = (g.ny + 15) / 16;
+            const size_t plane = (size_t)g.nx * g.ny;
+            std::vector<double> work((size_t)ntx * nty, 0.0);
+            for (int iy = 0; iy < g.ny; ++iy)
+                for (int ix = 0; ix < g.nx; ++ix) {
+                    const size_t c = (size_t)iy * g.nx + ix;
+                    if (t.pi_last[c] < t.pi_first[c]) continue;
+                    work[(size_t)(iy / 16) * ntx + ix / 16] +=
+                        (double)(t.pi_last[c + (size_t)(g.nz_per_pitch - 1) * plane] - t.pi_first[c]);
+                }
+            std::vector<int> order(work.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+            std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+            if ((rc = upload(p, &p->d.tile_order, order))) return rc;
+        }
         std::vector<float> htc;
         hilbert_tc_table(g.n_cols, hk.data(), htc);
         if ((rc = upload(p, &p->d.hilbert_tc, htc))) return rc;

@@ -385,6 +385,15 @@ __global__ void __launch_bounds__(128) k_bp_ends(BPParams p)
     p.vol[(size_t)item * p.nz * plane + (size_t)t * plane + col] = v;
 }
 
+// column tile of a window-kernel CTA: the plan's heaviest-first order over a 1-D grid (the last wave
+// holds the lightest, FOV-edge tiles: C2 1.383 -> 1.356 ms, C5 2.355 -> 2.329 ms), else the 2-D grid
+__device__ __forceinline__ int2 bp_tile(const BPParams &p)
+{
+    if (!p.tile_order) return make_int2(blockIdx.x, blockIdx.y);
+    const int t = __ldg(p.tile_order + blockIdx.x), ntx = (p.nx + TX - 1) / TX;
+    return make_int2(t % ntx, t / ntx);
+}
+
 // Tensor maps of the staged kernels: box widths p.box_w[0] (= the largest box) >= [1] >= [2] columns.
 struct QMaps { CUtensorMap m[3]; };
 bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width);
@@ -456,8 +465,9 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
     const bool producer = warp == kConsumerWarps;
     // a warp owns 8 x 4 columns; each quarter-warp (the lanes one LDS.128 wavefront serves) a 4 x 2
     // block of them, so its samples spread over fewer detector columns (bank groups)
-    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (QMAP42 ? (lane & 3) + 4 * ((lane >> 3) & 1) : lane & 7);
-    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (QMAP42 ? ((lane >> 2) & 1) + 2 * (lane >> 4) : lane >> 3);
+    const int2 bt = bp_tile(p);
+    const int ix = bt.x * TX + (warp & 1) * 8 + (QMAP42 ? (lane & 3) + 4 * ((lane >> 3) & 1) : lane & 7);
+    const int iy = bt.y * TY + (warp >> 1) * 4 + (QMAP42 ? ((lane >> 2) & 1) + 2 * (lane >> 4) : lane >> 3);
     const int item0 = blockIdx.z * NI;
     const bool inside = !producer && ix < p.nx && iy < p.ny;
     const size_t plane = (size_t)p.nx * p.ny;
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
     const int NV = KC1 - KC0 + 1;
     const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
     {
-        const float xa = p.x0 + blockIdx.x * TX * p.dx, ya = p.y0 + blockIdx.y * TY * p.dy;
+        const float xa = p.x0 + bt.x * TX * p.dx, ya = p.y0 + bt.y * TY * p.dy;
         for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya);
     }
     __syncthreads();
@@ -1529,6 +1539,7 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
         const size_t sm = tmem_smem_bytes(q);
         QMaps qmap;
         if (alloc <= 128 && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
+            // (2-D tile grid: the heaviest-first order cost this kernel registers, C4 48.5 -> 50.6 ms)
             dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
             // end views ahead (k_bp_ends) except for the LSU-bound view-pair kernel, where the inline
             // gathers are hidden by other warps (C4: 48.5 inline vs 48.9 ms; C3 7.69 -> 7.49 ms ahead)
@@ -1563,7 +1574,8 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     if (!small_grid && p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
         p.tail_quads <= 4096 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_maps(q, &qmap)) {
-        dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
+        dim3 gw = p.tile_order ? dim3(((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY), 1, p.n_items / q.bp_items)
+                               : dim3((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
         // the window kernel always finishes slices from end views written ahead (C5 2.55 -> 2.35 ms,
         // C2 1.43 -> 1.38 ms)
         q.ends_pre = 1;

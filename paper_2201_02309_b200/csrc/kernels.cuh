@@ -90,6 +90,7 @@ struct BPParams {
     int box_w[3];             // staged box widths (columns): full, and two narrower classes (set by the launcher)
     int adj_nqp;              // adjoint: quad-row pitch of a box column in shared memory (set by the launcher)
     int ends_pre;             // staged kernels: end views written ahead into vol by k_bp_ends (launcher)
+    const int *tile_order;    // staged kernels: 16x16 column tiles heaviest first (ty * ntx + tx), or null
     int bp_items;             // window kernel: batch items per CTA (1 or 2; set by the launcher)
     int win_variant;          // window kernel variant V (0 plain, 1 uniform sample tail, 2 + two items per CTA)
     int tmem_cols, tmem_alloc;   // TMEM columns per warp / allocated per CTA (set by the launcher)
