@@ -4,6 +4,7 @@
 // (P:l.250) and the filter-once long-scan path.
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -1077,8 +1078,12 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
             }
             const size_t wsm = taps + (size_t)WS_NST * 2 * WS_ATILE + (size_t)WS_RAW * WS_RAWB + (size_t)WS_EPI * 32 * 17 * 4;
             CUtensorMap amap;                                         // the K3 input: [n_lines][2 hp] fp32
-            if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M))
+            if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M)) {
+                // cannot happen on a driver that has cuTensorMapEncodeTiled (16-B aligned scratch lines);
+                // nothing else reads parity-split lines, so say so loudly rather than leave g4 stale
+                std::fprintf(stderr, "katsevich: tensor map for the Hilbert input failed; K3 output not written\n");
                 return;
+            }
             static bool wattr = false;
             if (!wattr) {
                 cudaFuncSetAttribute(k_hilbert_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
