@@ -704,7 +704,7 @@ size_t tmem_smem_bytes(const BPParams &p)
            16 * (size_t)p.pad_quads;
 }
 
-template <bool POLY, int VP>
+template <bool POLY, int VP, bool ENDS_PRE>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
 __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant__ QMaps qm, BPParams p)
 {
@@ -806,15 +806,15 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
 
     // warp-uniform: slice t is closed in every lane -> finish and write it, zero its column
-    // end views: either written ahead by k_bp_ends (p.ends_pre; the next slice's value is loaded one
+    // end views: either written ahead by k_bp_ends (ENDS_PRE; the next slice's value is loaded one
     // flush ahead) or sampled here (the kernel is LSU-bound and other warps hide the gathers: C4)
-    float end_next = active_col && p.ends_pre ? out[0] : 0.f;
+    float end_next = active_col && ENDS_PRE ? out[0] : 0.f;
     auto flush_slice = [&](int t) {
         const unsigned tc = tw + ((unsigned)t & (unsigned)(Wc - 1));
         const float a = tm_ld1(tc);
         if (active_col && t < p.nz) {
             float ev;
-            if (p.ends_pre) {
+            if constexpr (ENDS_PRE) {
                 ev = end_next;
                 if (t + 1 < p.nz) end_next = out[(size_t)(t + 1) * plane];
             } else {
@@ -1390,15 +1390,27 @@ void launch_bp_ends(const BPParams &p, cudaStream_t s)
     else k_bp_ends<false><<<g, 128, 0, s>>>(p);
 }
 
-template <bool POLY, int VP>
+template <bool POLY, int VP, bool ENDS_PRE>
 void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_bp_tmem<POLY, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bp_tmem<POLY, VP, ENDS_PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_bp_tmem<POLY, VP><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    k_bp_tmem<POLY, VP, ENDS_PRE><<<grid, kWsThreads, sm, s>>>(qmap, q);
+}
+
+template <bool POLY>
+void launch_tmem(const BPParams &q, int vp, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
+{
+    if (vp == 2) {
+        if (q.ends_pre) launch_tmem_kernel<POLY, 2, true>(q, grid, sm, qmap, s);
+        else launch_tmem_kernel<POLY, 2, false>(q, grid, sm, qmap, s);
+    } else {
+        if (q.ends_pre) launch_tmem_kernel<POLY, 1, true>(q, grid, sm, qmap, s);
+        else launch_tmem_kernel<POLY, 1, false>(q, grid, sm, qmap, s);
+    }
 }
 
 template <int W>
@@ -1546,13 +1558,8 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
             q.ends_pre = vp == 2 ? 0 : 1;
             if (const char *e = std::getenv("KATS_BP_ENDS")) q.ends_pre = std::string(e) == "pre";
             if (q.ends_pre) launch_bp_ends(q, s);
-            if (vp == 2) {
-                if (p.poly) launch_tmem_kernel<true, 2>(q, gw, sm, qmap, s);
-                else launch_tmem_kernel<false, 2>(q, gw, sm, qmap, s);
-            } else {
-                if (p.poly) launch_tmem_kernel<true, 1>(q, gw, sm, qmap, s);
-                else launch_tmem_kernel<false, 1>(q, gw, sm, qmap, s);
-            }
+            if (p.poly) launch_tmem<true>(q, vp, gw, sm, qmap, s);
+            else launch_tmem<false>(q, vp, gw, sm, qmap, s);
             return KATS_BP_TMEM;
         }
     }
