@@ -1200,20 +1200,26 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             atomicMin(&rect[2], q_lo); atomicMax(&rect[3], q_hi);
         }
         if (work) {
-            int *c0 = pl + (lane & 1) * cpy + ci * NQP;                  // odd lanes: the shifted copy
+            // the four components' bases (one LEA per address); odd lanes: the shifted copy
+            int *const c0 = pl + (lane & 1) * cpy + ci * NQP, *const c1 = c0 + nbox;
+            int *const c2 = c1 + nbox, *const c3 = c2 + nbox;
             const float e0 = w0 * S01, e1 = w1 * S01, f0 = w0 * S23, f1 = w1 * S23;
             const int nt = t_hi - t_lo + 1;
-            // rotated start: lane L begins ~L rows below lane 0 (consecutive banks for a shared column)
+            // rotated start: lane L begins ~L rows below lane 0 (consecutive banks for a shared column);
+            // every lane walks its nt slices in lockstep, wrapping from t_hi to t_lo
             int t = t_lo + (int)((float)lane * __frcp_rn(step)) % nt;
+            const float Plo = fmaf((float)t_lo, step, base);
+            float P = fmaf((float)t, step, base);
             for (int i = 0; i < nt; ++i) {
-                const float P = fmaf((float)t, step, base);
                 const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
                 const float yy = yc[t], yP = yy * P;
                 atomicAdd(c0 + r, (int)(__float_as_uint(fmaf(e0, yy, kMagic)) - kMagicBits));
-                atomicAdd(c0 + nbox + r, (int)(__float_as_uint(fmaf(e1, yy, kMagic)) - kMagicBits));
-                atomicAdd(c0 + 2 * nbox + r, (int)(__float_as_uint(fmaf(f0, yP, kMagic)) - kMagicBits));
-                atomicAdd(c0 + 3 * nbox + r, (int)(__float_as_uint(fmaf(f1, yP, kMagic)) - kMagicBits));
-                t = t == t_hi ? t_lo : t + 1;
+                atomicAdd(c1 + r, (int)(__float_as_uint(fmaf(e1, yy, kMagic)) - kMagicBits));
+                atomicAdd(c2 + r, (int)(__float_as_uint(fmaf(f0, yP, kMagic)) - kMagicBits));
+                atomicAdd(c3 + r, (int)(__float_as_uint(fmaf(f1, yP, kMagic)) - kMagicBits));
+                const bool wrap = t == t_hi;
+                t = wrap ? t_lo : t + 1;
+                P = wrap ? Plo : P + step;
             }
         }
         __syncthreads();                                               // the view's scatter and bounds are done
