@@ -105,6 +105,55 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin_col(FilterParams p, int
     }
 }
 
+// Same computation in two phases per (view, K12_TL-column tile): the CTA first computes g2 of the
+// tile's nr x K12_TL samples (Eqs. 8-9) into shared memory, then the tile's npsi x K12_TL κ-line
+// samples (Eqs. 10-11) read their two g2 rows from there.  A thread keeps one column and walks
+// rows (phase 1) / κ-lines (phase 2) K12_RS apart with pointer increments: no per-item index
+// division, unconditional unrolled loads (ncu, C4: the column walk spends ~77 instructions per
+// sample on index math and a dependent table -> stencil chain, 34 us per 256-view chunk).
+// α-derivative at the edges as g2_at: lp = min(l+1, nc-1), lm = max(l-1, 0), scale 1/((lp-lm)Δα).
+constexpr int K12_TL = 64, K12_THREADS = 256, K12_RS = K12_THREADS / K12_TL;
+
+__global__ void __launch_bounds__(K12_THREADS) k_deriv_fwd_rebin_tile(FilterParams p)
+{
+    extern __shared__ float g2s[];   // [nr][K12_TL]
+    const int lt = threadIdx.x % K12_TL, r0 = threadIdx.x / K12_TL;
+    const int nc = p.nc, l = blockIdx.x * K12_TL + lt, v = blockIdx.y;
+    const bool col_ok = l < nc;
+    const int lc = col_ok ? l : nc - 1;
+    const int lp = min(lc + 1, nc - 1), lm = max(lc - 1, 0);
+    const float sa = (lp - lm == 2) ? p.inv_2dalpha : p.inv_dalpha, sq = p.inv_2dlam;
+    const int64_t g = p.view0 + v;
+    const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+    const int vs = p.nr * nc;
+    const float *r = p.sino + (size_t)raw * vs + (size_t)r0 * nc;
+    float *gs = g2s + r0 * K12_TL + lt;
+#pragma unroll 4
+    for (int m = r0; m < p.nr; m += K12_RS) {
+        const float dq = (__ldg(r + lc + vs) - __ldg(r + lc - vs)) * sq;
+        const float da = (__ldg(r + lp) - __ldg(r + lm)) * sa;
+        *gs = __ldg(p.wlen + m) * (dq + da);
+        r += K12_RS * nc;
+        gs += K12_RS * K12_TL;
+    }
+    __syncthreads();
+    if (!col_ok) return;
+    const size_t pitch = p.k3_in_split ? (size_t)(2 * p.hp) : (size_t)nc;
+    const int co = p.k3_in_split ? (l & 1) * p.hp + (l >> 1) : l;
+    float *out = p.g3 + ((size_t)v * p.npsi + r0) * pitch + co;
+    const RebinEntry *t = p.fr + (size_t)r0 * nc + l;
+    const float *gcol = g2s + lt;
+#pragma unroll 4
+    for (int i = r0; i < p.npsi; i += K12_RS) {
+        const RebinEntry en = *t;
+        const int ia = max(en.idx, 0);
+        const float a = gcol[ia * K12_TL], b = gcol[(ia + 1) * K12_TL];
+        *out = en.idx >= 0 ? fmaf(en.frac, b - a, a) : 0.f;
+        t += K12_RS * nc;
+        out += K12_RS * pitch;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: g4 = Σ_l' K[l-l'] g3[l'] along each κ-line (Eq. 12, h_H = 1/(πs) of
 //     Eq. e4, band-limited kernel of DESIGN.md reading A10: only odd
@@ -955,6 +1004,11 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     if (k12 == "sample") {
         const int bx = std::min(256, (p.nc + 31) / 32 * 32);
         k_deriv_fwd_rebin<<<dim3((p.nc + bx - 1) / bx, (p.npsi + kPsiPer - 1) / kPsiPer, p.n_views), bx, 0, s>>>(p);
+        return;
+    }
+    const size_t plane = (size_t)p.nr * K12_TL * sizeof(float);
+    if (k12 == "tile" && plane + (size_t)K12_TL * sizeof(float) <= 48 * 1024) {
+        k_deriv_fwd_rebin_tile<<<dim3((p.nc + K12_TL - 1) / K12_TL, p.n_views), K12_THREADS, plane + K12_TL * sizeof(float), s>>>(p);
         return;
     }
     const int seg = k12.rfind("col", 0) == 0 && std::atoi(k12.c_str() + 3) > 0 ? std::atoi(k12.c_str() + 3) : 8;

@@ -83,6 +83,8 @@ struct katsevich_plan {
     void *copy_stream2 = nullptr;           // device->host
     void *bp_streams[2] = {nullptr, nullptr};  // alternating per-pitch backprojection streams (low priority)
     void *filter_stream = nullptr;          // filter chunks (highest priority)
+    void *filter_xs[2] = {nullptr, nullptr};     // device entry points: extra filter-chunk streams
+    void *fork_events[3] = {nullptr, nullptr, nullptr};  // fork / joins of filter_xs
     void *dg_scratch = nullptr;             // data generation: phantom / counter / upsampled scratch
     size_t dg_scratch_bytes = 0;
     std::vector<void *> sync_events;

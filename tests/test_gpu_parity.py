@@ -230,7 +230,7 @@ def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("k12", ["sample", "col3"])
+@pytest.mark.parametrize("k12", ["sample", "col3", "tile"])
 @pytest.mark.parametrize("name", ["T1", "C1"])
 def test_k12_variants_match_oracle(name, k12, monkeypatch):
     """Steps 1-3 (g3) by the alternate K12 kernels: one thread per sample, and the column walk
