@@ -249,3 +249,20 @@ def test_k12_variants_match_oracle(name, k12, monkeypatch):
         got = out[s].cpu().numpy().astype(np.float64)
         e = np.linalg.norm(got - ref[s]) / np.linalg.norm(ref[s])
         assert e <= STAGE_REL, f"{s}: rel L2 {e:.3e}"
+
+
+@pytest.mark.parametrize("name,n_psi", [("T1", 2), ("T1", 14), ("T3", 22), ("T3", 87), ("C1", 65)])
+def test_reconstruct_n_psi_matches_oracle(name, n_psi):
+    """Non-default κ-line counts (P:l.132 leaves n_ψ free; DESIGN A6 default 2 n_w + 1):
+    the degenerate two-line case, n_w + 1 and ~4 n_w + 1 (more lines than a K3 tile holds).
+    Same seeded sinogram, oracle and GPU built with the same n_ψ."""
+    import torch
+    from oracle import oracle
+    cfg, sino, _, contrast = _case(name)
+    cfg = dict(cfg, n_psi=n_psi)
+    ref = oracle.reconstruct(cfg, sino, cfg["scan_v0"], 0, cfg["n_pitches"])
+    p = _plan(cfg)
+    assert p.table_info()["n_psi"] == n_psi
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    _check(vol.cpu().numpy(), ref, contrast)
