@@ -19,7 +19,16 @@ namespace {
 
 // Views per filter chunk: 256 keeps a wide-κ chunk's g3/g4 L2-resident (C4: 2 x 24 MB); with few
 // κ-lines a chunk grows so the tensor-core Hilbert launch has enough CTAs to hide its per-CTA latency.
-static int filter_chunk_views(const katsevich_plan *p) { return 256 * std::max(1, 128 / std::max(1, p->t.n_psi)); }
+// KATS_FILTER_CHUNK_MUL (A/B tests; read once per process so workspace sizing and use agree):
+// multiplier on the default chunk of 256 * max(1, 128 / n_psi) views
+static int filter_chunk_views(const katsevich_plan *p)
+{
+    static const int mul = [] {
+        const char *e = std::getenv("KATS_FILTER_CHUNK_MUL");
+        return e ? std::max(1, std::min(64, std::atoi(e))) : 1;
+    }();
+    return mul * 256 * std::max(1, 128 / std::max(1, p->t.n_psi));
+}
 // Filter chunks in flight at once on the device entry points (one chunk scratch each; run_filter)
 constexpr int kFilterStreamsMax = 2;   // 3 measured no faster (C4 51.0 vs 50.8 ms, C5 equal)
 
