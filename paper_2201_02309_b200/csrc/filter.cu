@@ -961,36 +961,55 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_hilbert_tc2(FilterParams p, 
 // ---------------------------------------------------------------------------
 constexpr int K4_COLS = 32;
 
+// VPB views per CTA (grid.y = ceil(n_views / VPB)): the view-independent rebin entry and cos α_l
+// are loaded once per (row, column) and the VPB views' g4 gathers are issued back to back.
+template <int VPB>
 __global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
 {
-    extern __shared__ float tile[];            // [nr + 3][K4_COLS + 1], rows m = -2 .. nr
+    extern __shared__ float tile[];            // [VPB][nr + 3][K4_COLS + 1], rows m = -2 .. nr
     const int nc = p.nc, nr = p.nr, nq = nr + 2;
     const int l0 = blockIdx.x * K4_COLS;
-    const int v = blockIdx.y;
+    const int v0 = blockIdx.y * VPB;
+    const int nv = min(VPB, p.n_views - v0);
     const int cols = min(K4_COLS, nc - l0);
-    const int ld = K4_COLS + 1;
-    for (int e = threadIdx.x; e < (nr + 3) * ld; e += blockDim.x) {
+    const int ld = K4_COLS + 1, tsz = (nr + 3) * ld;
+    for (int e = threadIdx.x; e < tsz; e += blockDim.x) {
         const int mm = e / ld, ll = e - mm * ld, m = mm - 2, l = l0 + ll;
-        float out = 0.f;
+        float out[VPB];
+#pragma unroll
+        for (int j = 0; j < VPB; ++j) out[j] = 0.f;
         if (m >= 0 && m < nr && l < nc && ll <= cols) {
             const RebinEntry r = p.br[m * nc + l];
             if (r.idx >= 0) {
-                const float *g = p.g4 + ((size_t)v * p.npsi + r.idx) * nc + l;
-                const float a = g[0], b = g[nc];
-                out = __ldg(p.cos_alpha + l) * fmaf(r.frac, b - a, a);
+                const float ca = __ldg(p.cos_alpha + l);
+                const float *g = p.g4 + ((size_t)v0 * p.npsi + r.idx) * nc + l;
+                const size_t vs = (size_t)p.npsi * nc;
+                float a[VPB], b[VPB];
+#pragma unroll
+                for (int j = 0; j < VPB; ++j)
+                    if (j < nv) { a[j] = g[j * vs]; b[j] = g[j * vs + nc]; }
+#pragma unroll
+                for (int j = 0; j < VPB; ++j)
+                    if (j < nv) out[j] = ca * fmaf(r.frac, b[j] - a[j], a[j]);
             }
-            if (p.gF && ll < cols) p.gF[((size_t)v * nr + m) * nc + l] = out;
+            if (p.gF && ll < cols)
+#pragma unroll
+                for (int j = 0; j < VPB; ++j)
+                    if (j < nv) p.gF[((size_t)(v0 + j) * nr + m) * nc + l] = out[j];
         }
-        tile[e] = out;
+#pragma unroll
+        for (int j = 0; j < VPB; ++j) tile[j * tsz + e] = out[j];
     }
     __syncthreads();
-    float4 *q = p.gq + ((size_t)v * nc + l0) * nq;
-    for (int e = threadIdx.x; e < cols * nq; e += blockDim.x) {
-        const int ll = e / nq, r = e - ll * nq;        // r = quad row; taps rows r-2, r-1
-        const float *t0 = tile + r * ld + ll;
+    const int per = cols * nq;
+    for (int e = threadIdx.x; e < nv * per; e += blockDim.x) {
+        const int j = e / per, e1 = e - j * per;
+        const int ll = e1 / nq, r = e1 - ll * nq;       // r = quad row; taps rows r-2, r-1
+        const float *t0 = tile + j * tsz + r * ld + ll;
         const float a0 = t0[0], a1 = t0[1], c0 = t0[ld], c1 = t0[ld + 1];
         const float rc = (float)(r - (nr + 2) / 2);      // centred quad row
-        q[e] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0, c1 - a1);
+        p.gq[((size_t)(v0 + j) * nc + l0) * nq + e1] =
+            make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0, c1 - a1);
     }
 }
 
@@ -1198,16 +1217,28 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
     k_hilbert<<<(unsigned)((n_lines + lpb - 1) / lpb), threads, smem, s>>>(p, n_lines, lpb);
 }
 
-void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
+template <int VPB>
+static void launch_k4(const FilterParams &p, cudaStream_t s)
 {
-    dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, p.n_views);
-    size_t smem = sizeof(float) * (size_t)(p.nr + 3) * (K4_COLS + 1);
+    dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, (p.n_views + VPB - 1) / VPB);
+    size_t smem = sizeof(float) * VPB * (size_t)(p.nr + 3) * (K4_COLS + 1);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_bwd_rebin_cos, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bwd_rebin_cos<VPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    k_bwd_rebin_cos<<<grid, 256, smem, s>>>(p);
+    k_bwd_rebin_cos<VPB><<<grid, 256, smem, s>>>(p);
+}
+
+void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
+{
+    // KATS_K4_VPB (A/B): views per CTA.  2 by default (scripts/ab/gpu_k4vpb.sh: C5 4.37 -> 4.29 ms,
+    // C3 9.38 -> 9.31 ms, C2 / C4 unchanged; 4 views: C5 4.23 ms but C4's K4 1.14 -> 1.32 ms)
+    const char *e = std::getenv("KATS_K4_VPB");
+    const int vpb = e ? std::atoi(e) : 2;
+    if (vpb >= 4) launch_k4<4>(p, s);
+    else if (vpb == 2) launch_k4<2>(p, s);
+    else launch_k4<1>(p, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -266,3 +266,23 @@ def test_reconstruct_n_psi_matches_oracle(name, n_psi):
     vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
     torch.cuda.synchronize()
     _check(vol.cpu().numpy(), ref, contrast)
+
+
+@pytest.mark.parametrize("vpb", ["1", "2", "4"])
+@pytest.mark.parametrize("name", ["T1", "T3"])
+def test_k4_views_per_cta_match_oracle(name, vpb, monkeypatch):
+    """K4 with 1, 2 or 4 views per CTA (KATS_K4_VPB; ragged view tails): gF per stage and the
+    reconstructed volume against the oracle."""
+    import torch
+    from oracle import oracle
+    monkeypatch.setenv("KATS_K4_VPB", vpb)
+    cfg, sino, ref, contrast = _case(name)
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    out = p.filter(torch.from_numpy(sino).cuda(), cfg["scan_v0"], v0 + 1, nv - 3, stages=("gF",))
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    gref = oracle.filter_views(cfg, sino, cfg["scan_v0"], v0 + 1, nv - 3, stages=("gF",))["gF"]
+    got = out["gF"].cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(got - gref) / np.linalg.norm(gref) <= STAGE_REL
+    _check(vol.cpu().numpy(), ref, contrast)
