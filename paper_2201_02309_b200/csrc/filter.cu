@@ -105,6 +105,56 @@ __global__ void __launch_bounds__(128) k_deriv_fwd_rebin_col(FilterParams p, int
     }
 }
 
+// Column walk over VPB views per thread (KATS_K12=colv2 / colv4): the view-independent rebin
+// entries are loaded once for the VPB views and their stencil loads are issued together.
+template <int VPB>
+__global__ void __launch_bounds__(128) k_deriv_fwd_rebin_colv(FilterParams p, int seg)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x, vb = blockIdx.y * VPB;
+    const int i0 = blockIdx.z * seg, i1 = min(i0 + seg, p.npsi);   // this thread's κ-lines
+    if (l >= p.nc) return;
+    const int nv = min(VPB, p.n_views - vb);
+    const float *gv[VPB];
+#pragma unroll
+    for (int j = 0; j < VPB; ++j) {
+        const int64_t g = p.view0 + vb + min(j, nv - 1);
+        const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+        gv[j] = p.sino + (size_t)raw * p.nr * p.nc;
+    }
+    int r0 = -2, r1 = -2;                                          // cached rows and their g2
+    float c0[VPB], c1[VPB];
+#pragma unroll
+    for (int j = 0; j < VPB; ++j) c0[j] = c1[j] = 0.f;
+    for (int i = i0; i < i1; ++i) {
+        const RebinEntry e = p.fr[i * p.nc + l];
+        float o[VPB];
+        if (e.idx >= 0) {
+            const int m = e.idx;
+            float a[VPB], b[VPB];
+            if (m == r0) {
+                const bool hit = m + 1 == r1;
+#pragma unroll
+                for (int j = 0; j < VPB; ++j) { a[j] = c0[j]; b[j] = hit ? c1[j] : g2_at(p, gv[j], m + 1, l); }
+            } else if (m == r1) {
+#pragma unroll
+                for (int j = 0; j < VPB; ++j) { a[j] = c1[j]; b[j] = g2_at(p, gv[j], m + 1, l); }
+            } else {
+#pragma unroll
+                for (int j = 0; j < VPB; ++j) { a[j] = g2_at(p, gv[j], m, l); b[j] = g2_at(p, gv[j], m + 1, l); }
+            }
+            r0 = m; r1 = m + 1;
+#pragma unroll
+            for (int j = 0; j < VPB; ++j) { c0[j] = a[j]; c1[j] = b[j]; o[j] = fmaf(e.frac, b[j] - a[j], a[j]); }
+        } else {
+#pragma unroll
+            for (int j = 0; j < VPB; ++j) o[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < VPB; ++j)
+            if (j < nv) p.g3[k3in_off(p, (size_t)(vb + j) * p.npsi + i, l)] = o[j];
+    }
+}
+
 // Same computation in two phases per (view, K12_TL-column tile): the CTA first computes g2 of the
 // tile's nr x K12_TL samples (Eqs. 8-9) into shared memory, then the tile's npsi x K12_TL κ-line
 // samples (Eqs. 10-11) read their two g2 rows from there.  A thread keeps one column and walks
@@ -1028,6 +1078,13 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     const size_t plane = (size_t)p.nr * K12_TL * sizeof(float);
     if (k12 == "tile" && plane + (size_t)K12_TL * sizeof(float) <= 48 * 1024) {
         k_deriv_fwd_rebin_tile<<<dim3((p.nc + K12_TL - 1) / K12_TL, p.n_views), K12_THREADS, plane + K12_TL * sizeof(float), s>>>(p);
+        return;
+    }
+    // default: the column walk over two views per thread (scripts/ab/gpu_k12v.sh: C5 4.29 -> 4.22 ms,
+    // C3 9.30 -> 9.27, C2 / C4 unchanged; colv4 no better); "col8" = one view per thread
+    if (k12.empty() || k12 == "colv2" || k12 == "colv4") {
+        if (k12 != "colv4") k_deriv_fwd_rebin_colv<2><<<dim3((p.nc + 127) / 128, (p.n_views + 1) / 2, (p.npsi + 7) / 8), 128, 0, s>>>(p, 8);
+        else k_deriv_fwd_rebin_colv<4><<<dim3((p.nc + 127) / 128, (p.n_views + 3) / 4, (p.npsi + 7) / 8), 128, 0, s>>>(p, 8);
         return;
     }
     const int seg = k12.rfind("col", 0) == 0 && std::atoi(k12.c_str() + 3) > 0 ? std::atoi(k12.c_str() + 3) : 8;

@@ -99,12 +99,17 @@ def test_backproject_only_matches_oracle(name):
     _check(got.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("n_slabs,winv", [(3, None), (4, None), (4, "0")])
-def test_batch_matches_oracle(n_slabs, winv, monkeypatch):
+@pytest.mark.parametrize("n_slabs,winv,k12", [(3, None, None), (4, None, None), (4, "0", None), (3, None, "colv4")])
+def test_batch_matches_oracle(n_slabs, winv, k12, monkeypatch):
     """Independent one-pitch slabs (C5-shaped, small): reconstruct_batch, odd and
     even batches (even batches may pair items per CTA in the window kernel), and
-    the plain window kernel forced (KATS_BP_WINV=0)."""
+    the plain window kernel forced (KATS_BP_WINV=0), and K12 over 4 views per thread across
+    slab ends (KATS_K12=colv4)."""
     import torch
+    if k12 is None:
+        monkeypatch.delenv("KATS_K12", raising=False)
+    else:
+        monkeypatch.setenv("KATS_K12", k12)
     from oracle import oracle
     from synth import configs, synth
     if winv is None:
@@ -230,11 +235,12 @@ def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("k12", ["sample", "col3", "tile"])
+@pytest.mark.parametrize("k12", ["sample", "col3", "col8", "tile", "colv2", "colv4"])
 @pytest.mark.parametrize("name", ["T1", "C1"])
 def test_k12_variants_match_oracle(name, k12, monkeypatch):
-    """Steps 1-3 (g3) by the alternate K12 kernels: one thread per sample, and the column walk
-    with a ragged κ-line segment (3 lines per thread; the default walks 8)."""
+    """Steps 1-3 (g3) by the alternate K12 kernels: one thread per sample, the column walk
+    with a ragged κ-line segment (3 lines per thread; the default walks 8), the shared-memory
+    tile, and the column walk over 2 / 4 views per thread (ragged view tails)."""
     import torch
     from oracle import oracle
     monkeypatch.setenv("KATS_K12", k12)
