@@ -17,17 +17,25 @@ using namespace kats;
 
 namespace {
 
-// Views per filter chunk: 256 keeps a wide-κ chunk's g3/g4 L2-resident (C4: 2 x 24 MB); with few
+// Base views per filter chunk: 256 keeps a wide-κ chunk's g3/g4 L2-resident (C4: 2 x 24 MB); with few
 // κ-lines a chunk grows so the tensor-core Hilbert launch has enough CTAs to hide its per-CTA latency.
-// KATS_FILTER_CHUNK_MUL (A/B tests; read once per process so workspace sizing and use agree):
-// multiplier on the default chunk of 256 * max(1, 128 / n_psi) views
-static int filter_chunk_views(const katsevich_plan *p)
+// The device entry points (katsevich_reconstruct, _batch) take chunks device_chunk_mul() times
+// larger; the host-staged path keeps the base chunk (its H2D copy is pipelined per chunk) and the
+// adjoint the base chunk.
+static int filter_chunk_views(const katsevich_plan *p, int mul = 1)
+{
+    return mul * 256 * std::max(1, 128 / std::max(1, p->t.n_psi));
+}
+// KATS_FILTER_CHUNK_MUL (A/B tests; read once per process so workspace sizing and use agree).
+// Default 4 (scripts/ab/gpu_fchunk.sh, two runs each: C5 4.21 -> 4.14 ms, C3 9.25 -> 9.12 ms,
+// C2 1.73 -> 1.71 ms, C4 50.85 -> 50.78 ms; fewer, fuller K3 launches outweigh L2 residency)
+static int device_chunk_mul()
 {
     static const int mul = [] {
         const char *e = std::getenv("KATS_FILTER_CHUNK_MUL");
-        return e ? std::max(1, std::min(64, std::atoi(e))) : 1;
+        return e ? std::max(1, std::min(64, std::atoi(e))) : 4;
     }();
-    return mul * 256 * std::max(1, 128 / std::max(1, p->t.n_psi));
+    return mul;
 }
 // Filter chunks in flight at once on the device entry points (one chunk scratch each; run_filter)
 constexpr int kFilterStreamsMax = 2;   // 3 measured no faster (C4 51.0 vs 50.8 ms, C5 equal)
@@ -125,9 +133,9 @@ int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
     return (int64_t)(n_pitches - 1) * p->g.views_per_turn + (t.bp_hi - t.bp_lo + 1);
 }
 
-size_t filter_chunk_bytes(const katsevich_plan *p)
+size_t filter_chunk_bytes(const katsevich_plan *p, int mul = 1)
 {
-    return 2 * sizeof(float) * (size_t)filter_chunk_views(p) * p->t.n_psi * g3_line_pitch(p->g.n_cols);
+    return 2 * sizeof(float) * (size_t)filter_chunk_views(p, mul) * p->t.n_psi * g3_line_pitch(p->g.n_cols);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -179,7 +187,7 @@ static int filter_streams(katsevich_plan *p)
 // stream waits for all of them at the end).  C5 4.75 -> 4.31 ms per step with two streams.
 int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float4 *gq,
                float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s, bool overlapped = false,
-               int64_t slab_views = 0, bool multi = false)
+               int64_t slab_views = 0, bool multi = false, int chunk_mul = 1)
 {
     FilterParams f = filter_params(p);
     // running concurrently with the TMEM backprojection: K3 uses the fp32 direct convolution
@@ -191,7 +199,7 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
     const size_t qs = quad_view_elems(p);
     const size_t ps_dbg = (size_t)p->t.n_psi * p->g.n_cols;              // debug stage arrays: plain lines
     const size_t ps = (size_t)p->t.n_psi * g3_line_pitch(p->g.n_cols);  // scratch lines
-    const int kFilterChunk = filter_chunk_views(p);
+    const int kFilterChunk = filter_chunk_views(p, chunk_mul);
     const int64_t nchunks = (n_out + kFilterChunk - 1) / kFilterChunk;
     const int ns = multi && !dbg3 && !dbg4 && !dbgF ? (int)std::min<int64_t>(filter_streams(p), nchunks) : 1;
     cudaStream_t st[kFilterStreamsMax] = {s};
@@ -200,7 +208,7 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
         KCHECK(p, cudaEventRecord((cudaEvent_t)p->fork_events[0], s));
         for (int i = 1; i < ns; ++i) KCHECK(p, cudaStreamWaitEvent(st[i], (cudaEvent_t)p->fork_events[0], 0));
     }
-    const size_t chunk_floats = align_up(filter_chunk_bytes(p)) / sizeof(float);
+    const size_t chunk_floats = align_up(filter_chunk_bytes(p, chunk_mul)) / sizeof(float);
     for (int64_t v0 = 0; v0 < n_out; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, n_out - v0);
         const int c = (int)((v0 / kFilterChunk) % ns);
@@ -458,7 +466,7 @@ int katsevich_workspace_bytes(const katsevich_plan *p, int32_t n_pitches, size_t
     const int64_t nslab = p->t.bp_hi - p->t.bp_lo + 1;
     // reconstruct: filtered quads over the union of views; batch: per slab
     size_t gf = sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, n_pitches), nslab * n_pitches);
-    *bytes = align_up(gf) + kFilterStreamsMax * align_up(filter_chunk_bytes(p));   // chunk scratches (run_filter)
+    *bytes = align_up(gf) + kFilterStreamsMax * align_up(filter_chunk_bytes(p, device_chunk_mul()));   // chunk scratches (run_filter)
     return KATS_OK;
 }
 
@@ -526,7 +534,8 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
 {
     int rc = check_device_plan(p);
     if (rc) return rc;
-    const int kFilterChunk = filter_chunk_views(p);
+    const int dm = device_chunk_mul();
+    const int kFilterChunk = filter_chunk_views(p, dm);
     if (!sino || !vol || !workspace) return KATS_ERR_NULL;
     if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
     size_t need;
@@ -553,7 +562,7 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     const char *pe = std::getenv("KATS_PIPELINE");
     if (n_pitches == 1 || !(pe && pe[0] == '1')) {
         // filter every needed view, then one backprojection launch over all pitches
-        rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s, false, 0, true);
+        rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s, false, 0, true, dm);
         if (rc) return rc;
         BPParams b = bp_params(p);
         b.gq = gq;
@@ -587,7 +596,7 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
             int64_t c_end = c_next;
             while (c_end < nchunks && u0 + c_end * kFilterChunk < filt_end) ++c_end;
             const int64_t a = u0 + c_next * kFilterChunk, n = std::min<int64_t>(c_end * kFilterChunk, nu) - c_next * kFilterChunk;
-            rc = run_filter(p, sino + (a - s0) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs);
+            rc = run_filter(p, sino + (a - s0) * rs, n, gq + (a - u0) * qs, scratch, nullptr, nullptr, nullptr, fs, false, 0, false, dm);
             if (rc) return rc;
             c_next = c_end;
         }
@@ -769,7 +778,7 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
     // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
     // keeps its own +-1 halo)
-    rc = run_filter(p, slabs + rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true);
+    rc = run_filter(p, slabs + rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true, device_chunk_mul());
     if (rc) return rc;
     (void)nslab;
     BPParams bp = bp_params(p);
