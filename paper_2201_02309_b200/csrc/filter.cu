@@ -1289,10 +1289,12 @@ static void launch_k4(const FilterParams &p, cudaStream_t s)
 
 void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
 {
-    // KATS_K4_VPB (A/B): views per CTA.  2 by default (scripts/ab/gpu_k4vpb.sh: C5 4.37 -> 4.29 ms,
-    // C3 9.38 -> 9.31 ms, C2 / C4 unchanged; 4 views: C5 4.23 ms but C4's K4 1.14 -> 1.32 ms)
+    // KATS_K4_VPB (A/B): views per CTA.  Default 4 for detectors of <= 32 rows, else 2
+    // (scripts/ab/gpu_k4vpb.sh: 2 vs 1 view C5 4.37 -> 4.29 ms, C3 9.38 -> 9.31 ms, C4 unchanged,
+    // 4 views made C4's K4 1.14 -> 1.32 ms; gpu_k4vpb2.sh, 4x chunks: 4 vs 2 views C5 4.14-4.24 ->
+    // 4.07 ms, C2 1.703 -> 1.696 ms)
     const char *e = std::getenv("KATS_K4_VPB");
-    const int vpb = e ? std::atoi(e) : 2;
+    const int vpb = e ? std::atoi(e) : (p.nr <= 32 ? 4 : 2);
     if (vpb >= 4) launch_k4<4>(p, s);
     else if (vpb == 2) launch_k4<2>(p, s);
     else launch_k4<1>(p, s);
