@@ -19,9 +19,9 @@ namespace {
 
 // Base views per filter chunk: 256 keeps a wide-κ chunk's g3/g4 L2-resident (C4: 2 x 24 MB); with few
 // κ-lines a chunk grows so the tensor-core Hilbert launch has enough CTAs to hide its per-CTA latency.
-// The device entry points (katsevich_reconstruct, _batch) take chunks device_chunk_mul() times
-// larger; the host-staged path keeps the base chunk (its H2D copy is pipelined per chunk) and the
-// adjoint the base chunk.
+// The device entry points (katsevich_reconstruct, _batch, the adjoints) take chunks
+// device_chunk_mul() times larger; the host-staged path keeps the base chunk (its H2D copy is
+// pipelined per chunk).
 static int filter_chunk_views(const katsevich_plan *p, int mul = 1)
 {
     return mul * 256 * std::max(1, 128 / std::max(1, p->t.n_psi));
@@ -620,6 +620,50 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     return KATS_OK;
 }
 
+// Steps 6..1 transposed (K4^T, K3^T = -K3, K12's rebin^T) over nu views in device_chunk_mul()-sized
+// chunks that alternate over the filter streams and chunk scratches like run_filter (chunks write
+// disjoint views of g1T; the caller's stream waits for all of them).
+static int run_filter_T(katsevich_plan *p, FilterParams f, const float4 *qT, float *scratch, float *g1T,
+                        int64_t nu, cudaStream_t s0)
+{
+    const int dm = device_chunk_mul();
+    const int kFilterChunk = filter_chunk_views(p, dm);
+    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t qs = quad_view_elems(p);
+    const size_t ps = (size_t)p->t.n_psi * g3_line_pitch(p->g.n_cols);
+    const size_t chunk_floats = align_up(filter_chunk_bytes(p, dm)) / sizeof(float);
+    const int64_t nchunks = (nu + kFilterChunk - 1) / kFilterChunk;
+    const int ns = (int)std::min<int64_t>(filter_streams(p), nchunks);
+    cudaStream_t st[kFilterStreamsMax] = {s0};
+    for (int i = 1; i < ns; ++i) st[i] = (cudaStream_t)p->filter_xs[i - 1];
+    if (ns > 1) {
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->fork_events[0], s0));
+        for (int i = 1; i < ns; ++i) KCHECK(p, cudaStreamWaitEvent(st[i], (cudaEvent_t)p->fork_events[0], 0));
+    }
+    for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
+        const int c = (int)((v0 / kFilterChunk) % std::max(ns, 1));
+        cudaStream_t s = st[c];
+        f.n_views = (int)std::min<int64_t>(kFilterChunk, nu - v0);
+        f.g3 = scratch + c * chunk_floats;                         // g3^T
+        f.g4 = f.g3 + (size_t)kFilterChunk * ps;                   // g4^T
+        { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos_T(f, qT + v0 * qs, s); }
+        KCHECK(p, cudaGetLastError());
+        FilterParams h = f;                                        // K3^T = -K3: reads g4^T, writes g3^T
+        h.g3 = f.g4;
+        h.g4 = f.g3;
+        h.sign = -1.f;
+        { LaunchScope ls(p, ST_K3, s); launch_hilbert(h, s); }
+        KCHECK(p, cudaGetLastError());
+        { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
+        KCHECK(p, cudaGetLastError());
+    }
+    for (int i = 1; i < ns; ++i) {
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->fork_events[i], st[i]));
+        KCHECK(p, cudaStreamWaitEvent(s0, (cudaEvent_t)p->fork_events[i], 0));
+    }
+    return KATS_OK;
+}
+
 // Adjoint of katsevich_reconstruct (NEXT-1): vol [n_pitches*nz][ny][nx] -> sino_out [sn][rows][cols]
 // (overwritten; views outside the pitches' slabs are 0).  Step 7^T into quad adjoints over the
 // union of filtered views, then steps 6..1 transposed per 256-view chunk, then the view/α
@@ -630,7 +674,6 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
 {
     int rc = check_device_plan(p);
     if (rc) return rc;
-    const int kFilterChunk = filter_chunk_views(p);
     if (!vol || !sino_out || !workspace) return KATS_ERR_NULL;
     if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
     size_t need;
@@ -650,7 +693,7 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
     float4 *qT = (float4 *)workspace;
     const size_t qbytes = align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches));
     float *scratch = (float *)((char *)workspace + qbytes);
-    float *g1T = (float *)((char *)workspace + qbytes + align_up(filter_chunk_bytes(p)));
+    float *g1T = (float *)((char *)workspace + qbytes + kFilterStreamsMax * align_up(filter_chunk_bytes(p, device_chunk_mul())));
     KCHECK(p, cudaMemsetAsync(qT, 0, sizeof(float4) * qs * (size_t)nu, s));
     KCHECK(p, cudaMemsetAsync(sino_out, 0, sizeof(float) * rs * (size_t)sn, s));
     BPParams b = bp_params(p);
@@ -671,23 +714,8 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
     FilterParams f = filter_params(p);
     f.hp = g3_half_pitch(p->g.n_cols);
     f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K4^T writes the lines K3^T reads
-    const size_t ps = (size_t)t.n_psi * g3_line_pitch(p->g.n_cols);
-    for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
-        const int nv = (int)std::min<int64_t>(kFilterChunk, nu - v0);
-        f.n_views = nv;
-        f.g4 = scratch + (size_t)kFilterChunk * ps;                // g4^T
-        f.g3 = scratch;                                            // g3^T
-        { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos_T(f, qT + v0 * qs, s); }
-        KCHECK(p, cudaGetLastError());
-        FilterParams h = f;                                        // K3^T = -K3: reads g4^T, writes g3^T
-        h.g3 = f.g4;
-        h.g4 = f.g3;
-        h.sign = -1.f;
-        { LaunchScope ls(p, ST_K3, s); launch_hilbert(h, s); }
-        KCHECK(p, cudaGetLastError());
-        { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
-        KCHECK(p, cudaGetLastError());
-    }
+    rc = run_filter_T(p, f, qT, scratch, g1T, nu, s);
+    if (rc) return rc;
     { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nu, sino_out + (u0 - 1 - s0) * rs, s); }
     KCHECK(p, cudaGetLastError());
     return KATS_OK;
@@ -706,7 +734,6 @@ int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, flo
     size_t need;
     katsevich_adjoint_batch_workspace_bytes(p, B, &need);
     if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
-    const int kFilterChunk = filter_chunk_views(p);
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const HostTables &t = p->t;
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
@@ -715,7 +742,7 @@ int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, flo
     float4 *qT = (float4 *)workspace;
     const size_t qbytes = align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nu));
     float *scratch = (float *)((char *)workspace + qbytes);
-    float *g1T = (float *)((char *)workspace + qbytes + align_up(filter_chunk_bytes(p)));
+    float *g1T = (float *)((char *)workspace + qbytes + kFilterStreamsMax * align_up(filter_chunk_bytes(p, device_chunk_mul())));
     KCHECK(p, cudaMemsetAsync(qT, 0, sizeof(float4) * qs * (size_t)nu, s));
     KCHECK(p, cudaMemsetAsync(slabs_out, 0, sizeof(float) * rs * (size_t)(nbp + 2) * B, s));
     BPParams b = bp_params(p);
@@ -736,23 +763,8 @@ int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, flo
     FilterParams f = filter_params(p);
     f.hp = g3_half_pitch(p->g.n_cols);
     f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K4^T writes the lines K3^T reads
-    const size_t ps = (size_t)t.n_psi * g3_line_pitch(p->g.n_cols);
-    for (int64_t v0 = 0; v0 < nu; v0 += kFilterChunk) {
-        const int nv = (int)std::min<int64_t>(kFilterChunk, nu - v0);
-        f.n_views = nv;
-        f.g4 = scratch + (size_t)kFilterChunk * ps;
-        f.g3 = scratch;
-        { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos_T(f, qT + v0 * qs, s); }
-        KCHECK(p, cudaGetLastError());
-        FilterParams h = f;
-        h.g3 = f.g4;
-        h.g4 = f.g3;
-        h.sign = -1.f;
-        { LaunchScope ls(p, ST_K3, s); launch_hilbert(h, s); }
-        KCHECK(p, cudaGetLastError());
-        { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
-        KCHECK(p, cudaGetLastError());
-    }
+    rc = run_filter_T(p, f, qT, scratch, g1T, nu, s);
+    if (rc) return rc;
     { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nbp, slabs_out, s, B); }
     KCHECK(p, cudaGetLastError());
     return KATS_OK;
