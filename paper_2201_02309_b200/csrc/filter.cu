@@ -1314,6 +1314,48 @@ void launch_bwd_rebin_cos(const FilterParams &p, cudaStream_t s)
 // (K4^T keeps its global read-modify-write: its npsi-deep column would cost occupancy.)
 constexpr int KT_THREADS = 64;
 
+// Two views per thread (KATS_K4T_VPB=2): the same per-view arithmetic, the rebin entry and cos α
+// loaded once for both views, their quad loads issued together.
+__global__ void __launch_bounds__(128) k_bwd_rebin_cos_T2(FilterParams p, const float4 *__restrict__ qT)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x, v0 = blockIdx.y * 2;
+    if (l >= p.nc) return;
+    const int nv = min(2, p.n_views - v0);
+    const int nc = p.nc, nr = p.nr, nq = nr + 2, c = (nr + 2) / 2;
+    for (int j = 0; j < nv; ++j)
+        for (int i = 0; i < p.npsi; ++i) p.g4[k3in_off(p, (size_t)(v0 + j) * p.npsi + i, l)] = 0.f;
+    const float ca = __ldg(p.cos_alpha + l);
+    const float4 *qa[2], *qb[2];
+    for (int j = 0; j < 2; ++j) {
+        const int v = v0 + min(j, nv - 1);
+        qa[j] = qT + ((size_t)v * nc + l) * nq;
+        qb[j] = l > 0 ? qa[j] - nq : nullptr;
+    }
+    for (int m = 0; m < nr; ++m) {
+        const float rh = (float)(m + 2 - c), rl = (float)(m + 1 - c);
+        float gt[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float4 A = qa[j][m + 2], B = qa[j][m + 1];
+            gt[j] = 0.5f * A.x - (A.z - rh * A.x) + 0.5f * B.x + (B.z - rl * B.x);
+            if (qb[j]) {
+                const float4 C = qb[j][m + 2], D = qb[j][m + 1];
+                gt[j] += 0.5f * C.y - (C.w - rh * C.y) + 0.5f * D.y + (D.w - rl * D.y);
+            }
+        }
+        const RebinEntry e = p.br[m * nc + l];
+        if (e.idx < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (j >= nv) break;
+            const size_t line0 = (size_t)(v0 + j) * p.npsi;
+            const float val = ca * gt[j];
+            p.g4[k3in_off(p, line0 + e.idx, l)] += (1.f - e.frac) * val;
+            p.g4[k3in_off(p, line0 + e.idx + 1, l)] += e.frac * val;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) k_bwd_rebin_cos_T(FilterParams p, const float4 *__restrict__ qT)
 {
     const int l = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
@@ -1389,6 +1431,11 @@ __global__ void __launch_bounds__(128) k_deriv_T(FilterParams p, const float *__
 
 void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s)
 {
+    const char *e = std::getenv("KATS_K4T_VPB");            // A/B: two views per thread
+    if (e && std::atoi(e) == 2) {
+        k_bwd_rebin_cos_T2<<<dim3((p.nc + 127) / 128, (p.n_views + 1) / 2), 128, 0, s>>>(p, qT);
+        return;
+    }
     k_bwd_rebin_cos_T<<<dim3((p.nc + 127) / 128, p.n_views), 128, 0, s>>>(p, qT);
 }
 

@@ -24,15 +24,18 @@ def _plan(cfg):
 
 
 @pytest.mark.parametrize("name,kernel", [("T1", None), ("T2", None), ("T3", None), ("C1", None),
-                                         ("T2", "l1"), ("C1", "l1")])
+                                         ("T2", "l1"), ("C1", "l1"), ("T3", "k4t1"), ("T3", "k4t2")])
 def test_adjoint_matches_oracle(name, kernel, monkeypatch):
     """kernel None: the shared-memory box kernel (footprints on the detector);
     'l1': the checked, direct-scatter kernel (as for plans whose footprints may
-    leave the detector)."""
+    leave the detector); 'k4t1' / 'k4t2': K4^T over one / two views per thread."""
     import torch
     from oracle import oracle
     from synth import configs
-    if kernel:
+    if kernel in ("k4t1", "k4t2"):
+        monkeypatch.setenv("KATS_K4T_VPB", kernel[-1])
+        monkeypatch.delenv("KATS_BP_KERNEL", raising=False)
+    elif kernel:
         monkeypatch.setenv("KATS_BP_KERNEL", kernel)
     else:
         monkeypatch.delenv("KATS_BP_KERNEL", raising=False)
