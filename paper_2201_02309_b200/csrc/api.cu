@@ -8,12 +8,52 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <utility>
 
 #include "kernels.cuh"
 
 using namespace kats;
+
+namespace kats {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device context: remember, per (kernel, device),
+// the largest opt-in made (a second plan on another device in the same process must opt in again)
+cudaError_t smem_opt_in(const void *kernel, size_t bytes)
+{
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &have = done[{kernel, dev}];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
+int device_sms()
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    static std::mutex mu;
+    static std::map<int, int> sms;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = sms.find(dev);
+    if (it != sms.end()) return it->second;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    sms[dev] = n;
+    return n;
+}
+
+}  // namespace kats
 
 namespace {
 
@@ -47,6 +87,12 @@ int cuda_fail(katsevich_plan *p, cudaError_t e, const char *where)
     if (p) {
         p->detail = std::string(where) + ": " + cudaGetErrorString(e);
     }
+    return KATS_ERR_CUDA;
+}
+
+int hilbert_fail(katsevich_plan *p)
+{
+    p->detail = "K3: cuTensorMapEncodeTiled failed for the Hilbert input lines (Hilbert not run)";
     return KATS_ERR_CUDA;
 }
 
@@ -91,12 +137,15 @@ struct LaunchScope {
     }
 };
 
+// table upload on the caller's stream; the sources are pageable vectors, whose H2D copies return once
+// the data is staged, so a vector may go out of scope before the stream reaches the copy
+// (katsevich_precompute synchronises the stream at the end)
 template <typename T>
-int upload(katsevich_plan *p, T **dst, const std::vector<T> &src)
+int upload(katsevich_plan *p, T **dst, const std::vector<T> &src, cudaStream_t s)
 {
     if (src.empty()) { *dst = nullptr; return KATS_OK; }
     KCHECK(p, cudaMalloc((void **)dst, sizeof(T) * src.size()));
-    KCHECK(p, cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+    KCHECK(p, cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, s));
     return KATS_OK;
 }
 
@@ -234,7 +283,7 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
             launch_deriv_fwd_rebin(f, s);
         }
         KCHECK(p, cudaGetLastError());
-        { LaunchScope ls(p, ST_K3, s); launch_hilbert(f, s); }
+        { LaunchScope ls(p, ST_K3, s); if (launch_hilbert(f, s)) return hilbert_fail(p); }
         KCHECK(p, cudaGetLastError());
         { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos(f, s); }
         KCHECK(p, cudaGetLastError());
@@ -310,6 +359,15 @@ BPParams bp_params(const katsevich_plan *p)
         b.nq_s = nq;
         b.bp_items = 1;
     }
+    {   // K5^T's int32 fixed-point box (backproject.cu k_bp_adjoint) holds <= 2^10 full-scale contributions
+        // per (box column, quad row) cell of one view and lane-parity copy: bound the count by the tile
+        // columns a detector column's ray strip can cover (a copy holds 128 of the 256) times the slices one
+        // quad row can hold (the smallest row step per slice is at the far side of the FOV)
+        const double vmax = g.R + p->t.r_fov;
+        const double strip = std::ceil(vmax * g.d_alpha / std::min(g.dx, g.dy) + 1.0) * std::ceil(16.0 * std::sqrt(2.0) + 1.0);
+        const double step_min = g.D / (vmax * g.d_w) * (g.pitch / g.nz_per_pitch);
+        b.adj_fixed_ok = std::min(128.0, strip) * (std::ceil(1.0 / step_min) + 1.0) <= 1024.0;
+    }
     b.zero = 0u;
     b.warp_span = p->t.warp_span;
     b.warp_span2 = p->t.warp_span2;
@@ -359,7 +417,7 @@ int katsevich_plan_create(const katsevich_geometry *geom, int cuda_device, katse
 int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
 {
     if (!p) return KATS_ERR_NULL;
-    (void)cuda_stream;
+    cudaStream_t us = (cudaStream_t)cuda_stream;
     p->precomputed = false;
     int rc = compute_host_tables(p->g, p->t, p->detail);
     if (rc < 0) return rc;
@@ -397,10 +455,10 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
             double kd = (d & 1) ? 2.0 * g.d_alpha / (kPi * std::sin(d * g.d_alpha)) : 0.0;
             hk[(size_t)(d + g.n_cols - 1)] = (float)kd;
         }
-        if ((rc = upload(p, &p->d.pi_k, pik)) || (rc = upload(p, &p->d.pi_w, piw)) ||
-            (rc = upload(p, &p->d.view, vg)) || (rc = upload(p, &p->d.fr, fr)) ||
-            (rc = upload(p, &p->d.br, br)) || (rc = upload(p, &p->d.cos_alpha, cosa)) ||
-            (rc = upload(p, &p->d.wlen, wlen)) || (rc = upload(p, &p->d.hilbert, hk)))
+        if ((rc = upload(p, &p->d.pi_k, pik, us)) || (rc = upload(p, &p->d.pi_w, piw, us)) ||
+            (rc = upload(p, &p->d.view, vg, us)) || (rc = upload(p, &p->d.fr, fr, us)) ||
+            (rc = upload(p, &p->d.br, br, us)) || (rc = upload(p, &p->d.cos_alpha, cosa, us)) ||
+            (rc = upload(p, &p->d.wlen, wlen, us)) || (rc = upload(p, &p->d.hilbert, hk, us)))
             return rc;
         {   // step-7 tiles heaviest first (work ~ the tile's summed view span over its columns), so the
             // last wave of CTAs holds the lightest tiles (FOV edge)
@@ -417,15 +475,15 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
             std::vector<int> order(work.size());
             for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
             std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
-            if ((rc = upload(p, &p->d.tile_order, order))) return rc;
+            if ((rc = upload(p, &p->d.tile_order, order, us))) return rc;
         }
         std::vector<float> htc;
         hilbert_tc_table(g.n_cols, hk.data(), htc);
-        if ((rc = upload(p, &p->d.hilbert_tc, htc))) return rc;
+        if ((rc = upload(p, &p->d.hilbert_tc, htc, us))) return rc;
         std::vector<float> hhk;
         hilbert_hk_table(g.n_cols, hk.data(), hhk);
-        if ((rc = upload(p, &p->d.hilbert_hk, hhk))) return rc;
-        KCHECK(p, cudaDeviceSynchronize());
+        if ((rc = upload(p, &p->d.hilbert_hk, hhk, us))) return rc;
+        KCHECK(p, cudaStreamSynchronize(us));
     }
     p->precomputed = true;
     if (const char *v = std::getenv("KATS_VERBOSE"); v && *v == '1')
@@ -652,7 +710,7 @@ static int run_filter_T(katsevich_plan *p, FilterParams f, const float4 *qT, flo
         h.g3 = f.g4;
         h.g4 = f.g3;
         h.sign = -1.f;
-        { LaunchScope ls(p, ST_K3, s); launch_hilbert(h, s); }
+        { LaunchScope ls(p, ST_K3, s); if (launch_hilbert(h, s)) return hilbert_fail(p); }
         KCHECK(p, cudaGetLastError());
         { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
         KCHECK(p, cudaGetLastError());

@@ -1344,9 +1344,36 @@ __global__ void k_bp_adjoint_ends(BPParams p)
     }
 }
 
+// grid.z carries (slices or z chunks) x items and is limited to 65535: split the items into groups
+template <typename F>
+static int for_item_groups(const BPParams &p, int zper, int even, F &&launch)
+{
+    int maxi = std::max(1, 65535 / std::max(1, zper));
+    if (even && maxi > 1) maxi &= ~1;
+    if (p.n_items <= maxi) return launch(p);
+    int rc = 0;
+    const size_t vol_item = (size_t)p.nz * p.nx * p.ny;
+    for (int b0 = 0; b0 < p.n_items; b0 += maxi) {
+        BPParams q = p;
+        q.n_items = std::min(maxi, p.n_items - b0);
+        q.off0 = p.off0 + (int64_t)b0 * p.item_views;
+        q.vol = p.vol + (size_t)b0 * vol_item;
+        rc = launch(q);
+        if (rc < 0) return rc;
+    }
+    return rc;
+}
+
+static int launch_backproject_adjoint_items(const BPParams &p, cudaStream_t s);
+
 int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
 {
     if (!p.windows_monotone) return -1;
+    return for_item_groups(p, p.nz, 0, [&](const BPParams &q) { return launch_backproject_adjoint_items(q, s); });
+}
+
+static int launch_backproject_adjoint_items(const BPParams &p, cudaStream_t s)
+{
     // box column stride: 0 mod 32 banks when a warp's lanes share detector columns (rows, spread by
     // the rotated start, pick the bank: C3, C4); odd when they spread over many columns (C5: ~1.7
     // columns per voxel, 56-column boxes; 0 mod 32 made every lane of a row hit one bank)
@@ -1357,13 +1384,10 @@ int launch_backproject_adjoint(const BPParams &p, cudaStream_t s)
     const size_t sm = sizeof(int) * 2 * (4 * (size_t)p.fp_cols_column * q.adj_nqp + 16) +
                       sizeof(float) * (size_t)TX * TY * (p.nz | 1) + sizeof(int) * (size_t)p.max_cta_views;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
-    if (!p.checked && p.staged && sm <= 200 * 1024) {        // KATS_BP_KERNEL=l1: the checked kernel (A/B)
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_bp_adjoint<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(k_bp_adjoint<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr = true;
-        }
+    // KATS_BP_KERNEL=l1: the checked kernel (A/B); also the fallback when the fixed-point box could overflow
+    if (!p.checked && p.staged && p.adj_fixed_ok && sm <= 200 * 1024) {
+        smem_opt_in((const void *)k_bp_adjoint<true>, 200 * 1024);
+        smem_opt_in((const void *)k_bp_adjoint<false>, 200 * 1024);
         if (p.poly) k_bp_adjoint<true><<<grid, TX * TY, sm, s>>>(q);
         else k_bp_adjoint<false><<<grid, TX * TY, sm, s>>>(q);
     } else {
@@ -1399,11 +1423,7 @@ void launch_bp_ends(const BPParams &p, cudaStream_t s)
 template <bool POLY, int VP, bool ENDS_PRE>
 void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bp_tmem<POLY, VP, ENDS_PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    smem_opt_in((const void *)k_bp_tmem<POLY, VP, ENDS_PRE>, 200 * 1024);
     k_bp_tmem<POLY, VP, ENDS_PRE><<<grid, kWsThreads, sm, s>>>(qmap, q);
 }
 
@@ -1422,17 +1442,13 @@ void launch_tmem(const BPParams &q, int vp, dim3 grid, size_t sm, const QMaps &q
 template <int W>
 void launch_window(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bp_window<true, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_window<false, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_window<true, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_bp_window<false, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if constexpr (W <= 16) {
-            cudaFuncSetAttribute(k_bp_window<true, W, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaFuncSetAttribute(k_bp_window<false, W, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        }
-        attr = true;
+    smem_opt_in((const void *)k_bp_window<true, W, 0>, 200 * 1024);
+    smem_opt_in((const void *)k_bp_window<false, W, 0>, 200 * 1024);
+    smem_opt_in((const void *)k_bp_window<true, W, 1>, 200 * 1024);
+    smem_opt_in((const void *)k_bp_window<false, W, 1>, 200 * 1024);
+    if constexpr (W <= 16) {
+        smem_opt_in((const void *)k_bp_window<true, W, 2>, 200 * 1024);
+        smem_opt_in((const void *)k_bp_window<false, W, 2>, 200 * 1024);
     }
     const int v = q.win_variant;
     if constexpr (W <= 16) {
@@ -1507,7 +1523,15 @@ bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int wid
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static int launch_backproject_items(const BPParams &p, cudaStream_t s);
+
 int launch_backproject(const BPParams &p, cudaStream_t s)
+{
+    const int zper = std::max({(p.nz + JZ - 1) / JZ, (p.nz + JZL - 1) / JZL, p.nz});   // k_bp_ends: nz per item
+    return for_item_groups(p, zper, 1, [&](const BPParams &q) { return launch_backproject_items(q, s); });
+}
+
+static int launch_backproject_items(const BPParams &p, cudaStream_t s)
 {
     const int nchunk = (p.nz + JZ - 1) / JZ;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, nchunk * p.n_items);
@@ -1520,7 +1544,7 @@ int launch_backproject(const BPParams &p, cudaStream_t s)
     // small grids: the staged kernels run one CTA per 16x16 column tile (and item); under one CTA per
     // SM the z-chunked L1 kernel's parallelism wins (C1, 16 tiles: K5 0.262 -> 0.074 ms)
     int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    nsm = device_sms();
     const int64_t staged_ctas = (int64_t)((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY) * p.n_items;
     const bool small_grid = staged_ctas < nsm && !want_tmem && !want_window;
     // TMEM-window kernel for wide windows (accumulators in tensor memory, 3 CTAs per SM); for

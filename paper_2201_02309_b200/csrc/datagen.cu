@@ -7,6 +7,7 @@
 // Scan ray of detector sample (v, m, l) (helix P:l.87-94, curved detector
 // P:l.117, l.311-349): source a(λ) = (R cos(λ+λ0), R sin(λ+λ0), z0 + hλ),
 // direction ∝ D sinα e_t − D cosα e_r + w e_z — the geometry step 7 inverts.
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -262,15 +263,19 @@ __global__ void k_add_noise(const float *__restrict__ g, int64_t n, int64_t idx0
 void launch_project_ellipsoids(const DataGenParams &p, const double *ell, int n, int64_t v0, int64_t nv, float *out,
                                cudaStream_t s)
 {
-    k_project_ellipsoids<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)nv), 128, sizeof(double) * 10 * (size_t)n, s>>>(
-        p, ell, n, v0, out);
+    const size_t smem = sizeof(double) * 10 * (size_t)n;            // <= 160 KB (the ABI caps n at 2048)
+    smem_opt_in((const void *)k_project_ellipsoids, smem);
+    for (int64_t c = 0; c < nv; c += 65535)                           // grid.z <= 65535 views per launch
+        k_project_ellipsoids<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)std::min<int64_t>(65535, nv - c)), 128, smem,
+                               s>>>(p, ell, n, v0 + c, out + (size_t)c * p.nr * p.nc);
 }
 
 void launch_project_volume(const DataGenParams &p, const float *vol, int nzv, float zv0, float dzv, int64_t v0,
                            int64_t nv, float *out, unsigned long long *n_trunc, cudaStream_t s)
 {
-    k_project_volume<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)nv), 128, 0, s>>>(p, vol, nzv, zv0, dzv, v0, out,
-                                                                                  n_trunc);
+    for (int64_t c = 0; c < nv; c += 65535)                           // grid.z <= 65535 views per launch
+        k_project_volume<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)std::min<int64_t>(65535, nv - c)), 128, 0, s>>>(
+            p, vol, nzv, zv0, dzv, v0 + c, out + (size_t)c * p.nr * p.nc, n_trunc);
 }
 
 void launch_degrade(const DataGenParams &p, const float *in, int64_t v0, int64_t nv, int stride, double I0, double var,

@@ -1164,7 +1164,7 @@ bool hilbert_split_input(const FilterParams &p)
     return hilbert_tc_nh(p.nc) > 256 || h == "ws";
 }
 
-void launch_hilbert(const FilterParams &p, cudaStream_t s)
+int launch_hilbert(const FilterParams &p, cudaStream_t s)
 {
     if (hilbert_tc_usable(p) && p.hilbert_overlap) {
         // next to the TMEM backprojection (3 CTAs x 128 columns, 62K registers per SM) a tensor-core
@@ -1172,8 +1172,7 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
         // (C4 host path 59.4 -> 56.5 ms)
         FilterParams q = p;
         q.hilbert_tc = nullptr;
-        launch_hilbert(q, s);
-        return;
+        return launch_hilbert(q, s);
     }
     // KATS_HILBERT=tc: the per-chunk tap-streaming kernels (A/B tests); =hk: Hankel cores for every width
     const char *he = std::getenv("KATS_HILBERT");
@@ -1191,11 +1190,7 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
         int nstage = 4;
         while (nstage > 2 && taps + nstage * stage > 110 * 1024) --nstage;
         const size_t smem = taps + nstage * stage;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_hilbert_hk, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-            attr = true;
-        }
+        smem_opt_in((const void *)k_hilbert_hk, 225 * 1024);
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
         // warp-specialized for wide detectors (hilbert_split_input: its input lines are parity-split);
         // at NH <= 256 the two-CTA persistent kernel is faster (C2 0.18 vs 0.21 ms)
@@ -1210,40 +1205,31 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
             CUtensorMap amap;                                         // the K3 input: [n_lines][2 hp] fp32
             if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M)) {
                 // cannot happen on a driver that has cuTensorMapEncodeTiled (16-B aligned scratch lines);
-                // nothing else reads parity-split lines, so say so loudly rather than leave g4 stale
-                std::fprintf(stderr, "katsevich: tensor map for the Hilbert input failed; K3 output not written\n");
-                return;
+                // nothing else reads parity-split lines: the caller turns this into KATS_ERR_CUDA
+                return -1;
             }
-            static bool wattr = false;
-            if (!wattr) {
-                cudaFuncSetAttribute(k_hilbert_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-                wattr = true;
-            }
+            smem_opt_in((const void *)k_hilbert_ws, 225 * 1024);
             int nsm2 = 148;
-            cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, 0);
+            nsm2 = device_sms();
             const int64_t items = (n_lines + TC_M - 1) / TC_M * ns;
             const int per = (int)std::min<int64_t>(items, std::max(1, nsm2 / 2));   // one CTA per SM, half per parity
             k_hilbert_ws<<<(unsigned)(2 * per), WS_THREADS, wsm, s>>>(amap, p, n_lines, ns);
-            return;
+            return 0;
         }
         const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
         int nsm = 148;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+        nsm = device_sms();
         const int per_par = (int)std::min<int64_t>(n_items, nsm);      // persistent: 2 CTAs per SM, one per parity
         k_hilbert_hk<<<(unsigned)(2 * per_par), HK_THREADS, smem, s>>>(p, n_lines, nstage, nsplit);
-        return;
+        return 0;
     }
     if (hilbert_tc_usable(p) && hilbert_tc_nh(p.nc) <= 256 && !p.hilbert_overlap) {
         const int NH = hilbert_tc_nh(p.nc);
         const size_t smem = (size_t)4 * TC_M * TC_KC * 4 + (size_t)4 * NH * TC_KC * 4;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_hilbert_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            attr = true;
-        }
+        smem_opt_in((const void *)k_hilbert_tc2, 220 * 1024);
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
         k_hilbert_tc2<<<(unsigned)((n_lines + TC_M - 1) / TC_M), TC2_THREADS, smem, s>>>(p, n_lines);
-        return;
+        return 0;
     }
     if (hilbert_tc_usable(p)) {
         const int NH = hilbert_tc_nh(p.nc);
@@ -1251,27 +1237,20 @@ void launch_hilbert(const FilterParams &p, cudaStream_t s)
         // double-buffer when two stages fit, except next to the backprojection (keep its footprint small)
         const int nstage = (!p.hilbert_overlap && 2 * stage <= 220 * 1024) ? 2 : 1;
         const size_t smem = nstage * stage;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_hilbert_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-            attr = true;
-        }
+        smem_opt_in((const void *)k_hilbert_tc, 225 * 1024);
         const int64_t n_lines = (int64_t)p.n_views * p.npsi;
         dim3 grid((unsigned)((n_lines + TC_M - 1) / TC_M), 2);
         k_hilbert_tc<<<grid, TC_THREADS, smem, s>>>(p, n_lines, nstage);
-        return;
+        return 0;
     }
     const int tpl = 2 * (((p.nc + 1) / 2 + HR - 1) / HR);
     const int lpb = tpl >= 256 ? 1 : 256 / tpl;
     const int64_t n_lines = (int64_t)p.n_views * p.npsi;
     size_t smem = sizeof(float) * (2 * (size_t)p.nc - 1 + 2 * (2 * HR + 4) + (size_t)lpb * p.nc);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_hilbert, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+    smem_opt_in((const void *)k_hilbert, 200 * 1024);
     const int threads = ((lpb * tpl + 31) / 32) * 32;
     k_hilbert<<<(unsigned)((n_lines + lpb - 1) / lpb), threads, smem, s>>>(p, n_lines, lpb);
+    return 0;
 }
 
 template <int VPB>
@@ -1279,11 +1258,7 @@ static void launch_k4(const FilterParams &p, cudaStream_t s)
 {
     dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, (p.n_views + VPB - 1) / VPB);
     size_t smem = sizeof(float) * VPB * (size_t)(p.nr + 3) * (K4_COLS + 1);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_bwd_rebin_cos<VPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+    smem_opt_in((const void *)k_bwd_rebin_cos<VPB>, 200 * 1024);
     k_bwd_rebin_cos<VPB><<<grid, 256, smem, s>>>(p);
 }
 
@@ -1406,27 +1381,29 @@ __global__ void __launch_bounds__(KT_THREADS) k_fwd_rebin_T(FilterParams p, floa
 
 // raw view v (absolute u0 - 1 .. u0 + nu) <- g1^T of filtered views v-1, v, v+1 (those in [u0, u0+nu))
 __global__ void __launch_bounds__(128) k_deriv_T(FilterParams p, const float *__restrict__ g1T, int64_t nu,
-                                                 float *__restrict__ out)
+                                                 int items, float *__restrict__ out)
 {
     const int l = blockIdx.x * blockDim.x + threadIdx.x, m = blockIdx.y;
-    const int64_t per = nu + 2;                                   // raw views of an item (slab of a batch)
-    const int64_t item = blockIdx.z / per, vr = blockIdx.z - item * per;   // raw view - (u0 - 1)
     if (l >= p.nc) return;
+    const int64_t per = nu + 2;                                   // raw views of an item (slab of a batch)
     const int nc = p.nc;
     const size_t rs = (size_t)p.nr * nc;
-    g1T += (size_t)item * nu * rs;                                // the stencils stay inside the item
-    out += (size_t)item * per * rs;
-    auto g = [&](int64_t f, int ll) -> float {                    // g1^T of filtered view f (relative to u0)
-        return (f >= 0 && f < nu) ? g1T[(size_t)f * rs + (size_t)m * nc + ll] : 0.f;
-    };
-    const int64_t f = vr - 1;                                     // this raw view as a filtered view
-    float acc = (g(f - 1, l) - g(f + 1, l)) * p.inv_2dlam;        // view stencil (g(v+1) - g(v-1)) / 2Δλ
-    // α stencil of the same view: centred inside, one-sided at both edges
-    if (l == 0) acc -= g(f, 0) * p.inv_dalpha;
-    if (l == nc - 1) acc += g(f, nc - 1) * p.inv_dalpha;
-    if (l >= 1) acc += g(f, l - 1) * (l - 1 == 0 ? p.inv_dalpha : p.inv_2dalpha);
-    if (l + 1 <= nc - 1) acc -= g(f, l + 1) * (l + 1 == nc - 1 ? p.inv_dalpha : p.inv_2dalpha);
-    out[(size_t)vr * rs + (size_t)m * nc + l] = acc;
+    // grid.z (<= 65535) strides over the items' raw views
+    for (int64_t z = blockIdx.z; z < per * items; z += gridDim.z) {
+        const int64_t item = z / per, vr = z - item * per;       // raw view - (u0 - 1)
+        const float *gi = g1T + (size_t)item * nu * rs;           // the stencils stay inside the item
+        auto g = [&](int64_t f, int ll) -> float {                // g1^T of filtered view f (relative to u0)
+            return (f >= 0 && f < nu) ? gi[(size_t)f * rs + (size_t)m * nc + ll] : 0.f;
+        };
+        const int64_t f = vr - 1;                                 // this raw view as a filtered view
+        float acc = (g(f - 1, l) - g(f + 1, l)) * p.inv_2dlam;    // view stencil (g(v+1) - g(v-1)) / 2Δλ
+        // α stencil of the same view: centred inside, one-sided at both edges
+        if (l == 0) acc -= g(f, 0) * p.inv_dalpha;
+        if (l == nc - 1) acc += g(f, nc - 1) * p.inv_dalpha;
+        if (l >= 1) acc += g(f, l - 1) * (l - 1 == 0 ? p.inv_dalpha : p.inv_2dalpha);
+        if (l + 1 <= nc - 1) acc -= g(f, l + 1) * (l + 1 == nc - 1 ? p.inv_dalpha : p.inv_2dalpha);
+        out[((size_t)item * per + vr) * rs + (size_t)m * nc + l] = acc;
+    }
 }
 
 void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s)
@@ -1441,13 +1418,15 @@ void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_
 
 void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s)
 {
+    smem_opt_in((const void *)k_fwd_rebin_T, sizeof(float) * p.nr * KT_THREADS);
     k_fwd_rebin_T<<<dim3((p.nc + KT_THREADS - 1) / KT_THREADS, p.n_views), KT_THREADS,
                     sizeof(float) * p.nr * KT_THREADS, s>>>(p, g1T);
 }
 
 void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s, int items)
 {
-    k_deriv_T<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)((nu + 2) * items)), 128, 0, s>>>(p, g1T, nu, out);
+    const int64_t nz = std::min<int64_t>((nu + 2) * items, 65535);
+    k_deriv_T<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)nz), 128, 0, s>>>(p, g1T, nu, items, out);
 }
 
 }  // namespace kats

@@ -8,6 +8,11 @@
 
 namespace kats {
 
+// Runtime helpers (api.cu).  Both act on the current device (the plan's: every entry point calls
+// cudaSetDevice first) and are thread-safe.
+cudaError_t smem_opt_in(const void *kernel, size_t bytes);   // dynamic shared-memory opt-in, once per device
+int device_sms();                                            // multiprocessor count of the current device
+
 // Filter steps 1-6 over `n_views` consecutive views.
 struct FilterParams {
     const float *sino;        // raw data of filtered view g = view0 + v at sino + raw(g) * rows*cols, raw(g) = g (+ 2 per
@@ -35,7 +40,7 @@ struct FilterParams {
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
-void launch_hilbert(const FilterParams &p, cudaStream_t s);           // K3:  Eq. 12
+int launch_hilbert(const FilterParams &p, cudaStream_t s);            // K3:  Eq. 12 (-1: input tensor map failed)
 bool hilbert_split_input(const FilterParams &p);                      // the K3 launch_hilbert picks reads split lines
 inline int g3_half_pitch(int nc) { return ((nc + 1) / 2 + 3) & ~3; }
 inline int g3_line_pitch(int nc) { return 2 * g3_half_pitch(nc); }   // >= nc; scratch line pitch
@@ -89,6 +94,7 @@ struct BPParams {
     int q_lo;                 // first staged quad row (interior samples reach quad rows q_lo ..)
     int box_w[3];             // staged box widths (columns): full, and two narrower classes (set by the launcher)
     int adj_nqp;              // adjoint: quad-row pitch of a box column in shared memory (set by the launcher)
+    bool adj_fixed_ok;        // adjoint: the int32 fixed-point box cannot overflow (<= 2^10 contributions per cell)
     int ends_pre;             // staged kernels: end views written ahead into vol by k_bp_ends (launcher)
     const int *tile_order;    // staged kernels: 16x16 column tiles heaviest first (ty * ntx + tx), or null
     int bp_items;             // window kernel: batch items per CTA (1 or 2; set by the launcher)

@@ -29,7 +29,7 @@ def _samples(cfg, n, seed, slices=None):
     t = np.linspace(0, 2 * np.pi, 48, endpoint=False)
     r = 0.5 * min(nx, ny) - 1
     rim = np.stack([(nx / 2 + r * np.cos(t)).astype(int), (ny / 2 + r * np.sin(t)).astype(int)], 1)
-    zs = [0, nz - 1] if slices is None else [slices[0], slices[-1]]
+    zs = [0, nz - 1] if slices is None else list(slices)
     for z in zs:
         idx.append(np.concatenate([rim, np.full((len(rim), 1), z)], 1))
         idx.append(np.array([[0, 0, z], [nx - 1, 0, z], [0, ny - 1, z], [nx - 1, ny - 1, z]]))
@@ -119,7 +119,10 @@ def test_c2_sampled():
         _check(g[idx[:, 2], idx[:, 1], idx[:, 0]].astype(np.float64), ref, contrast)
 
 
-def test_c3_one_slice_sampled():
+def test_c3_edge_and_mid_slices_sampled():
+    """C3 (one pitch, the one-view TMEM kernel with end views written ahead): the first two and
+    last two slices — where the fractional end weights and the window flush edges live — and a
+    mid slice, each with random voxels plus the FOV rim and the grid corners."""
     import torch
     import paper_2201_02309_b200 as k
     from synth import configs, synth
@@ -130,7 +133,8 @@ def test_c3_one_slice_sampled():
     sino = synth.project(cfg, cfg["phantom"], v0, nv)
     vol = p.reconstruct(torch.from_numpy(sino).cuda(), v0, 0, 1)
     torch.cuda.synchronize()
-    idx = _samples(cfg, 300, 30, slices=[40])       # one slice: the oracle filters ~700 views
+    # the oracle filters the union of the sampled voxels' PI windows (~the whole slab)
+    idx = _samples(cfg, 500, 30, slices=[0, 1, 31, 62, 63])
     ref = _oracle_voxels(cfg, sino, v0, 0, idx)
     g = vol.cpu().numpy()
     _check(g[idx[:, 2], idx[:, 1], idx[:, 0]].astype(np.float64), ref, _truth_contrast(cfg, cfg["phantom"], [0]))

@@ -292,3 +292,18 @@ def test_k4_views_per_cta_match_oracle(name, vpb, monkeypatch):
     got = out["gF"].cpu().numpy().astype(np.float64)
     assert np.linalg.norm(got - gref) / np.linalg.norm(gref) <= STAGE_REL
     _check(vol.cpu().numpy(), ref, contrast)
+
+
+def test_registration_case_matches_oracle():
+    """The oracle's registration pin (tests/test_oracle_recon.py: off-centre ~3-voxel ball,
+    λ0, z0 ≠ 0, centroid within 0.05 voxel) on the GPU: whole volume within the parity bar, and
+    the GPU reconstruction's own centroid within 0.05 voxel of the true centre."""
+    import torch
+    from oracle import oracle
+    from tests.test_oracle_recon import _centroid_error, _registration_case
+    cfg, c, sino, v0 = _registration_case()
+    ref = oracle.reconstruct(cfg, sino, v0, 0, 1)
+    p = _plan(cfg)
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), v0, 0, 1).cpu().numpy().astype(np.float64)
+    _check(vol, ref, 1.0)
+    assert np.abs(_centroid_error(vol, cfg, c)).max() < 0.05

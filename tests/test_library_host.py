@@ -66,6 +66,35 @@ def test_host_tables_bit_exact_vs_oracle(name):
     assert p.pitch_views(5) == (fv + 5 * vt, nv)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name,pitch", [("C2", 1), ("C3", 0), ("C4", 7), ("C5", 0)])
+def test_host_tables_bit_exact_full_configs(name, pitch):
+    """North-star acceptance criterion 1 at the bench sizes (SURVEY §8(c) acceptance; PAPER.md
+    l.191-231 precompute steps 1-3): the product's PI-limits (T_pi k_first/k_last), forward and
+    backward rebin indices (T_fr, T_br) are bit-exact against the oracle's independent solvers on
+    the FULL C2, C3, C4 grids and the real C5 256x256x10 grid; end weights and fractions to 1e-9.
+    The oracle recomputes pitch `pitch` at absolute coordinates (no periodic reuse: C4 pitch 7 is
+    the last pitch the bench reconstructs, C2 pitch 1 its second), so this also checks the
+    periodic table against per-pitch recomputation at full size."""
+    from oracle import oracle
+    cfg = configs.get(name)
+    p = k.Plan(cfg, device=-1)
+    p.precompute()
+    t = p.export_tables()
+    fi, ff, bi, bf = oracle.rebin_tables(cfg)
+    assert np.array_equal(fi, t["fr_idx"]) and np.array_equal(bi, t["br_idx"])
+    assert np.abs(ff - t["fr_frac"]).max() < 1e-9 and np.abs(bf - t["br_frac"]).max() < 1e-9
+    del fi, ff, bi, bf
+    kf, kl, wf, wl = oracle.bp_weights(cfg, pitch)
+    shift = pitch * cfg["views_per_turn"]
+    m = kl >= kf
+    assert m.sum() > 0.7 * m.size                              # the FOV covers most of the grid
+    assert np.array_equal(np.where(m, kf - shift, 0), t["pi_first"])
+    assert np.array_equal(np.where(m, kl - shift, -1), t["pi_last"])
+    assert np.abs(np.where(m, wf, 0.0) - np.where(m, t["w_first"], 0.0)).max() < 1e-9
+    assert np.abs(np.where(m, wl, 0.0) - np.where(m, t["w_last"], 0.0)).max() < 1e-9
+
+
 def test_paper_layout_slab_and_td_coverage():
     """C5 (the paper's layout, zero-margin detector): no TD warning; slab [-125, 454]
     (SURVEY: BP views [-124, 453] + derivative halo)."""

@@ -207,3 +207,29 @@ def test_backward_rebin_of_constant_lines_returns_constant():
     assert np.abs(g4 - g4[0][None, :]).max() < 1e-9 * np.abs(g4).max()
     want = np.where(bi >= 0, np.cos(al)[None, :] * g4[0][None, :], 0.0)
     assert np.abs(gF - want).max() < 1e-9 * np.abs(g4).max()
+
+
+def test_post_cosine_golden_value():
+    """Step 6 (Eq. 15, g^F = cos α · g5) at the paper's half fan angle α = 19.4808° (P:l.322):
+    with constant κ-lines (view trick) g5 = g4, so gF / g4 at a column placed at that angle is
+    the golden post-cosine weight 0.94276 (tests/golden/paper_numbers.json)."""
+    gold = GOLD["post_cosine"]
+    a_m = math.radians(gold["alpha_deg"])
+    # paper layout (R, D as its numbers need, reading A1), rows tall enough that every κ-line sample
+    # is on the detector (so the κ-lines stay constant); 41 columns, the last one at α = 19.4808°
+    cfg = _cfg(R=1085.6, D=595.0, P=7 * math.pi, n_rows=16, d_w=1.0, n_cols=41, d_alpha=a_m / 20,
+               alpha_offset=0.0, r_fov=math.sqrt(2) * 256.0)
+    al, w = _grid(cfg)
+    assert abs(al[-1] - a_m) < 1e-15
+    rng = np.random.default_rng(11)
+    H = 1.0 + rng.random(cfg["n_cols"])
+    cw = np.sqrt(cfg["D"] ** 2 + w ** 2) / cfg["D"]
+    g = _view_trick_sino(cfg, cw, H).astype(np.float32)
+    out = oracle.filter_views(cfg, g, -1, 0, 1, stages=("g4", "gF"))
+    g4, gF = out["g4"][0], out["gF"][0]
+    _, _, bi, _ = oracle.rebin_tables(cfg)
+    assert np.abs(g4 - g4[0][None, :]).max() < 1e-6 * np.abs(g4).max()     # fp32 input rounding
+    rows = np.nonzero(bi[:, -1] >= 0)[0]
+    assert rows.size >= 4
+    ratio = gF[rows, -1] / g4[0, -1]
+    assert np.abs(ratio - gold["value"]).max() < gold["tol"]
