@@ -8,13 +8,18 @@ quoted on).  One step = one full reconstruction of the rank's pitches
 (filter steps 1-6 on every needed view + PI-limited backprojection of every
 pitch), inputs already resident in HBM.
 
-Multi-GPU (torchrun): pitch sharding, weak scaling — rank r reconstructs its
-own 8 pitches [8r, 8r+8) of an (8N)-pitch scan from its own view range; no
-collective on the data path.  `--gather` adds the NCCL
-gather of the volume slabs to rank 0 inside the timed region.
+Multi-GPU (torchrun): the C4 scan's 8 pitches split across the
+N ranks (strong scaling): rank r reconstructs pitches [8r/N, 8(r+1)/N) from
+the views they need (its pitches plus the PI-window overlap) and NCCL gathers
+the volume slabs to rank 0 INSIDE the timed region, point to point, per pitch
+group: the send of group i overlaps the backprojection of group i+1
+(katsevich_reconstruct_grouped marks each group with a CUDA event).  The
+compute-only time (no gather) is reported beside it.  `--scaling weak`: every
+rank reconstructs its own 8 pitches of an 8N-pitch scan, no collective.
 
-`--impl reference`: the CPU oracle (oracle/) timed on the host cores on a
-bounded sample of the same workload, extrapolated to the same metric.
+`--impl reference`: the CPU oracle (oracle/) timed on the host cores, each step
+one whole slice of the workload (every voxel of the slice and the filtering of
+every view its PI windows need), measured, not extrapolated.
 """
 from __future__ import annotations
 
@@ -152,13 +157,16 @@ def n_filtered_views(plan, cfg, n_items, batch):
 
 
 def filter_stage_rooflines(plan, cfg, stats, steps, nu, hbm_peak):
-    """Achieved GB/s of each filter stage's ALGORITHMIC HBM bytes (each input read once, each output
-    written once; g3/g4 of a 256-view chunk may in fact stay in L2) against the HBM peak."""
+    """Achieved GB/s of each filter stage's ALGORITHMIC HBM bytes as SURVEY §8(d) counts them (each
+    input read once, each output written once, 4 B per fp32 element: K12 reads the raw views and
+    writes g3, K3 reads g3 and writes g4, K4 reads g4 and writes gF) against the HBM peak.  K4 in
+    fact writes gF as 2x2 tap quads (16 B per (row + 2, column)): those bytes are
+    reported beside, not counted."""
     npsi = plan.table_info()["n_psi"]
     nr, nc = cfg["n_rows"], cfg["n_cols"]
     by = {"K12_deriv_fwd_rebin": 4.0 * (nu + 2) * nr * nc + 4.0 * nu * npsi * nc,
           "K3_hilbert": 8.0 * nu * npsi * nc,
-          "K4_bwd_rebin_cos": 4.0 * nu * npsi * nc + 16.0 * nu * nc * (nr + 2)}
+          "K4_bwd_rebin_cos": 4.0 * nu * npsi * nc + 4.0 * nu * nr * nc}
     out = {}
     for k, b in by.items():
         ms = stats["busy_ms"].get(k, 0.0) / steps
@@ -166,6 +174,8 @@ def filter_stage_rooflines(plan, cfg, stats, steps, nu, hbm_peak):
             gbs = b / (ms * 1e-3) / 1e9
             out[k] = {"ms_per_step": ms, "algorithmic_bytes": b, "achieved_gbs": gbs, "hbm_peak_gbs": hbm_peak,
                       "frac": gbs / hbm_peak}
+    if "K4_bwd_rebin_cos" in out:
+        out["K4_bwd_rebin_cos"]["quad_bytes_written"] = 16.0 * nu * nc * (nr + 2)
     return out
 
 
@@ -207,6 +217,8 @@ def run_ours(args):
     vt = cfg["views_per_turn"]
 
     # ---- inputs (seeded, synthetic; generated on the host, moved to HBM before timing) ----
+    from paper_2201_02309_b200 import dist as kd
+    gather = False
     if batch:
         from synth import configs
         v0, nv = plan.pitch_views(0)
@@ -215,36 +227,81 @@ def run_ours(args):
         first_pitch, n_items = 0, batch
     else:
         if args.scaling == "weak":
-            first_pitch = rank * pitches
-        else:  # strong: the config's pitches split across ranks
-            per = math.ceil(pitches / world)
-            first_pitch = rank * per
-            pitches = max(0, min(per, cfg["n_pitches"] - first_pitch))
+            shards = [kd.weak_shard(pitches, r) for r in range(world)]
+        else:  # strong (default): the config's pitches split [P r / N, P (r+1) / N)
+            shards = kd.pitch_shards(cfg["n_pitches"], world)
+        me = shards[rank]
+        first_pitch, pitches = me.first_pitch, me.n_pitches
+        if pitches < 1:
+            raise SystemExit(f"rank {rank}: no pitch to reconstruct ({cfg['n_pitches']} pitches over {world} ranks)")
         v0, nv = plan.scan_views(first_pitch, pitches)
         host_in = synth.project(cfg, rank_phantom(cfg, first_pitch - (first_pitch % cfg["n_pitches"])), v0, nv)
         n_items = pitches
+        gather = world > 1 and args.scaling == "strong" and not args.no_gather
     dev_in = torch.from_numpy(host_in).to(dev)
     vol_shape = (n_items * cfg["nz"], cfg["ny"], cfg["nx"]) if not batch else (batch, cfg["nz"], cfg["ny"], cfg["nx"])
-    out = torch.empty(vol_shape, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    groups, gobj, full, evs, side = 1, None, None, None, None
+    if gather:
+        # rank 0 owns the whole volume and reconstructs its own pitches straight into its slice;
+        # the others send each pitch group as soon as its backprojection is done
+        groups = max(1, min(args.gather_groups, pitches))
+        gobj = kd.SlabGather(shards, cfg["nz"], parts=groups)
+        if rank == 0:
+            full = torch.empty((cfg["n_pitches"] * cfg["nz"], cfg["ny"], cfg["nx"]), dtype=torch.float32, device=dev)
+            out = full[gobj.rows(me)]
+        else:
+            out = torch.empty(vol_shape, dtype=torch.float32, device=dev)
+        evs = [torch.cuda.Event() for _ in range(groups)]
+        for e in evs:
+            e.record(stream)                  # creates the events (handles for the C ABI)
+        side = torch.cuda.Stream(dev)
+    else:
+        out = torch.empty(vol_shape, dtype=torch.float32, device=dev)
 
-    def step():
+    def step(with_gather=True):
         if batch:
             plan.reconstruct_batch(dev_in, out=out, stream=stream)
-        else:
+            return
+        if not (gather and with_gather):
             plan.reconstruct(dev_in, v0, first_pitch, pitches, out=out, stream=stream)
+            return
+        works = gobj.post_recvs(full) if rank == 0 else []
+        plan.reconstruct_grouped(dev_in, v0, first_pitch, pitches, groups, group_events=evs, out=out, stream=stream)
+        if rank != 0:
+            for i in range(groups):
+                with torch.cuda.stream(side):          # the send of group i waits for group i only
+                    side.wait_event(evs[i])
+                    works.append(gobj.send(rank, i, out[gobj.local_rows(rank, i)]))
+        for w in works:
+            w.wait()                                   # the caller's stream waits for the transfers
 
-    gather_buf = None
-    if args.gather and world > 1:
-        gather_buf = [torch.empty_like(out) for _ in range(world)] if rank == 0 else None
-
-    def maybe_gather():
-        if args.gather and world > 1:
-            dist.gather(out, gather_buf, dst=0)
+    def timed_loop(n, with_gather=True):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            step(with_gather)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)     # max over ranks
+            t = float(tt.item())
+        return t
 
     for _ in range(args.warmup):
-        step(); maybe_gather()
+        step()
     torch.cuda.synchronize()
+    compute_only_ms = None
+    if gather:
+        for _ in range(max(1, args.warmup // 2)):
+            step(False)
+        compute_only_ms = timed_loop(args.steps, False) / args.steps
     plan.profile_read(reset=True)
     plan.profile_enable(True)
     if world > 1:
@@ -253,23 +310,10 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step(); maybe_gather()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms = timed_loop(args.steps)
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
     stats = plan.profile_read(reset=True)
     plan.profile_enable(False)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        if world > 1:
-            dist.barrier()
     ms_step = ms / args.steps
 
     # ---- K5 in isolation: the same step with one backprojection launch over all of the rank's
@@ -386,14 +430,19 @@ def run_ours(args):
                           "what": "alpha stride 4 + 'Gaussian+Poisson' (I0 1e5, var 0.5), Philox4x32-10"}}
         del sino_g, sino_v
 
+    items_all, launches_all = n_items, stats["total_launches"]
+    if world > 1:
+        tt = torch.tensor([n_items, launches_all], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        items_all, launches_all = int(tt[0].item()), int(tt[1].item())
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     U_pitch = count_updates(plan)
     U_rank = U_pitch * n_items
-    U_all = U_rank * world
-    vols_all = (n_items * world) / (cfg["n_pitches"] if not batch else batch)
+    U_all = U_pitch * items_all                    # units every rank processed
+    vols_all = items_all / (cfg["n_pitches"] if not batch else batch)
     value = U_all / (ms_step * 1e-3)
     # roofline of the dominant kernel (K5 backprojection), CUDA events recorded by the library on
     # the launching streams. Per-pitch K5 launches run on two alternating streams and overlap, so
@@ -425,12 +474,19 @@ def run_ours(args):
         "config": {"workload": f"{cfg['name']}: {cfg['desc']}", "volume_xyz": [cfg["nx"], cfg["ny"], cfg["nz"] * cfg["n_pitches"]],
                    "detector": [cfg["n_rows"], cfg["n_cols"]], "views_per_turn": vt,
                    "scan_views_per_rank": int(host_in.shape[0]) if not batch else int(host_in.shape[1]),
-                   "pitches_per_rank": n_items, "parallelism": f"pitch-sharded x{world}",
+                   "pitches_per_rank": n_items,
+                   "parallelism": (f"pitch-sharded x{world}" + (f", NCCL point-to-point gather of the volume slabs to "
+                                   f"rank 0 inside the timed region ({groups} overlapped pitch groups per rank)"
+                                   if gather else "")) if not batch else f"batch replicas x{world}",
                    "l2": "inputs larger than L2 (scan %.0f MB, filtered views %.0f MB > 126 MB L2)" % (
-                       host_in.nbytes / 1e6, host_in.nbytes / 1e6)},
+                       host_in.nbytes / 1e6,
+                       16.0 * n_filtered_views(plan, cfg, n_items, batch) * cfg["n_cols"] * (cfg["n_rows"] + 2) / 1e6)},
         "volumes_per_s": vols_all / (ms_step * 1e-3),
         "updates_per_step": U_all,
-        "gpu_launches": stats["total_launches"],
+        "compute_only": None if compute_only_ms is None else {
+            "ms_per_step": compute_only_ms, "value": U_all / (compute_only_ms * 1e-3), "unit": "updates/s",
+            "note": "the same step without the gather (max over ranks)"},
+        "gpu_launches": launches_all,
         "stage_busy_share_of_step": share,
         "filter_stages": filter_stage_rooflines(plan, cfg, stats, args.steps, n_filtered_views(plan, cfg, n_items, batch),
                                                 peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])),
@@ -480,79 +536,121 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-# --- CPU oracle timing (bounded sample, extrapolated) -----------------------
-def _oracle_sample(cfg, seed=0, n_b=32768):
-    """Time the oracle on a bounded sample of one pitch of `cfg`:
-    (a) steps 1-6 on 132 views minus the separately timed rebin-map setup
-    the oracle runs in each call, (b) step 7 on n_b
-    uniformly sampled voxels of the pitch (random filtered data).  The pitch's
-    update count and slab length are estimated from the same sample."""
-    from oracle import oracle
-    from synth import synth
-    rng = np.random.default_rng(seed)
-    t0 = time.perf_counter()
-    oracle.rebin_tables(cfg)                      # the oracle's per-call setup inside filter_views
-    t_setup = time.perf_counter() - t0
-    n_f = 132
-    raw = synth.random_array((n_f + 2, cfg["n_rows"], cfg["n_cols"]), seed)
-    t0 = time.perf_counter()
-    oracle.filter_views(cfg, raw, 0, 1, n_f)
-    t_f = max(1e-12, (time.perf_counter() - t0 - t_setup) / n_f)
-    idx = np.stack([rng.integers(0, cfg["nx"], n_b), rng.integers(0, cfg["ny"], n_b),
-                    rng.integers(0, cfg["nz"], n_b)], 1)
-    kf, kl, _, _ = oracle.bp_weights_voxels(cfg, 0, idx)
-    m = kl >= kf
-    k_lo, k_hi = int(kf[m].min()), int(kl[m].max())
-    u = np.where(m, kl - kf + 1, 0)
-    gF = rng.standard_normal((k_hi - k_lo + 1, cfg["n_rows"], cfg["n_cols"]))
-    t0 = time.perf_counter()
-    oracle.backproject_voxels(cfg, 0, gF, k_lo, idx)
-    t_b = time.perf_counter() - t0
-    u_s = int(u.sum())
-    t_u = t_b / max(1, u_s)
-    n_vox = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    return dict(t_f=t_f, t_setup=t_setup, t_u=t_u, U_pitch=int(u.mean() * n_vox), nbp=k_hi - k_lo + 1,
-                sample=f"steps 1-6 on {n_f} views and step 7 on {n_b} uniformly sampled voxels ({u_s} updates) of pitch 0")
+# --- CPU oracle timing (measured on bounded samples, no extrapolation) -------
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
 
 
-def _extrapolate(cfg, s):
-    n_p = cfg["n_pitches"] if not cfg.get("batch") else cfg["batch"]
-    # the oracle filters each pitch's slab (no filter-once) and backprojects every voxel
-    t_total = s["t_setup"] + n_p * (s["nbp"] * s["t_f"] + s["U_pitch"] * s["t_u"])
-    return n_p * s["U_pitch"] / t_total, t_total, n_p
+class OracleSlice:
+    """One whole slice of the workload as the oracle's unit of timed work: every voxel of slice j
+    of pitch 0 (step 7 over each voxel's PI window) and steps 1-6 on every view those windows
+    need, from seeded random data of the workload's shape.  The oracle's per-geometry filter set-up
+    (Hilbert kernel, rebin maps) is built once outside the timed calls (oracle.PreparedFilter)."""
+
+    def __init__(self, cfg):
+        from oracle import oracle
+        self.cfg = cfg
+        t0 = time.perf_counter()
+        self.filt = oracle.PreparedFilter(cfg)
+        self.t_filter_setup = time.perf_counter() - t0
+
+    def run(self, j, seed=0):
+        from oracle import oracle
+        from synth import synth
+        cfg = self.cfg
+        nx, ny = cfg["nx"], cfg["ny"]
+        iy, ix = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        idx = np.stack([ix.ravel(), iy.ravel(), np.full(nx * ny, j)], 1).astype(np.int32)
+        kf, kl, _, _ = oracle.bp_weights_voxels(cfg, 0, idx)      # tables: not timed (precompute)
+        m = kl >= kf
+        lo, hi = int(kf[m].min()), int(kl[m].max())
+        n = hi - lo + 1
+        raw = synth.random_array((n + 2, cfg["n_rows"], cfg["n_cols"]), seed)
+        t0 = time.perf_counter()
+        gF = self.filt.gF(raw, lo - 1, lo, n)
+        t_f = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.backproject_voxels(cfg, 0, gF, lo, idx)
+        t_b = time.perf_counter() - t0
+        return dict(updates=int(np.where(m, kl - kf + 1, 0).sum()), views=n, voxels=nx * ny, t_filter=t_f,
+                    t_bp=t_b, slice=j)
 
 
 def cpu_baseline(cfg):
-    s = _oracle_sample(cfg)
-    value, t_total, n_p = _extrapolate(cfg, s)
-    return {"value": value, "unit": "updates/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": s["sample"] + f"; extrapolated to {n_p} pitches x ({s['nbp']} views + {s['U_pitch']:.4g} updates)",
-            "seconds_per_view_filter": s["t_f"], "seconds_per_update": s["t_u"],
-            "extrapolated_seconds": t_total}
+    """The oracle (fp64, OpenMP) on this host, measured: (1) one whole slice of the workload —
+    every voxel and the filtering of every view it needs — the rate of the metric; (2) the
+    oracle's own precompute for one pitch (rebin maps + PI windows of every voxel, P:l.265
+    "implemented by the CPU"); (3) the whole C1 reconstruction (BASELINE configs[0], "CPU oracle
+    in seconds") single-thread and all-core."""
+    from oracle import oracle
+    from synth import configs, synth
+    oracle.set_threads(0)
+    threads = oracle.get_threads()
+    t0 = time.perf_counter()
+    oracle.rebin_tables(cfg)
+    oracle.bp_weights(cfg, 0)
+    t_pre = time.perf_counter() - t0
+    sl = OracleSlice(cfg)
+    r = sl.run(cfg["nz"] // 2)
+    t = r["t_filter"] + r["t_bp"]
+    c1 = configs.get("C1")
+    sino1 = synth.project(c1, c1["phantom"], c1["scan_v0"], c1["scan_nv"])
+    kf1, kl1, _, _ = oracle.bp_weights(c1, 0)
+    u1 = int(np.where(kl1 >= kf1, kl1 - kf1 + 1, 0).sum())
+    c1t = {}
+    for nt in (1, threads):
+        oracle.set_threads(nt)
+        t0 = time.perf_counter()
+        oracle.reconstruct(c1, sino1, c1["scan_v0"], 0, 1)
+        c1t[nt] = time.perf_counter() - t0
+    oracle.set_threads(0)
+    return {"value": r["updates"] / t, "unit": "updates/s", "cores": threads, "kind": "oracle",
+            "sample": (f"{cfg['name']} slice {r['slice']} of pitch 0, measured whole: all {r['voxels']} voxels "
+                       f"({r['updates']} voxel-view updates) + steps 1-6 on the {r['views']} views their PI "
+                       f"windows need; seeded random data, fp64, {threads} OpenMP threads"),
+            "seconds": t, "seconds_filter": r["t_filter"], "seconds_backprojection": r["t_bp"],
+            "seconds_per_view_filter": r["t_filter"] / r["views"], "seconds_per_update": r["t_bp"] / r["updates"],
+            "precompute_seconds": {"tables_one_pitch": t_pre, "filter_setup": sl.t_filter_setup,
+                                   "what": "oracle rebin maps + PI windows of every voxel of one pitch (bisection)"},
+            "c1_full_reconstruction_seconds": {"threads_1": c1t[1], f"threads_{threads}": c1t[threads],
+                                               "updates": u1,
+                                               "what": "whole C1 pitch (64^3, filter + backprojection) incl. the "
+                                                       "oracle's per-call rebin maps and PI windows"}}
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the CPU oracle, unmodified, timed on the
+    host cores.  Each step is one whole slice of the workload (OracleSlice, the slices taken in
+    turn), so a step is a bounded, fully measured piece of the same work; value = updates of the
+    K timed steps / their time."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import oracle
     cfg = workload(args.config)
-    samples = []
-    for i in range(args.warmup + args.steps):
-        s = _oracle_sample(cfg, seed=i, n_b=8192)
-        if i >= args.warmup:
-            samples.append(s)
-    s = dict(samples[0])
-    for key in ("t_f", "t_setup", "t_u"):
-        s[key] = float(np.median([x[key] for x in samples]))
-    value, t_total, n_p = _extrapolate(cfg, s)
+    oracle.set_threads(0)
+    threads = oracle.get_threads()
+    sl = OracleSlice(cfg)
+    nz = cfg["nz"]
+    for i in range(args.warmup):
+        sl.run((nz // 2 + i) % nz, seed=i)
+    runs = [sl.run((nz // 2 + args.warmup + i) % nz, seed=args.warmup + i) for i in range(args.steps)]
+    t = sum(r["t_filter"] + r["t_bp"] for r in runs)
+    upd = sum(r["updates"] for r in runs)
+    value = upd / t
     line = {"impl": "reference", "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_total * 1e3,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random arrays of the workload's shapes)",
-            "config": {"workload": f"{cfg['name']}: {cfg['desc']}"},
-            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": "per step: " + s["sample"] + "; median over steps, extrapolated"},
+            "config": {"workload": f"{cfg['name']}: {cfg['desc']}",
+                       "step": "one whole slice of pitch 0 (all its voxels + the filtering of the views they need)"},
+            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "oracle",
+                             "sample": f"per step one whole {cfg['name']} slice ({runs[0]['voxels']} voxels, "
+                                       f"~{upd // args.steps} updates, ~{runs[0]['views']} filtered views), measured"},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -564,12 +662,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--gather", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default): the config's pitches split over the ranks + NCCL gather to rank 0; "
+                         "weak: 8 pitches per rank of a longer scan, no collective")
+    ap.add_argument("--no-gather", action="store_true", help="strong scaling without the volume gather")
+    ap.add_argument("--gather-groups", type=int, default=2,
+                    help="pitch groups per rank whose sends overlap the next group's backprojection")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-adjoint", action="store_true", help="skip the adjoint (NEXT-1) measurement")
     ap.add_argument("--no-datagen", action="store_true", help="skip the data-generation (NEXT-3) measurement")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -123,6 +123,19 @@ int katsevich_reconstruct(katsevich_plan *plan, const float *sino, int64_t sino_
                           int32_t first_pitch, int32_t n_pitches, float *vol,
                           void *workspace, size_t workspace_bytes, void *cuda_stream);
 
+/* katsevich_reconstruct whose backprojection runs in n_groups launches over consecutive pitch
+ * groups (group i = pitches first_pitch + [n_pitches*i/n_groups, n_pitches*(i+1)/n_groups)), after
+ * one filter pass over the union of the views.  If group_done is not NULL, group_done[i] (a
+ * caller-created cudaEvent_t, or NULL to skip) is recorded on cuda_stream once group i's volume
+ * slices are written, so a consumer on another stream — e.g. the NCCL send of finished pitch slabs
+ * in a pitch-sharded run (SURVEY §8(e), P:l.246, l.265) — overlaps the remaining groups.
+ * Results equal katsevich_reconstruct's bit for bit.  1 <= n_groups <= n_pitches
+ * (KATS_ERR_ARGUMENT otherwise). */
+int katsevich_reconstruct_grouped(katsevich_plan *plan, const float *sino, int64_t sino_first_view,
+                                  int64_t sino_n_views, int32_t first_pitch, int32_t n_pitches, float *vol,
+                                  void *workspace, size_t workspace_bytes, void *cuda_stream,
+                                  int32_t n_groups, void **group_done);
+
 /* B independent one-pitch slabs (the network's embedded layer, P:l.284-286):
  * slabs [B][n_views][rows][cols] (device), each holding pitch 0's views
  * katsevich_pitch_views(plan, 0, ...); vols [B][nz][ny][nx] (device). */

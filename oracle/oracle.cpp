@@ -23,6 +23,7 @@
 #include <cstring>
 #include <vector>
 #include <algorithm>
+#include <omp.h>
 
 extern "C" {
 
@@ -622,21 +623,52 @@ void ora_pitch_slab(const ora_geom *g, int32_t pitch, int64_t *first_view, int64
 /* Filter views [v_first, v_first + n_out) of a sinogram whose first view is
  * s0 (needs views v_first-1 .. v_first+n_out).  Optional outputs (double):
  * g2 [n_out][rows][cols], g3/g4 [n_out][n_psi][cols], gF [n_out][rows][cols]. */
-int ora_filter(const ora_geom *g, const float *sino, int64_t s0, int64_t sn,
-               int64_t v_first, int64_t n_out, double *g2, double *g3, double *g4, double *gF)
+/* The filter's per-geometry set-up (Hilbert kernel, rebin maps), built once so
+ * bench.py's cpu_baseline can time steps 1-6 alone (test infrastructure: no
+ * arithmetic differs from ora_filter, which is prepare + run + free). */
+struct ora_filter_ctx { G o; std::vector<double> K; Rebin rb; };
+
+ora_filter_ctx *ora_filter_prepare(const ora_geom *g)
 {
-    G o = make(g);
+    ora_filter_ctx *c = new ora_filter_ctx;
+    c->o = make(g);
+    c->K = hilbert_kernel(c->o);
+    c->rb = rebin_maps(c->o);
+    return c;
+}
+
+void ora_filter_free(ora_filter_ctx *c) { delete c; }
+
+int ora_filter_run(const ora_filter_ctx *c, const float *sino, int64_t s0, int64_t sn,
+                   int64_t v_first, int64_t n_out, double *g2, double *g3, double *g4, double *gF)
+{
+    const G &o = c->o;
     if (v_first - 1 < s0 || v_first + n_out + 1 > s0 + sn) return -1;
-    std::vector<double> K = hilbert_kernel(o);
-    Rebin rb = rebin_maps(o);
-    const size_t rs = (size_t)g->n_rows * g->n_cols, ps = (size_t)o.n_psi * g->n_cols;
+    const size_t rs = (size_t)o.g.n_rows * o.g.n_cols, ps = (size_t)o.n_psi * o.g.n_cols;
     #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t i = 0; i < n_out; ++i)
-        filter_view(o, sino, s0, v_first + i, K, rb,
+        filter_view(o, sino, s0, v_first + i, c->K, c->rb,
                     g2 ? g2 + i * rs : nullptr, g3 ? g3 + i * ps : nullptr,
                     g4 ? g4 + i * ps : nullptr, gF ? gF + i * rs : nullptr);
     return 0;
 }
+
+/* Filter views [v_first, v_first + n_out) of a sinogram whose first view is
+ * s0 (needs views v_first-1 .. v_first+n_out).  Optional outputs (double):
+ * g2 [n_out][rows][cols], g3/g4 [n_out][n_psi][cols], gF [n_out][rows][cols]. */
+int ora_filter(const ora_geom *g, const float *sino, int64_t s0, int64_t sn,
+               int64_t v_first, int64_t n_out, double *g2, double *g3, double *g4, double *gF)
+{
+    if (v_first - 1 < s0 || v_first + n_out + 1 > s0 + sn) return -1;
+    ora_filter_ctx *c = ora_filter_prepare(g);
+    const int rc = ora_filter_run(c, sino, s0, sn, v_first, n_out, g2, g3, g4, gF);
+    ora_filter_free(c);
+    return rc;
+}
+
+/* OpenMP threads for the following oracle calls (bench.py: single-thread vs all-core timing). */
+void ora_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }
+int ora_get_threads(void) { return omp_get_max_threads(); }
 
 /* Backproject a full pitch volume [nz][ny][nx] from filtered views gF
  * (views gF0 .. gF0+gFn-1, absolute).  Returns 1 if some voxel's PI-window

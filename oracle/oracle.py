@@ -79,6 +79,12 @@ def lib():
             "ora_resample_alpha": (None, [_G, _D, ctypes.c_int64, ctypes.c_int32, _D]),
             "ora_add_noise": (ctypes.c_int, [_G, _D, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
                                              ctypes.c_double, ctypes.c_uint64, ctypes.c_int, _D, _I64, _D]),
+            "ora_filter_prepare": (ctypes.c_void_p, [_G]),
+            "ora_filter_free": (None, [ctypes.c_void_p]),
+            "ora_filter_run": (ctypes.c_int, [ctypes.c_void_p, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, _D, _D, _D, _D]),
+            "ora_set_threads": (None, [ctypes.c_int]),
+            "ora_get_threads": (ctypes.c_int, []),
             "ora_philox": (None, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                   ctypes.POINTER(ctypes.c_uint32)]),
         }
@@ -198,6 +204,40 @@ def filter_views(cfg, sino, s0, v_first, n_out, stages=("gF",)):
     if rc != 0:
         raise ValueError("oracle filter: sinogram does not cover the requested views")
     return out
+
+
+class PreparedFilter:
+    """Steps 1-6 with the per-geometry set-up (Hilbert kernel, rebin maps) built once, so that
+    bench.py can time the filter alone; the same arithmetic as filter_views."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        self._g = geom(cfg)
+        self._ctx = lib().ora_filter_prepare(ctypes.byref(self._g))
+
+    def gF(self, sino, s0, v_first, n_out):
+        nr, nc = self.cfg["n_rows"], self.cfg["n_cols"]
+        sino = np.ascontiguousarray(sino, dtype=np.float32)
+        out = np.empty((n_out, nr, nc))
+        rc = lib().ora_filter_run(self._ctx, _p(sino, _F), s0, sino.shape[0], v_first, n_out,
+                                  None, None, None, _p(out, _D))
+        if rc != 0:
+            raise ValueError("oracle filter: sinogram does not cover the requested views")
+        return out
+
+    def __del__(self):
+        if getattr(self, "_ctx", None):
+            lib().ora_filter_free(self._ctx)
+            self._ctx = None
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the following oracle calls (0: all processors)."""
+    lib().ora_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().ora_get_threads())
 
 
 def backproject(cfg, pitch, gF, gF0):

@@ -53,6 +53,8 @@ SIGNATURES = {
     "katsevich_workspace_bytes": (ctypes.c_int, [_P, _I32, _PSZ]),
     "katsevich_workspace_bytes_host": (ctypes.c_int, [_P, _I32, _PSZ]),
     "katsevich_reconstruct": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _SZ, _P]),
+    "katsevich_reconstruct_grouped": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _SZ, _P, _I32,
+                                                     ctypes.POINTER(ctypes.c_void_p)]),
     "katsevich_reconstruct_batch": (ctypes.c_int, [_P, _P, _I32, _P, _P, _SZ, _P]),
     "katsevich_reconstruct_host": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _SZ, _P]),
     "katsevich_filter": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I32, _P, _P, _P, _P]),

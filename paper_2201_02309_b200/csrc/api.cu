@@ -590,12 +590,21 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
                           int32_t first_pitch, int32_t n_pitches, float *vol,
                           void *workspace, size_t workspace_bytes, void *cuda_stream)
 {
+    return katsevich_reconstruct_grouped(p, sino, s0, sn, first_pitch, n_pitches, vol, workspace, workspace_bytes,
+                                         cuda_stream, 1, nullptr);
+}
+
+int katsevich_reconstruct_grouped(katsevich_plan *p, const float *sino, int64_t s0, int64_t sn,
+                                  int32_t first_pitch, int32_t n_pitches, float *vol,
+                                  void *workspace, size_t workspace_bytes, void *cuda_stream,
+                                  int32_t n_groups, void **group_done)
+{
     int rc = check_device_plan(p);
     if (rc) return rc;
     const int dm = device_chunk_mul();
     const int kFilterChunk = filter_chunk_views(p, dm);
     if (!sino || !vol || !workspace) return KATS_ERR_NULL;
-    if (n_pitches < 1 || sn < 3) return KATS_ERR_ARGUMENT;
+    if (n_pitches < 1 || sn < 3 || n_groups < 1 || n_groups > n_pitches) return KATS_ERR_ARGUMENT;
     size_t need;
     katsevich_workspace_bytes(p, n_pitches, &need);
     if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
@@ -618,19 +627,25 @@ int katsevich_reconstruct(katsevich_plan *p, const float *sino, int64_t s0, int6
     float4 *gq = (float4 *)workspace;
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * quad_view_elems(p) * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
     const char *pe = std::getenv("KATS_PIPELINE");
-    if (n_pitches == 1 || !(pe && pe[0] == '1')) {
-        // filter every needed view, then one backprojection launch over all pitches
+    if (n_pitches == 1 || n_groups > 1 || group_done || !(pe && pe[0] == '1')) {
+        // filter every needed view once, then one backprojection launch per pitch group (default: one
+        // group); group_done[i] marks the end of group i's launch on the caller's stream
         rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s, false, 0, true, dm);
         if (rc) return rc;
-        BPParams b = bp_params(p);
-        b.gq = gq;
-        b.gq_views = nu;
-        b.off0 = (int64_t)first_pitch * vt - u0;
-        b.item_views = vt;
-        b.n_items = n_pitches;
-        b.vol = vol;
-        { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
-        KCHECK(p, cudaGetLastError());
+        const size_t vpitch = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
+        for (int gi = 0; gi < n_groups; ++gi) {
+            const int a = (int)((int64_t)n_pitches * gi / n_groups), e = (int)((int64_t)n_pitches * (gi + 1) / n_groups);
+            BPParams b = bp_params(p);
+            b.gq = gq;
+            b.gq_views = nu;
+            b.off0 = (int64_t)(first_pitch + a) * vt - u0;
+            b.item_views = vt;
+            b.n_items = e - a;
+            b.vol = vol + (size_t)a * vpitch;
+            { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(b, s); }
+            KCHECK(p, cudaGetLastError());
+            if (group_done && group_done[gi]) KCHECK(p, cudaEventRecord((cudaEvent_t)group_done[gi], s));
+        }
         return KATS_OK;
     }
     // Pipelined (KATS_PIPELINE=1; worthwhile when filtering is a large share of the step): pitch k

@@ -81,6 +81,65 @@ def gather_volumes(local, shards, nz: int, dst: int = 0, group=None):
     return None
 
 
+def sub_blocks(shard: Shard, parts: int):
+    """Split a rank's pitch block into min(parts, n_pitches) contiguous sub-blocks, sub-block i =
+    pitches [n i / parts, n (i + 1) / parts) of the block — the pitch groups of
+    katsevich_reconstruct_grouped, and the unit of the overlapped gather (sub-block i travels while
+    sub-block i+1 is backprojected)."""
+    n = shard.n_pitches
+    g = max(1, min(parts, n))
+    return [Shard(shard.rank, shard.first_pitch + n * i // g, n * (i + 1) // g - n * i // g)
+            for i in range(g)] if n else []
+
+
+class SlabGather:
+    """Point-to-point gather of every rank's volume slabs into rank `dst`'s full volume
+    (NCCL carries only the gather of the pitch slabs), per sub-block so that
+    the transfer of a finished sub-block overlaps the reconstruction of the next one.
+
+    Every transfer is one isend/irecv pair between the owner and `dst` (the same pattern on both
+    sides, so NCCL uses the same two-rank communicator for the pair); `dst` writes its own
+    sub-blocks directly into its slice of `full` and receives the others there (no staging copy).
+    Usage per step:  works = g.post_recvs(full) on dst (its own sub-block i goes straight into
+    full[g.rows(g.blocks[dst][i])]); on the others, after sub-block i is reconstructed into
+    local[g.local_rows(rank, i)]:  works.append(g.send(rank, i, that slice)); finally
+    for w in works: w.wait()."""
+
+    def __init__(self, shards, nz: int, parts: int = 2, dst: int = 0, group=None):
+        self.shards = list(shards)
+        self.nz = nz
+        self.dst = dst
+        self.group = group
+        self.base = self.shards[0].first_pitch
+        self.blocks = [sub_blocks(s, parts) for s in self.shards]
+
+    def rows(self, block: Shard):
+        """Slice of the full (gathered) volume's slices holding `block`."""
+        a = (block.first_pitch - self.base) * self.nz
+        return slice(a, a + block.n_pitches * self.nz)
+
+    def local_rows(self, rank: int, i: int):
+        """Slice of rank `rank`'s own volume [n_pitches*nz] holding its sub-block i."""
+        b = self.blocks[rank][i]
+        a = (b.first_pitch - self.shards[rank].first_pitch) * self.nz
+        return slice(a, a + b.n_pitches * self.nz)
+
+    def post_recvs(self, full):
+        import torch.distributed as dist
+        works = []
+        for r, blocks in enumerate(self.blocks):
+            if r == self.dst:
+                continue
+            for b in blocks:
+                works.append(dist.irecv(full[self.rows(b)], src=r, group=self.group))
+        return works
+
+    def send(self, rank: int, i: int, tensor):
+        import torch.distributed as dist
+        assert rank != self.dst
+        return dist.isend(tensor, dst=self.dst, group=self.group)
+
+
 def check_view_ranges(view_ranges):
     """reduce_view_halos' precondition: increasing starts, overlaps only between neighbours."""
     starts = [v for v, n in view_ranges if n]

@@ -142,6 +142,27 @@ class Plan:
                                                 _stream_handle(stream)))
         return out
 
+    def reconstruct_grouped(self, sino, sino_first_view: int, first_pitch: int, n_pitches: int, groups: int,
+                            group_events=None, out=None, stream=None):
+        """katsevich_reconstruct_grouped: one filter pass, then the backprojection in `groups`
+        launches over consecutive pitch groups; group_events[i] (torch.cuda.Event, already
+        created) is recorded on `stream` when group i's slices are written."""
+        import torch
+        assert sino.is_cuda and sino.dtype == torch.float32 and sino.is_contiguous()
+        if out is None:
+            out = torch.empty(self._vol_shape(n_pitches), dtype=torch.float32, device=sino.device)
+        ws = self._workspace(self.workspace_bytes(n_pitches))
+        evs = None
+        if group_events is not None:
+            assert len(group_events) == groups
+            assert all(e is None or e.cuda_event for e in group_events), "record each event once to create it"
+            evs = (ctypes.c_void_p * groups)(*[ctypes.c_void_p(e.cuda_event) if e is not None else None
+                                               for e in group_events])
+        self._check(lib().katsevich_reconstruct_grouped(self._h, _ptr(sino), sino_first_view, sino.shape[0],
+                                                        first_pitch, n_pitches, _ptr(out), _ptr(ws), ws.numel(),
+                                                        _stream_handle(stream), groups, evs))
+        return out
+
     def reconstruct_batch(self, slabs, out=None, stream=None):
         """slabs: cuda float32 [B][n_views][rows][cols] of pitch-0 slabs."""
         import torch
