@@ -204,6 +204,64 @@ __global__ void __launch_bounds__(K12_THREADS) k_deriv_fwd_rebin_tile(FilterPara
     }
 }
 
+
+// Row form (default): a CTA = 8 warps on one 32-column block (lane = column) and a run of nvb
+// consecutive views.  Per view, the warps first form g2 = D/sqrt(D²+w²)·(∂_q + ∂_α)g of the block's
+// nr rows in shared memory (Eqs. 8-9; coalesced raw rows, the ±1-view and ±1-column stencil reads
+// hit L1/L2), then its npsi κ-line samples (Eqs. 10-11) from there, with the block's rebin entries
+// staged in shared memory once for all the CTA's views.  Warps walk rows / κ-lines, so no index
+// division; the g2 tile is double-buffered (one barrier per view).  Same fp32 arithmetic as g2_at.
+constexpr int K12R_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * K12R_WARPS) k_deriv_fwd_rebin_rows(FilterParams p, int nvb)
+{
+    extern __shared__ float k12s[];
+    const int nr = p.nr, nc = p.nc, npsi = p.npsi, rs = nr * nc;
+    float2 *tab = reinterpret_cast<float2 *>(k12s);                // [npsi][32]: (idx bits, frac)
+    float *g2s = k12s + 2 * npsi * 32;                              // [2][nr][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int l = blockIdx.x * 32 + lane;
+    const bool col_ok = l < nc;
+    const int lc = col_ok ? l : nc - 1;
+    const int lp = min(lc + 1, nc - 1), lm = max(lc - 1, 0);
+    const float sa = (lp - lm == 2) ? p.inv_2dalpha : p.inv_dalpha, sq = p.inv_2dlam;
+    for (int i = warp; i < npsi; i += K12R_WARPS) {
+        const RebinEntry e = p.fr[(size_t)i * nc + lc];
+        tab[i * 32 + lane] = make_float2(__int_as_float(e.idx), e.frac);
+    }
+    const int v0 = blockIdx.y * nvb, nv = min(nvb, p.n_views - v0);
+    const size_t pitch = p.k3_in_split ? (size_t)(2 * p.hp) : (size_t)nc;
+    const int co = p.k3_in_split ? (l & 1) * p.hp + (l >> 1) : l;
+    for (int j = 0; j < nv; ++j) {
+        const int64_t g = p.view0 + v0 + j;
+        const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+        const float *gv = p.sino + (size_t)raw * rs;
+        float *buf = g2s + (j & 1) * nr * 32;
+        for (int m = warp; m < nr; m += K12R_WARPS) {
+            const float *r = gv + (size_t)m * nc;
+            const float dq = (__ldg(r + lc + rs) - __ldg(r + lc - rs)) * sq;
+            const float da = (__ldg(r + lp) - __ldg(r + lm)) * sa;
+            buf[m * 32 + lane] = __ldg(p.wlen + m) * (dq + da);
+        }
+        // (view j+2 rewrites this buffer only after every thread passed view j+1's barrier, i.e.
+        // after its reads of view j below)
+        __syncthreads();
+        if (col_ok) {
+            float *out = p.g3 + (size_t)(v0 + j) * npsi * pitch + co;
+            for (int i = warp; i < npsi; i += K12R_WARPS) {
+                const float2 e = tab[i * 32 + lane];
+                const int ia = __float_as_int(e.x);
+                float o = 0.f;
+                if (ia >= 0) {
+                    const float a = buf[ia * 32 + lane], b = buf[(ia + 1) * 32 + lane];
+                    o = fmaf(e.y, b - a, a);
+                }
+                out[(size_t)i * pitch] = o;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: g4 = Σ_l' K[l-l'] g3[l'] along each κ-line (Eq. 12, h_H = 1/(πs) of
 //     Eq. e4, band-limited kernel of DESIGN.md reading A10: only odd
@@ -1063,6 +1121,72 @@ __global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
     }
 }
 
+
+// Row form (default): a CTA = 8 warps on one 32-column block (lane = column) and VPB views.  Phase 1:
+// warps walk the rows m = -2 .. nr of the [nr + 3][33] g5·cos α tile (the rebin entry and cos α
+// loaded once for the VPB views, their g4 gathers issued together); phase 2: the block's quads in
+// their global order (column-major, rows contiguous), the (column, quad row) of a thread advanced
+// incrementally — no index division in either loop.  Same fp32 arithmetic as k_bwd_rebin_cos.
+template <int VPB>
+__global__ void __launch_bounds__(256) k_bwd_rebin_cos_rows(FilterParams p)
+{
+    extern __shared__ float tile[];            // [VPB][nr + 3][33], rows m = -2 .. nr
+    const int nc = p.nc, nr = p.nr, nq = nr + 2, ld = K4_COLS + 1, tsz = (nr + 3) * ld;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int l0 = blockIdx.x * K4_COLS, v0 = blockIdx.y * VPB;
+    const int nv = min(VPB, p.n_views - v0);
+    const int cols = min(K4_COLS, nc - l0);
+    const size_t vs = (size_t)p.npsi * nc;
+    for (int mm = warp; mm < nr + 3; mm += 8) {
+        const int m = mm - 2;
+        for (int ll = lane; ll < ld; ll += 32) {
+            const int l = l0 + ll;
+            float out[VPB];
+#pragma unroll
+            for (int j = 0; j < VPB; ++j) out[j] = 0.f;
+            if (m >= 0 && m < nr && l < nc) {
+                const RebinEntry r = p.br[m * nc + l];
+                if (r.idx >= 0) {
+                    const float ca = __ldg(p.cos_alpha + l);
+                    const float *g = p.g4 + ((size_t)v0 * p.npsi + r.idx) * nc + l;
+                    float a[VPB], b[VPB];
+#pragma unroll
+                    for (int j = 0; j < VPB; ++j)
+                        if (j < nv) { a[j] = g[j * vs]; b[j] = g[j * vs + nc]; }
+#pragma unroll
+                    for (int j = 0; j < VPB; ++j)
+                        if (j < nv) out[j] = ca * fmaf(r.frac, b[j] - a[j], a[j]);
+                }
+                if (p.gF && ll < cols)
+#pragma unroll
+                    for (int j = 0; j < VPB; ++j)
+                        if (j < nv) p.gF[((size_t)(v0 + j) * nr + m) * nc + l] = out[j];
+            }
+#pragma unroll
+            for (int j = 0; j < VPB; ++j) tile[j * tsz + mm * ld + ll] = out[j];
+        }
+    }
+    __syncthreads();
+    const int per = cols * nq;
+    const int ll0 = tid / nq, r0 = tid - ll0 * nq, DL = 256 / nq, DR = 256 - DL * nq;
+    const float rcen = (float)((nr + 2) / 2);
+    for (int j = 0; j < nv; ++j) {
+        float4 *dst = p.gq + ((size_t)(v0 + j) * nc + l0) * nq;
+        const float *tj = tile + j * tsz;
+        int ll = ll0, r = r0;
+        for (int e = tid; e < per; e += 256) {
+            const float *t0 = tj + r * ld + ll;       // r = quad row; taps rows r-2, r-1
+            const float a0 = t0[0], a1 = t0[1], c0 = t0[ld], c1 = t0[ld + 1];
+            const float rc = (float)r - rcen;         // centred quad row
+            dst[e] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0,
+                                 c1 - a1);
+            ll += DL;
+            r += DR;
+            if (r >= nq) { r -= nq; ++ll; }
+        }
+    }
+}
+
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
 {
     // column walk, 8 κ-lines per thread (two-row g2 cache; measured best on every config: C4 1.69 ->
@@ -1070,6 +1194,19 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     // KATS_K12=sample: one thread per sample (8 κ-lines unrolled); colN: N κ-lines per thread
     const char *ke = std::getenv("KATS_K12");
     const std::string k12 = ke ? ke : "";
+    if (k12.empty() || k12 == "rows") {
+        // views per CTA: as many as keep >= 4 CTAs per SM in the launch (the block's rebin entries are
+        // staged once per CTA), at most 16
+        const int nb = (p.nc + 31) / 32;
+        int nvb = 16;
+        while (nvb > 1 && (int64_t)nb * ((p.n_views + nvb - 1) / nvb) < 4 * device_sms()) nvb /= 2;
+        const size_t smem = sizeof(float) * (2 * (size_t)p.npsi * 32 + 2 * (size_t)p.nr * 32);
+        if (smem <= 200 * 1024) {
+            smem_opt_in((const void *)k_deriv_fwd_rebin_rows, smem);
+            k_deriv_fwd_rebin_rows<<<dim3(nb, (p.n_views + nvb - 1) / nvb), 32 * K12R_WARPS, smem, s>>>(p, nvb);
+            return;
+        }
+    }
     if (k12 == "sample") {
         const int bx = std::min(256, (p.nc + 31) / 32 * 32);
         k_deriv_fwd_rebin<<<dim3((p.nc + bx - 1) / bx, (p.npsi + kPsiPer - 1) / kPsiPer, p.n_views), bx, 0, s>>>(p);
@@ -1080,9 +1217,9 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
         k_deriv_fwd_rebin_tile<<<dim3((p.nc + K12_TL - 1) / K12_TL, p.n_views), K12_THREADS, plane + K12_TL * sizeof(float), s>>>(p);
         return;
     }
-    // default: the column walk over two views per thread (scripts/ab/gpu_k12v.sh: C5 4.29 -> 4.22 ms,
-    // C3 9.30 -> 9.27, C2 / C4 unchanged; colv4 no better); "col8" = one view per thread
-    if (k12.empty() || k12 == "colv2" || k12 == "colv4") {
+    // round-1 default: the column walk over two views per thread (scripts/ab/gpu_k12v.sh: C5 4.29 ->
+    // 4.22 ms, C3 9.30 -> 9.27, C2 / C4 unchanged; colv4 no better); "col8" = one view per thread
+    if (k12.empty() || k12 == "rows" || k12 == "colv2" || k12 == "colv4") {
         if (k12 != "colv4") k_deriv_fwd_rebin_colv<2><<<dim3((p.nc + 127) / 128, (p.n_views + 1) / 2, (p.npsi + 7) / 8), 128, 0, s>>>(p, 8);
         else k_deriv_fwd_rebin_colv<4><<<dim3((p.nc + 127) / 128, (p.n_views + 3) / 4, (p.npsi + 7) / 8), 128, 0, s>>>(p, 8);
         return;
@@ -1258,6 +1395,12 @@ static void launch_k4(const FilterParams &p, cudaStream_t s)
 {
     dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, (p.n_views + VPB - 1) / VPB);
     size_t smem = sizeof(float) * VPB * (size_t)(p.nr + 3) * (K4_COLS + 1);
+    const char *ke = std::getenv("KATS_K4");                  // A/B: "tile" = the round-1 kernel
+    if (!(ke && std::string(ke) == "tile")) {
+        smem_opt_in((const void *)k_bwd_rebin_cos_rows<VPB>, smem);
+        k_bwd_rebin_cos_rows<VPB><<<grid, 256, smem, s>>>(p);
+        return;
+    }
     smem_opt_in((const void *)k_bwd_rebin_cos<VPB>, 200 * 1024);
     k_bwd_rebin_cos<VPB><<<grid, 256, smem, s>>>(p);
 }

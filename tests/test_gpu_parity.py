@@ -235,10 +235,10 @@ def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("k12", ["sample", "col3", "col8", "tile", "colv2", "colv4"])
+@pytest.mark.parametrize("k12", ["rows", "sample", "col3", "col8", "tile", "colv2", "colv4"])
 @pytest.mark.parametrize("name", ["T1", "C1"])
 def test_k12_variants_match_oracle(name, k12, monkeypatch):
-    """Steps 1-3 (g3) by the alternate K12 kernels: one thread per sample, the column walk
+    """Steps 1-3 (g3) by the K12 kernels: the row form (default), one thread per sample, the column walk
     with a ragged κ-line segment (3 lines per thread; the default walks 8), the shared-memory
     tile, and the column walk over 2 / 4 views per thread (ragged view tails)."""
     import torch
@@ -274,14 +274,16 @@ def test_reconstruct_n_psi_matches_oracle(name, n_psi):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
+@pytest.mark.parametrize("k4", ["rows", "tile"])
 @pytest.mark.parametrize("vpb", ["1", "2", "4"])
 @pytest.mark.parametrize("name", ["T1", "T3"])
-def test_k4_views_per_cta_match_oracle(name, vpb, monkeypatch):
-    """K4 with 1, 2 or 4 views per CTA (KATS_K4_VPB; ragged view tails): gF per stage and the
-    reconstructed volume against the oracle."""
+def test_k4_views_per_cta_match_oracle(name, vpb, k4, monkeypatch):
+    """K4 (row form, default, and the round-1 tile kernel) with 1, 2 or 4 views per CTA
+    (KATS_K4_VPB; ragged view tails): gF per stage and the reconstructed volume against the oracle."""
     import torch
     from oracle import oracle
     monkeypatch.setenv("KATS_K4_VPB", vpb)
+    monkeypatch.setenv("KATS_K4", k4)
     cfg, sino, ref, contrast = _case(name)
     p = _plan(cfg)
     v0, nv = p.pitch_views(0)
