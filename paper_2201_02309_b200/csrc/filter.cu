@@ -209,9 +209,11 @@ __global__ void __launch_bounds__(K12_THREADS) k_deriv_fwd_rebin_tile(FilterPara
 // consecutive views.  Per view, the warps first form g2 = D/sqrt(D²+w²)·(∂_q + ∂_α)g of the block's
 // nr rows in shared memory (Eqs. 8-9; coalesced raw rows, the ±1-view and ±1-column stencil reads
 // hit L1/L2), then its npsi κ-line samples (Eqs. 10-11) from there, with the block's rebin entries
-// staged in shared memory once for all the CTA's views.  Warps walk rows / κ-lines, so no index
-// division; the g2 tile is double-buffered (one barrier per view).  Same fp32 arithmetic as g2_at.
-constexpr int K12R_WARPS = 8;
+// staged in shared memory once for all the CTA's views.  The raw stencil values of view j+1 are
+// loaded into registers before view j's κ-line samples, so their latency overlaps that work; the
+// g2 tile is double-buffered (one barrier per view).  Warps walk rows / κ-lines: no index
+// division.  Same fp32 arithmetic as g2_at.
+constexpr int K12R_WARPS = 8, K12R_MAXR = 8;   // rows per warp: nr <= 64
 
 __global__ void __launch_bounds__(32 * K12R_WARPS) k_deriv_fwd_rebin_rows(FilterParams p, int nvb)
 {
@@ -232,17 +234,36 @@ __global__ void __launch_bounds__(32 * K12R_WARPS) k_deriv_fwd_rebin_rows(Filter
     const int v0 = blockIdx.y * nvb, nv = min(nvb, p.n_views - v0);
     const size_t pitch = p.k3_in_split ? (size_t)(2 * p.hp) : (size_t)nc;
     const int co = p.k3_in_split ? (l & 1) * p.hp + (l >> 1) : l;
-    for (int j = 0; j < nv; ++j) {
+    float nx_[K12R_MAXR], pv_[K12R_MAXR], rt_[K12R_MAXR], lt_[K12R_MAXR];   // view j's stencil reads
+    auto load_view = [&](int j) {
         const int64_t g = p.view0 + v0 + j;
         const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
         const float *gv = p.sino + (size_t)raw * rs;
-        float *buf = g2s + (j & 1) * nr * 32;
-        for (int m = warp; m < nr; m += K12R_WARPS) {
-            const float *r = gv + (size_t)m * nc;
-            const float dq = (__ldg(r + lc + rs) - __ldg(r + lc - rs)) * sq;
-            const float da = (__ldg(r + lp) - __ldg(r + lm)) * sa;
-            buf[m * 32 + lane] = __ldg(p.wlen + m) * (dq + da);
+#pragma unroll
+        for (int q = 0; q < K12R_MAXR; ++q) {
+            const int m = warp + q * K12R_WARPS;
+            if (m < nr) {
+                const float *r = gv + (size_t)m * nc;
+                nx_[q] = __ldg(r + lc + rs);
+                pv_[q] = __ldg(r + lc - rs);
+                rt_[q] = __ldg(r + lp);
+                lt_[q] = __ldg(r + lm);
+            }
         }
+    };
+    if (nv > 0) load_view(0);
+    for (int j = 0; j < nv; ++j) {
+        float *buf = g2s + (j & 1) * nr * 32;
+#pragma unroll
+        for (int q = 0; q < K12R_MAXR; ++q) {
+            const int m = warp + q * K12R_WARPS;
+            if (m < nr) {
+                const float dq = (nx_[q] - pv_[q]) * sq;
+                const float da = (rt_[q] - lt_[q]) * sa;
+                buf[m * 32 + lane] = __ldg(p.wlen + m) * (dq + da);
+            }
+        }
+        if (j + 1 < nv) load_view(j + 1);                          // in flight through the samples below
         // (view j+2 rewrites this buffer only after every thread passed view j+1's barrier, i.e.
         // after its reads of view j below)
         __syncthreads();
@@ -1122,68 +1143,95 @@ __global__ void __launch_bounds__(256) k_bwd_rebin_cos(FilterParams p)
 }
 
 
-// Row form (default): a CTA = 8 warps on one 32-column block (lane = column) and VPB views.  Phase 1:
-// warps walk the rows m = -2 .. nr of the [nr + 3][33] g5·cos α tile (the rebin entry and cos α
-// loaded once for the VPB views, their g4 gathers issued together); phase 2: the block's quads in
-// their global order (column-major, rows contiguous), the (column, quad row) of a thread advanced
-// incrementally — no index division in either loop.  Same fp32 arithmetic as k_bwd_rebin_cos.
-template <int VPB>
-__global__ void __launch_bounds__(256) k_bwd_rebin_cos_rows(FilterParams p)
+// Row form (default): a CTA = 256 threads on one 32-column block and a run of view groups of VPB
+// views.  A thread owns the same (row, column) entries of the [nr + 3][33] g5·cos α tile in every
+// group (rows m = -2 .. nr, columns c0 .. c0+32; index advanced incrementally, no division), so their
+// rebin entries and cos α stay in registers for the whole run; the g4 gathers of group i+1 are
+// issued before group i's quads are written.  Phase 2 writes the block's quads in their global order
+// (column-major, rows contiguous).  Same fp32 arithmetic as k_bwd_rebin_cos.
+// K4R_E: tile entries per thread, (nr + 3) * 33 <= 256 * K4R_E (4: nr <= 28, 9: nr <= 66)
+template <int VPB, int K4R_E>
+__global__ void __launch_bounds__(256) k_bwd_rebin_cos_rows(FilterParams p, int ngroups)
 {
-    extern __shared__ float tile[];            // [VPB][nr + 3][33], rows m = -2 .. nr
+    extern __shared__ float tile[];            // [2][VPB][nr + 3][33], rows m = -2 .. nr
     const int nc = p.nc, nr = p.nr, nq = nr + 2, ld = K4_COLS + 1, tsz = (nr + 3) * ld;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-    const int l0 = blockIdx.x * K4_COLS, v0 = blockIdx.y * VPB;
-    const int nv = min(VPB, p.n_views - v0);
+    const int tid = threadIdx.x;
+    const int l0 = blockIdx.x * K4_COLS;
     const int cols = min(K4_COLS, nc - l0);
     const size_t vs = (size_t)p.npsi * nc;
-    for (int mm = warp; mm < nr + 3; mm += 8) {
-        const int m = mm - 2;
-        for (int ll = lane; ll < ld; ll += 32) {
-            const int l = l0 + ll;
-            float out[VPB];
+    // this thread's tile entries e = tid + 256 i: rebin entry (idx < 0: zero), cos α, column
+    int eidx[K4R_E], eoff[K4R_E];
+    float efr[K4R_E], eca[K4R_E];
+    {
+        int mm = tid / ld, ll = tid - mm * ld;
+        const int DM = 256 / ld, DL = 256 - DM * ld;
 #pragma unroll
-            for (int j = 0; j < VPB; ++j) out[j] = 0.f;
-            if (m >= 0 && m < nr && l < nc) {
+        for (int i = 0; i < K4R_E; ++i) {
+            const int m = mm - 2, l = l0 + ll;
+            eidx[i] = -1; efr[i] = 0.f; eca[i] = 0.f; eoff[i] = mm * ld + ll;
+            if (mm >= nr + 3) eoff[i] = -1;
+            else if (m >= 0 && m < nr && l < nc) {
                 const RebinEntry r = p.br[m * nc + l];
-                if (r.idx >= 0) {
-                    const float ca = __ldg(p.cos_alpha + l);
-                    const float *g = p.g4 + ((size_t)v0 * p.npsi + r.idx) * nc + l;
-                    float a[VPB], b[VPB];
-#pragma unroll
-                    for (int j = 0; j < VPB; ++j)
-                        if (j < nv) { a[j] = g[j * vs]; b[j] = g[j * vs + nc]; }
-#pragma unroll
-                    for (int j = 0; j < VPB; ++j)
-                        if (j < nv) out[j] = ca * fmaf(r.frac, b[j] - a[j], a[j]);
-                }
-                if (p.gF && ll < cols)
-#pragma unroll
-                    for (int j = 0; j < VPB; ++j)
-                        if (j < nv) p.gF[((size_t)(v0 + j) * nr + m) * nc + l] = out[j];
+                eidx[i] = r.idx;
+                efr[i] = r.frac;
+                eca[i] = __ldg(p.cos_alpha + l);
             }
-#pragma unroll
-            for (int j = 0; j < VPB; ++j) tile[j * tsz + mm * ld + ll] = out[j];
+            mm += DM; ll += DL;
+            if (ll >= ld) { ll -= ld; ++mm; }
         }
     }
-    __syncthreads();
-    const int per = cols * nq;
-    const int ll0 = tid / nq, r0 = tid - ll0 * nq, DL = 256 / nq, DR = 256 - DL * nq;
+    const int ll0 = tid / nq, r0 = tid - ll0 * nq, DL2 = 256 / nq, DR2 = 256 - DL2 * nq;
     const float rcen = (float)((nr + 2) / 2);
-    for (int j = 0; j < nv; ++j) {
-        float4 *dst = p.gq + ((size_t)(v0 + j) * nc + l0) * nq;
-        const float *tj = tile + j * tsz;
-        int ll = ll0, r = r0;
-        for (int e = tid; e < per; e += 256) {
-            const float *t0 = tj + r * ld + ll;       // r = quad row; taps rows r-2, r-1
-            const float a0 = t0[0], a1 = t0[1], c0 = t0[ld], c1 = t0[ld + 1];
-            const float rc = (float)r - rcen;         // centred quad row
-            dst[e] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)), c0 - a0,
-                                 c1 - a1);
-            ll += DL;
-            r += DR;
-            if (r >= nq) { r -= nq; ++ll; }
+    const int per = cols * nq;
+    float ga[K4R_E][VPB], gb[K4R_E][VPB];
+    auto gather = [&](int grp) {
+        const int v0 = (blockIdx.y * ngroups + grp) * VPB;
+#pragma unroll
+        for (int i = 0; i < K4R_E; ++i)
+            if (eidx[i] >= 0) {
+                const float *g = p.g4 + ((size_t)v0 * p.npsi + eidx[i]) * nc + l0 + (eoff[i] % ld);
+#pragma unroll
+                for (int j = 0; j < VPB; ++j)
+                    if (v0 + j < p.n_views) { ga[i][j] = g[j * vs]; gb[i][j] = g[j * vs + nc]; }
+            }
+    };
+    const int g_end = min(ngroups, (p.n_views - blockIdx.y * ngroups * VPB + VPB - 1) / VPB);
+    if (g_end > 0) gather(0);
+    for (int grp = 0; grp < g_end; ++grp) {
+        const int v0 = (blockIdx.y * ngroups + grp) * VPB;
+        const int nv = min(VPB, p.n_views - v0);
+        float *tb = tile + (grp & 1) * VPB * tsz;
+#pragma unroll
+        for (int i = 0; i < K4R_E; ++i) {
+            if (eoff[i] < 0) continue;
+#pragma unroll
+            for (int j = 0; j < VPB; ++j) {
+                const float out = eidx[i] >= 0 && j < nv ? eca[i] * fmaf(efr[i], gb[i][j] - ga[i][j], ga[i][j]) : 0.f;
+                tb[j * tsz + eoff[i]] = out;
+                if (p.gF && eidx[i] >= 0 && j < nv) {
+                    const int mm = eoff[i] / ld, ll = eoff[i] - mm * ld;      // debug path only
+                    if (ll < cols) p.gF[((size_t)(v0 + j) * nr + mm - 2) * nc + l0 + ll] = out;
+                }
+            }
         }
+        if (grp + 1 < g_end) gather(grp + 1);                    // in flight through the quads below
+        __syncthreads();
+        for (int j = 0; j < nv; ++j) {
+            float4 *dst = p.gq + ((size_t)(v0 + j) * nc + l0) * nq;
+            const float *tj = tb + j * tsz;
+            int ll = ll0, r = r0;
+            for (int e = tid; e < per; e += 256) {
+                const float *t0 = tj + r * ld + ll;       // r = quad row; taps rows r-2, r-1
+                const float a0 = t0[0], a1 = t0[1], c0 = t0[ld], c1 = t0[ld + 1];
+                const float rc = (float)r - rcen;         // centred quad row
+                dst[e] = make_float4(fmaf(-rc, c0 - a0, 0.5f * (a0 + c0)), fmaf(-rc, c1 - a1, 0.5f * (a1 + c1)),
+                                     c0 - a0, c1 - a1);
+                ll += DL2;
+                r += DR2;
+                if (r >= nq) { r -= nq; ++ll; }
+            }
+        }
+        // (group grp+2 rewrites this tile buffer only after every thread passed group grp+1's barrier)
     }
 }
 
@@ -1396,9 +1444,21 @@ static void launch_k4(const FilterParams &p, cudaStream_t s)
     dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, (p.n_views + VPB - 1) / VPB);
     size_t smem = sizeof(float) * VPB * (size_t)(p.nr + 3) * (K4_COLS + 1);
     const char *ke = std::getenv("KATS_K4");                  // A/B: "tile" = the round-1 kernel
-    if (!(ke && std::string(ke) == "tile")) {
-        smem_opt_in((const void *)k_bwd_rebin_cos_rows<VPB>, smem);
-        k_bwd_rebin_cos_rows<VPB><<<grid, 256, smem, s>>>(p);
+    const int tiles = (p.nr + 3) * (K4_COLS + 1);
+    if (!(ke && std::string(ke) == "tile") && tiles <= 256 * 9) {
+        // view groups per CTA: as many as keep >= 4 CTAs per SM (entries held over the run), at most 8
+        const int nb = (p.nc + K4_COLS - 1) / K4_COLS, groups = (p.n_views + VPB - 1) / VPB;
+        int ng = 8;
+        while (ng > 1 && (int64_t)nb * ((groups + ng - 1) / ng) < 4 * device_sms()) ng /= 2;
+        const size_t sm2 = 2 * smem;
+        const dim3 g2(nb, (groups + ng - 1) / ng);
+        if (tiles <= 256 * 4) {
+            smem_opt_in((const void *)k_bwd_rebin_cos_rows<VPB, 4>, sm2);
+            k_bwd_rebin_cos_rows<VPB, 4><<<g2, 256, sm2, s>>>(p, ng);
+        } else {
+            smem_opt_in((const void *)k_bwd_rebin_cos_rows<VPB, 9>, sm2);
+            k_bwd_rebin_cos_rows<VPB, 9><<<g2, 256, sm2, s>>>(p, ng);
+        }
         return;
     }
     smem_opt_in((const void *)k_bwd_rebin_cos<VPB>, 200 * 1024);

@@ -1,13 +1,16 @@
 """Summarise one kernel of an `ncu --set full` report (.ncu-rep) into the key metrics this repo
 judges kernels by: duration, instructions, issue and pipe utilisation, shared-memory wavefronts
 and bank conflicts, DRAM/L2 traffic, occupancy limits and the top warp-stall reasons.
-Usage: python scripts/ncu_summary.py REPORT.ncu-rep "header line" > profiles/....txt"""
+Usage: python scripts/ncu_summary.py REPORT.ncu-rep "header line" [kernel-substring] > profiles/....txt
+(with several kernels in the report, the first whose name contains kernel-substring)"""
 import csv, io, re, subprocess, sys
 
 rep, header = sys.argv[1], (sys.argv[2] if len(sys.argv) > 2 else "")
+want = sys.argv[3] if len(sys.argv) > 3 else ""
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-h, units, v = rows[0], rows[1], rows[2]
+h, units = rows[0], rows[1]
+v = next(r for r in rows[2:] if want in r[h.index("Kernel Name")])
 KEYS = [
     "Kernel Name", "gpu__time_duration.sum", "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size",
     "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_registers",
