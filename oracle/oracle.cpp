@@ -236,24 +236,16 @@ Rebin rebin_maps(const G &o)
  * g(v) at sino[v - s0]; writes optional stage outputs (double, [rows][cols] or
  * [n_psi][cols]).  Discretisation readings: A5 (centred differences, one-sided
  * at the α edges), A9 (linear rebins, 0 outside), A10 (band-limited Hilbert). */
-void filter_view(const G &o, const float *sino, int64_t s0, int64_t v,
-                 const std::vector<double> &Kh, const Rebin &rb,
-                 double *g2o, double *g3o, double *g4o, double *gFo)
+/* Steps 2-6 of one view from its g1 = step 1's output [rows][cols] (double). */
+void filter_from_g1(const G &o, const double *g1, const std::vector<double> &Kh, const Rebin &rb,
+                    double *g2o, double *g3o, double *g4o, double *gFo)
 {
     const int nr = o.g.n_rows, nc = o.g.n_cols, np = o.n_psi;
-    auto g = [&](int64_t vv, int m, int l) { return (double)sino[((vv - s0) * nr + m) * (int64_t)nc + l]; };
     std::vector<double> g2((size_t)nr * nc), g3((size_t)np * nc), g4((size_t)np * nc);
-    /* Step 1, Eq. (8): g1 = (∂_q + ∂_α) g |_{q=λ}; step 2, Eq. (9): g2 = D/sqrt(D²+w²) g1 */
+    /* Step 2, Eq. (9): g2 = D/sqrt(D²+w²) g1 */
     for (int m = 0; m < nr; ++m) {
         double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + w_m(o, m) * w_m(o, m));
-        for (int l = 0; l < nc; ++l) {
-            double dq = (g(v + 1, m, l) - g(v - 1, m, l)) / (2.0 * o.dlam);
-            double da;
-            if (l == 0) da = (g(v, m, 1) - g(v, m, 0)) / o.g.d_alpha;
-            else if (l == nc - 1) da = (g(v, m, nc - 1) - g(v, m, nc - 2)) / o.g.d_alpha;
-            else da = (g(v, m, l + 1) - g(v, m, l - 1)) / (2.0 * o.g.d_alpha);
-            g2[(size_t)m * nc + l] = wgt * (dq + da);
-        }
+        for (int l = 0; l < nc; ++l) g2[(size_t)m * nc + l] = wgt * g1[(size_t)m * nc + l];
     }
     /* Step 3, Eqs. (10)-(11): g3(α,ψ) = g2(α, w_κ(α,ψ)), linear in w, 0 outside */
     for (int i = 0; i < np; ++i)
@@ -280,6 +272,53 @@ void filter_view(const G &o, const float *sino, int64_t s0, int64_t v,
     if (g2o) std::memcpy(g2o, g2.data(), sizeof(double) * g2.size());
     if (g3o) std::memcpy(g3o, g3.data(), sizeof(double) * g3.size());
     if (g4o) std::memcpy(g4o, g4.data(), sizeof(double) * g4.size());
+}
+
+/* ---------- Filtering steps 1-6 for one view (P:l.117-154, Eqs. 8-15) ----------
+ * g(v) at sino[v - s0]; writes optional stage outputs (double, [rows][cols] or
+ * [n_psi][cols]).  Discretisation readings: A5 (centred differences, one-sided
+ * at the α edges), A9 (linear rebins, 0 outside), A10 (band-limited Hilbert). */
+void filter_view(const G &o, const float *sino, int64_t s0, int64_t v,
+                 const std::vector<double> &Kh, const Rebin &rb,
+                 double *g2o, double *g3o, double *g4o, double *gFo)
+{
+    const int nr = o.g.n_rows, nc = o.g.n_cols;
+    auto g = [&](int64_t vv, int m, int l) { return (double)sino[((vv - s0) * nr + m) * (int64_t)nc + l]; };
+    std::vector<double> g1((size_t)nr * nc);
+    /* Step 1, Eq. (8): g1 = (∂_q + ∂_α) g |_{q=λ} */
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            double dq = (g(v + 1, m, l) - g(v - 1, m, l)) / (2.0 * o.dlam);
+            double da;
+            if (l == 0) da = (g(v, m, 1) - g(v, m, 0)) / o.g.d_alpha;
+            else if (l == nc - 1) da = (g(v, m, nc - 1) - g(v, m, nc - 2)) / o.g.d_alpha;
+            else da = (g(v, m, l + 1) - g(v, m, l - 1)) / (2.0 * o.g.d_alpha);
+            g1[(size_t)m * nc + l] = dq + da;
+        }
+    filter_from_g1(o, g1.data(), Kh, rb, g2o, g3o, g4o, gFo);
+}
+
+/* NEXT-4: Noo's half-sample derivative, the 2x2x2-cube scheme of [Noo2003a] (the
+ * reference PAPER.md l.115 cites for implementing Eq. (8); reading A25).  g1 lives at the
+ * cube centre (λ_{k+½}, α_{l+½}, w_{m+½}) of raw views k, k+1, columns l, l+1 and rows m, m+1:
+ *   ∂_q g ≈ 1/(4Δλ) Σ_{i,j ∈ {0,1}} [g(k+1, m+j, l+i) - g(k, m+j, l+i)]
+ *   ∂_α g ≈ 1/(4Δα) Σ_{i,j ∈ {0,1}} [g(k+i, m+j, l+1) - g(k+i, m+j, l)]
+ *   g1 = ∂_q g + ∂_α g                                             (Eq. 8's chain rule)
+ * on (n_rows - 1) x (n_cols - 1) half-shifted samples; o is the PHYSICAL geometry. */
+void deriv_half(const G &o, const float *sino, int64_t s0, int64_t k, double *g1)
+{
+    const int nr = o.g.n_rows, nc = o.g.n_cols;
+    auto g = [&](int64_t vv, int m, int l) { return (double)sino[((vv - s0) * nr + m) * (int64_t)nc + l]; };
+    for (int m = 0; m + 1 < nr; ++m)
+        for (int l = 0; l + 1 < nc; ++l) {
+            double dq = 0.0, da = 0.0;
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j) {
+                    dq += g(k + 1, m + j, l + i) - g(k, m + j, l + i);
+                    da += g(k + i, m + j, l + 1) - g(k + i, m + j, l);
+                }
+            g1[(size_t)m * (nc - 1) + l] = dq / (4.0 * o.dlam) + da / (4.0 * o.g.d_alpha);
+        }
 }
 
 /* Band-limited kernel of h_H(sin(α-α')) dα' (A10):
@@ -664,6 +703,33 @@ int ora_filter(const ora_geom *g, const float *sino, int64_t s0, int64_t sn,
     const int rc = ora_filter_run(c, sino, s0, sn, v_first, n_out, g2, g3, g4, gF);
     ora_filter_free(c);
     return rc;
+}
+
+/* NEXT-4: half-sample derivative of raw views (physical geometry g): g1 [n_out][rows-1][cols-1] for
+ * the half-shifted views v_first + ½ .. (needs raw views v_first .. v_first + n_out). */
+int ora_deriv_half(const ora_geom *g, const float *sino, int64_t s0, int64_t sn, int64_t v_first, int64_t n_out,
+                   double *g1)
+{
+    G o = make(g);
+    if (v_first < s0 || v_first + n_out + 1 > s0 + sn) return -1;
+    const size_t vs = (size_t)(g->n_rows - 1) * (g->n_cols - 1);
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_out; ++i) deriv_half(o, sino, s0, v_first + i, g1 + i * vs);
+    return 0;
+}
+
+/* Steps 2-6 from step-1 output g1 [n][rows][cols] (double) in the geometry g (for the half-sample
+ * derivative: the half-shifted grid's geometry, reading A25).  Outputs as ora_filter. */
+void ora_filter_g1(const ora_geom *g, const double *g1, int64_t n, double *g2, double *g3, double *g4, double *gF)
+{
+    G o = make(g);
+    std::vector<double> K = hilbert_kernel(o);
+    Rebin rb = rebin_maps(o);
+    const size_t rs = (size_t)g->n_rows * g->n_cols, ps = (size_t)o.n_psi * g->n_cols;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n; ++i)
+        filter_from_g1(o, g1 + i * rs, K, rb, g2 ? g2 + i * rs : nullptr, g3 ? g3 + i * ps : nullptr,
+                       g4 ? g4 + i * ps : nullptr, gF ? gF + i * rs : nullptr);
 }
 
 /* OpenMP threads for the following oracle calls (bench.py: single-thread vs all-core timing). */

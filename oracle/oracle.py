@@ -84,6 +84,9 @@ def lib():
             "ora_filter_run": (ctypes.c_int, [ctypes.c_void_p, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                               ctypes.c_int64, _D, _D, _D, _D]),
             "ora_set_threads": (None, [ctypes.c_int]),
+            "ora_deriv_half": (ctypes.c_int, [_G, _F, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, _D]),
+            "ora_filter_g1": (None, [_G, _D, ctypes.c_int64, _D, _D, _D, _D]),
             "ora_get_threads": (ctypes.c_int, []),
             "ora_philox": (None, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                   ctypes.POINTER(ctypes.c_uint32)]),
@@ -269,6 +272,61 @@ def reconstruct(cfg, sino, s0, k0, n_pitches):
     rc = lib().ora_reconstruct(ctypes.byref(g), _p(sino, _F), s0, sino.shape[0], k0, n_pitches, _p(vol, _D))
     if rc:
         raise ValueError("oracle reconstruct: sinogram does not cover a requested pitch slab")
+    return vol
+
+
+# ---- NEXT-4: Noo's half-sample derivative (reading A25) ----
+
+def half_sample_cfg(cfg):
+    """Geometry of the half-shifted grid the half-sample derivative produces (reading A25): samples
+    (λ_{k+½}, α_{l+½}, w_{m+½}) are those of a detector with one row and one column fewer (same
+    spacings, offsets: α_{l+½} = (l - (n_c - 2)/2 + offset) Δα, w_{m+½} = (m - (n_r - 2)/2) Δw) on the
+    same helix parametrised from λ0 + Δλ/2 and z0 + P Δλ / (4π) (Eq. 1: a(λ_{k+½}) = a'(λ_k)).  The
+    voxel grid, FOV and pitch are unchanged; the κ-line count defaults to 2 (n_r - 1) + 1."""
+    import math
+    dlam = 2 * math.pi / cfg["views_per_turn"]
+    return dict(cfg, n_rows=cfg["n_rows"] - 1, n_cols=cfg["n_cols"] - 1,
+                lambda0=cfg.get("lambda0", 0.0) + 0.5 * dlam,
+                z0=cfg.get("z0", 0.0) + cfg["P"] * dlam / (4 * math.pi))
+
+
+def deriv_half(cfg, sino, s0, v_first, n_out):
+    """g1 [n_out][rows-1][cols-1] on the half-shifted grid for half-views v_first+½ .. (raw views
+    v_first .. v_first + n_out of a sinogram whose first view is s0)."""
+    sino = np.ascontiguousarray(sino, dtype=np.float32)
+    out = np.empty((n_out, cfg["n_rows"] - 1, cfg["n_cols"] - 1))
+    g = geom(cfg)
+    if lib().ora_deriv_half(ctypes.byref(g), _p(sino, _F), s0, sino.shape[0], v_first, n_out, _p(out, _D)):
+        raise ValueError("oracle deriv_half: sinogram does not cover the requested views")
+    return out
+
+
+def filter_g1(cfg, g1, stages=("gF",)):
+    """Steps 2-6 from step-1 output g1 [n][rows][cols] in geometry cfg."""
+    d = derived(cfg)
+    nr, nc, npsi = cfg["n_rows"], cfg["n_cols"], d["n_psi"]
+    g1 = np.ascontiguousarray(g1, dtype=np.float64)
+    n = g1.shape[0]
+    shapes = {"g2": (n, nr, nc), "g3": (n, npsi, nc), "g4": (n, npsi, nc), "gF": (n, nr, nc)}
+    out = {s: np.empty(shapes[s]) for s in stages}
+    g = geom(cfg)
+    lib().ora_filter_g1(ctypes.byref(g), _p(g1, _D), n, _p(out.get("g2"), _D), _p(out.get("g3"), _D),
+                        _p(out.get("g4"), _D), _p(out.get("gF"), _D))
+    return out
+
+
+def reconstruct_half(cfg, sino, s0, k0, n_pitches):
+    """reconstruct() with Noo's half-sample derivative (reading A25): per pitch, the half-shifted
+    grid's slab [K_lo, K_hi] (its PI windows on the views λ_{k+½}), step 1 by the 2x2x2 cube from raw
+    views K_lo .. K_hi + 1, steps 2-7 on the half-shifted grid."""
+    vc = half_sample_cfg(cfg)
+    vol = np.empty((n_pitches * cfg["nz"], cfg["ny"], cfg["nx"]))
+    for i, k in enumerate(range(k0, k0 + n_pitches)):
+        fv, nv = pitch_slab(vc, k)
+        klo, n = fv + 1, nv - 2
+        g1 = deriv_half(cfg, sino, s0, klo, n)
+        gF = filter_g1(vc, g1)["gF"]
+        vol[i * cfg["nz"]:(i + 1) * cfg["nz"]] = backproject(vc, k, gF, klo)
     return vol
 
 

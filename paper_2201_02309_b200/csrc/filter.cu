@@ -283,6 +283,82 @@ __global__ void __launch_bounds__(32 * K12R_WARPS) k_deriv_fwd_rebin_rows(Filter
     }
 }
 
+// Warp-per-view form: each warp of a CTA owns one view (of a run of vpw views) on one 32-column
+// block (lane = column): g2 of the block's rows into a warp-private shared-memory tile, then the
+// npsi κ-line samples from it — no CTA barrier in the view loop; the block's rebin entries are
+// staged once per CTA.  HALF (NEXT-4, reading A25): Noo's 2x2x2 half-sample derivative
+// on the half-shifted grid (the plan's effective geometry: nr, nc are the shifted grid's sizes,
+// raw views have nr + 1 rows and nc + 1 columns; effective view g reads raw views raw(g), raw(g)+1).
+template <bool HALF>
+__global__ void __launch_bounds__(256) k_deriv_fwd_rebin_wv(FilterParams p, int vpw)
+{
+    extern __shared__ float k12s[];
+    const int nr = p.nr, nc = p.nc, npsi = p.npsi;
+    const int rnc = HALF ? nc + 1 : nc, rs = HALF ? (nr + 1) * (nc + 1) : nr * nc;   // raw row / view
+    float2 *tab = reinterpret_cast<float2 *>(k12s);                // [npsi][32]: (idx bits, frac)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *g2w = k12s + 2 * npsi * 32 + warp * nr * 32;            // this warp's [nr][32]
+    const int l = blockIdx.x * 32 + lane;
+    const bool col_ok = l < nc;
+    const int lc = col_ok ? l : nc - 1;
+    for (int i = warp; i < npsi; i += 8) {
+        const RebinEntry e = p.fr[(size_t)i * nc + lc];
+        tab[i * 32 + lane] = make_float2(__int_as_float(e.idx), e.frac);
+    }
+    __syncthreads();
+    const size_t pitch = p.k3_in_split ? (size_t)(2 * p.hp) : (size_t)nc;
+    const int co = p.k3_in_split ? (l & 1) * p.hp + (l >> 1) : l;
+    for (int jj = 0; jj < vpw; ++jj) {
+        const int j = (blockIdx.y * 8 + warp) * vpw + jj;
+        if (j >= p.n_views) break;
+        const int64_t g = p.view0 + j;
+        const int64_t raw = p.slab_views ? g + (HALF ? 1 : 2) * (g / p.slab_views) : g;
+        const float *gv = p.sino + (size_t)raw * rs;
+        if constexpr (HALF) {
+            // rolling rows: raw row m of views k, k+1 at columns l, l+1
+            const float sq = 0.25f * p.inv_2dlam * 2.f, sa = 0.25f * p.inv_dalpha;    // 1/(4Δλ), 1/(4Δα)
+            const float *r0 = gv + lc, *r1 = gv + rs + lc;
+            float a0 = __ldg(r0), a1 = __ldg(r0 + 1), b0 = __ldg(r1), b1 = __ldg(r1 + 1);
+#pragma unroll 4
+            for (int m = 0; m < nr; ++m) {
+                r0 += rnc; r1 += rnc;
+                const float c0 = __ldg(r0), c1 = __ldg(r0 + 1), d0 = __ldg(r1), d1 = __ldg(r1 + 1);
+                // view differences (k+1) - k over the 2x2 (row, column) face, column differences over (view, row)
+                const float dq = ((b0 - a0) + (b1 - a1)) + ((d0 - c0) + (d1 - c1));
+                const float da = ((a1 - a0) + (b1 - b0)) + ((c1 - c0) + (d1 - d0));
+                g2w[m * 32 + lane] = __ldg(p.wlen + m) * fmaf(dq, sq, da * sa);
+                a0 = c0; a1 = c1; b0 = d0; b1 = d1;
+            }
+        } else {
+            const int lp = min(lc + 1, nc - 1), lm = max(lc - 1, 0);
+            const float sa = (lp - lm == 2) ? p.inv_2dalpha : p.inv_dalpha, sq = p.inv_2dlam;
+#pragma unroll 4
+            for (int m = 0; m < nr; ++m) {
+                const float *r = gv + (size_t)m * nc;
+                const float dq = (__ldg(r + lc + rs) - __ldg(r + lc - rs)) * sq;
+                const float da = (__ldg(r + lp) - __ldg(r + lm)) * sa;
+                g2w[m * 32 + lane] = __ldg(p.wlen + m) * (dq + da);
+            }
+        }
+        __syncwarp();
+        if (col_ok) {
+            float *out = p.g3 + (size_t)j * npsi * pitch + co;
+#pragma unroll 4
+            for (int i = 0; i < npsi; ++i) {
+                const float2 e = tab[i * 32 + lane];
+                const int ia = __float_as_int(e.x);
+                float o = 0.f;
+                if (ia >= 0) {
+                    const float a = g2w[ia * 32 + lane], b = g2w[(ia + 1) * 32 + lane];
+                    o = fmaf(e.y, b - a, a);
+                }
+                out[(size_t)i * pitch] = o;
+            }
+        }
+        __syncwarp();                                               // before the next view's g2
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3: g4 = Σ_l' K[l-l'] g3[l'] along each κ-line (Eq. 12, h_H = 1/(πs) of
 //     Eq. e4, band-limited kernel of DESIGN.md reading A10: only odd
@@ -1242,7 +1318,24 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     // KATS_K12=sample: one thread per sample (8 κ-lines unrolled); colN: N κ-lines per thread
     const char *ke = std::getenv("KATS_K12");
     const std::string k12 = ke ? ke : "";
-    if (k12.empty() || k12 == "rows") {
+    const size_t wv_smem = sizeof(float) * (2 * (size_t)p.npsi * 32 + 8 * (size_t)p.nr * 32);
+    if (p.half || (k12 == "wv" && wv_smem <= 200 * 1024)) {
+        // warp per view (the half-sample derivative has only this form): views per warp as many as
+        // keep >= 4 CTAs per SM, at most 8
+        const int nb = (p.nc + 31) / 32;
+        int vpw = 8;
+        while (vpw > 1 && (int64_t)nb * ((p.n_views + 8 * vpw - 1) / (8 * vpw)) < 4 * device_sms()) vpw /= 2;
+        const dim3 grid(nb, (p.n_views + 8 * vpw - 1) / (8 * vpw));
+        if (p.half) {
+            smem_opt_in((const void *)k_deriv_fwd_rebin_wv<true>, wv_smem);
+            k_deriv_fwd_rebin_wv<true><<<grid, 256, wv_smem, s>>>(p, vpw);
+        } else {
+            smem_opt_in((const void *)k_deriv_fwd_rebin_wv<false>, wv_smem);
+            k_deriv_fwd_rebin_wv<false><<<grid, 256, wv_smem, s>>>(p, vpw);
+        }
+        return;
+    }
+    if ((k12.empty() || k12 == "rows") && p.nr <= K12R_WARPS * K12R_MAXR) {
         // views per CTA: as many as keep >= 4 CTAs per SM in the launch (the block's rebin entries are
         // staged once per CTA), at most 16
         const int nb = (p.nc + 31) / 32;
@@ -1443,9 +1536,12 @@ static void launch_k4(const FilterParams &p, cudaStream_t s)
 {
     dim3 grid((p.nc + K4_COLS - 1) / K4_COLS, (p.n_views + VPB - 1) / VPB);
     size_t smem = sizeof(float) * VPB * (size_t)(p.nr + 3) * (K4_COLS + 1);
-    const char *ke = std::getenv("KATS_K4");                  // A/B: "tile" = the round-1 kernel
+    // KATS_K4=rows: the row form (entries in registers over a run of view groups); measured slower
+    // than the tile kernel on every config (scripts/ab/gpu_k12k4rows.sh: C5 K4 0.94 vs 0.68 ms,
+    // C2 0.31 vs 0.11 ms), so the tile kernel stays the default
+    const char *ke = std::getenv("KATS_K4");
     const int tiles = (p.nr + 3) * (K4_COLS + 1);
-    if (!(ke && std::string(ke) == "tile") && tiles <= 256 * 9) {
+    if (ke && std::string(ke) == "rows" && tiles <= 256 * 9) {
         // view groups per CTA: as many as keep >= 4 CTAs per SM (entries held over the run), at most 8
         const int nb = (p.nc + K4_COLS - 1) / K4_COLS, groups = (p.n_views + VPB - 1) / VPB;
         int ng = 8;

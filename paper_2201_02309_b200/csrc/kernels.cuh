@@ -37,6 +37,7 @@ struct FilterParams {
     int k3_in_split;          // K3's input lines are parity-split (even columns, then odd, each hp floats): written
                               // by K12 (forward) / K4^T (adjoint) when the warp-specialized K3 reads them
     int hp;                   // half pitch of a parity-split line (floats, multiple of 4)
+    int half;                 // NEXT-4: Noo's half-sample derivative (raw views have nr+1 rows, nc+1 columns)
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11

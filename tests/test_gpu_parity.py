@@ -235,7 +235,7 @@ def test_bp_end_views_ahead_or_inline(kernel, ends, monkeypatch):
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("k12", ["rows", "sample", "col3", "col8", "tile", "colv2", "colv4"])
+@pytest.mark.parametrize("k12", ["wv", "rows", "sample", "col3", "col8", "tile", "colv2", "colv4"])
 @pytest.mark.parametrize("name", ["T1", "C1"])
 def test_k12_variants_match_oracle(name, k12, monkeypatch):
     """Steps 1-3 (g3) by the K12 kernels: the row form (default), one thread per sample, the column walk
