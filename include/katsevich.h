@@ -74,8 +74,17 @@ typedef struct {
     double  dx, dy;
     int32_t nz_per_pitch;    /* slices per pitch; dz = pitch / nz_per_pitch */
     int32_t n_psi;           /* κ-lines ψ_i on [-π/2-α_m, π/2+α_m] (P:l.132); 0 => 2·n_rows+1 */
-    int32_t flags;           /* reserved, must be 0 */
+    int32_t flags;           /* 0, or KATS_FLAG_HALF_SAMPLE */
 } katsevich_geometry;
+
+/* Method variant flags (katsevich_geometry.flags):
+ * KATS_FLAG_HALF_SAMPLE — step 1 (Eq. 8) by Noo's 2x2x2 half-sample derivative
+ *   ([Noo2003a], cited at P:l.115; reading A25): g1 on the grid shifted by half a sample in
+ *   λ, α and w, where steps 2-7 then run — every table (T_pi, T_fr, T_br) and the filtered data
+ *   (katsevich_filter's g3/g4/gF, katsevich_export_tables) live on that grid: n_rows-1 rows,
+ *   n_cols-1 columns, views at λ_{k+½}.  Filtered view k needs raw views k and k+1 (no lower halo):
+ *   katsevich_pitch_views / _scan_views report the raw views.  Needs 3 <= n_rows <= 65, n_cols >= 3. */
+#define KATS_FLAG_HALF_SAMPLE 1
 
 typedef struct katsevich_plan katsevich_plan;
 

@@ -182,6 +182,11 @@ int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
     return (int64_t)(n_pitches - 1) * p->g.views_per_turn + (t.bp_hi - t.bp_lo + 1);
 }
 
+// raw sinogram views: the caller's detector; filtered view u needs raw views u - halo_lo(p) .. u + 1
+// (centred λ difference; the half-sample derivative reads u and u + 1)
+size_t raw_view_elems(const katsevich_plan *p) { return (size_t)p->graw.n_rows * p->graw.n_cols; }
+int halo_lo(const katsevich_plan *p) { return p->half ? 0 : 1; }
+
 size_t filter_chunk_bytes(const katsevich_plan *p, int mul = 1)
 {
     return 2 * sizeof(float) * (size_t)filter_chunk_views(p, mul) * p->t.n_psi * g3_line_pitch(p->g.n_cols);
@@ -203,6 +208,7 @@ FilterParams filter_params(const katsevich_plan *p)
     f.cos_alpha = p->d.cos_alpha; f.hilbert = p->d.hilbert; f.hilbert_tc = p->d.hilbert_tc;
     f.hilbert_hk = p->d.hilbert_hk;
     f.sign = 1.f;
+    f.half = p->half ? 1 : 0;
     return f;
 }
 
@@ -408,7 +414,9 @@ int katsevich_plan_create(const katsevich_geometry *geom, int cuda_device, katse
     }
     katsevich_plan *p = new (std::nothrow) katsevich_plan;
     if (!p) return KATS_ERR_ARGUMENT;
-    p->g = *geom;
+    p->graw = *geom;
+    p->half = (geom->flags & KATS_FLAG_HALF_SAMPLE) != 0;
+    p->g = p->half ? half_sample_geometry(*geom) : *geom;
     p->device = cuda_device;
     *out = p;
     return KATS_OK;
@@ -499,8 +507,8 @@ int katsevich_pitch_views(const katsevich_plan *p, int32_t pitch, int64_t *first
 {
     if (!p || !first_view || !n_views) return KATS_ERR_NULL;
     if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
-    *first_view = (int64_t)pitch * p->g.views_per_turn + p->t.bp_lo - 1;
-    *n_views = (int32_t)(p->t.bp_hi - p->t.bp_lo + 3);
+    *first_view = (int64_t)pitch * p->g.views_per_turn + p->t.bp_lo - halo_lo(p);
+    *n_views = (int32_t)(p->t.bp_hi - p->t.bp_lo + 2 + halo_lo(p));
     return KATS_OK;
 }
 
@@ -510,8 +518,8 @@ int katsevich_scan_views(const katsevich_plan *p, int32_t first_pitch, int32_t n
     if (!p || !first_view || !n_views) return KATS_ERR_NULL;
     if (!p->precomputed) return KATS_ERR_NOT_PRECOMPUTED;
     if (n_pitches < 1) return KATS_ERR_ARGUMENT;
-    *first_view = (int64_t)first_pitch * p->g.views_per_turn + p->t.bp_lo - 1;
-    *n_views = n_union_views(p, n_pitches) + 2;
+    *first_view = (int64_t)first_pitch * p->g.views_per_turn + p->t.bp_lo - halo_lo(p);
+    *n_views = n_union_views(p, n_pitches) + 1 + halo_lo(p);
     return KATS_OK;
 }
 
@@ -532,9 +540,9 @@ int katsevich_workspace_bytes_host(const katsevich_plan *p, int32_t n_pitches, s
 {
     int rc = katsevich_workspace_bytes(p, n_pitches, bytes);
     if (rc) return rc;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     const size_t vol = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch * n_pitches;
-    *bytes += align_up(sizeof(float) * rs * (size_t)(n_union_views(p, n_pitches) + 2)) + align_up(sizeof(float) * vol);
+    *bytes += align_up(sizeof(float) * rs * (size_t)(n_union_views(p, n_pitches) + 1 + halo_lo(p))) + align_up(sizeof(float) * vol);
     return KATS_OK;
 }
 
@@ -612,9 +620,9 @@ int katsevich_reconstruct_grouped(katsevich_plan *p, const float *sino, int64_t 
     const HostTables &t = p->t;
     const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;                  // first filtered view
     const int64_t nu = n_union_views(p, n_pitches);
-    if (u0 - 1 < s0 || u0 + nu + 1 > s0 + sn) {
-        // reconstructible pitches k need [k vt + bp_lo - 1, k vt + bp_hi + 1] inside the scan
-        double ka = std::ceil((double)(s0 - (t.bp_lo - 1)) / vt);
+    if (u0 - halo_lo(p) < s0 || u0 + nu + 1 > s0 + sn) {
+        // reconstructible pitches k need [k vt + bp_lo - halo, k vt + bp_hi + 1] inside the scan
+        double ka = std::ceil((double)(s0 - (t.bp_lo - halo_lo(p))) / vt);
         double kb = std::floor((double)(s0 + sn - 1 - (t.bp_hi + 1)) / vt);
         char buf[200];
         std::snprintf(buf, sizeof buf, "sinogram views [%lld, %lld) do not cover pitches [%d, %d); reconstructible pitches: %.0f..%.0f",
@@ -623,7 +631,7 @@ int katsevich_reconstruct_grouped(katsevich_plan *p, const float *sino, int64_t 
         return KATS_ERR_COVERAGE;
     }
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     float4 *gq = (float4 *)workspace;
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * quad_view_elems(p) * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
     const char *pe = std::getenv("KATS_PIPELINE");
@@ -756,12 +764,12 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
     const HostTables &t = p->t;
     const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;
     const int64_t nu = n_union_views(p, n_pitches);
-    if (u0 - 1 < s0 || u0 + nu + 1 > s0 + sn) {
+    if (u0 - halo_lo(p) < s0 || u0 + nu + 1 > s0 + sn) {
         p->detail = "output sinogram views do not cover the pitches' slabs";
         return KATS_ERR_COVERAGE;
     }
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     const size_t qs = quad_view_elems(p);
     float4 *qT = (float4 *)workspace;
     const size_t qbytes = align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches));
@@ -789,7 +797,7 @@ int katsevich_adjoint(katsevich_plan *p, const float *vol, int32_t first_pitch, 
     f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K4^T writes the lines K3^T reads
     rc = run_filter_T(p, f, qT, scratch, g1T, nu, s);
     if (rc) return rc;
-    { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nu, sino_out + (u0 - 1 - s0) * rs, s); }
+    { LaunchScope ls(p, ST_K12, s); launch_deriv_T(f, g1T, nu, sino_out + (u0 - halo_lo(p) - s0) * rs, s); }
     KCHECK(p, cudaGetLastError());
     return KATS_OK;
 }
@@ -809,7 +817,7 @@ int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, flo
     if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const HostTables &t = p->t;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     const size_t qs = quad_view_elems(p);
     const int64_t nbp = t.bp_hi - t.bp_lo + 1, nu = nbp * B;
     float4 *qT = (float4 *)workspace;
@@ -817,7 +825,7 @@ int katsevich_adjoint_batch(katsevich_plan *p, const float *vols, int32_t B, flo
     float *scratch = (float *)((char *)workspace + qbytes);
     float *g1T = (float *)((char *)workspace + qbytes + kFilterStreamsMax * align_up(filter_chunk_bytes(p, device_chunk_mul())));
     KCHECK(p, cudaMemsetAsync(qT, 0, sizeof(float4) * qs * (size_t)nu, s));
-    KCHECK(p, cudaMemsetAsync(slabs_out, 0, sizeof(float) * rs * (size_t)(nbp + 2) * B, s));
+    KCHECK(p, cudaMemsetAsync(slabs_out, 0, sizeof(float) * rs * (size_t)(nbp + 1 + halo_lo(p)) * B, s));
     BPParams b = bp_params(p);
     b.gqT = qT;
     b.gq_views = nu;
@@ -855,15 +863,15 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const HostTables &t = p->t;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     const int64_t nbp = t.bp_hi - t.bp_lo + 1;        // filtered views per slab
-    const int64_t nslab = nbp + 2;                     // raw views per slab
+    const int64_t nslab = nbp + 1 + halo_lo(p);        // raw views per slab
     float4 *gq = (float4 *)workspace;
     const size_t qs = quad_view_elems(p);
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
     // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
     // keeps its own +-1 halo)
-    rc = run_filter(p, slabs + rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true, device_chunk_mul());
+    rc = run_filter(p, slabs + halo_lo(p) * rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true, device_chunk_mul());
     if (rc) return rc;
     (void)nslab;
     BPParams bp = bp_params(p);
@@ -912,10 +920,10 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
     cudaStream_t cs = (cudaStream_t)p->copy_stream, ds = (cudaStream_t)p->copy_stream2;
     const HostTables &t = p->t;
     const int vt = p->g.views_per_turn;
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     const size_t qs = quad_view_elems(p);
     const size_t vpitch = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
-    const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;   // first filtered view (= fv + 1)
+    const int64_t u0 = (int64_t)first_pitch * vt + t.bp_lo;   // first filtered view (= fv + halo)
     const int64_t nu = n_union_views(p, n_pitches);
     const int64_t nchunks = (nu + kFilterChunk - 1) / kFilterChunk;
     while ((int64_t)p->sync_events.size() < nchunks + 2 * n_pitches + 1) {
@@ -987,7 +995,7 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
 // ---- data generation (NEXT-3) ----
 static DataGenParams datagen_params(const katsevich_plan *p)
 {
-    const katsevich_geometry &g = p->g;
+    const katsevich_geometry &g = p->graw;                  // the physical scan (not the half-shifted grid)
     DataGenParams d{};
     d.R = g.R; d.D = g.D; d.h = g.pitch / (2.0 * kPi); d.lambda0 = g.lambda0; d.z0 = g.z0;
     d.dlam = 2.0 * kPi / g.views_per_turn; d.d_w = g.d_w; d.d_alpha = g.d_alpha; d.alpha_offset = g.alpha_offset;
@@ -1062,7 +1070,7 @@ int katsevich_degrade(katsevich_plan *p, const float *sino, int64_t first_view, 
         return KATS_ERR_ARGUMENT;
     cudaSetDevice(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    const size_t n = (size_t)n_views * p->g.n_rows * p->g.n_cols;
+    const size_t n = (size_t)n_views * raw_view_elems(p);
     int rc = plan_scratch(p, 256 + sizeof(float) * n);
     if (rc) return rc;
     unsigned *maxbits = (unsigned *)p->dg_scratch;
@@ -1081,11 +1089,11 @@ int katsevich_filter(katsevich_plan *p, const float *sino, int64_t s0, int64_t s
     if (rc) return rc;
     if (!sino || !gF) return KATS_ERR_NULL;
     if (n_out < 1) return KATS_ERR_ARGUMENT;
-    if (out_first_view - 1 < s0 || out_first_view + n_out + 1 > s0 + sn) {
-        p->detail = "sinogram does not hold the ±1 halo of the requested views";
+    if (out_first_view - halo_lo(p) < s0 || out_first_view + n_out + 1 > s0 + sn) {
+        p->detail = "sinogram does not hold the derivative halo of the requested views";
         return KATS_ERR_COVERAGE;
     }
-    const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
+    const size_t rs = raw_view_elems(p);
     cudaStream_t s = (cudaStream_t)cuda_stream;
     float *scratch = nullptr;
     float4 *gq = nullptr;

@@ -1319,7 +1319,11 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     const char *ke = std::getenv("KATS_K12");
     const std::string k12 = ke ? ke : "";
     const size_t wv_smem = sizeof(float) * (2 * (size_t)p.npsi * 32 + 8 * (size_t)p.nr * 32);
-    if (p.half || (k12 == "wv" && wv_smem <= 200 * 1024)) {
+    // default: warp per view for detectors of <= 32 rows, the row form above (scripts/ab/gpu_k12wv.sh,
+    // steps: C5 4.08 (round-1 column walk) / 4.32 (rows) / 3.95 ms (wv), C2 1.70 / 1.68 / 1.68,
+    // C3 9.13 / 9.01 / 9.23, C4 50.84 / 50.57 / 50.58)
+    const bool want_wv = k12 == "wv" || (k12.empty() && p.nr <= 32);
+    if (p.half || (want_wv && wv_smem <= 200 * 1024)) {
         // warp per view (the half-sample derivative has only this form): views per warp as many as
         // keep >= 4 CTAs per SM, at most 8
         const int nb = (p.nc + 31) / 32;
@@ -1722,8 +1726,51 @@ void launch_fwd_rebin_T(const FilterParams &p, float *g1T, cudaStream_t s)
                     sizeof(float) * p.nr * KT_THREADS, s>>>(p, g1T);
 }
 
+// K1^T of the half-sample derivative (NEXT-4): raw view r (relative to the first filtered view) of an
+// item receives from filtered views r-1 (as its upper view) and r (as its lower view), raw row mr from
+// rows mr-1, mr and raw column lr from columns lr-1, lr of the half-shifted grid, with the forward's
+// coefficients: 1/(4Δλ) (+ upper view, - lower) and 1/(4Δα) (+ right column, - left).
+__global__ void __launch_bounds__(128) k_deriv_half_T(FilterParams p, const float *__restrict__ g1T, int64_t nu,
+                                                      int items, float *__restrict__ out)
+{
+    const int lr = blockIdx.x * blockDim.x + threadIdx.x, mr = blockIdx.y;
+    const int nc = p.nc, nr = p.nr, rnc = nc + 1;
+    if (lr >= rnc) return;
+    const int64_t per = nu + 1;                                   // raw views of an item
+    const size_t rs = (size_t)nr * nc, rrs = (size_t)(nr + 1) * rnc;
+    const float sq = 0.25f * p.inv_2dlam * 2.f, sa = 0.25f * p.inv_dalpha;
+    for (int64_t z = blockIdx.z; z < per * items; z += gridDim.z) {
+        const int64_t item = z / per, r = z - item * per;
+        const float *gi = g1T + (size_t)item * nu * rs;
+        float acc = 0.f;
+#pragma unroll
+        for (int dk = 0; dk < 2; ++dk) {
+            const int64_t k = r - 1 + dk;                         // dk 0: this raw view is k's upper view
+            if (k < 0 || k >= nu) continue;
+            const float cq = dk == 0 ? sq : -sq;
+#pragma unroll
+            for (int dm = 0; dm < 2; ++dm) {
+                const int m = mr - 1 + dm;
+                if (m < 0 || m >= nr) continue;
+#pragma unroll
+                for (int dl = 0; dl < 2; ++dl) {
+                    const int l = lr - 1 + dl;                    // dl 0: this raw column is l's right column
+                    if (l < 0 || l >= nc) continue;
+                    acc = fmaf(gi[(size_t)k * rs + (size_t)m * nc + l], cq + (dl == 0 ? sa : -sa), acc);
+                }
+            }
+        }
+        out[((size_t)item * per + r) * rrs + (size_t)mr * rnc + lr] = acc;
+    }
+}
+
 void launch_deriv_T(const FilterParams &p, const float *g1T, int64_t nu, float *out, cudaStream_t s, int items)
 {
+    if (p.half) {
+        const int64_t nz = std::min<int64_t>((nu + 1) * items, 65535);
+        k_deriv_half_T<<<dim3((p.nc + 1 + 127) / 128, p.nr + 1, (unsigned)nz), 128, 0, s>>>(p, g1T, nu, items, out);
+        return;
+    }
     const int64_t nz = std::min<int64_t>((nu + 2) * items, 65535);
     k_deriv_T<<<dim3((p.nc + 127) / 128, p.nr, (unsigned)nz), 128, 0, s>>>(p, g1T, nu, items, out);
 }

@@ -63,7 +63,9 @@ struct ProfRecord { int stage; void *ev0; void *ev1; };
 }  // namespace kats
 
 struct katsevich_plan {
-    katsevich_geometry g{};
+    katsevich_geometry g{};                 // effective geometry of the filtered grid (tables, kernels)
+    katsevich_geometry graw{};              // the caller's geometry (raw sinogram, data generation)
+    bool half = false;                      // NEXT-4: Noo's half-sample derivative (g = half-shifted grid)
     int device = -1;
     bool precomputed = false;
     kats::HostTables t;
@@ -94,4 +96,5 @@ namespace kats {
 // precompute.cpp
 int validate(const katsevich_geometry &g, std::string &detail);
 int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string &detail);
+katsevich_geometry half_sample_geometry(const katsevich_geometry &g);   // DESIGN.md reading A25
 }  // namespace kats

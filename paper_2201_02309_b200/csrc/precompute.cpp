@@ -170,13 +170,32 @@ int validate(const katsevich_geometry &g, std::string &detail)
     if (g.nx < 1 || g.ny < 1 || g.nz_per_pitch < 1) return bad("empty voxel grid");
     if (!(g.dx > 0) || !(g.dy > 0)) return bad("voxel spacing <= 0");
     if (g.n_psi != 0 && g.n_psi < 2) return bad("n_psi must be 0 or >= 2");
-    if (g.flags != 0) return bad("flags must be 0");
+    if (g.flags & ~KATS_FLAG_HALF_SAMPLE) return bad("unknown flags");
+    if ((g.flags & KATS_FLAG_HALF_SAMPLE) && (g.n_rows < 3 || g.n_cols < 3))
+        return bad("the half-sample derivative needs n_rows >= 3 and n_cols >= 3");
+    if ((g.flags & KATS_FLAG_HALF_SAMPLE) && g.n_rows > 65) return bad("the half-sample derivative needs n_rows <= 65");
     if (!std::isfinite(g.lambda0) || !std::isfinite(g.z0) || !std::isfinite(g.alpha_offset)) return bad("non-finite parameter");
     double half_fan = (0.5 * (g.n_cols - 1) + std::fabs(g.alpha_offset)) * g.d_alpha;
     if (!(half_fan < 0.5 * kPi)) return bad("detector fan reaches |alpha| >= pi/2");
     Geo o = derive(g);
     if (g.r_fov < 0 || !(o.r_fov < g.R)) return bad("r_fov >= R (FOV cylinder must lie inside the helix)");
     return KATS_OK;
+}
+
+// Noo's half-sample derivative (NEXT-4; reading A25) produces g1 at (λ_{k+½}, α_{l+½},
+// w_{m+½}): the samples of a detector with one row and one column fewer (same spacings and α offset)
+// on the same helix parametrised from λ0 + Δλ/2, z0 + h Δλ/2 (a(λ_{k+½}) = a'(λ_k), Eq. 1).  Steps
+// 2-7 and every table use that grid; the voxel grid and the FOV are unchanged.
+katsevich_geometry half_sample_geometry(const katsevich_geometry &g)
+{
+    katsevich_geometry e = g;
+    const double dlam = 2.0 * kPi / g.views_per_turn;
+    e.n_rows = g.n_rows - 1;
+    e.n_cols = g.n_cols - 1;
+    e.lambda0 = g.lambda0 + 0.5 * dlam;
+    e.z0 = g.z0 + g.pitch / (2.0 * kPi) * 0.5 * dlam;
+    e.flags = 0;
+    return e;
 }
 
 int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string &detail)

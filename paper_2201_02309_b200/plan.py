@@ -23,7 +23,7 @@ def geometry_from_config(cfg: dict) -> KatsevichGeometry:
         r_fov=cfg.get("r_fov", 0.0), n_rows=cfg["n_rows"], d_w=cfg["d_w"], n_cols=cfg["n_cols"],
         d_alpha=cfg["d_alpha"], alpha_offset=cfg.get("alpha_offset", 0.0),
         views_per_turn=cfg["views_per_turn"], nx=cfg["nx"], ny=cfg["ny"], dx=cfg["dx"],
-        dy=cfg.get("dy", cfg["dx"]), nz_per_pitch=cfg["nz"], n_psi=cfg.get("n_psi", 0), flags=0)
+        dy=cfg.get("dy", cfg["dx"]), nz_per_pitch=cfg["nz"], n_psi=cfg.get("n_psi", 0), flags=cfg.get("flags", 0))
 
 
 def _stream_handle(stream):
@@ -101,14 +101,22 @@ class Plan:
         self._check(lib().katsevich_table_info(self._h, ctypes.byref(n), ctypes.byref(lo), ctypes.byref(hi)))
         return dict(n_psi=n.value, bp_lo=lo.value, bp_hi=hi.value)
 
+    def filtered_grid(self):
+        """(rows, cols) of the filtered data and the tables: the detector, or for the half-sample
+        derivative (KATS_FLAG_HALF_SAMPLE) the half-shifted grid with one row and column fewer."""
+        g = self.geometry
+        h = 1 if g.flags & 1 else 0
+        return g.n_rows - h, g.n_cols - h
+
     def export_tables(self):
         g = self.geometry
+        nr_f, nc_f = self.filtered_grid()
         info = self.table_info()
         nvox = (g.nz_per_pitch, g.ny, g.nx)
         out = dict(pi_first=np.empty(nvox, np.int32), pi_last=np.empty(nvox, np.int32),
                    w_first=np.empty(nvox), w_last=np.empty(nvox),
-                   fr_idx=np.empty((info["n_psi"], g.n_cols), np.int32), fr_frac=np.empty((info["n_psi"], g.n_cols)),
-                   br_idx=np.empty((g.n_rows, g.n_cols), np.int32), br_frac=np.empty((g.n_rows, g.n_cols)))
+                   fr_idx=np.empty((info["n_psi"], nc_f), np.int32), fr_frac=np.empty((info["n_psi"], nc_f)),
+                   br_idx=np.empty((nr_f, nc_f), np.int32), br_frac=np.empty((nr_f, nc_f)))
         P32, PD = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)
         self._check(lib().katsevich_export_tables(
             self._h, out["pi_first"].ctypes.data_as(P32), out["pi_last"].ctypes.data_as(P32),
@@ -273,9 +281,10 @@ class Plan:
         g = self.geometry
         npsi = self.table_info()["n_psi"]
         dev = sino.device
-        gF = torch.empty((n_out, g.n_rows, g.n_cols), dtype=torch.float32, device=dev)
-        g3 = torch.empty((n_out, npsi, g.n_cols), dtype=torch.float32, device=dev) if "g3" in stages else None
-        g4 = torch.empty((n_out, npsi, g.n_cols), dtype=torch.float32, device=dev) if "g4" in stages else None
+        nr_f, nc_f = self.filtered_grid()
+        gF = torch.empty((n_out, nr_f, nc_f), dtype=torch.float32, device=dev)
+        g3 = torch.empty((n_out, npsi, nc_f), dtype=torch.float32, device=dev) if "g3" in stages else None
+        g4 = torch.empty((n_out, npsi, nc_f), dtype=torch.float32, device=dev) if "g4" in stages else None
         self._check(lib().katsevich_filter(self._h, _ptr(sino), sino_first_view, sino.shape[0], out_first_view, n_out,
                                            _ptr(g3) if g3 is not None else None,
                                            _ptr(g4) if g4 is not None else None, _ptr(gF), _stream_handle(stream)))

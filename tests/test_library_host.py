@@ -114,7 +114,7 @@ def test_td_warning_when_rows_too_short():
 
 @pytest.mark.parametrize("field,value", [("R", -1.0), ("D", 0.0), ("pitch", 0.0), ("views_per_turn", 2),
                                          ("n_cols", 1), ("n_rows", 1), ("d_w", 0.0), ("r_fov", 600.0),
-                                         ("flags", 1), ("n_psi", 1), ("d_alpha", 0.5)])
+                                         ("flags", 2), ("n_psi", 1), ("d_alpha", 0.5)])
 def test_invalid_geometry_rejected(field, value):
     g = k.geometry_from_config(configs.get("T1"))
     setattr(g, field, value)
@@ -180,3 +180,27 @@ def test_hilbert_hankel_core_table(nc):
         ref = np.where(np.abs(d) <= nc - 1, taps[np.clip(d + nc - 1, 0, 2 * nc - 2)], np.float32(0))
         assert np.array_equal(hi + lo, ref)
         assert not np.any(hi.view(np.uint32) & 0x1FFF)          # exactly representable in TF32
+
+
+@pytest.mark.parametrize("name", ["T1", "T3", "C1"])
+def test_half_sample_plan_tables_and_views(name):
+    """KATS_FLAG_HALF_SAMPLE (NEXT-4, reading A25): the plan's tables are those of the half-shifted
+    grid — bit-exact against the oracle's independent tables of oracle.half_sample_cfg — and a
+    pitch's raw views are the shifted grid's slab [K_lo, K_hi] plus the one raw view above it."""
+    from oracle import oracle
+    cfg = dict(configs.get(name), flags=1)
+    vc = oracle.half_sample_cfg(configs.get(name))
+    p = k.Plan(cfg, device=-1)
+    p.precompute()
+    assert p.filtered_grid() == (cfg["n_rows"] - 1, cfg["n_cols"] - 1)
+    t = p.export_tables()
+    fi, ff, bi, bf = oracle.rebin_tables(vc)
+    assert np.array_equal(fi, t["fr_idx"]) and np.array_equal(bi, t["br_idx"])
+    assert np.abs(ff - t["fr_frac"]).max() < 1e-9 and np.abs(bf - t["br_frac"]).max() < 1e-9
+    kf, kl, wf, wl = oracle.bp_weights(vc, 0)
+    m = kl >= kf
+    assert np.array_equal(np.where(m, kf, 0), t["pi_first"])
+    assert np.array_equal(np.where(m, kl, -1), t["pi_last"])
+    assert np.abs(wf - t["w_first"]).max() < 1e-9 and np.abs(wl - t["w_last"]).max() < 1e-9
+    fv, nv = oracle.pitch_slab(vc, 2)                 # [K_lo - 1, K_hi + 1] of the shifted grid
+    assert p.pitch_views(2) == (fv + 1, nv - 1)
