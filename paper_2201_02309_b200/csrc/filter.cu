@@ -1284,9 +1284,9 @@ __global__ void __launch_bounds__(256) k_bwd_rebin_cos_rows(FilterParams p, int 
             for (int j = 0; j < VPB; ++j) {
                 const float out = eidx[i] >= 0 && j < nv ? eca[i] * fmaf(efr[i], gb[i][j] - ga[i][j], ga[i][j]) : 0.f;
                 tb[j * tsz + eoff[i]] = out;
-                if (p.gF && eidx[i] >= 0 && j < nv) {
-                    const int mm = eoff[i] / ld, ll = eoff[i] - mm * ld;      // debug path only
-                    if (ll < cols) p.gF[((size_t)(v0 + j) * nr + mm - 2) * nc + l0 + ll] = out;
+                if (p.gF && j < nv) {                                   // debug path only
+                    const int mm = eoff[i] / ld, ll = eoff[i] - mm * ld;
+                    if (mm >= 2 && mm < nr + 2 && ll < cols) p.gF[((size_t)(v0 + j) * nr + mm - 2) * nc + l0 + ll] = out;
                 }
             }
         }
