@@ -284,11 +284,14 @@ int katsevich_profile_read(katsevich_plan *plan, katsevich_stats *out, int reset
 /* Variant of the most recent step-7 (K5) launch of this plan: 0 none yet,
  * KATS_BP_L1 (chunked kernel, global-memory reads; used for plans whose
  * footprints leave the detector), KATS_BP_WINDOW (register sliding window),
- * KATS_BP_TMEM (tensor-memory sliding window, the default).  The environment
- * variable KATS_BP_KERNEL=window|l1 forces a variant for A/B tests. */
+ * KATS_BP_TMEM (tensor-memory sliding window, the default), KATS_BP_ITEMS (batches whose windows
+ * hold <= 8 slices, e.g. the paper's 16-slab training batch: the CTA's slabs share each view's
+ * geometry).  The environment variables KATS_BP_KERNEL=window|l1 and KATS_BP_ITEMS=0|N force variants
+ * for A/B tests. */
 #define KATS_BP_L1 1
 #define KATS_BP_WINDOW 2
 #define KATS_BP_TMEM 3
+#define KATS_BP_ITEMS 4   /* batches of narrow-window slabs (C5): per-view geometry shared by the CTA's slabs */
 int katsevich_bp_kernel(const katsevich_plan *plan);
 
 void katsevich_destroy(katsevich_plan *plan);

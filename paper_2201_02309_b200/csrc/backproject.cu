@@ -1017,6 +1017,269 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"((unsigned)p.tmem_alloc));
 }
 
+// ---------------------------------------------------------------------------
+// Items kernel (batches of one-pitch slabs whose windows hold <= 8 slices: the paper's training
+// layer, C5).  All NI slabs of a CTA share the tile's geometry, so the per-(x, y, view) setup — v*,
+// α*, the column, the row positions of the lane's open slices — is computed once per view and
+// reused for the NI slabs, whose boxes stream through the ring one slab after the other (slot
+// sequence (view 0, slab 0), (view 0, slab 1), ...).  A lane's accumulators live in tensor memory,
+// 8 columns per slab in window-relative order (register j = slice t_lo + j of the lane): when a
+// lane's window closes a slice it writes that slice's interior sum and shifts its 8 columns down
+// (a per-lane flush; TMEM ld/st are warp-wide but each lane owns its row), so sampling touches only
+// the lane's own open slices — a warp loop over the warp's widest window with a per-lane predicate,
+// no samples of slices outside a lane's window.  The fractional end views and the Δλ/2π scale
+// follow in k_bp_ends_add.
+// ---------------------------------------------------------------------------
+constexpr int kMaxItemSlots = 16;
+
+template <bool POLY>
+__global__ void __launch_bounds__(kWsThreads, 2) k_bp_items(const __grid_constant__ QMaps qm, BPParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch, NI = p.bp_items;
+    const int vq = (BW * NQ + 7) & ~7;                                   // quads per slot (one slab's box)
+    float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
+    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vq * 16);
+    __shared__ __align__(8) unsigned long long s_full[kMaxItemSlots], s_empty[kMaxItemSlots];
+    __shared__ int s_k0, s_k1;
+    __shared__ unsigned s_tmem;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = warp == kConsumerWarps;
+    const int2 bt = bp_tile(p);
+    const int ix = bt.x * TX + (warp & 1) * 8 + (lane & 7);
+    const int iy = bt.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int item0 = blockIdx.z * NI;
+    const bool inside = !producer && ix < p.nx && iy < p.ny;
+    const size_t plane = (size_t)p.nx * p.ny;
+    const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const int2 *pik = p.pi_k + col;
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
+    const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
+
+    if (warp == 0) {    // TMEM: NI x 8 columns per warp, warps w and w + 4 share a lane quarter
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"((unsigned)__cvta_generic_to_shared(&s_tmem)), "r"((unsigned)p.tmem_alloc));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        s_k0 = INT_MAX; s_k1 = INT_MIN;
+        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, TX * TY); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int K0 = INT_MAX, K1 = INT_MIN;
+    if (inside) {
+        const int2 e0 = pik[0];
+        if (e0.x <= e0.y) { K0 = e0.x + 1; K1 = pik[(size_t)(p.nz - 1) * plane].y - 1; }
+    }
+    int wk0 = K0, wk1 = K1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wk0 = min(wk0, __shfl_xor_sync(0xffffffffu, wk0, o));
+        wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
+    }
+    if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    __syncthreads();
+    const int KC0 = s_k0, KC1 = s_k1;
+    const int NV = KC1 - KC0 + 1;
+    const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
+    {
+        const float xa = p.x0 + bt.x * TX * p.dx, ya = p.y0 + bt.y * TY * p.dy;
+        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya);
+    }
+    __syncthreads();
+
+    if (producer) {
+        if (NV > 0 && lane == 0) {
+            const int vbase = (int)(p.off0 + (int64_t)item0 * p.item_views) + KC0;
+            int sl = 0;
+            unsigned phase = 0;
+            int seq = 0;
+            for (int n = 0; n < NV; ++n) {
+                const int bc = boxc[n], cls = bc >> 16;
+                const unsigned bytes = (unsigned)(p.box_w[cls] * NQ) * 16u;
+                for (int b = 0; b < NI; ++b, ++seq) {
+                    if (seq >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
+                    const unsigned full = full0 + 8u * sl;
+                    mbar_expect_tx(full, bytes);
+                    tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qm.m[cls], 2 * p.q_lo, bc & 0xFFFF,
+                            vbase + (int)(b * p.item_views) + n, full);
+                    if (++sl == S) { sl = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else {
+        // ---- consumer warps ----
+        const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * NI * 8);
+        {
+            float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int b = 0; b < NI; ++b) tm_st8(tw + 8u * b, z);
+            tm_wait_st();
+        }
+        const unsigned slot0 = stage_sa - (kMagicBits + (unsigned)p.q_lo) * 16u;
+        float *out = p.vol + (size_t)item0 * p.nz * plane + col;
+        const size_t item_stride = (size_t)p.nz * plane;
+        const bool active_col = inside && K0 <= K1;
+        int t_lo = 0, t_hi = -1;
+        int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
+        int sl = 0;
+        unsigned phase = 0;
+        for (int n = 0; n < NV; ++n) {
+            const int k = KC0 + n;
+            int d = 0;                                               // slices this lane closes at view k
+            if (active_col) {
+                while (k >= next_open) {
+                    ++t_hi;
+                    if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+                    next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
+                }
+                while (k >= next_close) {
+                    ++t_lo; ++d;
+                    next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
+                }
+            }
+            const int dmax = __reduce_max_sync(0xffffffffu, d);
+            if (dmax > 0) {
+                // per-lane flush: the closed slices' interior sums go out, the window shifts down
+                for (int b = 0; b < NI; ++b) {
+                    float a8[8];
+                    tm_ld8_nowait(tw + 8u * b, a8);
+                    tm_wait_ld8(a8);
+                    for (int st = 0; st < dmax; ++st) {
+                        const bool f = st < d;
+                        if (f) out[(size_t)b * item_stride + (size_t)(t_lo - d + st) * plane] = a8[0];
+#pragma unroll
+                        for (int j = 0; j < 7; ++j) a8[j] = f ? a8[j + 1] : a8[j];
+                        a8[7] = f ? 0.f : a8[7];
+                    }
+                    tm_st8(tw + 8u * b, a8);
+                }
+                tm_wait_st();
+            }
+            const bool work = active_col && t_hi >= t_lo && k <= K1;
+            const int n_act = work ? t_hi - t_lo + 1 : 0;
+            const int nw = __reduce_max_sync(0xffffffffu, n_act);
+            if (nw > 0) {
+                // the lane's geometry for view k, shared by the NI slabs
+                const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+                float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f;
+                int ci = 0;
+                if (work) {
+                    const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+                    const float u = fmaf(y, vg.x, -x * vg.y);
+                    const float inv_v = rcp_approx(vstar);
+                    float colpos;
+                    if (POLY) {
+                        const float tt = u * inv_v, q = tt * tt;
+                        float a = p.at[6];
+                        a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+                        a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+                        colpos = fmaf(tt, a, p.col_c);
+                    } else {
+                        colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+                    }
+                    const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
+                    const int l = __float2int_rz(cp);
+                    const float fa = cp - __int2float_rn(l);
+                    w1 = fa * inv_v;
+                    w0 = inv_v - w1;
+                    const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+                    step = sc * p.dz;
+                    base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));   // slice t_lo
+                    ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
+                }
+                // row positions and quad offsets of the lane's window entries j = 0..7
+                float pj[8];
+                unsigned oj[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    pj[j] = fmaf((float)j, step, base);
+                    oj[j] = __float_as_uint(pj[j] + p.qmagic) * 16u;
+                }
+                const unsigned cbase = (unsigned)ci * p.col_bytes;
+                for (int b = 0; b < NI; ++b) {
+                    mbar_wait(full0 + 8u * sl, phase);
+                    const unsigned colbase = (slot0 + (unsigned)sl * p.slot_bytes + cbase) ^ p.zero;
+                    float a8[8];
+                    tm_ld8_nowait(tw + 8u * b, a8);
+                    float v[8][2];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        v[j][0] = v[j][1] = 0.f;
+                        if (j < nw && j < n_act) {
+                            const float4 g = lds128(colbase + oj[j]);
+                            upk(fma2(pk(g.z, g.w), pk(pj[j], pj[j]), pk(g.x, g.y)), v[j][0], v[j][1]);
+                        }
+                    }
+                    mbar_arrive(empty0 + 8u * sl);
+                    if (++sl == S) { sl = 0; phase ^= 1u; }
+                    tm_wait_ld8(a8);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j < nw) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
+                    tm_st8(tw + 8u * b, a8);
+                }
+                tm_wait_st();
+            } else {
+                for (int b = 0; b < NI; ++b) {                       // nothing to sample: release the slots
+                    mbar_wait(full0 + 8u * sl, phase);
+                    mbar_arrive(empty0 + 8u * sl);
+                    if (++sl == S) { sl = 0; phase ^= 1u; }
+                }
+            }
+        }
+        // every window has closed by K1 + 1: the lane's remaining open slices t_lo .. nz-1 (the TMEM loads
+        // are warp-wide, the stores per lane)
+        for (int b = 0; b < NI; ++b) {
+            float a8[8];
+            tm_ld8_nowait(tw + 8u * b, a8);
+            tm_wait_ld8(a8);
+            if (active_col) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (t_lo + j < p.nz) out[(size_t)b * item_stride + (size_t)(t_lo + j) * plane] = a8[j];
+            } else if (inside) {
+                for (int t = 0; t < p.nz; ++t) out[(size_t)b * item_stride + (size_t)t * plane] = 0.f;
+            }
+        }
+    }
+    // release TMEM once every consumer warp is done with it
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"((unsigned)p.tmem_alloc));
+}
+
+// vol = (interior sum + the two fractional end views) * Δλ/2π for every voxel (after k_bp_items)
+template <bool POLY>
+__global__ void __launch_bounds__(128) k_bp_ends_add_t(BPParams p)
+{
+    const int ix = blockIdx.x * blockDim.x + threadIdx.x, iy = blockIdx.y;
+    const int t = blockIdx.z % p.nz, item = blockIdx.z / p.nz;
+    if (ix >= p.nx) return;
+    const size_t plane = (size_t)p.nx * p.ny, col = (size_t)iy * p.nx + ix;
+    float *o = p.vol + (size_t)item * p.nz * plane + (size_t)t * plane + col;
+    const int2 e = p.pi_k[(size_t)t * plane + col];
+    float v = *o;
+    if (e.x <= e.y) {
+        const float2 w = p.pi_w[(size_t)t * plane + col];
+        const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item * p.item_views) * p.viewbytes);
+        const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+        u64 ends = 0ull;
+        tap_checked<POLY>(p, qbase, e.x, x, y, 0.f, t, w.x, ends);
+        tap_checked<POLY>(p, qbase, e.y, x, y, 0.f, t, w.y, ends);
+        float ea, eb;
+        upk(ends, ea, eb);
+        v += ea + eb;
+    }
+    *o = v * p.scale;
+}
+
 // plain gF [n][nr][nc] -> column-major sum/difference tap quads [n][nc][nr+2] (debug entry point)
 __global__ void k_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc)
 {
@@ -1591,6 +1854,48 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
             if (p.poly) launch_tmem<true>(q, vp, gw, sm, qmap, s);
             else launch_tmem<false>(q, vp, gw, sm, qmap, s);
             return KATS_BP_TMEM;
+        }
+    }
+    // items kernel: a batch of slabs whose windows hold <= 8 slices (C5): NI slabs per CTA share the
+    // per-view geometry (KATS_BP_ITEMS=0 disables, =N forces N slabs per CTA)
+    {
+        int ni = 0;
+        const char *ie = std::getenv("KATS_BP_ITEMS");
+        if (ie) ni = std::atoi(ie);
+        else if (p.n_items >= 4 && p.max_active <= 8) ni = p.n_items % 8 == 0 ? 8 : p.n_items % 4 == 0 ? 4 : 0;
+        if (ni > 0 && (!small_grid || ie) && p.staged && !p.checked && p.windows_monotone && p.max_active <= 8 &&
+            p.n_items % ni == 0 && ni <= 16 && 2 * p.nq_s <= 256 && p.fp_cols_column <= 256 && p.gq_views > 0) {
+            BPParams q = p;
+            q.bp_items = ni;
+            q.tmem_alloc = 32;
+            while (q.tmem_alloc < 2 * 8 * ni) q.tmem_alloc *= 2;       // 2 warps per TMEM lane quarter
+            const int vq = (p.fp_cols_column * p.nq_s + 7) & ~7;
+            q.slot_bytes = 16u * (unsigned)vq;
+            q.col_bytes = 16u * (unsigned)p.nq_s;
+            // ring: as many one-slab slots (<= 16) as leave room for 2 CTAs per SM (and TMEM: 2 x alloc <= 512)
+            q.nbatch = kMaxItemSlots;
+            auto smem_of = [&](const BPParams &r) {
+                return kBoxesBytes + (size_t)r.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)r.max_cta_views +
+                       16 * (size_t)r.tail_quads;
+            };
+            while (q.nbatch > 2 && smem_of(q) > 110 * 1024) --q.nbatch;
+            const size_t sm = smem_of(q);
+            QMaps qmap;
+            if (q.tmem_alloc <= 256 && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
+                dim3 gw = p.tile_order ? dim3(((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY), 1, p.n_items / ni)
+                                       : dim3((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / ni);
+                if (p.poly) {
+                    smem_opt_in((const void *)k_bp_items<true>, sm);
+                    k_bp_items<true><<<gw, kWsThreads, sm, s>>>(qmap, q);
+                } else {
+                    smem_opt_in((const void *)k_bp_items<false>, sm);
+                    k_bp_items<false><<<gw, kWsThreads, sm, s>>>(qmap, q);
+                }
+                dim3 ge((p.nx + 127) / 128, p.ny, p.nz * p.n_items);
+                if (p.poly) k_bp_ends_add_t<true><<<ge, 128, 0, s>>>(q);
+                else k_bp_ends_add_t<false><<<ge, 128, 0, s>>>(q);
+                return KATS_BP_ITEMS;
+            }
         }
     }
     BPParams q = p;

@@ -298,7 +298,7 @@ class Plan:
                                                 _stream_handle(stream)))
         return out
 
-    BP_KERNELS = {0: None, 1: "k_backproject", 2: "k_bp_window", 3: "k_bp_tmem"}
+    BP_KERNELS = {0: None, 1: "k_backproject", 2: "k_bp_window", 3: "k_bp_tmem", 4: "k_bp_items"}
 
     def bp_kernel(self):
         """Name of the step-7 kernel variant the last backprojection launched

@@ -173,6 +173,33 @@ def test_coverage_error_names_pitches():
     assert ei.value.code == -4 and "reconstructible" in str(ei.value)
 
 
+@pytest.mark.parametrize("n_slabs,ni", [(4, "4"), (6, "2"), (3, "3")])
+def test_batch_items_kernel_matches_oracle(n_slabs, ni, monkeypatch):
+    """The items kernel (batches whose windows hold <= 8 slices, the default for C5-shaped batches:
+    the slabs of a CTA share each view's geometry, per-lane window-relative TMEM accumulators)
+    forced on T2 with 4, 2 and 3 slabs per CTA, against the oracle per slab."""
+    import torch
+    from oracle import oracle
+    from synth import configs, synth
+    monkeypatch.setenv("KATS_BP_ITEMS", ni)
+    cfg = configs.get("T2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    slabs, refs, contrasts = [], [], []
+    for s in range(n_slabs):
+        ph = configs.random_ellipsoids(10 + s, 6, 180.0, -5.0, cfg["P"] + 5.0)
+        sino = synth.project(cfg, ph, v0, nv)
+        slabs.append(sino)
+        refs.append(oracle.reconstruct(cfg, sino, v0, 0, 1))
+        t = synth.volume_truth(cfg, ph, 0)
+        contrasts.append(t.max() - t.min())
+    got = p.reconstruct_batch(torch.from_numpy(np.stack(slabs)).cuda())
+    torch.cuda.synchronize()
+    assert p.bp_kernel() == "k_bp_items"
+    for b in range(n_slabs):
+        _check(got[b].cpu().numpy(), refs[b], contrasts[b])
+
+
 @pytest.mark.parametrize("variant,vp,kernel", [(None, None, "k_backproject"), ("tmem", None, "k_bp_tmem"),
                                                ("tmem", "1", "k_bp_tmem"), ("tmem", "2", "k_bp_tmem"),
                                                ("window", None, "k_bp_window"), ("window", "winv1", "k_bp_window"),
