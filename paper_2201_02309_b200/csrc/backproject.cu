@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include <cuda.h>
 
@@ -1201,27 +1202,35 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_items(const __grid_constan
                     oj[j] = __float_as_uint(pj[j] + p.qmagic) * 16u;
                 }
                 const unsigned cbase = (unsigned)ci * p.col_bytes;
-                for (int b = 0; b < NI; ++b) {
+                const unsigned amask = (1u << n_act) - 1u;               // the lane's open window entries
+                // one slab: its box in slot sl; J window entries sampled (J = 4 covers most views)
+                auto slab = [&](auto Jc, int b) {
+                    constexpr int J = decltype(Jc)::value;
                     mbar_wait(full0 + 8u * sl, phase);
                     const unsigned colbase = (slot0 + (unsigned)sl * p.slot_bytes + cbase) ^ p.zero;
                     float a8[8];
                     tm_ld8_nowait(tw + 8u * b, a8);
-                    float v[8][2];
+                    float4 g[J];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        v[j][0] = v[j][1] = 0.f;
-                        if (j < nw && j < n_act) {
-                            const float4 g = lds128(colbase + oj[j]);
-                            upk(fma2(pk(g.z, g.w), pk(pj[j], pj[j]), pk(g.x, g.y)), v[j][0], v[j][1]);
-                        }
+                    for (int j = 0; j < J; ++j) {
+                        g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (amask & (1u << j)) g[j] = lds128(colbase + oj[j]);   // only the lane's own slices
                     }
                     mbar_arrive(empty0 + 8u * sl);
                     if (++sl == S) { sl = 0; phase ^= 1u; }
                     tm_wait_ld8(a8);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (j < nw) a8[j] = fmaf(v[j][0], w0, fmaf(v[j][1], w1, a8[j]));
+                    for (int j = 0; j < J; ++j) {
+                        float v0, v1;
+                        upk(fma2(pk(g[j].z, g[j].w), pk(pj[j], pj[j]), pk(g[j].x, g[j].y)), v0, v1);
+                        a8[j] = fmaf(v0, w0, fmaf(v1, w1, a8[j]));
+                    }
                     tm_st8(tw + 8u * b, a8);
+                };
+                if (nw <= 4) {
+                    for (int b = 0; b < NI; ++b) slab(std::integral_constant<int, 4>{}, b);
+                } else {
+                    for (int b = 0; b < NI; ++b) slab(std::integral_constant<int, 8>{}, b);
                 }
                 tm_wait_st();
             } else {
