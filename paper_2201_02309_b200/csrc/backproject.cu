@@ -1865,13 +1865,14 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
             return KATS_BP_TMEM;
         }
     }
-    // items kernel: a batch of slabs whose windows hold <= 8 slices (C5): NI slabs per CTA share the
-    // per-view geometry (KATS_BP_ITEMS=0 disables, =N forces N slabs per CTA)
+    // items kernel (KATS_BP_ITEMS=N: N slabs per CTA): a batch of slabs whose windows hold <= 8 slices
+    // (C5), the CTA's slabs sharing each view's geometry.  Measured slower than the register window
+    // with two slabs per CTA (C5 K5 busy 2.43-2.48 vs 2.33 ms, scripts/ab/gpu_items2.sh: 2 CTAs per
+    // SM for TMEM and a 6-box ring leave the box delivery and TMEM loads exposed), so opt-in only
     {
         int ni = 0;
         const char *ie = std::getenv("KATS_BP_ITEMS");
         if (ie) ni = std::atoi(ie);
-        else if (p.n_items >= 4 && p.max_active <= 8) ni = p.n_items % 8 == 0 ? 8 : p.n_items % 4 == 0 ? 4 : 0;
         if (ni > 0 && (!small_grid || ie) && p.staged && !p.checked && p.windows_monotone && p.max_active <= 8 &&
             p.n_items % ni == 0 && ni <= 16 && 2 * p.nq_s <= 256 && p.fp_cols_column <= 256 && p.gq_views > 0) {
             BPParams q = p;
