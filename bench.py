@@ -136,8 +136,17 @@ def bp_smem_bytes_per_update():
 
 
 def smem_peak_gbs(sm_mhz):
-    # shared-memory data pipe: 128 B/clk per SM (1 LSU wavefront/clk), 148 SMs
-    return 148 * 128 * sm_mhz * 1e6 / 1e9
+    """K5's roofline denominator: the MEASURED LDS.128 throughput of this GPU model
+    (scripts/micro/smem_peak.cu, profiles/smem_peak.json) when present, else the derived
+    148 SMs x 128 B/clk (one LSU wavefront per clock) at sm_mhz.  Returns (GB/s, source)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "smem_peak.json")) as f:
+            d = json.load(f)
+        return float(d["smem_lds128_gbs"]), ("measured LDS.128 throughput (scripts/micro/smem_peak.cu, "
+                                              f"profiles/smem_peak.json: {d['bytes_per_clk_per_sm_at_max']:.1f} "
+                                              "B/clk/SM at the max clock)")
+    except Exception:
+        return 148 * 128 * sm_mhz * 1e6 / 1e9, f"derived: 148 SMs x 128 B/clk x {sm_mhz} MHz"
 
 
 PAPER_CONTEXT = {
@@ -454,7 +463,7 @@ def run_ours(args):
     achieved_tflops = U_rank * bp_flops_per_update() / (k5_busy * 1e-3) / 1e12
     peaks, src = _peaks()
     fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    smem_peak = smem_peak_gbs(peaks.get("sm_max_mhz", 1965.0))
+    smem_peak, smem_src = smem_peak_gbs(peaks.get("sm_max_mhz", 1965.0))
     achieved_smem = U_rank * bp_smem_bytes_per_update() / (k5_busy * 1e-3) / 1e9
     bp_kernel = plan.bp_kernel()
     share = {s: stats["busy_ms"][s] / args.steps / ms_step for s in stats["busy_ms"] if stats["busy_ms"][s] > 0}
@@ -498,8 +507,7 @@ def run_ours(args):
                      "bytes_per_update": bp_smem_bytes_per_update(),
                      "k5_busy_ms_per_step": k5_busy, "k5_launches_per_step": k5_launches_per_step,
                      "k5_ms_per_launch": k5_ms_launch, "k5_updates_per_s": U_rank / (k5_busy * 1e-3),
-                     "peak_source": f"148 SMs x 128 B/clk shared-memory pipe x {peaks.get('sm_max_mhz', 1965.0)} MHz "
-                                    f"({src} sm_max); DESIGN.md §5",
+                     "peak_source": smem_src + "; DESIGN.md §5",
                      "secondary_hbm": None if not ncu_traffic(cfg["name"]) else {
                          "achieved": ncu_traffic(cfg["name"]) / (iso["k5_ms_per_launch"] * 1e-3) / 1e9
                          if iso else None,
