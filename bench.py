@@ -329,26 +329,29 @@ def run_ours(args):
     # pitches after all filtering (KATS_PIPELINE=0, the default), so no other kernel shares the GPU
     # with it (differs from the timed region only when KATS_PIPELINE=1 is set) ----
     iso = None
-    if not batch:
-        old_env = os.environ.get("KATS_PIPELINE")
-        os.environ["KATS_PIPELINE"] = "0"
+    st_iso = None
+    saved = {e: os.environ.get(e) for e in ("KATS_PIPELINE", "KATS_FILTER_STREAMS")}
+    os.environ["KATS_PIPELINE"] = "0"
+    os.environ["KATS_FILTER_STREAMS"] = "1"       # one filter stream: every kernel runs alone
+    step()
+    torch.cuda.synchronize()
+    plan.profile_read(reset=True)
+    plan.profile_enable(True)
+    n_iso = 3
+    for _ in range(n_iso):
         step()
-        torch.cuda.synchronize()
-        plan.profile_read(reset=True)
-        plan.profile_enable(True)
-        n_iso = 3
-        for _ in range(n_iso):
-            step()
-        torch.cuda.synchronize()
-        st_iso = plan.profile_read(reset=True)
-        plan.profile_enable(False)
-        if old_env is None:
-            del os.environ["KATS_PIPELINE"]
+    torch.cuda.synchronize()
+    st_iso = plan.profile_read(reset=True)
+    plan.profile_enable(False)
+    for e, v in saved.items():
+        if v is None:
+            os.environ.pop(e, None)
         else:
-            os.environ["KATS_PIPELINE"] = old_env
-        k = "K5_backproject"
-        iso = {"k5_ms_per_launch": st_iso["ms"][k] / max(1, st_iso["launches"][k]),
-               "launches": st_iso["launches"][k] // n_iso}
+            os.environ[e] = v
+    k = "K5_backproject"
+    iso = {"k5_ms_per_launch": st_iso["ms"][k] / max(1, st_iso["launches"][k]),
+           "launches": st_iso["launches"][k] // n_iso}
+    st_iso = {"busy_ms": dict(st_iso["ms"]), "n": n_iso}
 
     # ---- e2e: host (pinned) in -> host out through katsevich_reconstruct_host ----
     e2e = None
@@ -499,6 +502,9 @@ def run_ours(args):
         "stage_busy_share_of_step": share,
         "filter_stages": filter_stage_rooflines(plan, cfg, stats, args.steps, n_filtered_views(plan, cfg, n_items, batch),
                                                 peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])),
+        "filter_stages_isolated": filter_stage_rooflines(plan, cfg, st_iso, st_iso["n"],
+                                                         n_filtered_views(plan, cfg, n_items, batch),
+                                                         peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])),
         "paper_context": PAPER_CONTEXT,
         "precompute_s": t_pre,
         "roofline": {"bound": "smem", "kernel": bp_kernel, "achieved": achieved_smem, "peak": smem_peak,
