@@ -355,18 +355,22 @@ def run_ours(args):
 
     # ---- e2e: host (pinned) in -> host out through katsevich_reconstruct_host ----
     e2e = None
-    if not batch:
+    if True:
         pin_in = torch.from_numpy(host_in).pin_memory()
         pin_out = torch.empty(vol_shape, dtype=torch.float32).pin_memory()
+        if batch:       # the training batch from host memory: katsevich_reconstruct_batch_host
+            run_host = lambda: plan.reconstruct_batch_host(pin_in, out_host=pin_out, stream=stream)
+        else:
+            run_host = lambda: plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
         for _ in range(2):
-            plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
+            run_host()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t1 = time.perf_counter()
         ne = max(3, min(args.steps, 10))
         for _ in range(ne):
-            plan.reconstruct_host(pin_in, v0, first_pitch, pitches, out_host=pin_out, stream=stream)
+            run_host()
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t1) * 1e3 / ne
         if world > 1:

@@ -151,6 +151,17 @@ int katsevich_reconstruct_grouped(katsevich_plan *plan, const float *sino, int64
 int katsevich_reconstruct_batch(katsevich_plan *plan, const float *slabs, int32_t B, float *vols,
                                 void *workspace, size_t workspace_bytes, void *cuda_stream);
 
+/* Workspace bytes for katsevich_reconstruct_batch_host (adds the device slabs and volumes). */
+int katsevich_workspace_bytes_batch_host(const katsevich_plan *plan, int32_t B, size_t *bytes);
+
+/* katsevich_reconstruct_batch with HOST slabs [B][n_views][rows][cols] and volumes [B][nz][ny][nx]:
+ * the batch runs in groups of slabs whose host->device copies, filtering, backprojection and
+ * device->host copies overlap on separate streams (the paper's training layer fed from host
+ * memory, P:l.284-304).  Synchronises `cuda_stream` before returning; pinned host memory gives
+ * asynchronous copies.  Same results as katsevich_reconstruct_batch. */
+int katsevich_reconstruct_batch_host(katsevich_plan *plan, const float *host_slabs, int32_t B, float *host_vols,
+                                     void *workspace, size_t workspace_bytes, void *cuda_stream);
+
 /* katsevich_reconstruct with HOST sinogram and volume: copies the needed
  * views host->device, reconstructs and copies the volume device->host inside
  * the call (synchronises `cuda_stream` before returning).  Pinned host

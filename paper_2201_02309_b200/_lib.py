@@ -56,6 +56,8 @@ SIGNATURES = {
     "katsevich_reconstruct_grouped": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _SZ, _P, _I32,
                                                      ctypes.POINTER(ctypes.c_void_p)]),
     "katsevich_reconstruct_batch": (ctypes.c_int, [_P, _P, _I32, _P, _P, _SZ, _P]),
+    "katsevich_workspace_bytes_batch_host": (ctypes.c_int, [_P, _I32, ctypes.POINTER(_SZ)]),
+    "katsevich_reconstruct_batch_host": (ctypes.c_int, [_P, _P, _I32, _P, _P, _SZ, _P]),
     "katsevich_reconstruct_host": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _SZ, _P]),
     "katsevich_filter": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I32, _P, _P, _P, _P]),
     "katsevich_backproject": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _P, _P]),

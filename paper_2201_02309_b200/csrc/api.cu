@@ -886,6 +886,97 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     return KATS_OK;
 }
 
+int katsevich_workspace_bytes_batch_host(const katsevich_plan *p, int32_t B, size_t *bytes)
+{
+    int rc = katsevich_workspace_bytes(p, B, bytes);
+    if (rc) return rc;
+    const int64_t nslab = p->t.bp_hi - p->t.bp_lo + 2 + halo_lo(p);
+    const size_t vol = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
+    *bytes += align_up(sizeof(float) * raw_view_elems(p) * (size_t)nslab * B) + align_up(sizeof(float) * vol * B);
+    return KATS_OK;
+}
+
+// katsevich_reconstruct_batch with host slabs and volumes: the batch runs in groups of slabs; group
+// i's slabs are copied in on one stream, filtered on the highest-priority stream as soon as they
+// land, backprojected on a third, and their volumes copied out on a fourth while the next group
+// runs, so the PCIe transfers overlap the kernels.  Synchronises before returning.
+int katsevich_reconstruct_batch_host(katsevich_plan *p, const float *host_slabs, int32_t B, float *host_vols,
+                                     void *workspace, size_t workspace_bytes, void *cuda_stream)
+{
+    int rc = check_device_plan(p);
+    if (rc) return rc;
+    if (!host_slabs || !host_vols || !workspace) return KATS_ERR_NULL;
+    if (B < 1) return KATS_ERR_ARGUMENT;
+    size_t need, base;
+    katsevich_workspace_bytes_batch_host(p, B, &need);
+    katsevich_workspace_bytes(p, B, &base);
+    if (workspace_bytes < need) { p->detail = "workspace too small"; return KATS_ERR_WORKSPACE; }
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    if (!p->copy_stream) {
+        cudaStream_t a, b;
+        KCHECK(p, cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        KCHECK(p, cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+        p->copy_stream = a;
+        p->copy_stream2 = b;
+    }
+    rc = ensure_bp_streams(p);
+    if (rc) return rc;
+    const HostTables &t = p->t;
+    const size_t rs = raw_view_elems(p), qs = quad_view_elems(p);
+    const int64_t nbp = t.bp_hi - t.bp_lo + 1, nslab = nbp + 1 + halo_lo(p);
+    const size_t vpitch = (size_t)p->g.nx * p->g.ny * p->g.nz_per_pitch;
+    // groups of 4 slabs (even groups keep the window kernel's slab pairs)
+    const int gs = B % 4 == 0 ? 4 : B % 2 == 0 ? 2 : 1, ng = B / gs;
+    rc = ensure_events(p, 3 * (size_t)ng + 1);
+    if (rc) return rc;
+    float4 *gq = (float4 *)workspace;
+    float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
+    float *dslabs = (float *)((char *)workspace + base);
+    float *dvols = (float *)((char *)dslabs + align_up(sizeof(float) * rs * (size_t)nslab * B));
+    cudaStream_t cs = (cudaStream_t)p->copy_stream, ds = (cudaStream_t)p->copy_stream2;
+    cudaStream_t fs = (cudaStream_t)p->filter_stream, bs = (cudaStream_t)p->bp_streams[0];
+    cudaEvent_t e_start = (cudaEvent_t)p->sync_events[3 * ng];
+    KCHECK(p, cudaEventRecord(e_start, s));                   // the caller's pending work comes first
+    KCHECK(p, cudaStreamWaitEvent(cs, e_start, 0));
+    KCHECK(p, cudaStreamWaitEvent(fs, e_start, 0));
+    KCHECK(p, cudaStreamWaitEvent(bs, e_start, 0));
+    const size_t gslab = rs * (size_t)nslab * gs;             // floats of one group's slabs
+    for (int g = 0; g < ng; ++g) {
+        KCHECK(p, cudaMemcpyAsync(dslabs + g * gslab, host_slabs + g * gslab, sizeof(float) * gslab,
+                                  cudaMemcpyHostToDevice, cs));
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[g], cs));
+    }
+    for (int g = 0; g < ng; ++g) {
+        KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[g], 0));
+        rc = run_filter(p, dslabs + g * gslab + halo_lo(p) * rs, nbp * gs, gq + (size_t)g * gs * nbp * qs, scratch,
+                        nullptr, nullptr, nullptr, fs, false, nbp);
+        if (rc) return rc;
+        cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[ng + g];
+        KCHECK(p, cudaEventRecord(e_filt, fs));
+        KCHECK(p, cudaStreamWaitEvent(bs, e_filt, 0));
+        BPParams bp = bp_params(p);
+        bp.gq = gq;
+        bp.gq_views = nbp * B;
+        bp.off0 = -t.bp_lo + (int64_t)g * gs * nbp;
+        bp.item_views = nbp;
+        bp.n_items = gs;
+        bp.vol = dvols + (size_t)g * gs * vpitch;
+        { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(bp, bs); }
+        KCHECK(p, cudaGetLastError());
+        cudaEvent_t e_bp = (cudaEvent_t)p->sync_events[2 * ng + g];
+        KCHECK(p, cudaEventRecord(e_bp, bs));
+        KCHECK(p, cudaStreamWaitEvent(ds, e_bp, 0));
+        KCHECK(p, cudaMemcpyAsync(host_vols + (size_t)g * gs * vpitch, bp.vol, sizeof(float) * vpitch * gs,
+                                  cudaMemcpyDeviceToHost, ds));
+    }
+    KCHECK(p, cudaStreamSynchronize(ds));
+    KCHECK(p, cudaStreamSynchronize(cs));
+    KCHECK(p, cudaStreamSynchronize(bs));
+    KCHECK(p, cudaStreamSynchronize(fs));
+    KCHECK(p, cudaStreamSynchronize(s));
+    return KATS_OK;
+}
+
 int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_t s0, int64_t sn,
                                int32_t first_pitch, int32_t n_pitches, float *host_vol,
                                void *workspace, size_t workspace_bytes, void *cuda_stream)

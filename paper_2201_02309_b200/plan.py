@@ -185,6 +185,24 @@ class Plan:
                                                       _stream_handle(stream)))
         return out
 
+    def reconstruct_batch_host(self, slabs_host, out_host=None, stream=None):
+        """Host (numpy or pinned torch CPU) slabs [B][n_views][rows][cols] in, host volumes
+        [B][nz][ny][nx] out; copies overlapped with the kernels inside the call."""
+        import torch
+        if isinstance(slabs_host, np.ndarray):
+            slabs_host = torch.from_numpy(np.ascontiguousarray(slabs_host, dtype=np.float32))
+        B = slabs_host.shape[0]
+        assert slabs_host.shape[1] == self.pitch_views(0)[1]
+        g = self.geometry
+        if out_host is None:
+            out_host = torch.empty((B, g.nz_per_pitch, g.ny, g.nx), dtype=torch.float32)
+        b = ctypes.c_size_t()
+        self._check(lib().katsevich_workspace_bytes_batch_host(self._h, B, ctypes.byref(b)))
+        ws = self._workspace(b.value)
+        self._check(lib().katsevich_reconstruct_batch_host(self._h, _ptr(slabs_host), B, _ptr(out_host), _ptr(ws),
+                                                           ws.numel(), _stream_handle(stream)))
+        return out_host
+
     def reconstruct_host(self, sino_host, sino_first_view: int, first_pitch: int = 0, n_pitches: int = 1,
                          out_host=None, stream=None):
         """Host (numpy or pinned torch CPU) sinogram in, host volume out; copies inside the call."""

@@ -336,3 +336,20 @@ def test_registration_case_matches_oracle():
     vol = p.reconstruct(torch.from_numpy(sino).cuda(), v0, 0, 1).cpu().numpy().astype(np.float64)
     _check(vol, ref, 1.0)
     assert np.abs(_centroid_error(vol, cfg, c)).max() < 0.05
+
+
+@pytest.mark.parametrize("n_slabs", [4, 6, 3])
+def test_batch_host_entry_point_equals_device(n_slabs):
+    """katsevich_reconstruct_batch_host (host slabs in, host volumes out, groups of slabs with the
+    copies overlapped) gives the device batch path's volumes; checked on T2 with 4, 6 and 3 slabs
+    (groups of 4, 2 and 1)."""
+    import torch
+    from synth import configs, synth
+    cfg = configs.get("T2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    slabs = np.stack([synth.project(cfg, configs.random_ellipsoids(20 + s, 6, 180.0, -5.0, cfg["P"] + 5.0), v0, nv)
+                      for s in range(n_slabs)])
+    dev = p.reconstruct_batch(torch.from_numpy(slabs).cuda()).cpu().numpy()
+    host = p.reconstruct_batch_host(torch.from_numpy(slabs).pin_memory()).numpy()
+    assert np.linalg.norm(host - dev) / np.linalg.norm(dev) <= 1e-6
