@@ -888,31 +888,6 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
             PM = add2(PM, S2);
         }
     };
-    // the same for a group some lane's window does not cover: only the lane's own slices (mask bits)
-    // are gathered, so no shared-memory wavefront serves a slice outside a lane's window (the masked
-    // accumulate below reads v only under the same bits)
-    auto sample8m = [&](unsigned colbase, u64 PM, u64 S2, float (&v)[8][2], unsigned mask) {
-#pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-            const u64 Q = add2(PM, pk(p.qmagic, p.qmagic));
-            float q0, q1, p0, p1;
-            upk(Q, q0, q1);
-            upk(PM, p0, p1);
-            if (mask & (1u << j)) {
-                const float4 g0 = lds128(colbase + __float_as_uint(q0) * 16u);
-                upk(fma2(pk(g0.z, g0.w), pk(p0, p0), pk(g0.x, g0.y)), v[j][0], v[j][1]);
-            }
-            if (mask & (2u << j)) {
-                const float4 g1 = lds128(colbase + __float_as_uint(q1) * 16u);
-                upk(fma2(pk(g1.z, g1.w), pk(p1, p1), pk(g1.x, g1.y)), v[j + 1][0], v[j + 1][1]);
-            }
-            PM = add2(PM, S2);
-        }
-    };
-    auto lane_mask = [&](int tb, int lo, int hi, bool work) -> unsigned {
-        const int jl = min(max(lo - tb, 0), 8), jh = min(max(hi - tb + 1, 0), 8);
-        return work ? ((0xffu << jl) & ((1u << jh) - 1u)) : 0u;
-    };
     // a8 += w0 v0 + w1 v1 for the slices of the group inside the lane's window (fast: every slice)
     auto accum8 = [&](float (&a8)[8], const float (&v)[8][2], float w0, float w1, bool fast, int tb, int lo, int hi,
                       bool work) {
@@ -958,12 +933,10 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
                 float a8[8];
                 tm_ld8_nowait(tw + cc, a8);
                 float v[8][2];
-                const bool fast = tb >= lo_full && tb + 7 <= hi_full;
-                if (fast) sample8(colbase, PM, S2, v);
-                else sample8m(colbase, PM, S2, v, lane_mask(tb, t_lo, t_hi, work));
+                sample8(colbase, PM, S2, v);
                 PM = add2(PM, S8);
                 tm_wait_ld8(a8);
-                accum8(a8, v, w0, w1, fast, tb, t_lo, t_hi, work);
+                accum8(a8, v, w0, w1, tb >= lo_full && tb + 7 <= hi_full, tb, t_lo, t_hi, work);
                 tm_st8(tw + cc, a8);
                 cc = (cc + 8u) & wmask;
             }
@@ -1015,14 +988,11 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
                 float a8[8];
                 tm_ld8_nowait(tw + cc, a8);
                 float v[8][2];
-                const bool fastA = tb >= lo_fA && tb + 7 <= hi_fA, fastB = tb >= lo_fB && tb + 7 <= hi_fB;
-                if (fastA) sample8(colA, PMA, S2A, v);
-                else sample8m(colA, PMA, S2A, v, lane_mask(tb, loA, hiA, workA));
+                sample8(colA, PMA, S2A, v);
                 tm_wait_ld8(a8);
-                accum8(a8, v, w0A, w1A, fastA, tb, loA, hiA, workA);
-                if (fastB) sample8(colB, PMB, S2B, v);
-                else sample8m(colB, PMB, S2B, v, lane_mask(tb, loB, hiB, workB));
-                accum8(a8, v, w0B, w1B, fastB, tb, loB, hiB, workB);
+                accum8(a8, v, w0A, w1A, tb >= lo_fA && tb + 7 <= hi_fA, tb, loA, hiA, workA);
+                sample8(colB, PMB, S2B, v);
+                accum8(a8, v, w0B, w1B, tb >= lo_fB && tb + 7 <= hi_fB, tb, loB, hiB, workB);
                 tm_st8(tw + cc, a8);
                 PMA = add2(PMA, S8A);
                 PMB = add2(PMB, S8B);
