@@ -1442,8 +1442,11 @@ bool hilbert_split_input(const FilterParams &p)
     if (!hilbert_tc_usable(p) || p.hilbert_overlap || !p.hilbert_hk) return false;
     const char *he = std::getenv("KATS_HILBERT");
     const std::string h = he ? he : "";
-    if (h == "tc" || h == "hk" || h == "hk1") return false;
-    return hilbert_tc_nh(p.nc) > 256 || h == "ws";
+    if (h == "tc" || h == "hk" || h == "hk1" || h == "tc2") return false;
+    // round 2 (scripts/ab/gpu_k3ws.sh, K3 isolated / step): also the narrow detectors — C4 (NH 96)
+    // 1.09 -> 0.87 ms / 50.8 -> 50.2 ms, C2 (NH 192) 1.678 -> 1.664 ms; at NH 64 (C1) the Hankel
+    // kernel is faster (step 0.129 tc2 / 0.135 ws / 0.122 ms hk)
+    return hilbert_tc_nh(p.nc) > 64 || h == "ws";
 }
 
 int launch_hilbert(const FilterParams &p, cudaStream_t s)
@@ -1458,9 +1461,9 @@ int launch_hilbert(const FilterParams &p, cudaStream_t s)
     }
     // KATS_HILBERT=tc: the per-chunk tap-streaming kernels (A/B tests); =hk: Hankel cores for every width
     const char *he = std::getenv("KATS_HILBERT");
-    const bool force_tc = he && std::string(he) == "tc",
+    const bool force_tc = he && (std::string(he) == "tc" || std::string(he) == "tc2"),
                force_hk = he && (std::string(he) == "hk" || std::string(he) == "hk1" || std::string(he) == "ws");
-    if (p.k3_in_split || (hilbert_tc_usable(p) && p.hilbert_hk && !force_tc && (hilbert_tc_nh(p.nc) > 128 || force_hk))) {
+    if (p.k3_in_split || (hilbert_tc_usable(p) && p.hilbert_hk && !force_tc && (hilbert_tc_nh(p.nc) > 32 || force_hk))) {
         const int NH = hilbert_tc_nh(p.nc);
         // halves only where 2 CTAs per SM pay for reading A twice (C3 NH 384: 1.20 -> 1.13 ms;
         // C5 NH 320: 1.32 -> 1.59 ms, measured)
