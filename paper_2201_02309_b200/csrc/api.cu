@@ -869,20 +869,59 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     float4 *gq = (float4 *)workspace;
     const size_t qs = quad_view_elems(p);
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, B), nbp * B)));
-    // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
-    // keeps its own +-1 halo)
-    rc = run_filter(p, slabs + halo_lo(p) * rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true, device_chunk_mul());
-    if (rc) return rc;
     (void)nslab;
-    BPParams bp = bp_params(p);
-    bp.gq = gq;
-    bp.gq_views = nbp * B;
-    bp.off0 = -t.bp_lo;
-    bp.item_views = nbp;
-    bp.n_items = B;
-    bp.vol = vols;
-    { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(bp, s); }
-    KCHECK(p, cudaGetLastError());
+    // groups of slabs (KATS_BATCH_GROUPS, default 1): group g+1 is filtered on the highest-priority
+    // stream while group g backprojects on a low-priority one, so the filter fills the SMs the
+    // backprojection leaves idle (group sizes stay even for the window kernel's slab pairs)
+    int ng = 1;
+    if (const char *e = std::getenv("KATS_BATCH_GROUPS")) ng = std::max(1, std::atoi(e));
+    while (ng > 1 && (B % ng != 0 || ((B / ng) % 2 != 0 && B % 2 == 0))) --ng;
+    if (ng == 1) {
+        // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
+        // keeps its own +-1 halo)
+        rc = run_filter(p, slabs + halo_lo(p) * rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true, device_chunk_mul());
+        if (rc) return rc;
+        BPParams bp = bp_params(p);
+        bp.gq = gq;
+        bp.gq_views = nbp * B;
+        bp.off0 = -t.bp_lo;
+        bp.item_views = nbp;
+        bp.n_items = B;
+        bp.vol = vols;
+        { LaunchScope ls(p, ST_K5, s); p->last_bp_kernel = launch_backproject(bp, s); }
+        KCHECK(p, cudaGetLastError());
+        return KATS_OK;
+    }
+    rc = ensure_bp_streams(p);
+    if (rc) return rc;
+    rc = ensure_events(p, 2 * (size_t)ng + 1);
+    if (rc) return rc;
+    const int gs = B / ng;
+    cudaStream_t fs = (cudaStream_t)p->filter_stream;
+    cudaEvent_t e_fork = (cudaEvent_t)p->sync_events[2 * ng];
+    KCHECK(p, cudaEventRecord(e_fork, s));
+    KCHECK(p, cudaStreamWaitEvent(fs, e_fork, 0));
+    for (int g = 0; g < ng; ++g) {
+        rc = run_filter(p, slabs + ((size_t)g * gs * nslab + halo_lo(p)) * rs, nbp * gs, gq + (size_t)g * gs * nbp * qs,
+                        scratch, nullptr, nullptr, nullptr, fs, false, nbp, true, device_chunk_mul());
+        if (rc) return rc;
+        cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[ng + g];
+        KCHECK(p, cudaEventRecord(e_filt, fs));
+        cudaStream_t bs = (cudaStream_t)p->bp_streams[g & 1];
+        KCHECK(p, cudaStreamWaitEvent(bs, e_filt, 0));
+        BPParams bp = bp_params(p);
+        bp.gq = gq;
+        bp.gq_views = nbp * B;
+        bp.off0 = -t.bp_lo + (int64_t)g * gs * nbp;
+        bp.item_views = nbp;
+        bp.n_items = gs;
+        bp.vol = vols + (size_t)g * gs * p->g.nx * p->g.ny * p->g.nz_per_pitch;
+        { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(bp, bs); }
+        KCHECK(p, cudaGetLastError());
+        KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[g], bs));
+    }
+    for (int g = std::max(0, ng - 2); g < ng; ++g)                 // join (each bp stream is in order)
+        KCHECK(p, cudaStreamWaitEvent(s, (cudaEvent_t)p->sync_events[g], 0));
     return KATS_OK;
 }
 

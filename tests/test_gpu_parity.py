@@ -173,6 +173,29 @@ def test_coverage_error_names_pitches():
     assert ei.value.code == -4 and "reconstructible" in str(ei.value)
 
 
+@pytest.mark.parametrize("n_slabs,groups", [(4, "2"), (8, "4"), (6, "3")])
+def test_batch_groups_match_oracle(n_slabs, groups, monkeypatch):
+    """reconstruct_batch in slab groups (KATS_BATCH_GROUPS: group g+1 filtered while group g
+    backprojects) against the oracle per slab."""
+    import torch
+    from oracle import oracle
+    from synth import configs, synth
+    monkeypatch.setenv("KATS_BATCH_GROUPS", groups)
+    cfg = configs.get("T2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    slabs, refs = [], []
+    for s in range(n_slabs):
+        ph = configs.random_ellipsoids(30 + s, 6, 180.0, -5.0, cfg["P"] + 5.0)
+        sino = synth.project(cfg, ph, v0, nv)
+        slabs.append(sino)
+        refs.append(oracle.reconstruct(cfg, sino, v0, 0, 1))
+    got = p.reconstruct_batch(torch.from_numpy(np.stack(slabs)).cuda())
+    torch.cuda.synchronize()
+    for b in range(n_slabs):
+        _check(got[b].cpu().numpy(), refs[b], 1.0)
+
+
 @pytest.mark.parametrize("n_slabs,ni", [(4, "4"), (6, "2"), (3, "3")])
 def test_batch_items_kernel_matches_oracle(n_slabs, ni, monkeypatch):
     """The items kernel (batches whose windows hold <= 8 slices, the default for C5-shaped batches:
