@@ -73,8 +73,8 @@ def test_c4_all_pitches_sampled():
     vol = p.reconstruct(torch.from_numpy(sino).cuda(), v0, 0, cfg["n_pitches"])
     torch.cuda.synchronize()
     contrast = _truth_contrast(cfg, cfg["phantom"], [0])
-    for pitch, seed in ((0, 1), (3, 2), (7, 3)):
-        idx = _samples(cfg, 600, seed)
+    for pitch in range(cfg["n_pitches"]):                    # every pitch of the 512^3 volume
+        idx = _samples(cfg, 600 if pitch in (0, 3, 7) else 250, 1 + pitch)
         ref = _oracle_voxels(cfg, sino, v0, pitch, idx)
         g = vol[pitch * cfg["nz"]:(pitch + 1) * cfg["nz"]].cpu().numpy()
         got = g[idx[:, 2], idx[:, 1], idx[:, 0]].astype(np.float64)
@@ -93,8 +93,8 @@ def test_c5_batch_sampled():
     slabs = np.stack([synth.project(cfg, ph, v0, nv) for ph in phs])
     vols = p.reconstruct_batch(torch.from_numpy(slabs).cuda())
     torch.cuda.synchronize()
-    for b in (0, 9, 15):
-        idx = _samples(cfg, 400, 10 + b)
+    for b in range(16):                                        # every slab of the batch
+        idx = _samples(cfg, 400 if b in (0, 9, 15) else 150, 10 + b)
         ref = _oracle_voxels(cfg, slabs[b], v0, 0, idx)
         g = vols[b].cpu().numpy()
         got = g[idx[:, 2], idx[:, 1], idx[:, 0]].astype(np.float64)
