@@ -74,7 +74,7 @@ typedef struct {
     double  dx, dy;
     int32_t nz_per_pitch;    /* slices per pitch; dz = pitch / nz_per_pitch */
     int32_t n_psi;           /* κ-lines ψ_i on [-π/2-α_m, π/2+α_m] (P:l.132); 0 => 2·n_rows+1 */
-    int32_t flags;           /* 0, or KATS_FLAG_HALF_SAMPLE */
+    int32_t flags;           /* 0 or an OR of KATS_FLAG_HALF_SAMPLE, KATS_FLAG_HANN */
 } katsevich_geometry;
 
 /* Method variant flags (katsevich_geometry.flags):
@@ -85,6 +85,11 @@ typedef struct {
  *   n_cols-1 columns, views at λ_{k+½}.  Filtered view k needs raw views k and k+1 (no lower halo):
  *   katsevich_pitch_views / _scan_views report the raw views.  Needs 3 <= n_rows <= 65, n_cols >= 3. */
 #define KATS_FLAG_HALF_SAMPLE 1
+/* KATS_FLAG_HANN — step 4 (Eq. 12) with the Hann-apodised Hilbert filter (reading A26): the
+ *   kernel's frequency response -i sgn(σ) times cos²(πσΔα), i.e. the band-limited kernel of reading
+ *   A10 applied to each κ-line smoothed by [1/4, 1/2, 1/4] along α (zeros beyond the detector).  A
+ *   noise/resolution trade-off for noisy sparse-view data (P:l.396-404); the adjoint is exact. */
+#define KATS_FLAG_HANN 2
 
 typedef struct katsevich_plan katsevich_plan;
 

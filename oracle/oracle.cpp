@@ -37,6 +37,7 @@ typedef struct {
     int32_t nx, ny; double dx, dy;           /* x_i = (i - nx/2) dx  (P:l.316) */
     int32_t nz;                              /* slices per pitch: z_j = j P / nz (P:l.357, l.740) */
     int32_t n_psi;                           /* κ-lines (0 -> 2 n_rows + 1) */
+    int32_t apod;                            /* NEXT-4: 1 = Hann-apodised Hilbert filter (reading A26) */
 } ora_geom;
 
 }  // extern "C"
@@ -236,6 +237,19 @@ Rebin rebin_maps(const G &o)
  * g(v) at sino[v - s0]; writes optional stage outputs (double, [rows][cols] or
  * [n_psi][cols]).  Discretisation readings: A5 (centred differences, one-sided
  * at the α edges), A9 (linear rebins, 0 outside), A10 (band-limited Hilbert). */
+/* NEXT-4, reading A26: the Hann-apodised Hilbert filter — step 4's kernel with its frequency response
+ * -i sgn(σ) multiplied by the Hann window cos²(πσΔα) (σ in cycles per radian; 1 at DC, 0 at the
+ * Nyquist frequency 1/(2Δα)), i.e. K applied to the κ-line smoothed by [1/4, 1/2, 1/4] along α
+ * (zeros beyond the detector columns, as Eq. 12's sum).  The smoothing matrix is symmetric, so it is
+ * its own transpose in the adjoint. */
+void hann_smooth(const G &o, double *line)
+{
+    const int nc = o.g.n_cols;
+    std::vector<double> t(line, line + nc);
+    for (int l = 0; l < nc; ++l)
+        line[l] = 0.5 * t[l] + 0.25 * ((l > 0 ? t[l - 1] : 0.0) + (l + 1 < nc ? t[l + 1] : 0.0));
+}
+
 /* Steps 2-6 of one view from its g1 = step 1's output [rows][cols] (double). */
 void filter_from_g1(const G &o, const double *g1, const std::vector<double> &Kh, const Rebin &rb,
                     double *g2o, double *g3o, double *g4o, double *gFo)
@@ -254,11 +268,19 @@ void filter_from_g1(const G &o, const double *g1, const std::vector<double> &Kh,
             int m = rb.fi[t]; double f = rb.ff[t];
             g3[t] = m < 0 ? 0.0 : (1.0 - f) * g2[(size_t)m * nc + l] + f * g2[(size_t)(m + 1) * nc + l];
         }
-    /* Step 4, Eq. (12) with h_H(s) = 1/(πs) (Eq. e4): g4(α_l) = Σ_l' K[l-l'] g3(α_l') */
+    /* Step 4, Eq. (12) with h_H(s) = 1/(πs) (Eq. e4): g4(α_l) = Σ_l' K[l-l'] g3(α_l')
+     * (apodised variant, A26: on the Hann-smoothed κ-line; the g3 stage output stays unsmoothed) */
+    std::vector<double> g3a;
+    const double *g3h = g3.data();
+    if (o.g.apod) {
+        g3a = g3;
+        for (int i = 0; i < np; ++i) hann_smooth(o, g3a.data() + (size_t)i * nc);
+        g3h = g3a.data();
+    }
     for (int i = 0; i < np; ++i)
         for (int l = 0; l < nc; ++l) {
             double acc = 0.0;
-            for (int lp = 0; lp < nc; ++lp) acc += Kh[(size_t)(l - lp + nc - 1)] * g3[(size_t)i * nc + lp];
+            for (int lp = 0; lp < nc; ++lp) acc += Kh[(size_t)(l - lp + nc - 1)] * g3h[(size_t)i * nc + lp];
             g4[(size_t)i * nc + l] = acc;
         }
     /* Steps 5-6, Eqs. (13)-(15): g5 = g4(α, ψ̂(α,w)), linear in ψ; gF = cosα g5 */
@@ -438,6 +460,8 @@ void filter_view_T(const G &o, const std::vector<double> &Kh, const Rebin &rb, c
             for (int l = 0; l < nc; ++l) acc += Kh[(size_t)(l - lp + nc - 1)] * g4T[(size_t)i * nc + l];
             g3T[(size_t)i * nc + lp] = acc;
         }
+    if (o.g.apod)                                 /* the symmetric smoothing is its own transpose */
+        for (int i = 0; i < np; ++i) hann_smooth(o, g3T.data() + (size_t)i * nc);
     /* step 3^T: g3 = lerp_w(g2) */
     for (int i = 0; i < np; ++i)
         for (int l = 0; l < nc; ++l) {

@@ -209,6 +209,7 @@ FilterParams filter_params(const katsevich_plan *p)
     f.hilbert_hk = p->d.hilbert_hk;
     f.sign = 1.f;
     f.half = p->half ? 1 : 0;
+    f.apod = (p->g.flags & KATS_FLAG_HANN) ? 1 : 0;
     return f;
 }
 
@@ -282,13 +283,17 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
             d.g3 = dbg3 + v0 * ps_dbg;
             { LaunchScope ls(p, ST_K12, s); launch_deriv_fwd_rebin(d, s); }
             KCHECK(p, cudaGetLastError());
-            if (!f.k3_in_split) f.g3 = d.g3;
+            if (!f.k3_in_split && !f.apod) f.g3 = d.g3;            // (apodised: K3's input is smoothed in place)
         }
-        if (!dbg3 || f.k3_in_split) {
+        if (!dbg3 || f.k3_in_split || f.apod) {
             LaunchScope ls(p, ST_K12, s);
             launch_deriv_fwd_rebin(f, s);
         }
         KCHECK(p, cudaGetLastError());
+        if (f.apod) {                                              // reading A26: K3's input lines smoothed
+            { LaunchScope ls(p, ST_K3, s); launch_hann_smooth(f, f.g3, (int64_t)nv * f.npsi, f.k3_in_split, s); }
+            KCHECK(p, cudaGetLastError());
+        }
         { LaunchScope ls(p, ST_K3, s); if (launch_hilbert(f, s)) return hilbert_fail(p); }
         KCHECK(p, cudaGetLastError());
         { LaunchScope ls(p, ST_K4, s); launch_bwd_rebin_cos(f, s); }
@@ -735,6 +740,10 @@ static int run_filter_T(katsevich_plan *p, FilterParams f, const float4 *qT, flo
         h.sign = -1.f;
         { LaunchScope ls(p, ST_K3, s); if (launch_hilbert(h, s)) return hilbert_fail(p); }
         KCHECK(p, cudaGetLastError());
+        if (f.apod) {                                              // A26: the smoothing is symmetric
+            { LaunchScope ls(p, ST_K3, s); launch_hann_smooth(f, h.g4, (int64_t)f.n_views * f.npsi, 0, s); }
+            KCHECK(p, cudaGetLastError());
+        }
         { LaunchScope ls(p, ST_K12, s); launch_fwd_rebin_T(f, g1T + v0 * rs, s); }
         KCHECK(p, cudaGetLastError());
     }

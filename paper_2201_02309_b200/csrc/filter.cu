@@ -359,6 +359,35 @@ __global__ void __launch_bounds__(256) k_deriv_fwd_rebin_wv(FilterParams p, int 
     }
 }
 
+// NEXT-4, reading A26 (Hann-apodised Hilbert): each κ-line smoothed in place by [1/4, 1/2, 1/4] along
+// α (zeros beyond the detector columns) before K3; the same symmetric smoothing after K3^T in the
+// adjoint.  A warp per line, the line staged in shared memory (plain or parity-split layout).
+__global__ void __launch_bounds__(256) k_hann_smooth(FilterParams p, float *lines, int64_t n_lines, int split)
+{
+    extern __shared__ float hs[];
+    const int nc = p.nc, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *t = hs + warp * nc;
+    const size_t pitch = split ? (size_t)(2 * p.hp) : (size_t)nc;
+    for (int64_t ln = (int64_t)blockIdx.x * 8 + warp; ln < n_lines; ln += (int64_t)gridDim.x * 8) {
+        float *L = lines + (size_t)ln * pitch;
+        for (int l = lane; l < nc; l += 32) t[l] = L[split ? (l & 1) * p.hp + (l >> 1) : l];
+        __syncwarp();
+        for (int l = lane; l < nc; l += 32) {
+            const float o = 0.5f * t[l] + 0.25f * ((l > 0 ? t[l - 1] : 0.f) + (l + 1 < nc ? t[l + 1] : 0.f));
+            L[split ? (l & 1) * p.hp + (l >> 1) : l] = o;
+        }
+        __syncwarp();
+    }
+}
+
+void launch_hann_smooth(const FilterParams &p, float *lines, int64_t n_lines, int split, cudaStream_t s)
+{
+    const size_t smem = sizeof(float) * 8 * (size_t)p.nc;
+    smem_opt_in((const void *)k_hann_smooth, smem);
+    const int64_t blocks = std::min<int64_t>((n_lines + 7) / 8, 16 * (int64_t)device_sms());
+    k_hann_smooth<<<(unsigned)std::max<int64_t>(blocks, 1), 256, smem, s>>>(p, lines, n_lines, split);
+}
+
 // ---------------------------------------------------------------------------
 // K3: g4 = Σ_l' K[l-l'] g3[l'] along each κ-line (Eq. 12, h_H = 1/(πs) of
 //     Eq. e4, band-limited kernel of DESIGN.md reading A10: only odd

@@ -38,11 +38,13 @@ struct FilterParams {
                               // by K12 (forward) / K4^T (adjoint) when the warp-specialized K3 reads them
     int hp;                   // half pitch of a parity-split line (floats, multiple of 4)
     int half;                 // NEXT-4: Noo's half-sample derivative (raw views have nr+1 rows, nc+1 columns)
+    int apod;                 // NEXT-4: Hann-apodised Hilbert (K3's input lines smoothed [1/4, 1/2, 1/4])
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
 int launch_hilbert(const FilterParams &p, cudaStream_t s);            // K3:  Eq. 12 (-1: input tensor map failed)
 bool hilbert_split_input(const FilterParams &p);                      // the K3 launch_hilbert picks reads split lines
+void launch_hann_smooth(const FilterParams &p, float *lines, int64_t n_lines, int split, cudaStream_t s);  // A26, in place
 inline int g3_half_pitch(int nc) { return ((nc + 1) / 2 + 3) & ~3; }
 inline int g3_line_pitch(int nc) { return 2 * g3_half_pitch(nc); }   // >= nc; scratch line pitch
 size_t hilbert_tc_table_floats(int nc);

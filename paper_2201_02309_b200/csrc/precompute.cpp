@@ -170,7 +170,7 @@ int validate(const katsevich_geometry &g, std::string &detail)
     if (g.nx < 1 || g.ny < 1 || g.nz_per_pitch < 1) return bad("empty voxel grid");
     if (!(g.dx > 0) || !(g.dy > 0)) return bad("voxel spacing <= 0");
     if (g.n_psi != 0 && g.n_psi < 2) return bad("n_psi must be 0 or >= 2");
-    if (g.flags & ~KATS_FLAG_HALF_SAMPLE) return bad("unknown flags");
+    if (g.flags & ~(KATS_FLAG_HALF_SAMPLE | KATS_FLAG_HANN)) return bad("unknown flags");
     if ((g.flags & KATS_FLAG_HALF_SAMPLE) && (g.n_rows < 3 || g.n_cols < 3))
         return bad("the half-sample derivative needs n_rows >= 3 and n_cols >= 3");
     if ((g.flags & KATS_FLAG_HALF_SAMPLE) && g.n_rows > 65) return bad("the half-sample derivative needs n_rows <= 65");
@@ -194,7 +194,7 @@ katsevich_geometry half_sample_geometry(const katsevich_geometry &g)
     e.n_cols = g.n_cols - 1;
     e.lambda0 = g.lambda0 + 0.5 * dlam;
     e.z0 = g.z0 + g.pitch / (2.0 * kPi) * 0.5 * dlam;
-    e.flags = 0;
+    e.flags = g.flags & ~KATS_FLAG_HALF_SAMPLE;    // other variants carry over to the shifted grid
     return e;
 }
 
