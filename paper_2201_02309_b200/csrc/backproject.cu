@@ -1264,6 +1264,192 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_items(const __grid_constan
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"((unsigned)p.tmem_alloc));
 }
 
+// Register form of the items kernel (NI = 4 slabs per CTA): the lane's window-relative accumulators
+// acc[b][j] (slab b, slice t_lo + j) stay in registers (32 of them), shifted down with selects when
+// the lane closes a slice, so a slab's pass over a view is its box wait, the lane's own gathers and
+// their accumulates — no TMEM round trip; the geometry is computed once per view for the 4 slabs.
+constexpr int kItemsR = 4;
+
+template <bool POLY>
+__global__ void __launch_bounds__(kWsThreads, 3) k_bp_items_reg(const __grid_constant__ QMaps qm, BPParams p)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch;
+    const int vq = (BW * NQ + 7) & ~7;
+    float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
+    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vq * 16);
+    __shared__ __align__(8) unsigned long long s_full[kMaxItemSlots], s_empty[kMaxItemSlots];
+    __shared__ int s_k0, s_k1;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = warp == kConsumerWarps;
+    const int2 bt = bp_tile(p);
+    const int ix = bt.x * TX + (warp & 1) * 8 + (lane & 7);
+    const int iy = bt.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int item0 = blockIdx.z * kItemsR;
+    const bool inside = !producer && ix < p.nx && iy < p.ny;
+    const size_t plane = (size_t)p.nx * p.ny;
+    const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
+    const int2 *pik = p.pi_k + col;
+    const unsigned full0 = (unsigned)__cvta_generic_to_shared(&s_full[0]);
+    const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
+    if (tid == 0) {
+        s_k0 = INT_MAX; s_k1 = INT_MIN;
+        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, TX * TY); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int K0 = INT_MAX, K1 = INT_MIN;
+    if (inside) {
+        const int2 e0 = pik[0];
+        if (e0.x <= e0.y) { K0 = e0.x + 1; K1 = pik[(size_t)(p.nz - 1) * plane].y - 1; }
+    }
+    int wk0 = K0, wk1 = K1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wk0 = min(wk0, __shfl_xor_sync(0xffffffffu, wk0, o));
+        wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
+    }
+    if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+    const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
+    __syncthreads();
+    const int KC0 = s_k0, KC1 = s_k1;
+    const int NV = KC1 - KC0 + 1;
+    const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
+    {
+        const float xa = p.x0 + bt.x * TX * p.dx, ya = p.y0 + bt.y * TY * p.dy;
+        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya);
+    }
+    __syncthreads();
+
+    if (producer) {
+        if (NV <= 0 || lane != 0) return;
+        const int vbase = (int)(p.off0 + (int64_t)item0 * p.item_views) + KC0;
+        int sl = 0, seq = 0;
+        unsigned phase = 0;
+        for (int n = 0; n < NV; ++n) {
+            const int bc = boxc[n], cls = bc >> 16;
+            const unsigned bytes = (unsigned)(p.box_w[cls] * NQ) * 16u;
+            for (int b = 0; b < kItemsR; ++b, ++seq) {
+                if (seq >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
+                const unsigned full = full0 + 8u * sl;
+                mbar_expect_tx(full, bytes);
+                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qm.m[cls], 2 * p.q_lo, bc & 0xFFFF,
+                        vbase + (int)(b * p.item_views) + n, full);
+                if (++sl == S) { sl = 0; phase ^= 1u; }
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps ----
+    const unsigned slot0 = stage_sa - (kMagicBits + (unsigned)p.q_lo) * 16u;
+    float *out = p.vol + (size_t)item0 * p.nz * plane + col;
+    const size_t item_stride = (size_t)p.nz * plane;
+    const bool active_col = inside && K0 <= K1;
+    float acc[kItemsR][8];
+#pragma unroll
+    for (int b = 0; b < kItemsR; ++b)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[b][j] = 0.f;
+    int t_lo = 0, t_hi = -1;
+    int next_open = active_col ? K0 : INT_MAX, next_close = INT_MAX;
+    int sl = 0;
+    unsigned phase = 0;
+    for (int n = 0; n < NV; ++n) {
+        const int k = KC0 + n;
+        if (active_col) {
+            while (k >= next_open) {
+                ++t_hi;
+                if (t_hi == t_lo) next_close = pik[(size_t)t_lo * plane].y;
+                next_open = t_hi + 1 < p.nz ? pik[(size_t)(t_hi + 1) * plane].x + 1 : INT_MAX;
+            }
+            while (k >= next_close) {                            // slice t_lo closed: write it, shift down
+#pragma unroll
+                for (int b = 0; b < kItemsR; ++b) {
+                    out[(size_t)b * item_stride + (size_t)t_lo * plane] = acc[b][0];
+#pragma unroll
+                    for (int j = 0; j < 7; ++j) acc[b][j] = acc[b][j + 1];
+                    acc[b][7] = 0.f;
+                }
+                ++t_lo;
+                next_close = t_lo <= t_hi ? pik[(size_t)t_lo * plane].y : INT_MAX;
+            }
+        }
+        const bool work = active_col && t_hi >= t_lo && k <= K1;
+        const int n_act = work ? t_hi - t_lo + 1 : 0;
+        const int nw = __reduce_max_sync(0xffffffffu, n_act);
+        float w0 = 0.f, w1 = 0.f, base = 0.f, step = 0.f;
+        int ci = 0;
+        if (work) {
+            const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+            const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
+            const float u = fmaf(y, vg.x, -x * vg.y);
+            const float inv_v = rcp_approx(vstar);
+            float colpos;
+            if (POLY) {
+                const float tt = u * inv_v, q = tt * tt;
+                float a = p.at[6];
+                a = fmaf(a, q, p.at[5]); a = fmaf(a, q, p.at[4]); a = fmaf(a, q, p.at[3]);
+                a = fmaf(a, q, p.at[2]); a = fmaf(a, q, p.at[1]); a = fmaf(a, q, p.at[0]);
+                colpos = fmaf(tt, a, p.col_c);
+            } else {
+                colpos = fmaf(atan2f(u, vstar), p.inv_dalpha, p.col_c);
+            }
+            const float cp = fminf(fmaxf(colpos, 0.f), p.colmax);
+            const int l = __float2int_rz(cp);
+            const float fa = cp - __int2float_rn(l);
+            w1 = fa * inv_v;
+            w0 = inv_v - w1;
+            const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+            step = sc * p.dz;
+            base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));
+            ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
+        }
+        const unsigned amask = (1u << n_act) - 1u;
+        const unsigned cbase = (unsigned)ci * p.col_bytes;
+        auto slab = [&](auto Jc, int b) {
+            constexpr int J = decltype(Jc)::value;
+            mbar_wait(full0 + 8u * sl, phase);
+            const unsigned colbase = (slot0 + (unsigned)sl * p.slot_bytes + cbase) ^ p.zero;
+            float4 g[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float pj = fmaf((float)j, step, base);
+                if (amask & (1u << j)) g[j] = lds128(colbase + __float_as_uint(pj + p.qmagic) * 16u);
+            }
+            mbar_arrive(empty0 + 8u * sl);
+            if (++sl == S) { sl = 0; phase ^= 1u; }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const float pj = fmaf((float)j, step, base);
+                float v0, v1;
+                upk(fma2(pk(g[j].z, g[j].w), pk(pj, pj), pk(g[j].x, g[j].y)), v0, v1);
+                acc[b][j] = fmaf(v0, w0, fmaf(v1, w1, acc[b][j]));
+            }
+        };
+        if (nw <= 4) {
+#pragma unroll
+            for (int b = 0; b < kItemsR; ++b) slab(std::integral_constant<int, 4>{}, b);
+        } else {
+#pragma unroll
+            for (int b = 0; b < kItemsR; ++b) slab(std::integral_constant<int, 8>{}, b);
+        }
+    }
+    if (!inside) return;
+    if (!active_col) {
+        for (int b = 0; b < kItemsR; ++b)
+            for (int t = 0; t < p.nz; ++t) out[(size_t)b * item_stride + (size_t)t * plane] = 0.f;
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (t_lo + j < p.nz)
+#pragma unroll
+            for (int b = 0; b < kItemsR; ++b) out[(size_t)b * item_stride + (size_t)(t_lo + j) * plane] = acc[b][j];
+}
+
 // vol = (interior sum + the two fractional end views) * Δλ/2π for every voxel (after k_bp_items)
 template <bool POLY>
 __global__ void __launch_bounds__(128) k_bp_ends_add_t(BPParams p)
@@ -1891,6 +2077,27 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
             while (q.nbatch > 2 && smem_of(q) > 110 * 1024) --q.nbatch;
             const size_t sm = smem_of(q);
             QMaps qmap;
+            if (ni == kItemsR && !std::getenv("KATS_BP_ITEMS_TMEM")) {
+                // register accumulators (4 slabs): as deep a ring as leaves room for 3 CTAs per SM
+                q.nbatch = kMaxItemSlots;
+                while (q.nbatch > 2 && smem_of(q) > 74 * 1024) --q.nbatch;
+                const size_t smr = smem_of(q);
+                if (make_quad_maps(q, &qmap)) {
+                    dim3 gw = p.tile_order ? dim3(((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY), 1, p.n_items / ni)
+                                           : dim3((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / ni);
+                    if (p.poly) {
+                        smem_opt_in((const void *)k_bp_items_reg<true>, smr);
+                        k_bp_items_reg<true><<<gw, kWsThreads, smr, s>>>(qmap, q);
+                    } else {
+                        smem_opt_in((const void *)k_bp_items_reg<false>, smr);
+                        k_bp_items_reg<false><<<gw, kWsThreads, smr, s>>>(qmap, q);
+                    }
+                    dim3 ge((p.nx + 127) / 128, p.ny, p.nz * p.n_items);
+                    if (p.poly) k_bp_ends_add_t<true><<<ge, 128, 0, s>>>(q);
+                    else k_bp_ends_add_t<false><<<ge, 128, 0, s>>>(q);
+                    return KATS_BP_ITEMS;
+                }
+            }
             if (q.tmem_alloc <= 256 && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
                 dim3 gw = p.tile_order ? dim3(((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY), 1, p.n_items / ni)
                                        : dim3((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / ni);
