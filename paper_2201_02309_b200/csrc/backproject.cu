@@ -1295,7 +1295,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_items_reg(const __grid_con
     const unsigned empty0 = (unsigned)__cvta_generic_to_shared(&s_empty[0]);
     if (tid == 0) {
         s_k0 = INT_MAX; s_k1 = INT_MIN;
-        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, TX * TY); }
+        // one arrive per consumer warp releases a slot (lane 0, after the warp's gathers)
+        for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, kConsumerWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -1419,7 +1420,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_items_reg(const __grid_con
                 const float pj = fmaf((float)j, step, base);
                 if (amask & (1u << j)) g[j] = lds128(colbase + __float_as_uint(pj + p.qmagic) * 16u);
             }
-            mbar_arrive(empty0 + 8u * sl);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8u * sl);
             if (++sl == S) { sl = 0; phase ^= 1u; }
 #pragma unroll
             for (int j = 0; j < J; ++j) {
