@@ -1420,9 +1420,6 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_items_reg(const __grid_con
                 const float pj = fmaf((float)j, step, base);
                 if (amask & (1u << j)) g[j] = lds128(colbase + __float_as_uint(pj + p.qmagic) * 16u);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty0 + 8u * sl);
-            if (++sl == S) { sl = 0; phase ^= 1u; }
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const float pj = fmaf((float)j, step, base);
@@ -1430,6 +1427,9 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_items_reg(const __grid_con
                 upk(fma2(pk(g[j].z, g[j].w), pk(pj, pj), pk(g[j].x, g[j].y)), v0, v1);
                 acc[b][j] = fmaf(v0, w0, fmaf(v1, w1, acc[b][j]));
             }
+            __syncwarp();                                        // the warp's gathers from this slot are done
+            if (lane == 0) mbar_arrive(empty0 + 8u * sl);
+            if (++sl == S) { sl = 0; phase ^= 1u; }
         };
         if (nw <= 4) {
 #pragma unroll
