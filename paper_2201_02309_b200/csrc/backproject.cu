@@ -701,20 +701,26 @@ __host__ __device__ inline size_t tmem_head_bytes(const BPParams &p)
 size_t tmem_smem_bytes(const BPParams &p)
 {
     const int vq = (p.fp_cols_column * p.nq_s + 7) & ~7;
-    return tmem_head_bytes(p) + (size_t)p.nbatch * vq * sizeof(float4) + sizeof(int) * (size_t)p.max_cta_views +
-           16 * (size_t)p.pad_quads;
+    return tmem_head_bytes(p) + (size_t)p.nbatch * std::max(1, p.bp_items) * vq * sizeof(float4) +
+           sizeof(int) * (size_t)p.max_cta_views + 16 * (size_t)p.pad_quads;
 }
 
-template <bool POLY, int VP, bool ENDS_PRE>
+// PP = 2 (pitch pairs): the CTA backprojects two items (pitches) of the same tile: their windows,
+// per-view geometry, group setup and flush points are identical (pitch-relative tables), so all of
+// that is shared and only the samples double; each view's slot holds both items' boxes, each item
+// has its own Wc TMEM columns per warp; the flush writes raw interior sums (end views and the
+// Δλ/2π scale follow in k_bp_ends_add_t).  2 CTAs per SM.
+template <bool POLY, int VP, bool ENDS_PRE, int PP = 1>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant__ QMaps qm, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, PP == 1 ? 3 : 2) k_bp_tmem(const __grid_constant__ QMaps qm, BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch, Wc = p.tmem_cols;   // NQ: staged column pitch
     const int vq = (BW * NQ + 7) & ~7;
     const size_t head = tmem_head_bytes(p);                   // pad for reads below the first column
     float4 *stage = reinterpret_cast<float4 *>(smem + head);
-    int *boxc = reinterpret_cast<int *>(smem + head + (size_t)S * vq * 16);
+    int *boxc = reinterpret_cast<int *>(smem + head + (size_t)S * PP * vq * 16);
+    const unsigned box_bytes = 16u * (unsigned)vq;          // one item's box inside a slot
     __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
     __shared__ int s_k0, s_k1;
     __shared__ unsigned s_tmem;
@@ -724,7 +730,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     const bool producer = warp == kConsumerWarps;
     const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
     const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
-    const int item = blockIdx.z;
+    const int item = blockIdx.z * PP;
     const bool inside = !producer && ix < p.nx && iy < p.ny;
     const size_t plane = (size_t)p.nx * p.ny;
     const size_t col = (size_t)min(iy, p.ny - 1) * p.nx + min(ix, p.nx - 1);
@@ -781,8 +787,11 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
                 // the view's geometry record rides with its slot (released by the arrive below)
                 s_vg[sl] = __ldg(reinterpret_cast<const float4 *>(p.view) + (KC0 + n - p.view_lo));
                 const int bc = boxc[n], cls = bc >> 16;
-                mbar_expect_tx(full, (unsigned)(p.box_w[cls] * NQ) * 16u);
-                tma_box(stage_sa + (unsigned)(sl * vq) * 16u, &qm.m[cls], 2 * p.q_lo, bc & 0xFFFF, vbase + n, full);
+                mbar_expect_tx(full, (unsigned)(PP * p.box_w[cls] * NQ) * 16u);
+#pragma unroll
+                for (int b = 0; b < PP; ++b)
+                    tma_box(stage_sa + (unsigned)(sl * PP * vq) * 16u + (unsigned)b * box_bytes, &qm.m[cls], 2 * p.q_lo,
+                            bc & 0xFFFF, vbase + (int)(b * p.item_views) + n, full);
                 if (++sl == S) { sl = 0; phase ^= 1u; }
             }
         }
@@ -794,10 +803,10 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     // first staged quad row is q_lo)
     const unsigned slot0 = stage_sa - (kMagicBits + (unsigned)p.q_lo) * 16u;
     // slice t -> TMEM column t mod Wc of the warp's range (lane = TMEM lane)
-    const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * Wc);
+    const unsigned tw = s_tmem + (((unsigned)(warp & 3) * 32u) << 16) + (unsigned)((warp >> 2) * PP * Wc);
     {
         float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int c = 0; c < Wc; c += 8) tm_st8(tw + c, z);
+        for (int c = 0; c < PP * Wc; c += 8) tm_st8(tw + c, z);
         tm_wait_st();
     }
     const float2 *piw = p.pi_w + col;
@@ -810,7 +819,17 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     // end views: either written ahead by k_bp_ends (ENDS_PRE; the next slice's value is loaded one
     // flush ahead) or sampled here (the kernel is LSU-bound and other warps hide the gathers: C4)
     float end_next = active_col && ENDS_PRE ? out[0] : 0.f;
+    auto flush_pp = [&](int t) {                                  // pitch pairs: raw interior sums
+#pragma unroll
+        for (int b = 0; b < PP; ++b) {
+            const unsigned tc = tw + (unsigned)(b * Wc) + ((unsigned)t & (unsigned)(Wc - 1));
+            const float a = tm_ld1(tc);
+            if (active_col && t < p.nz) out[(size_t)b * p.nz * plane + (size_t)t * plane] = a;
+            tm_st1(tc, 0.f);
+        }
+    };
     auto flush_slice = [&](int t) {
+        if constexpr (PP > 1) { flush_pp(t); return; }
         const unsigned tc = tw + ((unsigned)t & (unsigned)(Wc - 1));
         const float a = tm_ld1(tc);
         if (active_col && t < p.nz) {
@@ -930,14 +949,17 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
             // every read stays within (warp span + 7) slices of an open slice: the pads cover that
             u64 PM = pk(fmaf((float)m0, step, base), fmaf((float)(m0 + 1), step, base));
             for (int tb = m0; tb <= hi_w; tb += 8) {                 // warp-uniform groups of 8 slices
-                float a8[8];
-                tm_ld8_nowait(tw + cc, a8);
-                float v[8][2];
-                sample8(colbase, PM, S2, v);
-                PM = add2(PM, S8);
-                tm_wait_ld8(a8);
-                accum8(a8, v, w0, w1, tb >= lo_full && tb + 7 <= hi_full, tb, t_lo, t_hi, work);
-                tm_st8(tw + cc, a8);
+#pragma unroll
+                for (int b = 0; b < PP; ++b) {
+                    float a8[8];
+                    tm_ld8_nowait(tw + (unsigned)(b * Wc) + cc, a8);
+                    float v[8][2];
+                    sample8(colbase + (unsigned)b * box_bytes, PM, S2, v);
+                    if (b == PP - 1) PM = add2(PM, S8);
+                    tm_wait_ld8(a8);
+                    accum8(a8, v, w0, w1, tb >= lo_full && tb + 7 <= hi_full, tb, t_lo, t_hi, work);
+                    tm_st8(tw + (unsigned)(b * Wc) + cc, a8);
+                }
                 cc = (cc + 8u) & wmask;
             }
             tm_wait_st();
@@ -985,15 +1007,18 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
             const u64 S2A = pk(2.f * stepA, 2.f * stepA), S2B = pk(2.f * stepB, 2.f * stepB);
             const u64 S8A = pk(8.f * stepA, 8.f * stepA), S8B = pk(8.f * stepB, 8.f * stepB);
             for (int tb = m0; tb <= hi_w; tb += 8) {
-                float a8[8];
-                tm_ld8_nowait(tw + cc, a8);
-                float v[8][2];
-                sample8(colA, PMA, S2A, v);
-                tm_wait_ld8(a8);
-                accum8(a8, v, w0A, w1A, tb >= lo_fA && tb + 7 <= hi_fA, tb, loA, hiA, workA);
-                sample8(colB, PMB, S2B, v);
-                accum8(a8, v, w0B, w1B, tb >= lo_fB && tb + 7 <= hi_fB, tb, loB, hiB, workB);
-                tm_st8(tw + cc, a8);
+#pragma unroll
+                for (int b = 0; b < PP; ++b) {
+                    float a8[8];
+                    tm_ld8_nowait(tw + (unsigned)(b * Wc) + cc, a8);
+                    float v[8][2];
+                    sample8(colA + (unsigned)b * box_bytes, PMA, S2A, v);
+                    tm_wait_ld8(a8);
+                    accum8(a8, v, w0A, w1A, tb >= lo_fA && tb + 7 <= hi_fA, tb, loA, hiA, workA);
+                    sample8(colB + (unsigned)b * box_bytes, PMB, S2B, v);
+                    accum8(a8, v, w0B, w1B, tb >= lo_fB && tb + 7 <= hi_fB, tb, loB, hiB, workB);
+                    tm_st8(tw + (unsigned)(b * Wc) + cc, a8);
+                }
                 PMA = add2(PMA, S8A);
                 PMB = add2(PMB, S8B);
                 cc = (cc + 8u) & wmask;
@@ -1009,7 +1034,8 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_tmem(const __grid_constant
     while (t_f <= hi_all) flush_slice(t_f++);
     tm_wait_st();
     if (inside && !active_col)
-        for (int t = 0; t < p.nz; ++t) out[(size_t)t * plane] = 0.f;
+        for (int b = 0; b < PP; ++b)
+            for (int t = 0; t < p.nz; ++t) out[(size_t)b * p.nz * plane + (size_t)t * plane] = 0.f;
     // release TMEM once every consumer warp is done with it
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(TX * TY));
@@ -1880,16 +1906,21 @@ void launch_bp_ends(const BPParams &p, cudaStream_t s)
     else k_bp_ends<false><<<g, 128, 0, s>>>(p);
 }
 
-template <bool POLY, int VP, bool ENDS_PRE>
+template <bool POLY, int VP, bool ENDS_PRE, int PP = 1>
 void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
-    smem_opt_in((const void *)k_bp_tmem<POLY, VP, ENDS_PRE>, 200 * 1024);
-    k_bp_tmem<POLY, VP, ENDS_PRE><<<grid, kWsThreads, sm, s>>>(qmap, q);
+    smem_opt_in((const void *)k_bp_tmem<POLY, VP, ENDS_PRE, PP>, 200 * 1024);
+    k_bp_tmem<POLY, VP, ENDS_PRE, PP><<<grid, kWsThreads, sm, s>>>(qmap, q);
 }
 
 template <bool POLY>
 void launch_tmem(const BPParams &q, int vp, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
+    if (q.bp_items == 2) {                                        // pitch pairs (ends added after)
+        if (vp == 2) launch_tmem_kernel<POLY, 2, false, 2>(q, grid, sm, qmap, s);
+        else launch_tmem_kernel<POLY, 1, false, 2>(q, grid, sm, qmap, s);
+        return;
+    }
     if (vp == 2) {
         if (q.ends_pre) launch_tmem_kernel<POLY, 2, true>(q, grid, sm, qmap, s);
         else launch_tmem_kernel<POLY, 2, false>(q, grid, sm, qmap, s);
@@ -2034,15 +2065,37 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
         int vp = q2.tmem_alloc == q1.tmem_alloc && q2.nbatch == q1.nbatch && q2.nbatch >= 4 ? 2 : 1;
         if (const char *ve = std::getenv("KATS_BP_VP")) vp = std::string(ve) == "1" ? 1 : 2;   // A/B tests
         BPParams q = vp == 2 ? q2 : q1;
+        // pitch pairs (KATS_BP_PP=2, A/B): two items per CTA share windows and geometry; TMEM and the
+        // slots double, so 2 CTAs per SM
+        int pp = 1;
+        if (const char *pe = std::getenv("KATS_BP_PP")) pp = std::atoi(pe) == 2 ? 2 : 1;
+        if (pp == 2 && p.n_items % 2 == 0) {
+            q.bp_items = 2;
+            int alloc2 = 32;
+            while (alloc2 < 2 * 2 * q.tmem_cols) alloc2 *= 2;
+            q.tmem_alloc = alloc2;
+            q.nbatch = kMaxSlots;
+            while (q.nbatch > 2 && tmem_smem_bytes(q) > 110 * 1024) q.nbatch /= 2;
+            if (alloc2 > 256 || (vp == 2 && q.nbatch < 4)) q = vp == 2 ? q2 : q1;   // does not fit: single items
+        }
         const int alloc = q.tmem_alloc;
         q.lg_nbatch = __builtin_ctz((unsigned)q.nbatch);
         q.slot_bytes = 16u * (unsigned)((p.fp_cols_column * p.nq_s + 7) & ~7);
         q.col_bytes = 16u * (unsigned)p.nq_s;
         const size_t sm = tmem_smem_bytes(q);
         QMaps qmap;
-        if (alloc <= 128 && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
+        if ((alloc <= 128 || (q.bp_items == 2 && alloc <= 256)) && sm <= 200 * 1024 && make_quad_maps(q, &qmap)) {
             // (2-D tile grid: the heaviest-first order cost this kernel registers, C4 48.5 -> 50.6 ms)
-            dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
+            dim3 gw((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
+            if (q.bp_items == 2) {
+                q.slot_bytes = 16u * 2u * (unsigned)((p.fp_cols_column * p.nq_s + 7) & ~7);
+                if (p.poly) launch_tmem<true>(q, vp, gw, sm, qmap, s);
+                else launch_tmem<false>(q, vp, gw, sm, qmap, s);
+                dim3 ge((p.nx + 127) / 128, p.ny, p.nz * p.n_items);
+                if (p.poly) k_bp_ends_add_t<true><<<ge, 128, 0, s>>>(q);
+                else k_bp_ends_add_t<false><<<ge, 128, 0, s>>>(q);
+                return KATS_BP_TMEM;
+            }
             // end views ahead (k_bp_ends) except for the LSU-bound view-pair kernel, where the inline
             // gathers are hidden by other warps (C4: 48.5 inline vs 48.9 ms; C3 7.69 -> 7.49 ms ahead)
             q.ends_pre = vp == 2 ? 0 : 1;

@@ -223,6 +223,21 @@ def test_batch_items_kernel_matches_oracle(n_slabs, ni, monkeypatch):
         _check(got[b].cpu().numpy(), refs[b], contrasts[b])
 
 
+@pytest.mark.parametrize("vp", ["1", "2"])
+def test_tmem_pitch_pairs_match_oracle(vp, monkeypatch):
+    """The TMEM kernel with two pitches per CTA (KATS_BP_PP=2: shared windows and geometry, raw sums
+    finished by k_bp_ends_add_t) on T2's two pitches, one and two views per pass."""
+    import torch
+    for env, val in (("KATS_BP_KERNEL", "tmem"), ("KATS_BP_PP", "2"), ("KATS_BP_VP", vp)):
+        monkeypatch.setenv(env, val)
+    cfg, sino, ref, contrast = _case("T2")
+    p = _plan(cfg)
+    vol = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"])
+    torch.cuda.synchronize()
+    assert p.bp_kernel() == "k_bp_tmem"
+    _check(vol.cpu().numpy(), ref, contrast)
+
+
 @pytest.mark.parametrize("variant,vp,kernel", [(None, None, "k_backproject"), ("tmem", None, "k_bp_tmem"),
                                                ("tmem", "1", "k_bp_tmem"), ("tmem", "2", "k_bp_tmem"),
                                                ("window", None, "k_bp_window"), ("window", "winv1", "k_bp_window"),
