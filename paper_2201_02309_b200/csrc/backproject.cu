@@ -2065,9 +2065,10 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
         int vp = q2.tmem_alloc == q1.tmem_alloc && q2.nbatch == q1.nbatch && q2.nbatch >= 4 ? 2 : 1;
         if (const char *ve = std::getenv("KATS_BP_VP")) vp = std::string(ve) == "1" ? 1 : 2;   // A/B tests
         BPParams q = vp == 2 ? q2 : q1;
-        // pitch pairs (KATS_BP_PP=2, A/B): two items per CTA share windows and geometry; TMEM and the
-        // slots double, so 2 CTAs per SM
-        int pp = 1;
+        // pitch pairs (default for an even number of items; KATS_BP_PP=1|2 for A/B): two items per CTA
+        // share windows, per-view geometry, group setup and flushes; TMEM and the slots double, so
+        // 2 CTAs per SM (scripts/ab/gpu_pp.sh: C4 K5 48.2 -> 45.5 ms, step 50.2 -> 47.4 ms)
+        int pp = 2;
         if (const char *pe = std::getenv("KATS_BP_PP")) pp = std::atoi(pe) == 2 ? 2 : 1;
         if (pp == 2 && p.n_items % 2 == 0) {
             q.bp_items = 2;
