@@ -1090,8 +1090,16 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
         copied_to = raw_end;
     }
     int64_t c_next = 0;                                       // next chunk to filter
-    for (int k = 0; k < n_pitches; ++k) {
-        const int64_t filt_end = (int64_t)(first_pitch + k) * vt + t.bp_hi + 1;   // exclusive
+    // pitches go to step 7 in pairs while at least three remain (a pair shares its windows and
+    // geometry in the TMEM kernel: pitch pairs), the last ones alone (shorter device->host tail);
+    // KATS_HOST_PAIRS=0: one pitch per launch
+    const char *hp = std::getenv("KATS_HOST_PAIRS");
+    const bool pairs = !(hp && hp[0] == '0');
+    int grp = 0, gi = 0;
+    for (int k = 0; k < n_pitches; k += grp, ++gi) {
+        grp = pairs && n_pitches - k >= 3 ? 2 : 1;
+        const int kl = k + grp - 1;                            // last pitch of the group
+        const int64_t filt_end = (int64_t)(first_pitch + kl) * vt + t.bp_hi + 1;   // exclusive
         while (c_next < nchunks && u0 + c_next * kFilterChunk < filt_end) {
             const int64_t a = u0 + c_next * kFilterChunk, n = std::min<int64_t>(kFilterChunk, nu - c_next * kFilterChunk);
             KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[c_next], 0));
@@ -1105,21 +1113,21 @@ int katsevich_reconstruct_host(katsevich_plan *p, const float *host_sino, int64_
         // pitch k's BP on alternating streams: its tail overlaps the next pitch's filter and BP
         cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[nchunks + n_pitches + k];
         KCHECK(p, cudaEventRecord(e_filt, fs));
-        cudaStream_t bs = (cudaStream_t)p->bp_streams[k & 1];
+        cudaStream_t bs = (cudaStream_t)p->bp_streams[gi & 1];
         KCHECK(p, cudaStreamWaitEvent(bs, e_filt, 0));
         BPParams b = bp_params(p);
         b.gq = gq;
         b.gq_views = nu;
         b.off0 = (int64_t)(first_pitch + k) * vt - u0;
         b.item_views = vt;
-        b.n_items = 1;
+        b.n_items = grp;
         b.vol = dvol + (size_t)k * vpitch;
         { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(b, bs); }
         KCHECK(p, cudaGetLastError());
         cudaEvent_t e_bp = (cudaEvent_t)p->sync_events[nchunks + k];
         KCHECK(p, cudaEventRecord(e_bp, bs));
         KCHECK(p, cudaStreamWaitEvent(ds, e_bp, 0));
-        KCHECK(p, cudaMemcpyAsync(host_vol + (size_t)k * vpitch, b.vol, sizeof(float) * vpitch,
+        KCHECK(p, cudaMemcpyAsync(host_vol + (size_t)k * vpitch, b.vol, sizeof(float) * vpitch * grp,
                                   cudaMemcpyDeviceToHost, ds));
     }
     KCHECK(p, cudaStreamSynchronize(ds));
