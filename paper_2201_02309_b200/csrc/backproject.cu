@@ -2067,10 +2067,14 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
         BPParams q = vp == 2 ? q2 : q1;
         // pitch pairs (default for an even number of items; KATS_BP_PP=1|2 for A/B): two items per CTA
         // share windows, per-view geometry, group setup and flushes; TMEM and the slots double, so
-        // 2 CTAs per SM (scripts/ab/gpu_pp.sh: C4 K5 48.2 -> 45.5 ms, step 50.2 -> 47.4 ms)
+        // 2 CTAs per SM (scripts/ab/gpu_pp.sh: C4 K5 48.2 -> 45.5 ms, step 50.2 -> 47.4 ms; 44.2 / 46.1 ms
+        // with one view per pass)
         int pp = 2;
         if (const char *pe = std::getenv("KATS_BP_PP")) pp = std::atoi(pe) == 2 ? 2 : 1;
         if (pp == 2 && p.n_items % 2 == 0) {
+            // the pair already shares the per-view work: one view per pass is faster with it (C4 K5
+            // 45.5 ms with view pairs, 44.2 ms without; scripts/ab: KATS_BP_VP under pitch pairs)
+            if (!std::getenv("KATS_BP_VP")) { vp = 1; q = q1; }
             q.bp_items = 2;
             int alloc2 = 32;
             while (alloc2 < 2 * 2 * q.tmem_cols) alloc2 *= 2;
