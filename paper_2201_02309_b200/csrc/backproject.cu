@@ -2072,6 +2072,7 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
         int pp = 2;
         if (const char *pe = std::getenv("KATS_BP_PP")) pp = std::atoi(pe) == 2 ? 2 : 1;
         if (pp == 2 && p.n_items % 2 == 0) {
+            const int vp0 = vp;
             // the pair already shares the per-view work: one view per pass is faster with it (C4 K5
             // 45.5 ms with view pairs, 44.2 ms without; scripts/ab: KATS_BP_VP under pitch pairs)
             if (!std::getenv("KATS_BP_VP")) { vp = 1; q = q1; }
@@ -2081,7 +2082,7 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
             q.tmem_alloc = alloc2;
             q.nbatch = kMaxSlots;
             while (q.nbatch > 2 && tmem_smem_bytes(q) > 110 * 1024) q.nbatch /= 2;
-            if (alloc2 > 256 || (vp == 2 && q.nbatch < 4)) q = vp == 2 ? q2 : q1;   // does not fit: single items
+            if (alloc2 > 256 || (vp == 2 && q.nbatch < 4)) { vp = vp0; q = vp == 2 ? q2 : q1; }   // single items
         }
         const int alloc = q.tmem_alloc;
         q.lg_nbatch = __builtin_ctz((unsigned)q.nbatch);
