@@ -397,7 +397,7 @@ __device__ __forceinline__ int2 bp_tile(const BPParams &p)
 
 // Tensor maps of the staged kernels: box widths p.box_w[0] (= the largest box) >= [1] >= [2] columns.
 struct QMaps { CUtensorMap m[3]; };
-bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width);
+bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width, int height = 0);
 // the three box widths of a plan: the full column box, 4/5 and 16/25 of it (C5: 56, 45, 36 columns;
 // the tile widths of its views average 35.5)
 inline void set_box_widths(BPParams &p)
@@ -415,6 +415,11 @@ bool make_quad_maps(BPParams &p, QMaps *m)
     return true;
 }
 
+// Window kernel: box widths x heights (4 height classes: the staged column and three shorter ones),
+// map index wcls * 4 + hcls
+struct QMapsW { CUtensorMap m[12]; };
+constexpr int kCropMaxZ = 64;      // row crop: per-slice tile windows in shared memory (nz <= 64)
+
 // staged box of view k for a CTA tile: first column c0 (clamped like plan_col) and the narrowest
 // width class covering the tile's corner-ray columns + 1 column of fp32 slack: c0 | class << 16
 template <bool POLY>
@@ -429,6 +434,50 @@ __device__ __forceinline__ int plan_col_cls(const BPParams &p, int k, float xa, 
     const int need = (int)floorf(cmax) + 2 - c0;
     const int cls = need <= p.box_w[2] ? 2 : need <= p.box_w[1] ? 1 : 0;
     return c0 | (cls << 16);
+}
+
+// the same, plus the quad rows of the view: the rows the tile's open slices [jlo, jhi] at view k
+// reach (corner rays bound 1/sqrt(u^2 + v*^2) over the tile; one row of slack either side), inside
+// the staged rows [q_lo, q_lo + nq_s); the shortest height class holding them and its first row r0:
+// c0 | wcls << 16 | hcls << 20 | r0 << 24.  kf/kl: per-slice tile windows (min first / max last
+// interior view over the tile's columns; nondecreasing in the slice)
+template <bool POLY>
+__device__ __forceinline__ int plan_box_crop(const BPParams &p, int k, float xa, float ya, const int *kf, const int *kl)
+{
+    const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+    const float xb = xa + (TX - 1) * p.dx, yb = ya + (TY - 1) * p.dy;
+    const float ca = col_of<POLY>(p, xa, ya, vg.x, vg.y), cb = col_of<POLY>(p, xb, ya, vg.x, vg.y);
+    const float cc = col_of<POLY>(p, xa, yb, vg.x, vg.y), cd = col_of<POLY>(p, xb, yb, vg.x, vg.y);
+    const float cmin = fminf(fminf(ca, cb), fminf(cc, cd)), cmax = fmaxf(fmaxf(ca, cb), fmaxf(cc, cd));
+    const int c0 = max(0, min((int)floorf(cmin) - 1, p.nc - p.fp_cols_column));
+    const int need = (int)floorf(cmax) + 2 - c0;
+    const int wcls = need <= p.box_w[2] ? 2 : need <= p.box_w[1] ? 1 : 0;
+    int jlo = -1, jhi = -1;
+    for (int j = 0; j < p.nz; ++j)
+        if (kf[j] <= k && k <= kl[j]) { if (jlo < 0) jlo = j; jhi = j; }
+    const int qa = p.q_lo, qb = p.q_lo + p.nq_s - 1;
+    int hcls = 3, r0 = qa;
+    if (jlo >= 0) {
+        float smin = 3.4e38f, smax = 0.f;
+        const float cx[4] = {xa, xb, xa, xb}, cy[4] = {ya, ya, yb, yb};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float vs = fmaf(-cx[q], vg.x, fmaf(-cy[q], vg.y, p.R)), us = fmaf(cy[q], vg.x, -cx[q] * vg.y);
+            const float sc = p.D_over_dw * rsqrtf(fmaf(us, us, vs * vs));
+            smin = fminf(smin, sc); smax = fmaxf(smax, sc);
+        }
+        const float dlo = fmaf((float)jlo, p.dz, -vg.z), dhi = fmaf((float)jhi, p.dz, -vg.z);
+        const float plo = p.row_c15 + (dlo >= 0.f ? smin * dlo : smax * dlo);
+        const float phi = p.row_c15 + (dhi >= 0.f ? smax * dhi : smin * dhi);
+        const int rlo = max(qa, (int)floorf(plo + 0.5f) - 1), rhi = min(qb, (int)floorf(phi + 0.5f) + 1);
+        const int nr = rhi - rlo + 1;
+        hcls = 0;
+#pragma unroll
+        for (int h = 1; h < 4; ++h)
+            if (nr <= p.box_h[h]) hcls = h;
+        r0 = min(rlo, qb + 1 - p.box_h[hcls]);
+    }
+    return c0 | (wcls << 16) | (hcls << 20) | (r0 << 24);
 }
 
 // ---------------------------------------------------------------------------
@@ -447,20 +496,27 @@ __device__ __forceinline__ int plan_col_cls(const BPParams &p, int k, float xa, 
 //   V = 2  + two batch items per CTA (C5: one-pitch slabs share the geometry, so each view's
 //          per-lane setup serves both boxes) + 4 x 2 column blocks per quarter-warp (fewer
 //          detector columns, hence bank groups, per LDS.128 wavefront).
-template <bool POLY, int W, int V>
+// RING (row-cropped boxes, p.crop): the views' boxes are variable-size regions of one byte ring
+// (p.ring_bytes) with 16 views of metadata (region offset, view geometry) in flight, instead of
+// fixed slots sized for the largest box; one producer lane allocates regions in view order and
+// waits for releases only when the ring is full.
+template <bool POLY, int W, int V, bool RING = false>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ QMaps qm, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ QMapsW qm, BPParams p)
 {
     constexpr int NI = V == 2 ? 2 : 1;
     constexpr bool TAIL = V >= 1, QMAP42 = V == 2;
     extern __shared__ __align__(128) unsigned char smem[];
-    const int BW = p.fp_cols_column, NQ = p.nq_s, S = p.nbatch;          // NQ: staged column pitch (quads)
+    const int BW = p.fp_cols_column, NQ = p.nq_s, S = RING ? kMaxSlots : p.nbatch;   // NQ: staged column pitch (quads)
     const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged box (128-B aligned)
     const int vs = NI * vq;                                              // quads per slot (NI items' boxes)
     float4 *stage = reinterpret_cast<float4 *>(smem + kBoxesBytes);
-    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (size_t)S * vs * 16);   // first column per view
+    int *boxc = reinterpret_cast<int *>(smem + kBoxesBytes + (RING ? (size_t)p.ring_bytes : (size_t)S * vs * 16));   // first column per view
     __shared__ __align__(8) unsigned long long s_full[kMaxSlots], s_empty[kMaxSlots];
     __shared__ int s_k0, s_k1;
+    __shared__ int s_kf[kCropMaxZ], s_kl[kCropMaxZ];             // row crop: per-slice tile windows
+    __shared__ unsigned s_off[RING ? kMaxSlots : 1], s_end[RING ? kMaxSlots : 1];   // ring: region offset / end
+    __shared__ float4 s_vgm[RING ? kMaxSlots : 1];                                  // ring: view geometry
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = warp == kConsumerWarps;
@@ -482,6 +538,8 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
         for (int i = 0; i < S; ++i) { mbar_init(full0 + 8u * i, 1); mbar_init(empty0 + 8u * i, TX * TY); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (p.crop)
+        for (int t = tid; t < p.nz; t += kWsThreads) { s_kf[t] = INT_MAX; s_kl[t] = INT_MIN; }
     __syncthreads();
     int K0 = INT_MAX, K1 = INT_MIN;
     if (inside) {
@@ -495,6 +553,18 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
         wk1 = max(wk1, __shfl_xor_sync(0xffffffffu, wk1, o));
     }
     if (lane == 0 && !producer) { atomicMin(&s_k0, wk0); atomicMax(&s_k1, wk1); }
+    if (p.crop && !producer) {                                          // per-slice tile windows
+        for (int t = 0; t < p.nz; ++t) {
+            int a = INT_MAX, b = INT_MIN;
+            if (inside && K0 <= K1) {
+                const int2 e = pik[(size_t)t * plane];
+                if (e.x + 1 <= e.y - 1) { a = e.x + 1; b = e.y - 1; }
+            }
+            a = __reduce_min_sync(0xffffffffu, a);
+            b = __reduce_max_sync(0xffffffffu, b);
+            if (lane == 0) { atomicMin(&s_kf[t], a); atomicMax(&s_kl[t], b); }
+        }
+    }
     const float x = p.x0 + ix * p.dx, y = p.y0 + iy * p.dy;
     const u64 qbase = reinterpret_cast<u64>(p.gq) + (u64)((p.off0 + (int64_t)item0 * p.item_views) * p.viewbytes);
     const u64 qitem = (u64)(p.item_views * p.viewbytes);                // bytes between items' views
@@ -504,10 +574,46 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
     const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage);
     {
         const float xa = p.x0 + bt.x * TX * p.dx, ya = p.y0 + bt.y * TY * p.dy;
-        for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya);
+        if (p.crop)
+            for (int n = tid; n < NV; n += kWsThreads) boxc[n] = plan_box_crop<POLY>(p, KC0 + n, xa, ya, s_kf, s_kl);
+        else
+            for (int n = tid; n < NV; n += kWsThreads)
+                boxc[n] = plan_col_cls<POLY>(p, KC0 + n, xa, ya) | (((unsigned)p.q_lo) << 24);   // hcls 0 = nq_s
     }
     __syncthreads();
 
+    if (RING && producer) {
+        if (NV <= 0 || lane != 0) return;
+        // ---- producer lane: view n's region [head, head + bytes) of the byte ring (absolute offsets;
+        // a region never wraps: the ring's tail is skipped), free once every older view is released ----
+        const int vbase = (int)(p.off0 + (int64_t)item0 * p.item_views) + KC0;
+        const unsigned RB = (unsigned)p.ring_bytes;
+        unsigned head = 0, hp = 0, rel_end = 0;
+        int o = 0;
+        for (int n = 0; n < NV; ++n) {
+            const int ms = n & (kMaxSlots - 1);
+            const int bc = boxc[n], wcls = (bc >> 16) & 15, hcls = (bc >> 20) & 15;
+            const unsigned bytes = (unsigned)(p.box_w[wcls] * p.box_h[hcls]) * 16u, bb = (bytes + 127u) & ~127u;
+            if (hp + NI * bb > RB) { head += RB - hp; hp = 0; }
+            while (o <= n - kMaxSlots || head + NI * bb > rel_end + RB) {
+                mbar_wait_sleep(empty0 + 8u * (o & (kMaxSlots - 1)), (unsigned)(o >> 4) & 1u);
+                rel_end = s_end[o & (kMaxSlots - 1)];
+                ++o;
+            }
+            s_end[ms] = head + NI * bb;
+            s_off[ms] = hp;
+            s_vgm[ms] = __ldg(reinterpret_cast<const float4 *>(p.view) + (KC0 + n - p.view_lo));
+            const unsigned full = full0 + 8u * ms;
+            mbar_expect_tx(full, NI * bytes);
+#pragma unroll
+            for (int i = 0; i < NI; ++i)
+                tma_box(stage_sa + hp + (unsigned)i * bb, &qm.m[wcls * 4 + hcls], 2 * (int)((unsigned)bc >> 24),
+                        bc & 0xFFFF, vbase + (int)(i * p.item_views) + n, full);
+            head += NI * bb;
+            hp += NI * bb;
+        }
+        return;
+    }
     if (producer) {
         if (NV <= 0) return;
         // ---- producer warp: lanes 0..3 stream one view's column boxes (NI items) each per round ----
@@ -519,12 +625,12 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
             for (int n = lane; n < NV; n += G) {
                 if (n >= S) mbar_wait_sleep(empty0 + 8u * sl, phase ^ 1u);
                 const unsigned full = full0 + 8u * sl;
-                const int bc = boxc[n], cls = bc >> 16;
-                mbar_expect_tx(full, NI * (unsigned)(p.box_w[cls] * NQ) * 16u);
+                const int bc = boxc[n], wcls = (bc >> 16) & 15, hcls = (bc >> 20) & 15;
+                mbar_expect_tx(full, NI * (unsigned)(p.box_w[wcls] * p.box_h[hcls]) * 16u);
 #pragma unroll
                 for (int i = 0; i < NI; ++i)
-                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qm.m[cls], 2 * p.q_lo, bc & 0xFFFF,
-                            vbase + (int)(i * p.item_views) + n, full);
+                    tma_box(stage_sa + (unsigned)(sl * vs + i * vq) * 16u, &qm.m[wcls * 4 + hcls], 2 * (int)((unsigned)bc >> 24),
+                            bc & 0xFFFF, vbase + (int)(i * p.item_views) + n, full);
                 sl += G;
                 if (sl >= S) { sl -= S; phase ^= 1u; }
             }
@@ -572,7 +678,7 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
             while (k >= next_close) flush();                      // slice t_lo's window closed
             const int n_act = t_hi - t_lo + 1;
             if (n_act > 0 && k <= K1) {
-                const float4 vg = __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
+                const float4 vg = RING ? s_vgm[sl] : __ldg(reinterpret_cast<const float4 *>(p.view) + (k - p.view_lo));
                 const float vstar = fmaf(-x, vg.x, fmaf(-y, vg.y, p.R));
                 const float u = fmaf(y, vg.x, -x * vg.y);
                 const float inv_v = rcp_approx(vstar);
@@ -593,7 +699,13 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
                 const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
                 const float step = sc * p.dz;
                 const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));    // entry 0 = slice t_lo
-                const int ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
+                const int bcn = boxc[n];
+                const int ci = min(max(l - (bcn & 0xFFFF), 0), BW - 1);
+                const unsigned H = (unsigned)p.box_h[(bcn >> 20) & 15], r0 = (unsigned)bcn >> 24;   // staged rows
+                // ring: the view's region and the item stride (its box rounded to 128 B)
+                const unsigned rbase = RING ? stage_sa + s_off[sl] : stage_sa + (unsigned)(sl * vs) * 16u;
+                const unsigned ibytes = RING ? ((unsigned)p.box_w[(bcn >> 16) & 15] * H * 16u + 127u) & ~127u
+                                             : (unsigned)vq * 16u;
                 const u64 S2 = pk(2.f * step, 2.f * step);
                 // (V >= 1) entries past every working lane's last open slice are not sampled at all
                 int n_w = W;
@@ -602,8 +714,7 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
                 for (int b = 0; b < NI; ++b) {
                     // XOR with a runtime zero keeps ptxas from re-splitting the magic offset: one LEA per sample
                     const unsigned colbase =
-                        (stage_sa + (unsigned)(sl * vs + b * vq + ci * NQ) * 16u - (kMagicBits + (unsigned)p.q_lo) * 16u) ^
-                        p.zero;
+                        (rbase + (unsigned)b * ibytes + (unsigned)ci * H * 16u - (kMagicBits + r0) * 16u) ^ p.zero;
                     u64 PM = pk(base, base + step);
 #pragma unroll
                     for (int g = 0; g < W; g += kGroup) {
@@ -1555,12 +1666,24 @@ __device__ __forceinline__ void red_add4(float4 *dst, float a, float b, float c,
 //    (starting 3 x lane slices in), so ATOMS rarely serialize.
 //  * y (scaled) is staged once in shared memory, column-major with an odd
 //    stride, so the rotated slice reads are conflict-free.
-template <bool POLY>
+//  * CS > 0: the four component planes sit CS ints apart (compile time), so one
+//    address per update serves all four atomics (immediate offsets); CS = 0:
+//    planes BW x NQP ints apart, one address per component.
+__device__ __forceinline__ void red_s32(unsigned saddr, int v)
+{
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void red_s32_off(unsigned saddr, int v)
+{
+    asm volatile("red.shared.add.s32 [%0+%1], %2;" ::"r"(saddr), "n"(OFF), "r"(v) : "memory");
+}
+template <bool POLY, int CS>
 __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
 {
     extern __shared__ __align__(128) unsigned char smem[];   // one symbol per TU: keep the TMA kernels' alignment
     const int BW = p.fp_cols_column, NQ = p.nr + 2, nzp = p.nz | 1;
-    const int NQP = p.adj_nqp, nbox = BW * NQP;                      // box column stride (launcher: 0 mod 32 or odd)
+    const int NQP = p.adj_nqp, nbox = CS > 0 ? CS : BW * NQP;        // box column stride (launcher: 0 mod 32 or odd)
     const int cpy = 4 * nbox + 16;                                     // second copy: 16 banks further
     int *pl = reinterpret_cast<int *>(smem);                           // [2 copies][4][BW][NQP] fixed-point components
     float *ys = reinterpret_cast<float *>(pl + 2 * cpy);               // [TX*TY][nzp] scale * y
@@ -1686,25 +1809,41 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             atomicMin(&rect[2], q_lo); atomicMax(&rect[3], q_hi);
         }
         if (work) {
-            // the four components' bases (one LEA per address); odd lanes: the shifted copy
-            int *const c0 = pl + (lane & 1) * cpy + ci * NQP, *const c1 = c0 + nbox;
-            int *const c2 = c1 + nbox, *const c3 = c2 + nbox;
+            // component 0's byte address of quad row 0 minus the magic bits (the row's magic-rounded
+            // float bits, times 4, complete it: one LEA per update); odd lanes: the shifted copy
+            const unsigned a0 = (unsigned)__cvta_generic_to_shared(pl + (lane & 1) * cpy + ci * NQP) - kMagicBits * 4u;
             const float e0 = w0 * S01, e1 = w1 * S01, f0 = w0 * S23, f1 = w1 * S23;
             const int nt = t_hi - t_lo + 1;
             // rotated start: lane L begins ~L rows below lane 0 (consecutive banks for a shared column);
-            // every lane walks its nt slices in lockstep, wrapping from t_hi to t_lo
-            int t = t_lo + (int)((float)lane * __frcp_rn(step)) % nt;
+            // every lane walks its nt slices in lockstep, wrapping from t_hi to t_lo (y by byte address)
+            const int t0 = t_lo + (int)((float)lane * __frcp_rn(step)) % nt;
+            const unsigned ylo = (unsigned)__cvta_generic_to_shared(yc + t_lo), yhi = ylo + 4u * (unsigned)(nt - 1);
+            unsigned ya = ylo + 4u * (unsigned)(t0 - t_lo);
             const float Plo = fmaf((float)t_lo, step, base);
-            float P = fmaf((float)t, step, base);
+            float P = fmaf((float)t0, step, base);
             for (int i = 0; i < nt; ++i) {
-                const int r = (int)(__float_as_uint(P + p.qmagic) - kMagicBits);
-                const float yy = yc[t], yP = yy * P;
-                atomicAdd(c0 + r, (int)(__float_as_uint(fmaf(e0, yy, kMagic)) - kMagicBits));
-                atomicAdd(c1 + r, (int)(__float_as_uint(fmaf(e1, yy, kMagic)) - kMagicBits));
-                atomicAdd(c2 + r, (int)(__float_as_uint(fmaf(f0, yP, kMagic)) - kMagicBits));
-                atomicAdd(c3 + r, (int)(__float_as_uint(fmaf(f1, yP, kMagic)) - kMagicBits));
-                const bool wrap = t == t_hi;
-                t = wrap ? t_lo : t + 1;
+                const unsigned ad = a0 + __float_as_uint(P + p.qmagic) * 4u;
+                float yy;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(yy) : "r"(ya));
+                const float yP = yy * P;
+                const int v0 = (int)(__float_as_uint(fmaf(e0, yy, kMagic)) - kMagicBits);
+                const int v1 = (int)(__float_as_uint(fmaf(e1, yy, kMagic)) - kMagicBits);
+                const int v2 = (int)(__float_as_uint(fmaf(f0, yP, kMagic)) - kMagicBits);
+                const int v3 = (int)(__float_as_uint(fmaf(f1, yP, kMagic)) - kMagicBits);
+                if constexpr (CS > 0) {
+                    red_s32_off<0>(ad, v0);
+                    red_s32_off<4 * CS>(ad, v1);
+                    red_s32_off<8 * CS>(ad, v2);
+                    red_s32_off<12 * CS>(ad, v3);
+                } else {
+                    const unsigned nb4 = 4u * (unsigned)nbox;
+                    red_s32(ad, v0);
+                    red_s32(ad + nb4, v1);
+                    red_s32(ad + 2u * nb4, v2);
+                    red_s32(ad + 3u * nb4, v3);
+                }
+                const bool wrap = ya == yhi;
+                ya = wrap ? ylo : ya + 4u;
                 P = wrap ? Plo : P + step;
             }
         }
@@ -1867,15 +2006,25 @@ static int launch_backproject_adjoint_items(const BPParams &p, cudaStream_t s)
     q.adj_nqp = p.fp_cols_column >= 48 ? ((p.nr + 2) | 1) : ((p.nr + 2 + 31) & ~31);
     if (const char *e = std::getenv("KATS_ADJ_PITCH"))
         q.adj_nqp = std::string(e) == "odd" ? ((p.nr + 2) | 1) : ((p.nr + 2 + 31) & ~31);
-    const size_t sm = sizeof(int) * 2 * (4 * (size_t)p.fp_cols_column * q.adj_nqp + 16) +
+    // component planes at a compile-time stride (1024 or 2048 ints) when the box fits one, so the four
+    // atomics of an update share one address (KATS_ADJ_CS=0: the runtime stride, A/B)
+    const size_t nbox = (size_t)p.fp_cols_column * q.adj_nqp;
+    // (only where the padding costs little shared memory: C5's 1064-int box at 2048 halved its CTAs per SM)
+    int cs = nbox <= 1024 ? 1024 : nbox <= 2048 ? 2048 : 0;
+    if (cs && 4 * (size_t)cs > 5 * nbox) cs = 0;
+    if (const char *e = std::getenv("KATS_ADJ_CS")) cs = std::atoi(e) == 0 ? 0 : cs;
+    const size_t sm = sizeof(int) * 2 * (4 * (cs ? (size_t)cs : nbox) + 16) +
                       sizeof(float) * (size_t)TX * TY * (p.nz | 1) + sizeof(int) * (size_t)p.max_cta_views;
     dim3 grid((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items);
     // KATS_BP_KERNEL=l1: the checked kernel (A/B); also the fallback when the fixed-point box could overflow
     if (!p.checked && p.staged && p.adj_fixed_ok && sm <= 200 * 1024) {
-        smem_opt_in((const void *)k_bp_adjoint<true>, 200 * 1024);
-        smem_opt_in((const void *)k_bp_adjoint<false>, 200 * 1024);
-        if (p.poly) k_bp_adjoint<true><<<grid, TX * TY, sm, s>>>(q);
-        else k_bp_adjoint<false><<<grid, TX * TY, sm, s>>>(q);
+        auto go = [&](auto kern) {
+            smem_opt_in((const void *)kern, 200 * 1024);
+            kern<<<grid, TX * TY, sm, s>>>(q);
+        };
+        if (cs == 1024) { if (p.poly) go(k_bp_adjoint<true, 1024>); else go(k_bp_adjoint<false, 1024>); }
+        else if (cs == 2048) { if (p.poly) go(k_bp_adjoint<true, 2048>); else go(k_bp_adjoint<false, 2048>); }
+        else { if (p.poly) go(k_bp_adjoint<true, 0>); else go(k_bp_adjoint<false, 0>); }
     } else {
         if (p.poly) k_bp_adjoint_checked<true><<<grid, TX * TY, 0, s>>>(p);
         else k_bp_adjoint_checked<false><<<grid, TX * TY, 0, s>>>(p);
@@ -1930,31 +2079,58 @@ void launch_tmem(const BPParams &q, int vp, dim3 grid, size_t sm, const QMaps &q
     }
 }
 
-template <int W>
-void launch_window(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
+// window kernel maps: every (width, height) class pair
+bool make_quad_maps_w(BPParams &p, QMapsW *m)
 {
-    smem_opt_in((const void *)k_bp_window<true, W, 0>, 200 * 1024);
-    smem_opt_in((const void *)k_bp_window<false, W, 0>, 200 * 1024);
-    smem_opt_in((const void *)k_bp_window<true, W, 1>, 200 * 1024);
-    smem_opt_in((const void *)k_bp_window<false, W, 1>, 200 * 1024);
-    if constexpr (W <= 16) {
-        smem_opt_in((const void *)k_bp_window<true, W, 2>, 200 * 1024);
-        smem_opt_in((const void *)k_bp_window<false, W, 2>, 200 * 1024);
+    set_box_widths(p);
+    for (int i = 0; i < 3; ++i)
+        for (int h = 0; h < 4; ++h)
+            if (!make_quad_map(p, p.gq_views, &m->m[i * 4 + h], p.box_w[i], p.box_h[h])) return false;
+    return true;
+}
+
+// height classes of the row crop: the staged column and the largest odd-bank-group heights (3 or 5
+// mod 8, as the staged pitch) <= 3/4, 3/5 and 3/10 of it (C5: 19, 13, 11, 5 quad rows)
+inline void set_box_heights(BPParams &p, bool crop)
+{
+    const int nq = p.nq_s;
+    p.box_h[0] = nq;
+    const float frac[3] = {0.75f, 0.6f, 0.3f};
+    for (int h = 1; h < 4; ++h) {
+        int v = crop ? (int)(frac[h - 1] * nq) : nq;
+        while (v > 3 && (v & 7) != 3 && (v & 7) != 5) --v;
+        v = std::max(3, std::min(v, p.box_h[h - 1]));
+        p.box_h[h] = v;
     }
+}
+
+template <int W>
+void launch_window(const BPParams &q, dim3 grid, size_t sm, const QMapsW &qmap, cudaStream_t s)
+{
+    auto go = [&](auto kern) {
+        smem_opt_in((const void *)kern, 200 * 1024);
+        kern<<<grid, kWsThreads, sm, s>>>(qmap, q);
+    };
     const int v = q.win_variant;
     if constexpr (W <= 16) {
+        if (q.ring_bytes > 0) {                                   // row-cropped boxes in a byte ring
+            if (v == 2) { if (q.poly) go(k_bp_window<true, W, 2, true>); else go(k_bp_window<false, W, 2, true>); }
+            else if (v == 1) { if (q.poly) go(k_bp_window<true, W, 1, true>); else go(k_bp_window<false, W, 1, true>); }
+            else { if (q.poly) go(k_bp_window<true, W, 0, true>); else go(k_bp_window<false, W, 0, true>); }
+            return;
+        }
         if (v == 2) {
-            if (q.poly) k_bp_window<true, W, 2><<<grid, kWsThreads, sm, s>>>(qmap, q);
-            else k_bp_window<false, W, 2><<<grid, kWsThreads, sm, s>>>(qmap, q);
+            if (q.poly) go(k_bp_window<true, W, 2>);
+            else go(k_bp_window<false, W, 2>);
             return;
         }
     }
     if (v == 1) {
-        if (q.poly) k_bp_window<true, W, 1><<<grid, kWsThreads, sm, s>>>(qmap, q);
-        else k_bp_window<false, W, 1><<<grid, kWsThreads, sm, s>>>(qmap, q);
+        if (q.poly) go(k_bp_window<true, W, 1>);
+        else go(k_bp_window<false, W, 1>);
     } else {
-        if (q.poly) k_bp_window<true, W, 0><<<grid, kWsThreads, sm, s>>>(qmap, q);
-        else k_bp_window<false, W, 0><<<grid, kWsThreads, sm, s>>>(qmap, q);
+        if (q.poly) go(k_bp_window<true, W, 0>);
+        else go(k_bp_window<false, W, 0>);
     }
 }
 
@@ -1998,8 +2174,9 @@ bool make_tensor_map_2d_f32(CUtensorMap *map, const float *base, uint64_t dim0, 
 
 // the quad array as a 3-D tensor of 8-byte elements: (2 * (nr+2) per column, nc columns, n_views);
 // box = full column height x fp_cols_column columns x 1 view
-bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width)
+bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int width, int height)
 {
+    if (height <= 0) height = p.nq_s;
     EncodeTiledFn fn = encode_tiled();
     if (!fn) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)2 * (p.nr + 2), (cuuint64_t)p.nc, (cuuint64_t)n_views};
@@ -2007,7 +2184,7 @@ bool make_quad_map(const BPParams &p, int64_t n_views, CUtensorMap *map, int wid
     // the box's column is p.nq_s quads from quad row p.q_lo (the rows interior samples can reach, |w| <=
     // w_L); rows past the detector are zero-filled (out of bounds); the pitch is an odd number of
     // 16-B bank groups
-    const cuuint32_t box[3] = {(cuuint32_t)(2 * p.nq_s), (cuuint32_t)width, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * height), (cuuint32_t)width, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float4 *>(p.gq), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -2189,11 +2366,26 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
     const size_t budget = (W > 0 && W * q.bp_items <= 16 ? 74 : 100) * 1024;
     q.nbatch = kMaxSlots;
     while (q.nbatch > 2 && backproject_smem_bytes(q) > budget) q.nbatch /= 2;
-    const size_t sm = backproject_smem_bytes(q);
-    QMaps qmap;
+    size_t sm = backproject_smem_bytes(q);
+    // row crop (default for short slabs, nz <= 16; KATS_BP_CROP=0|1 for A/B): each view's box holds only
+    // the quad rows of the tile's open slices (C5: 11.8 -> ~7 staged B/update), in a byte ring of
+    // variable-size regions (W <= 16: the 3-CTA budget, at least two of the largest views)
+    q.crop = p.nz <= 16;
+    if (const char *ce = std::getenv("KATS_BP_CROP")) q.crop = std::atoi(ce) != 0 && p.nz <= kCropMaxZ;
+    set_box_heights(q, q.crop);
+    q.ring_bytes = 0;
+    if (q.crop && W > 0 && W <= 16) {
+        const size_t rest = kBoxesBytes + sizeof(int) * (size_t)p.max_cta_views + 16 * (size_t)p.tail_quads;
+        const size_t maxview = (size_t)q.bp_items * (((size_t)p.fp_cols_column * p.nq_s * 16 + 127) & ~(size_t)127);
+        // (3 CTAs per SM: <= ~73.8 KB of dynamic shared memory next to the kernel's ~1.2 KB static)
+        const size_t rbudget = std::min(budget, (size_t)72 * 1024);
+        const size_t rb = rbudget > rest ? ((rbudget - rest) & ~(size_t)127) : 0;
+        if (rb >= 2 * maxview) { q.ring_bytes = (int)rb; sm = rest + rb; }
+    }
+    QMapsW qmap;
     if (!small_grid && p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
         p.tail_quads <= 4096 &&
-        p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_maps(q, &qmap)) {
+        p.fp_cols_column <= 256 && p.gq_views > 0 && make_quad_maps_w(q, &qmap)) {
         dim3 gw = p.tile_order ? dim3(((p.nx + TX - 1) / TX) * ((p.ny + TY - 1) / TY), 1, p.n_items / q.bp_items)
                                : dim3((p.nx + TX - 1) / TX, (p.ny + TY - 1) / TY, p.n_items / q.bp_items);
         // the window kernel always finishes slices from end views written ahead (C5 2.55 -> 2.35 ms,

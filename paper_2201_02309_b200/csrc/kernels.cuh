@@ -96,6 +96,9 @@ struct BPParams {
     int nq_s;                 // staged-kernel column pitch in quads: staged rows rounded up to 3 or 5 mod 8
     int q_lo;                 // first staged quad row (interior samples reach quad rows q_lo ..)
     int box_w[3];             // staged box widths (columns): full, and two narrower classes (set by the launcher)
+    int box_h[4];             // window kernel: staged box heights (quad rows), full and narrower classes (launcher)
+    int crop;                 // window kernel: crop each view's box to the rows of the tile's open slices
+    int ring_bytes;           // window kernel with cropped boxes: byte ring of variable-size view regions
     int adj_nqp;              // adjoint: quad-row pitch of a box column in shared memory (set by the launcher)
     bool adj_fixed_ok;        // adjoint: the int32 fixed-point box cannot overflow (<= 2^10 contributions per cell)
     int ends_pre;             // staged kernels: end views written ahead into vol by k_bp_ends (launcher)
