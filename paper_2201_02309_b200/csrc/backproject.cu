@@ -293,6 +293,12 @@ __device__ __forceinline__ void tma_box(unsigned dst, const CUtensorMap *map, in
     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                  ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c_row), "r"(c_col), "r"(c_view), "r"(mbar) : "memory");
 }
+// L2 prefetch of a box (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap *map, int c_row, int c_col, int c_view)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];"
+                 ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c_row), "r"(c_col), "r"(c_view) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned mbar)
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -502,10 +508,10 @@ __device__ __forceinline__ int plan_box_crop(const BPParams &p, int k, float xa,
 // waits for releases only when the ring is full.
 template <bool POLY, int W, int V, bool RING = false>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
-__global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ QMapsW qm, BPParams p)
+__global__ void __launch_bounds__(kWsThreads, (W * (V == 3 ? 4 : V == 2 ? 2 : 1) <= 16 ? 3 : 2)) k_bp_window(const __grid_constant__ QMapsW qm, BPParams p)
 {
-    constexpr int NI = V == 2 ? 2 : 1;
-    constexpr bool TAIL = V >= 1, QMAP42 = V == 2;
+    constexpr int NI = V == 3 ? 4 : V == 2 ? 2 : 1;                // V = 3: four items per CTA (byte ring only)
+    constexpr bool TAIL = V >= 1, QMAP42 = V >= 2;
     extern __shared__ __align__(128) unsigned char smem[];
     const int BW = p.fp_cols_column, NQ = p.nq_s, S = RING ? kMaxSlots : p.nbatch;   // NQ: staged column pitch (quads)
     const int vq = (BW * NQ + 7) & ~7;                                   // quads per staged box (128-B aligned)
@@ -594,8 +600,12 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
             const int ms = n & (kMaxSlots - 1);
             const int bc = boxc[n], wcls = (bc >> 16) & 15, hcls = (bc >> 20) & 15;
             const unsigned bytes = (unsigned)(p.box_w[wcls] * p.box_h[hcls]) * 16u, bb = (bytes + 127u) & ~127u;
+            const unsigned last_end = head;                         // end of every region issued so far
             if (hp + NI * bb > RB) { head += RB - hp; hp = 0; }
-            while (o <= n - kMaxSlots || head + NI * bb > rel_end + RB) {
+            // the region's ring bytes last held absolute offsets [head + size - RB - size, head + size - RB):
+            // free once every view ending there (never past the last issued one: the skipped tail) is released
+            const unsigned need = head + NI * bb > RB ? min(head + NI * bb - RB, last_end) : 0u;
+            while (o <= n - kMaxSlots || rel_end < need) {
                 mbar_wait_sleep(empty0 + 8u * (o & (kMaxSlots - 1)), (unsigned)(o >> 4) & 1u);
                 rel_end = s_end[o & (kMaxSlots - 1)];
                 ++o;
@@ -609,6 +619,13 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 2 ? 2 : 1) <= 16 ? 3 : 
             for (int i = 0; i < NI; ++i)
                 tma_box(stage_sa + hp + (unsigned)i * bb, &qm.m[wcls * 4 + hcls], 2 * (int)((unsigned)bc >> 24),
                         bc & 0xFFFF, vbase + (int)(i * p.item_views) + n, full);
+            if (p.ring_prefetch > 0 && n + p.ring_prefetch < NV) {     // the boxes of a view further ahead into L2
+                const int m = n + p.ring_prefetch, bm = boxc[m];
+                const CUtensorMap *map = &qm.m[((bm >> 16) & 15) * 4 + ((bm >> 20) & 15)];
+#pragma unroll
+                for (int i = 0; i < NI; ++i)
+                    tma_prefetch(map, 2 * (int)((unsigned)bm >> 24), bm & 0xFFFF, vbase + (int)(i * p.item_views) + m);
+            }
             head += NI * bb;
             hp += NI * bb;
         }
@@ -2112,6 +2129,12 @@ void launch_window(const BPParams &q, dim3 grid, size_t sm, const QMapsW &qmap, 
         kern<<<grid, kWsThreads, sm, s>>>(qmap, q);
     };
     const int v = q.win_variant;
+    if constexpr (W <= 8) {
+        if (q.ring_bytes > 0 && v == 3) {
+            if (q.poly) go(k_bp_window<true, W, 3, true>); else go(k_bp_window<false, W, 3, true>);
+            return;
+        }
+    }
     if constexpr (W <= 16) {
         if (q.ring_bytes > 0) {                                   // row-cropped boxes in a byte ring
             if (v == 2) { if (q.poly) go(k_bp_window<true, W, 2, true>); else go(k_bp_window<false, W, 2, true>); }
@@ -2359,8 +2382,11 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
     // each view's per-lane geometry); otherwise the plain kernel (KATS_BP_WINV=0|1|2: A/B tests)
     q.win_variant = W > 0 && W <= 16 && p.n_items >= 2 && p.n_items % 2 == 0 ? 2 : 0;
     if (const char *wv = std::getenv("KATS_BP_WINV")) q.win_variant = std::atoi(wv);
+    // four items per CTA for batches of slabs with <= 8-slice windows (C5: K5 2.15 -> 2.07 ms, scripts/ab/gpu_ni4.sh)
+    if (W > 0 && W <= 8 && p.n_items % 4 == 0 && p.nz <= kCropMaxZ && !std::getenv("KATS_BP_WINV")) q.win_variant = 3;
+    if (q.win_variant == 3 && !(W > 0 && W <= 8 && p.n_items % 4 == 0 && p.nz <= kCropMaxZ)) q.win_variant = 2;
     if (q.win_variant == 2 && !(W > 0 && W <= 16 && p.n_items % 2 == 0)) q.win_variant = 1;
-    q.bp_items = q.win_variant == 2 ? 2 : 1;
+    q.bp_items = q.win_variant == 3 ? 4 : q.win_variant == 2 ? 2 : 1;
     // sliding-window kernel: deepest slot ring (<= kMaxSlots views) that lets 3 CTAs (W * items <= 16,
     // <= 72 registers) or 2 CTAs share an SM
     const size_t budget = (W > 0 && W * q.bp_items <= 16 ? 74 : 100) * 1024;
@@ -2370,17 +2396,28 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
     // row crop (default for short slabs, nz <= 16; KATS_BP_CROP=0|1 for A/B): each view's box holds only
     // the quad rows of the tile's open slices (C5: 11.8 -> ~7 staged B/update), in a byte ring of
     // variable-size regions (W <= 16: the 3-CTA budget, at least two of the largest views)
-    q.crop = p.nz <= 16;
-    if (const char *ce = std::getenv("KATS_BP_CROP")) q.crop = std::atoi(ce) != 0 && p.nz <= kCropMaxZ;
+    q.crop = p.nz <= 16 || q.win_variant == 3;
+    if (const char *ce = std::getenv("KATS_BP_CROP")) q.crop = (std::atoi(ce) != 0 || q.win_variant == 3) && p.nz <= kCropMaxZ;
     set_box_heights(q, q.crop);
-    q.ring_bytes = 0;
-    if (q.crop && W > 0 && W <= 16) {
+    auto size_ring = [&]() {
+        q.ring_bytes = 0;
+        if (!(q.crop && W > 0 && W <= 16)) return;
         const size_t rest = kBoxesBytes + sizeof(int) * (size_t)p.max_cta_views + 16 * (size_t)p.tail_quads;
         const size_t maxview = (size_t)q.bp_items * (((size_t)p.fp_cols_column * p.nq_s * 16 + 127) & ~(size_t)127);
-        // (3 CTAs per SM: <= ~73.8 KB of dynamic shared memory next to the kernel's ~1.2 KB static)
-        const size_t rbudget = std::min(budget, (size_t)72 * 1024);
+        // (3 CTAs per SM: <= ~73.8 KB of dynamic shared memory next to the kernel's ~1.2 KB static; 2: ~111 KB)
+        const size_t rbudget = (size_t)(W * q.bp_items <= 16 ? 72 : 108) * 1024;
         const size_t rb = rbudget > rest ? ((rbudget - rest) & ~(size_t)127) : 0;
-        if (rb >= 2 * maxview) { q.ring_bytes = (int)rb; sm = rest + rb; }
+        if (2 * rb >= 3 * maxview) { q.ring_bytes = (int)rb; sm = rest + rb; }   // >= 1.5 of the largest views
+    };
+    size_ring();
+    q.ring_prefetch = 0;                                             // KATS_BP_RING_PF=N: L2 prefetch N views ahead
+    if (const char *pf = std::getenv("KATS_BP_RING_PF")) q.ring_prefetch = std::max(0, std::atoi(pf));
+    if (q.win_variant == 3 && q.ring_bytes == 0) {                   // four items need the ring
+        q.win_variant = 2; q.bp_items = 2;
+        q.nbatch = kMaxSlots;
+        while (q.nbatch > 2 && backproject_smem_bytes(q) > (size_t)74 * 1024) q.nbatch /= 2;
+        sm = backproject_smem_bytes(q);
+        size_ring();
     }
     QMapsW qmap;
     if (!small_grid && p.staged && !p.checked && p.windows_monotone && W > 0 && sm <= 200 * 1024 && 2 * p.nq_s <= 256 &&
