@@ -133,6 +133,39 @@ def test_batch_matches_oracle(n_slabs, winv, k12, monkeypatch):
         _check(got[b].cpu().numpy(), refs[b], contrasts[b])
 
 
+@pytest.mark.parametrize("n_slabs,winv,crop", [(4, None, None), (8, None, None), (2, None, None), (4, "2", None),
+                                              (4, "3", "0"), (4, "1", "1"), (3, "0", "1")])
+def test_batch_window_kernel_matches_oracle(n_slabs, winv, crop, monkeypatch):
+    """The window kernel on C5-shaped slabs (T2), forced past the small-grid rule: four slabs per
+    CTA on the byte ring of row-cropped boxes (the default for batches of 4k slabs: C5), two slabs
+    per CTA (ring), one slab, and the fixed-slot full-column boxes (KATS_BP_CROP=0)."""
+    import torch
+    from oracle import oracle
+    from synth import configs, synth
+    monkeypatch.setenv("KATS_BP_KERNEL", "window")
+    for var, val in (("KATS_BP_WINV", winv), ("KATS_BP_CROP", crop)):
+        if val is None:
+            monkeypatch.delenv(var, raising=False)
+        else:
+            monkeypatch.setenv(var, val)
+    cfg = configs.get("T2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    slabs, refs, contrasts = [], [], []
+    for s in range(n_slabs):
+        ph = configs.random_ellipsoids(100 + s, 6, 180.0, -5.0, cfg["P"] + 5.0)
+        sino = synth.project(cfg, ph, v0, nv)
+        slabs.append(sino)
+        refs.append(oracle.reconstruct(cfg, sino, v0, 0, 1))
+        t = synth.volume_truth(cfg, ph, 0)
+        contrasts.append(t.max() - t.min())
+    got = p.reconstruct_batch(torch.from_numpy(np.stack(slabs)).cuda())
+    torch.cuda.synchronize()
+    assert p.bp_kernel() == "k_bp_window"
+    for b in range(n_slabs):
+        _check(got[b].cpu().numpy(), refs[b], contrasts[b])
+
+
 def test_host_entry_point_matches_device():
     """The host entry point (copies overlapped; its K3 runs beside the backprojection as the
     fp32 direct convolution) agrees with the device path to fp32 rounding, and with the oracle."""
