@@ -10,6 +10,13 @@
  * own filter (direct-sum Hilbert) and backprojection.
  *
  * Parity pins: see tests/test_oracle_*.py and DESIGN.md "Oracle pins".
+ *
+ * NEXT-4 flat-detector variant (ora_geom.flat = 1; reading A27): the same seven steps in
+ * flat-detector coordinates (u, w) on the plane at distance D (Noo et al. 2003, the implementation
+ * PAPER.md l.115 cites): derivative at constant ray direction (∂_λ + (u²+D²)/D ∂_u + uw/D ∂_w),
+ * length weight D/√(D²+u²+w²), κ-lines w_κ(u,ψ) = DP/(2πR)(ψ + (ψ/tanψ) u/D) (Eq. 11 divided by
+ * cos α, u = D tan α), Hilbert kernel 1/(π(u−u')) along u, no post-cosine (the flat g^F equals the
+ * curved g^F of the same ray), backprojection at u* = D x·e_t/v*, w* = D (z − z_src)/v*.
  * Every function cites the passage it follows; readings of silent / ambiguous
  * points follow SURVEY.md §8(c) A1-A21 and are listed in DESIGN.md.
  *
@@ -38,6 +45,8 @@ typedef struct {
     int32_t nz;                              /* slices per pitch: z_j = j P / nz (P:l.357, l.740) */
     int32_t n_psi;                           /* κ-lines (0 -> 2 n_rows + 1) */
     int32_t apod;                            /* NEXT-4: 1 = Hann-apodised Hilbert filter (reading A26) */
+    int32_t flat;                            /* NEXT-4: 1 = flat detector: columns u_l = (l-(n_cols-1)/2+off) d_alpha
+                                                [mm on the plane at distance D] (reading A27) */
 } ora_geom;
 
 }  // extern "C"
@@ -67,6 +76,7 @@ G make(const ora_geom *in)
     return o;
 }
 
+/* detector column coordinate: α_l (curved, rad) or u_l (flat, mm) */
 inline double alpha_l(const G &o, int l) { return (l - 0.5 * (o.g.n_cols - 1) + o.g.alpha_offset) * o.g.d_alpha; }
 inline double w_m(const G &o, int m) { return (m - 0.5 * (o.g.n_rows - 1)) * o.g.d_w; }
 inline double psi_i(const G &o, int i) { return -o.psi_max + i * o.dpsi; }
@@ -127,10 +137,13 @@ void pi_line(const G &o, double x, double y, double z, double *li, double *lo)
     *lo = s + d;
 }
 
-/* ---------- κ-line height, Eq. (11) P:l.134-136 ---------- */
+/* ---------- κ-line height, Eq. (11) P:l.134-136 ----------
+ * flat (A27): the same κ-plane met by the plane at distance D: Eq. (11) / cos α at u = D tan α,
+ * i.e. DP/(2πR) (ψ + (ψ/tanψ) u/D) — a straight line in (u, w) */
 double w_kappa(const G &o, double alpha, double psi)
 {
     double r = std::fabs(psi) < 1e-8 ? 1.0 - psi * psi / 3.0 : psi / std::tan(psi);  /* ψ/tanψ -> 1 */
+    if (o.g.flat) return o.kappa_scale * (psi + r * alpha / o.g.D);
     return o.kappa_scale * (psi * std::cos(alpha) + r * std::sin(alpha));
 }
 
@@ -256,11 +269,14 @@ void filter_from_g1(const G &o, const double *g1, const std::vector<double> &Kh,
 {
     const int nr = o.g.n_rows, nc = o.g.n_cols, np = o.n_psi;
     std::vector<double> g2((size_t)nr * nc), g3((size_t)np * nc), g4((size_t)np * nc);
-    /* Step 2, Eq. (9): g2 = D/sqrt(D²+w²) g1 */
-    for (int m = 0; m < nr; ++m) {
-        double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + w_m(o, m) * w_m(o, m));
-        for (int l = 0; l < nc; ++l) g2[(size_t)m * nc + l] = wgt * g1[(size_t)m * nc + l];
-    }
+    /* Step 2, Eq. (9): g2 = D/sqrt(D²+w²) g1 (flat, A27: D/sqrt(D²+u²+w²), the cosine of the ray to the
+     * central ray) */
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            const double uu = o.g.flat ? alpha_l(o, l) * alpha_l(o, l) : 0.0;
+            const double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + uu + w_m(o, m) * w_m(o, m));
+            g2[(size_t)m * nc + l] = wgt * g1[(size_t)m * nc + l];
+        }
     /* Step 3, Eqs. (10)-(11): g3(α,ψ) = g2(α, w_κ(α,ψ)), linear in w, 0 outside */
     for (int i = 0; i < np; ++i)
         for (int l = 0; l < nc; ++l) {
@@ -289,7 +305,7 @@ void filter_from_g1(const G &o, const double *g1, const std::vector<double> &Kh,
             size_t t = (size_t)m * nc + l;
             int i = rb.bi[t]; double f = rb.bf[t];
             double val = i < 0 ? 0.0 : (1.0 - f) * g4[(size_t)i * nc + l] + f * g4[(size_t)(i + 1) * nc + l];
-            if (gFo) gFo[t] = std::cos(alpha_l(o, l)) * val;
+            if (gFo) gFo[t] = (o.g.flat ? 1.0 : std::cos(alpha_l(o, l))) * val;   /* flat: no post-cosine (A27) */
         }
     if (g2o) std::memcpy(g2o, g2.data(), sizeof(double) * g2.size());
     if (g3o) std::memcpy(g3o, g3.data(), sizeof(double) * g3.size());
@@ -307,7 +323,9 @@ void filter_view(const G &o, const float *sino, int64_t s0, int64_t v,
     const int nr = o.g.n_rows, nc = o.g.n_cols;
     auto g = [&](int64_t vv, int m, int l) { return (double)sino[((vv - s0) * nr + m) * (int64_t)nc + l]; };
     std::vector<double> g1((size_t)nr * nc);
-    /* Step 1, Eq. (8): g1 = (∂_q + ∂_α) g |_{q=λ} */
+    /* Step 1, Eq. (8): g1 = (∂_q + ∂_α) g |_{q=λ}; flat (A27): the derivative at constant ray direction
+     * on the plane, (∂_q + (u²+D²)/D ∂_u + u w/D ∂_w) g, the w difference centred like α (one-sided at
+     * the row edges) */
     for (int m = 0; m < nr; ++m)
         for (int l = 0; l < nc; ++l) {
             double dq = (g(v + 1, m, l) - g(v - 1, m, l)) / (2.0 * o.dlam);
@@ -315,7 +333,17 @@ void filter_view(const G &o, const float *sino, int64_t s0, int64_t v,
             if (l == 0) da = (g(v, m, 1) - g(v, m, 0)) / o.g.d_alpha;
             else if (l == nc - 1) da = (g(v, m, nc - 1) - g(v, m, nc - 2)) / o.g.d_alpha;
             else da = (g(v, m, l + 1) - g(v, m, l - 1)) / (2.0 * o.g.d_alpha);
-            g1[(size_t)m * nc + l] = dq + da;
+            if (o.g.flat) {
+                const double u = alpha_l(o, l), w = w_m(o, m), D = o.g.D;
+                double dw;
+                if (nr == 1) dw = 0.0;
+                else if (m == 0) dw = (g(v, 1, l) - g(v, 0, l)) / o.g.d_w;
+                else if (m == nr - 1) dw = (g(v, nr - 1, l) - g(v, nr - 2, l)) / o.g.d_w;
+                else dw = (g(v, m + 1, l) - g(v, m - 1, l)) / (2.0 * o.g.d_w);
+                g1[(size_t)m * nc + l] = dq + (u * u + D * D) / D * da + u * w / D * dw;
+            } else {
+                g1[(size_t)m * nc + l] = dq + da;
+            }
         }
     filter_from_g1(o, g1.data(), Kh, rb, g2o, g3o, g4o, gFo);
 }
@@ -344,7 +372,8 @@ void deriv_half(const G &o, const float *sino, int64_t s0, int64_t k, double *g1
 }
 
 /* Band-limited kernel of h_H(sin(α-α')) dα' (A10):
- * K[d] = Δα (1 - cos πd) / (π sin(dΔα)), K[0] = 0; 1 - cos πd = 1 - (-1)^d. */
+ * K[d] = Δα (1 - cos πd) / (π sin(dΔα)), K[0] = 0; 1 - cos πd = 1 - (-1)^d.
+ * flat (A27): h_H(u-u') du' on the uniform u grid, K[d] = Δu (1 - cos πd) / (π dΔu) = (1 - cos πd)/(πd). */
 std::vector<double> hilbert_kernel(const G &o)
 {
     const int nc = o.g.n_cols;
@@ -352,9 +381,27 @@ std::vector<double> hilbert_kernel(const G &o)
     for (int d = -(nc - 1); d <= nc - 1; ++d) {
         if (d == 0) continue;
         double one_minus_cos = (d % 2 == 0) ? 0.0 : 2.0;
-        K[(size_t)(d + nc - 1)] = o.g.d_alpha * one_minus_cos / (PI * std::sin(d * o.g.d_alpha));
+        K[(size_t)(d + nc - 1)] = o.g.flat ? one_minus_cos / (PI * d)
+                                           : o.g.d_alpha * one_minus_cos / (PI * std::sin(d * o.g.d_alpha));
     }
     return K;
+}
+
+/* Detector coordinates of voxel (x, y, z) at view angle λ (index k): v*, the column coordinate
+ * (α* curved, u* flat) and w* (P:l.161-170; flat A27). */
+inline void project_voxel(const G &o, double x, double y, double z, double lam, double *vstar, double *acoord,
+                          double *wstar)
+{
+    double c = std::cos(lam + o.g.lambda0), s = std::sin(lam + o.g.lambda0);
+    *vstar = o.g.R - x * c - y * s;
+    const double ut = -x * s + y * c, dz = z - o.g.z0 - o.h * lam;
+    if (o.g.flat) {
+        *acoord = o.g.D * ut / *vstar;                       /* u* = D x·e_t / v* */
+        *wstar = o.g.D * dz / *vstar;                        /* w* = D (z - z_src) / v* */
+    } else {
+        *acoord = std::atan(ut / *vstar);                    /* α* (P:l.166) */
+        *wstar = o.g.D * std::cos(*acoord) / *vstar * dz;    /* w* (P:l.170) */
+    }
 }
 
 /* Bilinear sample of gF(view) at (α*, w*); 0 outside the sample range (A9). */
@@ -388,11 +435,8 @@ double bp_voxel(const G &o, double x, double y, double z, const double *gF, int6
     double acc = 0.0;
     for (int64_t k = kf; k <= kl; ++k) {
         double om = (k == kf) ? wf : (k == kl) ? wl : 1.0;   /* kf == kl: wf = t_o - t_i */
-        double lam = k * o.dlam;
-        double c = std::cos(lam + o.g.lambda0), s = std::sin(lam + o.g.lambda0);
-        double vstar = o.g.R - x * c - y * s;
-        double astar = std::atan((-x * s + y * c) / vstar);
-        double wstar = o.g.D * std::cos(astar) / vstar * (z - o.g.z0 - o.h * lam);
+        double vstar, astar, wstar;
+        project_voxel(o, x, y, z, k * o.dlam, &vstar, &astar, &wstar);
         acc += om * sample(o, gF + (size_t)(k - gF0) * vs, astar, wstar) / vstar;
     }
     return acc * o.dlam / (2.0 * PI);      /* +1/2π (step 7, P:l.157; reading A3) */
@@ -428,11 +472,8 @@ void bp_voxel_T(const G &o, double x, double y_, double z, double yv, double *gF
     const size_t vs = (size_t)o.g.n_rows * o.g.n_cols;
     for (int64_t k = kf; k <= kl; ++k) {
         double om = (k == kf) ? wf : (k == kl) ? wl : 1.0;
-        double lam = k * o.dlam;
-        double c = std::cos(lam + o.g.lambda0), s = std::sin(lam + o.g.lambda0);
-        double vstar = o.g.R - x * c - y_ * s;
-        double astar = std::atan((-x * s + y_ * c) / vstar);
-        double wstar = o.g.D * std::cos(astar) / vstar * (z - o.g.z0 - o.h * lam);
+        double vstar, astar, wstar;
+        project_voxel(o, x, y_, z, k * o.dlam, &vstar, &astar, &wstar);
         sample_T(o, gFT + (size_t)(k - gF0) * vs, astar, wstar, yv * om / vstar * o.dlam / (2.0 * PI));
     }
 }
@@ -449,7 +490,7 @@ void filter_view_T(const G &o, const std::vector<double> &Kh, const Rebin &rb, c
             size_t t = (size_t)m * nc + l;
             int i = rb.bi[t]; double f = rb.bf[t];
             if (i < 0) continue;
-            double v = std::cos(alpha_l(o, l)) * gFT[t];
+            double v = (o.g.flat ? 1.0 : std::cos(alpha_l(o, l))) * gFT[t];
             g4T[(size_t)i * nc + l] += (1.0 - f) * v;
             g4T[(size_t)(i + 1) * nc + l] += f * v;
         }
@@ -471,11 +512,13 @@ void filter_view_T(const G &o, const std::vector<double> &Kh, const Rebin &rb, c
             g2T[(size_t)m * nc + l] += (1.0 - f) * g3T[t];
             g2T[(size_t)(m + 1) * nc + l] += f * g3T[t];
         }
-    /* step 2^T: g2 = D/sqrt(D^2+w^2) g1 */
-    for (int m = 0; m < nr; ++m) {
-        double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + w_m(o, m) * w_m(o, m));
-        for (int l = 0; l < nc; ++l) g1T[(size_t)m * nc + l] = wgt * g2T[(size_t)m * nc + l];
-    }
+    /* step 2^T: g2 = D/sqrt(D^2 (+u^2) +w^2) g1 */
+    for (int m = 0; m < nr; ++m)
+        for (int l = 0; l < nc; ++l) {
+            const double uu = o.g.flat ? alpha_l(o, l) * alpha_l(o, l) : 0.0;
+            const double wgt = o.g.D / std::sqrt(o.g.D * o.g.D + uu + w_m(o, m) * w_m(o, m));
+            g1T[(size_t)m * nc + l] = wgt * g2T[(size_t)m * nc + l];
+        }
 }
 
 /* Step 1^T: g1(v) = (g(v+1) - g(v-1))/(2 dlam) + D_alpha g(v)  =>  scatter g1T(v). */
@@ -488,9 +531,20 @@ void deriv_T(const G &o, const double *g1T, int64_t v, double *outT, int64_t s0)
             double t = g1T[(size_t)m * nc + l];
             at(v + 1, m, l) += t / (2.0 * o.dlam);
             at(v - 1, m, l) -= t / (2.0 * o.dlam);
-            if (l == 0) { at(v, m, 1) += t / o.g.d_alpha; at(v, m, 0) -= t / o.g.d_alpha; }
-            else if (l == nc - 1) { at(v, m, nc - 1) += t / o.g.d_alpha; at(v, m, nc - 2) -= t / o.g.d_alpha; }
-            else { at(v, m, l + 1) += t / (2.0 * o.g.d_alpha); at(v, m, l - 1) -= t / (2.0 * o.g.d_alpha); }
+            double ta = t, tw = 0.0;                       /* flat (A27): the u and w stencils' weights */
+            if (o.g.flat) {
+                const double u = alpha_l(o, l), w = w_m(o, m), D = o.g.D;
+                ta = t * (u * u + D * D) / D;
+                tw = t * u * w / D;
+            }
+            if (l == 0) { at(v, m, 1) += ta / o.g.d_alpha; at(v, m, 0) -= ta / o.g.d_alpha; }
+            else if (l == nc - 1) { at(v, m, nc - 1) += ta / o.g.d_alpha; at(v, m, nc - 2) -= ta / o.g.d_alpha; }
+            else { at(v, m, l + 1) += ta / (2.0 * o.g.d_alpha); at(v, m, l - 1) -= ta / (2.0 * o.g.d_alpha); }
+            if (o.g.flat && nr > 1) {
+                if (m == 0) { at(v, 1, l) += tw / o.g.d_w; at(v, 0, l) -= tw / o.g.d_w; }
+                else if (m == nr - 1) { at(v, nr - 1, l) += tw / o.g.d_w; at(v, nr - 2, l) -= tw / o.g.d_w; }
+                else { at(v, m + 1, l) += tw / (2.0 * o.g.d_w); at(v, m - 1, l) -= tw / (2.0 * o.g.d_w); }
+            }
         }
 }
 
@@ -506,8 +560,9 @@ void scan_ray(const G &o, int64_t v, int m, int l, double src[3], double dir[3])
     const double c = std::cos(lam + o.g.lambda0), sn = std::sin(lam + o.g.lambda0);
     src[0] = o.g.R * c; src[1] = o.g.R * sn; src[2] = o.g.z0 + o.h * lam;
     const double a = alpha_l(o, l), w = w_m(o, m);
-    const double sa = std::sin(a), ca = std::cos(a);
-    double d[3] = {o.g.D * (-sa * sn - ca * c), o.g.D * (sa * c - ca * sn), w};
+    /* curved: D sinα e_t − D cosα e_r + w e_z; flat (A27): u e_t − D e_r + w e_z */
+    const double sa = o.g.flat ? a : o.g.D * std::sin(a), ca = o.g.flat ? o.g.D : o.g.D * std::cos(a);
+    double d[3] = {-sa * sn - ca * c, sa * c - ca * sn, w};
     const double n = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     dir[0] = d[0] / n; dir[1] = d[1] / n; dir[2] = d[2] / n;
 }

@@ -25,7 +25,7 @@ class OraGeom(ctypes.Structure):
         ("n_cols", ctypes.c_int32), ("d_alpha", ctypes.c_double), ("alpha_offset", ctypes.c_double),
         ("views_per_turn", ctypes.c_int32),
         ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("dx", ctypes.c_double), ("dy", ctypes.c_double),
-        ("nz", ctypes.c_int32), ("n_psi", ctypes.c_int32), ("apod", ctypes.c_int32),
+        ("nz", ctypes.c_int32), ("n_psi", ctypes.c_int32), ("apod", ctypes.c_int32), ("flat", ctypes.c_int32),
     ]
 
 
@@ -104,7 +104,8 @@ def geom(cfg: dict) -> OraGeom:
                    cfg.get("r_fov", 0.0), cfg["n_rows"], cfg["d_w"], cfg["n_cols"], cfg["d_alpha"],
                    cfg.get("alpha_offset", 0.0), cfg["views_per_turn"], cfg["nx"], cfg["ny"],
                    cfg["dx"], cfg.get("dy", cfg["dx"]), cfg["nz"], cfg.get("n_psi", 0),
-                   1 if cfg.get("flags", 0) & 2 else 0)          # NEXT-4: Hann-apodised Hilbert (A26)
+                   1 if cfg.get("flags", 0) & 2 else 0,          # NEXT-4: Hann-apodised Hilbert (A26)
+                   1 if cfg.get("flags", 0) & 4 else 0)          # NEXT-4: flat detector (A27)
 
 
 def _p(a, t):

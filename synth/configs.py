@@ -85,12 +85,18 @@ def _scan_range(views_per_turn: int, n_pitches: int, z0_turns: float = 0.0, firs
 
 def _mk(name, *, R, D, P, n_rows, d_w, n_cols, d_alpha, views_per_turn, nx, ny, dx, nz,
         n_pitches, phantom, alpha_offset=0.25, lambda0=0.0, z0=0.0, n_psi=0, r_fov=0.0,
-        batch=0, desc=""):
+        batch=0, desc="", flags=0):
     v0, nv = _scan_range(views_per_turn, n_pitches, z0 / P)
-    return dict(name=name, desc=desc, R=R, D=D, P=P, lambda0=lambda0, z0=z0, r_fov=r_fov,
-                n_rows=n_rows, d_w=d_w, n_cols=n_cols, d_alpha=d_alpha, alpha_offset=alpha_offset,
-                views_per_turn=views_per_turn, nx=nx, ny=ny, dx=dx, dy=dx, nz=nz, n_psi=n_psi,
-                n_pitches=n_pitches, phantom=phantom, scan_v0=v0, scan_nv=nv, batch=batch)
+    d = dict(name=name, desc=desc, R=R, D=D, P=P, lambda0=lambda0, z0=z0, r_fov=r_fov,
+             n_rows=n_rows, d_w=d_w, n_cols=n_cols, d_alpha=d_alpha, alpha_offset=alpha_offset,
+             views_per_turn=views_per_turn, nx=nx, ny=ny, dx=dx, dy=dx, nz=nz, n_psi=n_psi,
+             n_pitches=n_pitches, phantom=phantom, scan_v0=v0, scan_nv=nv, batch=batch)
+    if flags:
+        d["flags"] = flags
+    return d
+
+
+FLAT = 4        # KATS_FLAG_FLAT: flat detector, d_alpha = column pitch [mm] on the plane at distance D
 
 
 def get(name: str) -> dict:
@@ -151,6 +157,23 @@ def get(name: str) -> dict:
                    views_per_turn=200, nx=61, ny=53, dx=4.1, nz=19, n_pitches=3,
                    phantom=shepp_logan(110.0, 80.0, 1.5 * P), lambda0=-1.3, z0=-7.0,
                    desc="ragged odd-sized config, 3 pitches")
+    # ---- flat-detector variant (NEXT-4, reading A27): columns u_l = (l - (n-1)/2 + off) d_u ----
+    if n == "TF1":
+        # T3's scan and volume with a flat detector (131 x 7.2 mm columns cover u* = D tan α_m = 316 mm)
+        R, D = R_AAPM, D_AAPM
+        P = _pitch_mm(1.2, 21, 3.3, R, D)
+        return _mk("TF1", R=R, D=D, P=P, n_rows=21, d_w=3.3, n_cols=131, d_alpha=7.2,
+                   views_per_turn=200, nx=61, ny=53, dx=4.1, nz=19, n_pitches=3,
+                   phantom=shepp_logan(110.0, 80.0, 1.5 * P), lambda0=-1.3, z0=-7.0, flags=FLAT,
+                   desc="flat-detector ragged config, 3 pitches")
+    if n == "C2F":
+        # C2's volume and scan with a flat 36 x 368 detector (2 mm columns: u* up to 346 mm; 36 rows for
+        # the flat Tam-Danielsson window, which widens by 1 + u^2/D^2 towards the edges)
+        P = _pitch_mm(1.5, 32, DW_AAPM, R_AAPM, D_AAPM)          # 28.8 mm, as C2
+        return _mk("C2F", R=R_AAPM, D=D_AAPM, P=P, n_rows=36, d_w=DW_AAPM, n_cols=368,
+                   d_alpha=2.0, views_per_turn=576, nx=256, ny=256, dx=1.0, nz=32,
+                   n_pitches=2, phantom=shepp_logan(120.0, 120.0, P), flags=FLAT,
+                   desc="C2 volume, flat 36x368 detector (2 mm columns), 576 v/turn")
     raise KeyError(name)
 
 

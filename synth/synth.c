@@ -10,6 +10,7 @@
  *   detector pt   a(λ) + D sinα e_u + D cosα e_v + w e_z
  *                 e_u = (-sin(λ+λ0), cos(λ+λ0), 0),  e_v = (-cos(λ+λ0), -sin(λ+λ0), 0)
  *   (SPEC.md l.49-52 detector_ray).  View index v <-> λ = v·2π/views_per_turn.
+ *   Flat detector (flat = 1, NEXT-4): detector pt a(λ) + u e_u + D e_v + w e_z, u_l in mm.
  *   α_l = (l-(n_cols-1)/2+alpha_offset)·d_alpha,  w_m = (m-(n_rows-1)/2)·d_w.
  *
  * Phantom: list of ellipsoids {cx,cy,cz, a,b,c, phi, rho}; c <= 0 means an
@@ -27,7 +28,17 @@ typedef struct {
     int32_t n_rows; double d_w;
     int32_t n_cols; double d_alpha, alpha_offset;
     int32_t views_per_turn;
+    int32_t flat;            /* 1: flat detector, columns u_l [mm] on the plane at distance D */
 } synth_scan;
+
+/* unnormalised ray direction to detector column coordinate a (α or u) and row w */
+static void det_dir(const synth_scan *s, const double eu[2], const double ev[2], double a, double w, double d[3])
+{
+    double su = s->flat ? a : s->D * sin(a), sv = s->flat ? s->D : s->D * cos(a);
+    d[0] = su * eu[0] + sv * ev[0];
+    d[1] = su * eu[1] + sv * ev[1];
+    d[2] = w;
+}
 
 /* ellipsoid record: 8 doubles */
 enum { E_CX, E_CY, E_CZ, E_A, E_B, E_C, E_PHI, E_RHO, E_N };
@@ -76,9 +87,8 @@ void synth_project(const synth_scan *s, const double *ell, int32_t n_ell,
             float *row = out + ((size_t)iv * nr + m) * nc;
             for (int l = 0; l < nc; ++l) {
                 double al = ((double)l - 0.5 * (nc - 1) + s->alpha_offset) * s->d_alpha;
-                double sa = sin(al), ca = cos(al);
-                double d[3] = { s->D * (sa * eu[0] + ca * ev[0]),
-                                s->D * (sa * eu[1] + ca * ev[1]), w };
+                double d[3];
+                det_dir(s, eu, ev, al, w, d);
                 double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
                 d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
                 double acc = 0.0;
@@ -98,8 +108,9 @@ double synth_ray_quadrature(const synth_scan *s, const double *ell, int32_t n_el
 {
     double cl = cos(lam + s->lambda0), sl = sin(lam + s->lambda0);
     double o[3] = { s->R * cl, s->R * sl, s->z0 + s->P * lam / (2.0 * M_PI) };
-    double sa = sin(alpha), ca = cos(alpha);
-    double d[3] = { s->D * (-sa * sl - ca * cl), s->D * (sa * cl - ca * sl), w };
+    double eu[2] = { -sl, cl }, ev[2] = { -cl, -sl };
+    double d[3];
+    det_dir(s, eu, ev, alpha, w, d);
     double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
     double acc = 0.0;

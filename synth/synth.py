@@ -1,7 +1,7 @@
 """Seeded synthetic input generator (ctypes wrapper over libsynth.so).
 
 This module holds NO Katsevich arithmetic.  It produces:
-  * exact analytic helical curved-detector sinograms of ellipsoid phantoms
+  * exact analytic helical curved-detector (or, flags & 4, flat-detector) sinograms of ellipsoid phantoms
     (closed-form ray/ellipsoid chords; scan model of
     PAPER.md l.87-94 Eq. 1 and the curved detector of l.117 / l.311-349),
   * ground-truth phantom densities,
@@ -26,7 +26,7 @@ class SynthScan(ctypes.Structure):
         ("lambda0", ctypes.c_double), ("z0", ctypes.c_double),
         ("n_rows", ctypes.c_int32), ("d_w", ctypes.c_double),
         ("n_cols", ctypes.c_int32), ("d_alpha", ctypes.c_double), ("alpha_offset", ctypes.c_double),
-        ("views_per_turn", ctypes.c_int32),
+        ("views_per_turn", ctypes.c_int32), ("flat", ctypes.c_int32),
     ]
 
 
@@ -62,7 +62,7 @@ def lib():
 def _scan(g: dict) -> SynthScan:
     return SynthScan(g["R"], g["D"], g["P"], g.get("lambda0", 0.0), g.get("z0", 0.0),
                      g["n_rows"], g["d_w"], g["n_cols"], g["d_alpha"], g.get("alpha_offset", 0.0),
-                     g["views_per_turn"])
+                     g["views_per_turn"], 1 if g.get("flags", 0) & 4 else 0)
 
 
 def _ell(ellipsoids) -> np.ndarray:
