@@ -67,14 +67,14 @@ typedef struct {
     int32_t n_rows;          /* detector rows (w) */
     double  d_w;             /* row pitch at distance D */
     int32_t n_cols;          /* detector columns (α) */
-    double  d_alpha;         /* column pitch in fan angle */
+    double  d_alpha;         /* column pitch in fan angle (KATS_FLAG_FLAT: in mm on the detector plane) */
     double  alpha_offset;    /* fractional column offset in samples (quarter offset 0.25, P:l.328) */
     int32_t views_per_turn;  /* Δλ = 2π/views_per_turn (integer, so pitches are whole view strides) */
     int32_t nx, ny;          /* voxel grid */
     double  dx, dy;
     int32_t nz_per_pitch;    /* slices per pitch; dz = pitch / nz_per_pitch */
     int32_t n_psi;           /* κ-lines ψ_i on [-π/2-α_m, π/2+α_m] (P:l.132); 0 => 2·n_rows+1 */
-    int32_t flags;           /* 0 or an OR of KATS_FLAG_HALF_SAMPLE, KATS_FLAG_HANN */
+    int32_t flags;           /* 0 or an OR of KATS_FLAG_HALF_SAMPLE, KATS_FLAG_HANN, KATS_FLAG_FLAT */
 } katsevich_geometry;
 
 /* Method variant flags (katsevich_geometry.flags):
@@ -90,6 +90,15 @@ typedef struct {
  *   A10 applied to each κ-line smoothed by [1/4, 1/2, 1/4] along α (zeros beyond the detector).  A
  *   noise/resolution trade-off for noisy sparse-view data (P:l.396-404); the adjoint is exact. */
 #define KATS_FLAG_HANN 2
+/* KATS_FLAG_FLAT — a flat detector (reading A27): the plane at distance D from the source,
+ *   perpendicular to the central ray, columns u_l = (l-(n_cols-1)/2+alpha_offset)·d_alpha [mm], rows
+ *   w_m as for the curved detector.  Steps 1-7 in those coordinates after [Noo2003a] (the
+ *   implementation PAPER.md l.115 cites): the derivative at constant ray direction
+ *   (∂_λ + (u²+D²)/D ∂_u + uw/D ∂_w), the length weight D/√(D²+u²+w²), κ-lines
+ *   w_κ(u,ψ) = DP/(2πR)(ψ + (ψ/tanψ) u/D) (Eq. 11 over cos α at u = D tan α), the Hilbert kernel
+ *   1/(π(u−u')) along u, no post-cosine, and step 7 at u* = D x·e_t/v*, w* = D(z−z_src)/v*; the
+ *   adjoint transposes those steps.  Not with KATS_FLAG_HALF_SAMPLE (the plan is rejected). */
+#define KATS_FLAG_FLAT 4
 
 typedef struct katsevich_plan katsevich_plan;
 

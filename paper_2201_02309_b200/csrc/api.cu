@@ -154,7 +154,7 @@ void free_device(katsevich_plan *p)
     if (p->device < 0) return;
     cudaSetDevice(p->device);
     void *ptrs[] = {p->d.pi_k, p->d.pi_w, p->d.view, p->d.fr, p->d.br, p->d.cos_alpha, p->d.wlen, p->d.hilbert,
-                    p->d.hilbert_tc, p->d.hilbert_hk, p->d.tile_order};
+                    p->d.hilbert_tc, p->d.hilbert_hk, p->d.tile_order, p->d.flat_a};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     p->d = DeviceTables{};
@@ -210,6 +210,12 @@ FilterParams filter_params(const katsevich_plan *p)
     f.sign = 1.f;
     f.half = p->half ? 1 : 0;
     f.apod = (p->g.flags & KATS_FLAG_HANN) ? 1 : 0;
+    f.flat = (p->g.flags & KATS_FLAG_FLAT) ? 1 : 0;
+    f.flat_a = p->d.flat_a;
+    f.D = (float)p->g.D;
+    f.dw_over_D = (float)(p->g.d_w / p->g.D);
+    f.inv_dw = (float)(1.0 / p->g.d_w);
+    f.inv_2dw = (float)(0.5 / p->g.d_w);
     return f;
 }
 
@@ -339,6 +345,13 @@ BPParams bp_params(const katsevich_plan *p)
                                 0.016795583727292406};
     for (int i = 0; i < 7; ++i) b.at[i] = (float)(c[i] / g.d_alpha);
     b.poly = std::tan(p->t.alpha_m) <= 0.75;
+    b.uu = 1.f;
+    if (g.flags & KATS_FLAG_FLAT) {          // flat (reading A27): u* / Δu = (D/Δu) (u/v*), w* = D (z - z_src)/v*
+        for (int i = 0; i < 7; ++i) b.at[i] = 0.f;
+        b.at[0] = (float)(g.D / g.d_alpha);
+        b.poly = true;
+        b.uu = 0.f;
+    }
     b.checked = !p->t.interior_in_detector;
     b.fp_cols = p->t.fp_cols;
     b.max_cta_views = (int)(p->t.bp_hi - p->t.bp_lo + 1);
@@ -375,7 +388,8 @@ BPParams bp_params(const katsevich_plan *p)
         // columns a detector column's ray strip can cover (a copy holds 128 of the 256) times the slices one
         // quad row can hold (the smallest row step per slice is at the far side of the FOV)
         const double vmax = g.R + p->t.r_fov;
-        const double strip = std::ceil(vmax * g.d_alpha / std::min(g.dx, g.dy) + 1.0) * std::ceil(16.0 * std::sqrt(2.0) + 1.0);
+        const double colw = vmax * g.d_alpha / ((g.flags & KATS_FLAG_FLAT) ? g.D : 1.0);   // a column's width at v*
+        const double strip = std::ceil(colw / std::min(g.dx, g.dy) + 1.0) * std::ceil(16.0 * std::sqrt(2.0) + 1.0);
         const double step_min = g.D / (vmax * g.d_w) * (g.pitch / g.nz_per_pitch);
         b.adj_fixed_ok = std::min(128.0, strip) * (std::ceil(1.0 / step_min) + 1.0) <= 1024.0;
     }
@@ -457,17 +471,22 @@ int katsevich_precompute(katsevich_plan *p, void *cuda_stream)
         std::vector<RebinEntry> fr(t.fr_idx.size()), br(t.br_idx.size());
         for (size_t i = 0; i < fr.size(); ++i) fr[i] = {t.fr_idx[i], (float)t.fr_frac[i]};
         for (size_t i = 0; i < br.size(); ++i) br[i] = {t.br_idx[i], (float)t.br_frac[i]};
-        std::vector<float> cosa(g.n_cols), wlen(g.n_rows), hk(2 * (size_t)g.n_cols - 1);
-        for (int l = 0; l < g.n_cols; ++l)
-            cosa[l] = (float)std::cos(((double)l - 0.5 * (g.n_cols - 1) + g.alpha_offset) * g.d_alpha);
+        const bool flat = (g.flags & KATS_FLAG_FLAT) != 0;
+        std::vector<float> cosa(g.n_cols), wlen(g.n_rows), hk(2 * (size_t)g.n_cols - 1), fa(g.n_cols);
+        for (int l = 0; l < g.n_cols; ++l) {
+            const double a = ((double)l - 0.5 * (g.n_cols - 1) + g.alpha_offset) * g.d_alpha;
+            cosa[l] = flat ? 1.f : (float)std::cos(a);                       // Eq. (15); flat: none (A27)
+            fa[l] = flat ? (float)(a / g.D) : 0.f;
+        }
         for (int m = 0; m < g.n_rows; ++m) {
             double w = ((double)m - 0.5 * (g.n_rows - 1)) * g.d_w;
             wlen[m] = (float)(g.D / std::sqrt(g.D * g.D + w * w));          // Eq. (9)
         }
-        for (int d = -(g.n_cols - 1); d <= g.n_cols - 1; ++d) {            // reading A10
-            double kd = (d & 1) ? 2.0 * g.d_alpha / (kPi * std::sin(d * g.d_alpha)) : 0.0;
+        for (int d = -(g.n_cols - 1); d <= g.n_cols - 1; ++d) {            // reading A10 (flat: 1/(π(u-u')), A27)
+            double kd = (d & 1) ? (flat ? 2.0 / (kPi * d) : 2.0 * g.d_alpha / (kPi * std::sin(d * g.d_alpha))) : 0.0;
             hk[(size_t)(d + g.n_cols - 1)] = (float)kd;
         }
+        if (flat && (rc = upload(p, &p->d.flat_a, fa, us))) return rc;
         if ((rc = upload(p, &p->d.pi_k, pik, us)) || (rc = upload(p, &p->d.pi_w, piw, us)) ||
             (rc = upload(p, &p->d.view, vg, us)) || (rc = upload(p, &p->d.fr, fr, us)) ||
             (rc = upload(p, &p->d.br, br, us)) || (rc = upload(p, &p->d.cos_alpha, cosa, us)) ||
@@ -1147,6 +1166,7 @@ static DataGenParams datagen_params(const katsevich_plan *p)
     d.R = g.R; d.D = g.D; d.h = g.pitch / (2.0 * kPi); d.lambda0 = g.lambda0; d.z0 = g.z0;
     d.dlam = 2.0 * kPi / g.views_per_turn; d.d_w = g.d_w; d.d_alpha = g.d_alpha; d.alpha_offset = g.alpha_offset;
     d.dx = g.dx; d.dy = g.dy; d.nr = g.n_rows; d.nc = g.n_cols; d.nx = g.nx; d.ny = g.ny;
+    d.flat = (g.flags & KATS_FLAG_FLAT) ? 1 : 0;
     return d;
 }
 

@@ -109,7 +109,7 @@ __device__ __forceinline__ ViewSetup view_setup(const BPParams &p, u64 viewbase,
     const float fa = cp - __int2float_rn(l);
     const float w1 = fa * inv_v;
     s.W = pk(inv_v - w1, w1);
-    const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+    const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
     s.base = fmaf(sc, zb - vg.z, p.row_cc);
     s.qmagic = p.qmagic;
     s.step = sc * p.dz;
@@ -333,7 +333,7 @@ __device__ __forceinline__ int2 plan_box(const BPParams &p, int k, float xa, flo
         cmin = fminf(cmin, col_of<POLY>(p, cx[q], cy[q], vg.x, vg.y));
         const float vstar = fmaf(-cx[q], vg.x, fmaf(-cy[q], vg.y, p.R));
         const float u = fmaf(cy[q], vg.x, -cx[q] * vg.y);
-        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
         const float p0 = fmaf(sc, zb - vg.z, p.row_c15);
         pmin = fminf(pmin, fminf(p0, fmaf(sc, (JZ - 1) * p.dz, p0)));
     }
@@ -469,7 +469,7 @@ __device__ __forceinline__ int plan_box_crop(const BPParams &p, int k, float xa,
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const float vs = fmaf(-cx[q], vg.x, fmaf(-cy[q], vg.y, p.R)), us = fmaf(cy[q], vg.x, -cx[q] * vg.y);
-            const float sc = p.D_over_dw * rsqrtf(fmaf(us, us, vs * vs));
+            const float sc = p.D_over_dw * rsqrtf(fmaf(us * p.uu, us, vs * vs));
             smin = fminf(smin, sc); smax = fmaxf(smax, sc);
         }
         const float dlo = fmaf((float)jlo, p.dz, -vg.z), dhi = fmaf((float)jhi, p.dz, -vg.z);
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(kWsThreads, (W * (V == 3 ? 4 : V == 2 ? 2 : 1)
                 const int l = __float2int_rz(cp);
                 const float fa = cp - __int2float_rn(l);
                 const float w1 = fa * inv_v, w0 = inv_v - w1;
-                const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+                const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
                 const float step = sc * p.dz;
                 const float base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));    // entry 0 = slice t_lo
                 const int bcn = boxc[n];
@@ -1014,7 +1014,7 @@ __global__ void __launch_bounds__(kWsThreads, PP == 1 ? 3 : 2) k_bp_tmem(const _
         const float fa = cp - __int2float_rn(l);
         w1 = fa * inv_v;
         w0 = inv_v - w1;
-        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
         step = sc * p.dz;
         base = fmaf(sc, -vg.z, p.row_cc);                       // slice 0 (centred quad-row position)
         ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
@@ -1342,7 +1342,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_bp_items(const __grid_constan
                     const float fa = cp - __int2float_rn(l);
                     w1 = fa * inv_v;
                     w0 = inv_v - w1;
-                    const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+                    const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
                     step = sc * p.dz;
                     base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));   // slice t_lo
                     ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
@@ -1556,7 +1556,7 @@ __global__ void __launch_bounds__(kWsThreads, 3) k_bp_items_reg(const __grid_con
             const float fa = cp - __int2float_rn(l);
             w1 = fa * inv_v;
             w0 = inv_v - w1;
-            const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+            const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
             step = sc * p.dz;
             base = fmaf((float)t_lo, step, fmaf(sc, -vg.z, p.row_cc));
             ci = min(max(l - (boxc[n] & 0xFFFF), 0), BW - 1);
@@ -1808,7 +1808,7 @@ __global__ void __launch_bounds__(TX *TY, 2) k_bp_adjoint(BPParams p)
             const float fa = cp - __int2float_rn(l);
             w1 = fa * inv_v;
             w0 = inv_v - w1;
-            const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+            const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
             step = sc * p.dz;
             base = fmaf(sc, -vg.z, p.row_cc);
             ci = min(max(l - boxc[n], 0), BW - 1);
@@ -1939,7 +1939,7 @@ __global__ void __launch_bounds__(TX *TY) k_bp_adjoint_checked(BPParams p)
         const int l = __float2int_rz(colpos);
         const float fa = colpos - __int2float_rn(l);
         const float w1 = fa * inv_v, w0 = inv_v - w1;
-        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u, u, vstar * vstar));
+        const float sc = p.D_over_dw * rsqrt_approx(fmaf(u * p.uu, u, vstar * vstar));
         const float step = sc * p.dz, base = fmaf(sc, -vg.z, p.row_cc);
         float4 *qc = qT + (int64_t)k * (p.viewbytes / 16) + (int64_t)l * NQ;
         for (int t = t_lo; t <= t_hi; ++t) {

@@ -27,8 +27,9 @@ __device__ __forceinline__ void scan_ray(const DataGenParams &p, int64_t v, int 
     const double a = ((double)l - 0.5 * (p.nc - 1) + p.alpha_offset) * p.d_alpha;
     const double w = ((double)m - 0.5 * (p.nr - 1)) * p.d_w;
     double sa, ca;
-    sincos(a, &sa, &ca);
-    const double d0 = p.D * (-sa * sn - ca * c), d1 = p.D * (sa * c - ca * sn), d2 = w;
+    if (p.flat) { sa = a; ca = p.D; }                   // flat (A27): u e_t - D e_r + w e_z
+    else { sincos(a, &sa, &ca); sa *= p.D; ca *= p.D; }
+    const double d0 = -sa * sn - ca * c, d1 = sa * c - ca * sn, d2 = w;
     const double inv = rsqrt(d0 * d0 + d1 * d1 + d2 * d2);
     dir[0] = d0 * inv;
     dir[1] = d1 * inv;

@@ -44,6 +44,52 @@ __device__ __forceinline__ float g2_at(const FilterParams &p, const float *__res
     return __ldg(p.wlen + m) * (dq + da);
 }
 
+// Flat detector (NEXT-4, reading A27): g2 = D/sqrt(D²+u²+w²) (∂_q + (u²+D²)/D ∂_u + uw/D ∂_w) g,
+// the u and w differences centred, one-sided at the edges (as the α difference above).
+__device__ __forceinline__ float g2_at_flat(const FilterParams &p, const float *__restrict__ gv, int m, int l)
+{
+    const int vs = p.nr * p.nc, nc = p.nc;
+    const float *r = gv + m * nc;
+    const float dq = (__ldg(r + l + vs) - __ldg(r + l - vs)) * p.inv_2dlam;
+    float du, dw;
+    if (l == 0) du = (__ldg(r + 1) - __ldg(r)) * p.inv_dalpha;
+    else if (l == nc - 1) du = (__ldg(r + l) - __ldg(r + l - 1)) * p.inv_dalpha;
+    else du = (__ldg(r + l + 1) - __ldg(r + l - 1)) * p.inv_2dalpha;
+    if (m == 0) dw = (__ldg(r + nc + l) - __ldg(r + l)) * p.inv_dw;
+    else if (m == p.nr - 1) dw = (__ldg(r + l) - __ldg(r - nc + l)) * p.inv_dw;
+    else dw = (__ldg(r + nc + l) - __ldg(r - nc + l)) * p.inv_2dw;
+    const float a = __ldg(p.flat_a + l);                                   // u / D
+    const float wd = ((float)m - 0.5f * (float)(p.nr - 1)) * p.dw_over_D;   // w / D
+    const float g1 = dq + p.D * fmaf(a, a, 1.f) * du + a * (wd * p.D) * dw;
+    return rsqrtf(1.f + fmaf(a, a, wd * wd)) * g1;
+}
+
+// one thread per (view, column, kPsiPer κ-lines), as k_deriv_fwd_rebin below, with the flat g2
+constexpr int kPsiPerFlat = 8;
+__global__ void __launch_bounds__(256) k_deriv_fwd_rebin_flat(FilterParams p)
+{
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i0 = blockIdx.y * kPsiPerFlat;
+    const int v = blockIdx.z;
+    if (l >= p.nc) return;
+    const int64_t g = p.view0 + v;
+    const int64_t raw = p.slab_views ? g + 2 * (g / p.slab_views) : g;
+    const float *gv = p.sino + (size_t)raw * p.nr * p.nc;
+    const size_t line0 = (size_t)v * p.npsi + i0;
+#pragma unroll
+    for (int j = 0; j < kPsiPerFlat; ++j) {
+        if (i0 + j >= p.npsi) break;
+        const RebinEntry e = p.fr[(i0 + j) * p.nc + l];
+        float o = 0.f;
+        if (e.idx >= 0) {
+            const float a = g2_at_flat(p, gv, e.idx, l);
+            const float b = g2_at_flat(p, gv, e.idx + 1, l);
+            o = fmaf(e.frac, b - a, a);
+        }
+        p.g3[k3in_off(p, line0 + j, l)] = o;
+    }
+}
+
 // A CTA spans a whole detector row (narrow detectors) and kPsiPer κ-lines of one view: each
 // thread computes kPsiPer independent samples (loads in flight together); few, fat CTAs instead
 // of one per (view, κ-line) (C4: 66K CTAs of 128 threads per chunk were launch-rate bound).
@@ -1345,6 +1391,12 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
     // column walk, 8 κ-lines per thread (two-row g2 cache; measured best on every config: C4 1.69 ->
     // 1.42 ms vs the per-sample kernel, C3 0.67 -> 0.65, C5 0.72 -> 0.71 vs 32-line segments);
     // KATS_K12=sample: one thread per sample (8 κ-lines unrolled); colN: N κ-lines per thread
+    if (p.flat) {                                               // flat detector (A27): its own K12
+        const int bx = std::min(256, (p.nc + 31) / 32 * 32);
+        k_deriv_fwd_rebin_flat<<<dim3((p.nc + bx - 1) / bx, (p.npsi + kPsiPerFlat - 1) / kPsiPerFlat, p.n_views), bx, 0,
+                                 s>>>(p);
+        return;
+    }
     const char *ke = std::getenv("KATS_K12");
     const std::string k12 = ke ? ke : "";
     const size_t wv_smem = sizeof(float) * (2 * (size_t)p.npsi * 32 + 8 * (size_t)p.nr * 32);
@@ -1710,7 +1762,15 @@ __global__ void __launch_bounds__(KT_THREADS) k_fwd_rebin_T(FilterParams p, floa
             acc[(e.idx + 1) * KT_THREADS] += e.frac * t;
         }
         float *o = g1T + (size_t)v * p.nr * nc + l;
-        for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] = acc[m * KT_THREADS] * __ldg(p.wlen + m);
+        if (p.flat) {                                              // D/sqrt(D²+u²+w²) (A27)
+            const float a = __ldg(p.flat_a + l);
+            for (int m = 0; m < p.nr; ++m) {
+                const float wd = ((float)m - 0.5f * (float)(p.nr - 1)) * p.dw_over_D;
+                o[(size_t)m * nc] = acc[m * KT_THREADS] * rsqrtf(1.f + fmaf(a, a, wd * wd));
+            }
+        } else {
+            for (int m = 0; m < p.nr; ++m) o[(size_t)m * nc] = acc[m * KT_THREADS] * __ldg(p.wlen + m);
+        }
     }
 }
 
@@ -1732,11 +1792,32 @@ __global__ void __launch_bounds__(128) k_deriv_T(FilterParams p, const float *__
         };
         const int64_t f = vr - 1;                                 // this raw view as a filtered view
         float acc = (g(f - 1, l) - g(f + 1, l)) * p.inv_2dlam;    // view stencil (g(v+1) - g(v-1)) / 2Δλ
-        // α stencil of the same view: centred inside, one-sided at both edges
-        if (l == 0) acc -= g(f, 0) * p.inv_dalpha;
-        if (l == nc - 1) acc += g(f, nc - 1) * p.inv_dalpha;
-        if (l >= 1) acc += g(f, l - 1) * (l - 1 == 0 ? p.inv_dalpha : p.inv_2dalpha);
-        if (l + 1 <= nc - 1) acc -= g(f, l + 1) * (l + 1 == nc - 1 ? p.inv_dalpha : p.inv_2dalpha);
+        // α stencil of the same view: centred inside, one-sided at both edges (flat, A27: the u stencil,
+        // each source column's term weighted by (u²+D²)/D)
+        auto gu = [&](int ll) -> float {
+            if (!p.flat) return g(f, ll);
+            const float a = __ldg(p.flat_a + ll);
+            return g(f, ll) * p.D * fmaf(a, a, 1.f);
+        };
+        if (l == 0) acc -= gu(0) * p.inv_dalpha;
+        if (l == nc - 1) acc += gu(nc - 1) * p.inv_dalpha;
+        if (l >= 1) acc += gu(l - 1) * (l - 1 == 0 ? p.inv_dalpha : p.inv_2dalpha);
+        if (l + 1 <= nc - 1) acc -= gu(l + 1) * (l + 1 == nc - 1 ? p.inv_dalpha : p.inv_2dalpha);
+        if (p.flat) {
+            // the w stencil's transpose (weights u w / D of the source row), one-sided at both row edges
+            const int nr = p.nr;
+            const float a = __ldg(p.flat_a + l);
+            auto gw = [&](int mm) -> float {
+                const float wd = ((float)mm - 0.5f * (float)(nr - 1)) * p.dw_over_D;
+                return (f >= 0 && f < nu) ? gi[(size_t)f * rs + (size_t)mm * nc + l] * a * wd * p.D : 0.f;
+            };
+            if (m == 0) acc -= gw(0) * p.inv_dw;
+            if (m == 1) acc += gw(0) * p.inv_dw;
+            if (m == nr - 1) acc += gw(nr - 1) * p.inv_dw;
+            if (m == nr - 2) acc -= gw(nr - 1) * p.inv_dw;
+            if (m - 1 >= 1 && m - 1 <= nr - 2) acc += gw(m - 1) * p.inv_2dw;
+            if (m + 1 >= 1 && m + 1 <= nr - 2) acc -= gw(m + 1) * p.inv_2dw;
+        }
         out[((size_t)item * per + vr) * rs + (size_t)m * nc + l] = acc;
     }
 }

@@ -39,6 +39,9 @@ struct FilterParams {
     int hp;                   // half pitch of a parity-split line (floats, multiple of 4)
     int half;                 // NEXT-4: Noo's half-sample derivative (raw views have nr+1 rows, nc+1 columns)
     int apod;                 // NEXT-4: Hann-apodised Hilbert (K3's input lines smoothed [1/4, 1/2, 1/4])
+    int flat;                 // NEXT-4: flat detector (K12 flat: derivative at constant ray direction, 2-D length weight)
+    const float *flat_a;      // flat: u_l / D per column
+    float D, dw_over_D, inv_dw, inv_2dw;   // flat K12
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11
@@ -75,6 +78,7 @@ struct BPParams {
     float row_cc, qmagic;     // centred quad-row origin row_c15 - c and kMagic + c, c = (nr + 2) / 2
     float pm_lo, pm_hi;       // centred quad-row range of an in-detector sample (checked taps)
     float at[7];              // α*/Δα polynomial in t = u/v*: t·Σ at[i] t^(2i)
+    float uu;                 // 1: curved (w* = D(z-z_src)/sqrt(u²+v*²)); 0: flat detector (D(z-z_src)/v*; at = {D/Δu, 0..})
     float x0, dx, y0, dy, dz;
     float scale;              // Δλ / 2π
     bool poly;                // use the polynomial arctangent (|α| <= 36.8°)
@@ -121,6 +125,7 @@ void launch_make_quads(const float *gF, float4 *q, int64_t n, int nr, int nc, cu
 struct DataGenParams {
     double R, D, h, lambda0, z0, dlam, d_w, d_alpha, alpha_offset, dx, dy;
     int nr, nc, nx, ny;
+    int flat;                 // KATS_FLAG_FLAT: column coordinate u [mm] on the plane at distance D
 };
 void launch_project_ellipsoids(const DataGenParams &p, const double *ell, int n, int64_t v0, int64_t nv, float *out,
                                cudaStream_t s);

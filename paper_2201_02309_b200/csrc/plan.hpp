@@ -56,6 +56,7 @@ struct DeviceTables {
     float *hilbert_tc = nullptr;   // K3 tensor-core tap matrices (hi/lo TF32 split, UMMA layout)
     float *hilbert_hk = nullptr;   // K3 tensor-core Hankel tap cores (hi/lo TF32 split)
     int *tile_order = nullptr;     // step-7 column tiles (16x16), heaviest first (ty * ntx + tx)
+    float *flat_a = nullptr;       // KATS_FLAG_FLAT: u_l / D per column
 };
 
 struct ProfRecord { int stage; void *ev0; void *ev1; };

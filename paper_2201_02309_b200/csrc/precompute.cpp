@@ -21,6 +21,7 @@ namespace {
 struct Geo {
     double R, D, P, lam0, z0, dlam, h, r_fov, dw, da, aoff, dx, dy, dz;
     int nr, nc, nx, ny, nz, vt;
+    bool flat;                      // KATS_FLAG_FLAT: column coordinate u [mm] on the plane at distance D
 };
 
 Geo derive(const katsevich_geometry &g)
@@ -35,7 +36,19 @@ Geo derive(const katsevich_geometry &g)
     o.dw = g.d_w; o.da = g.d_alpha; o.aoff = g.alpha_offset;
     o.dx = g.dx; o.dy = g.dy; o.dz = g.pitch / g.nz_per_pitch;
     o.nr = g.n_rows; o.nc = g.n_cols; o.nx = g.nx; o.ny = g.ny; o.nz = g.nz_per_pitch;
+    o.flat = (g.flags & KATS_FLAG_FLAT) != 0;
     return o;
+}
+
+// Detector column position (fractional column index) and row scale (rows per unit of z - z_src) of
+// the ray from the source through (x, y) at view angle (c, s): curved α* = atan2(u, v*), w* =
+// D (z - z_src)/sqrt(u² + v*²) (P:l.161-170); flat (reading A27) u* = D u / v*, w* = D (z - z_src)/v*.
+inline void ray_col_scale(const Geo &o, double x, double y, double c, double s, double &col, double &sc)
+{
+    const double vs = o.R - x * c - y * s, us = -x * s + y * c;
+    const double a = o.flat ? o.D * us / vs : std::atan2(us, vs);
+    col = a / o.da + 0.5 * (o.nc - 1) - o.aoff;
+    sc = o.D / (o.flat ? vs : std::hypot(us, vs)) / o.dw;
 }
 
 // A12 canonical snapping: an argument within 1e-9 of an integer is that integer.
@@ -100,12 +113,13 @@ bool pi_line_newton(const Geo &o, double x, double y, double z, double &li, doub
     return ok && std::fabs(F) < 1e-9;
 }
 
-// Eq. (11): w_κ(α, ψ) = (DP/2πR)(ψ cos α + (ψ/tan ψ) sin α).
+// Eq. (11): w_κ(α, ψ) = (DP/2πR)(ψ cos α + (ψ/tan ψ) sin α); flat (reading A27): the same κ-plane on
+// the plane at distance D, (DP/2πR)(ψ + (ψ/tan ψ) u/D).
 inline double kappa_height(const Geo &o, double kappa, double alpha, double psi)
 {
     double q = std::fabs(psi) < 1e-6 ? 1.0 - psi * psi / 3.0 - psi * psi * psi * psi / 45.0
                                      : psi * std::cos(psi) / std::sin(psi);
-    (void)o;
+    if (o.flat) return kappa * (psi + q * alpha / o.D);
     return kappa * (psi * std::cos(alpha) + q * std::sin(alpha));
 }
 
@@ -170,13 +184,15 @@ int validate(const katsevich_geometry &g, std::string &detail)
     if (g.nx < 1 || g.ny < 1 || g.nz_per_pitch < 1) return bad("empty voxel grid");
     if (!(g.dx > 0) || !(g.dy > 0)) return bad("voxel spacing <= 0");
     if (g.n_psi != 0 && g.n_psi < 2) return bad("n_psi must be 0 or >= 2");
-    if (g.flags & ~(KATS_FLAG_HALF_SAMPLE | KATS_FLAG_HANN)) return bad("unknown flags");
+    if (g.flags & ~(KATS_FLAG_HALF_SAMPLE | KATS_FLAG_HANN | KATS_FLAG_FLAT)) return bad("unknown flags");
+    if ((g.flags & KATS_FLAG_FLAT) && (g.flags & KATS_FLAG_HALF_SAMPLE))
+        return bad("the half-sample derivative is not supported with the flat detector");
     if ((g.flags & KATS_FLAG_HALF_SAMPLE) && (g.n_rows < 3 || g.n_cols < 3))
         return bad("the half-sample derivative needs n_rows >= 3 and n_cols >= 3");
     if ((g.flags & KATS_FLAG_HALF_SAMPLE) && g.n_rows > 65) return bad("the half-sample derivative needs n_rows <= 65");
     if (!std::isfinite(g.lambda0) || !std::isfinite(g.z0) || !std::isfinite(g.alpha_offset)) return bad("non-finite parameter");
     double half_fan = (0.5 * (g.n_cols - 1) + std::fabs(g.alpha_offset)) * g.d_alpha;
-    if (!(half_fan < 0.5 * kPi)) return bad("detector fan reaches |alpha| >= pi/2");
+    if (!(g.flags & KATS_FLAG_FLAT) && !(half_fan < 0.5 * kPi)) return bad("detector fan reaches |alpha| >= pi/2");
     Geo o = derive(g);
     if (g.r_fov < 0 || !(o.r_fov < g.R)) return bad("r_fov >= R (FOV cylinder must lie inside the helix)");
     return KATS_OK;
@@ -278,8 +294,9 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
                     double k = e == 0 ? std::ceil(ti) : std::floor(to);
                     double lam = k * o.dlam;
                     double c = std::cos(lam + o.lam0), s = std::sin(lam + o.lam0);
-                    double vs = o.R - x * c - y * s, us = -x * s + y * c;
-                    double wst = o.D / std::hypot(us, vs) * (z - o.z0 - o.h * lam);
+                    double col, sc;
+                    ray_col_scale(o, x, y, c, s, col, sc);
+                    double wst = sc * o.dw * (z - o.z0 - o.h * lam);
                     wL = std::max(wL, std::fabs(wst));
                 }
             }
@@ -298,9 +315,11 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
     // Interior views (k_first < k < k_last) sample inside [λ_i, λ_o], so |w*| <= w_L and
     // |α*| <= α_m; with a relative margin well above fp32 rounding the kernel may skip the
     // per-sample detector test.
+    // (flat: |u*| <= D tan α_m over the FOV cylinder)
     const double a_lo = (-0.5 * (nc - 1) + o.aoff) * o.da, a_hi = (0.5 * (nc - 1) + o.aoff) * o.da;
+    const double a_m = o.flat ? o.D * std::tan(t.alpha_m) : t.alpha_m;
     t.interior_in_detector = wL <= 0.5 * (nr - 1) * o.dw * (1.0 - 1e-5) &&
-                             a_lo <= -t.alpha_m - 1e-5 * o.da && a_hi >= t.alpha_m + 1e-5 * o.da;
+                             a_lo <= -a_m - 1e-5 * o.da && a_hi >= a_m + 1e-5 * o.da;
     (void)root_fail;
 
     // ---- footprint box of one CTA (kTileX x kTileY columns, kChunkZ slices) on one
@@ -335,9 +354,8 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
                         double cmin = 1e300, cmax = -1e300, pmin = 1e300, pmax = -1e300;
                         const double cx[4] = {xa, xb, xa, xb}, cy[4] = {ya, ya, yb, yb};
                         for (int q = 0; q < 4; ++q) {
-                            const double vs = o.R - cx[q] * c - cy[q] * s, us = -cx[q] * s + cy[q] * c;
-                            const double col = std::atan2(us, vs) / o.da + 0.5 * (nc - 1) - o.aoff;
-                            const double sc = o.D / std::hypot(us, vs) / o.dw;
+                            double col, sc;
+                            ray_col_scale(o, cx[q], cy[q], c, s, col, sc);
                             const double p0 = sc * (zb - zc) + 0.5 * (nr - 1) + 1.5;
                             const double p1 = p0 + sc * (kChunkZ - 1) * o.dz;
                             cmin = std::min(cmin, col); cmax = std::max(cmax, col);
@@ -396,8 +414,8 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
                     double cmin = 1e300, cmax = -1e300;
                     const double cx[4] = {xa, xb, xa, xb}, cy[4] = {ya, ya, yb, yb};
                     for (int q = 0; q < 4; ++q) {
-                        const double vs = o.R - cx[q] * c - cy[q] * s, us = -cx[q] * s + cy[q] * c;
-                        const double col = std::atan2(us, vs) / o.da + 0.5 * (nc - 1) - o.aoff;
+                        double col, sc;
+                        ray_col_scale(o, cx[q], cy[q], c, s, col, sc);
                         cmin = std::min(cmin, col); cmax = std::max(cmax, col);
                     }
                     bw = std::max(bw, (int)(std::floor(cmax) - std::floor(cmin)) + 3);

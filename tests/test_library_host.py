@@ -39,7 +39,7 @@ def test_library_is_sm100a_code():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("name", ["T1", "T2", "T3", "C1", "C5"])
+@pytest.mark.parametrize("name", ["T1", "T2", "T3", "C1", "C5", "TF1", "C2F"])
 def test_host_tables_bit_exact_vs_oracle(name):
     from oracle import oracle
     cfg = configs.get(name)
@@ -204,3 +204,15 @@ def test_half_sample_plan_tables_and_views(name):
     assert np.abs(wf - t["w_first"]).max() < 1e-9 and np.abs(wl - t["w_last"]).max() < 1e-9
     fv, nv = oracle.pitch_slab(vc, 2)                 # [K_lo - 1, K_hi + 1] of the shifted grid
     assert p.pitch_views(2) == (fv + 1, nv - 1)
+
+
+def test_flat_flag_validation():
+    """KATS_FLAG_FLAT (4) is accepted alone and with the Hann filter; with the half-sample derivative
+    the plan is rejected (not supported)."""
+    cfg = configs.get("TF1")
+    for flags, ok in ((4, True), (4 | 2, True), (4 | 1, False)):
+        if ok:
+            k.Plan(dict(cfg, flags=flags), device=-1).precompute()
+        else:
+            with pytest.raises(k.KatsevichError):
+                k.Plan(dict(cfg, flags=flags), device=-1)
