@@ -216,6 +216,7 @@ FilterParams filter_params(const katsevich_plan *p)
     f.dw_over_D = (float)(p->g.d_w / p->g.D);
     f.inv_dw = (float)(1.0 / p->g.d_w);
     f.inv_2dw = (float)(0.5 / p->g.d_w);
+    f.br_monotone = p->t.br_monotone ? 1 : 0;
     return f;
 }
 

@@ -1822,8 +1822,78 @@ __global__ void __launch_bounds__(128) k_deriv_T(FilterParams p, const float *__
     }
 }
 
+// K4^T, streaming form (T_br monotone down each column): a CTA takes one view and 128 columns; the
+// quad-adjoint columns (rows contiguous) are staged through shared memory in chunks of rows with
+// coalesced loads, and each thread walks its column's rows in order keeping the two κ-lines the
+// current row feeds in registers: a line is written once, when the rows have moved past it (lines no
+// row reaches are written 0), so there is no read-modify-write and no separate zeroing pass.
+constexpr int K4T_COLS = 128, K4T_RC = 16, K4T_QP = K4T_RC + 3;     // rows per chunk; staged pitch (odd)
+__global__ void __launch_bounds__(K4T_COLS) k_bwd_rebin_cos_T_stream(FilterParams p, const float4 *__restrict__ qT)
+{
+    __shared__ float4 sq[(K4T_COLS + 1) * K4T_QP];                    // [column l0-1+c][quad row m0+1+r]
+    const int tid = threadIdx.x, l0 = blockIdx.x * K4T_COLS, l = l0 + tid, v = blockIdx.y;
+    const int nc = p.nc, nr = p.nr, nq = nr + 2, c = (nr + 2) / 2;
+    const size_t line0 = (size_t)v * p.npsi;
+    const float4 *qv = qT + (size_t)v * nc * nq;
+    const float ca = l < nc ? __ldg(p.cos_alpha + l) : 0.f;
+    int L = -1;                                                         // first line of the pair held
+    float a0 = 0.f, a1 = 0.f;
+    auto put = [&](int line, float val) { p.g4[k3in_off(p, line0 + line, l)] = val; };
+    for (int m0 = 0; m0 < nr; m0 += K4T_RC) {
+        const int rc = min(K4T_RC, nr - m0);
+        __syncthreads();
+        // quad rows m0+1 .. m0+rc+1 of columns l0-1 .. l0+127 (coalesced along each column's rows)
+        const int nrow = rc + 1;
+        for (int i = tid; i < (K4T_COLS + 1) * nrow; i += K4T_COLS) {
+            const int cc = i / nrow, r = i - cc * nrow, lc = l0 - 1 + cc;
+            sq[cc * K4T_QP + r] = (lc >= 0 && lc < nc) ? __ldg(qv + (size_t)lc * nq + m0 + 1 + r)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        if (l >= nc) continue;
+        const float4 *qa = sq + (tid + 1) * K4T_QP, *qb = sq + tid * K4T_QP;   // column l, column l-1
+        for (int j = 0; j < rc; ++j) {
+            const int m = m0 + j;
+            const float rh = (float)(m + 2 - c), rl = (float)(m + 1 - c);
+            const float4 A = qa[j + 1], B = qa[j];
+            float gt = 0.5f * A.x - (A.z - rh * A.x) + 0.5f * B.x + (B.z - rl * B.x);
+            if (l > 0) {
+                const float4 C = qb[j + 1], D = qb[j];
+                gt += 0.5f * C.y - (C.w - rh * C.y) + 0.5f * D.y + (D.w - rl * D.y);
+            }
+            const RebinEntry e = p.br[m * nc + l];
+            if (e.idx < 0) continue;
+            const float val = ca * gt, c0 = (1.f - e.frac) * val, c1 = e.frac * val;
+            if (L < 0) {
+                for (int i = 0; i < e.idx; ++i) put(i, 0.f);
+                L = e.idx; a0 = c0; a1 = c1;
+            } else if (e.idx == L) {
+                a0 += c0; a1 += c1;
+            } else if (e.idx == L + 1) {
+                put(L, a0);
+                L = e.idx; a0 = a1 + c0; a1 = c1;
+            } else {
+                put(L, a0); put(L + 1, a1);
+                for (int i = L + 2; i < e.idx; ++i) put(i, 0.f);
+                L = e.idx; a0 = c0; a1 = c1;
+            }
+        }
+    }
+    if (l >= nc) return;
+    int next = 0;
+    if (L >= 0) { put(L, a0); put(L + 1, a1); next = L + 2; }
+    for (int i = next; i < p.npsi; ++i) put(i, 0.f);
+}
+
 void launch_bwd_rebin_cos_T(const FilterParams &p, const float4 *qT, cudaStream_t s)
 {
+    // streaming form when T_br is monotone down every column (all configurations here; KATS_K4T=rmw: the
+    // read-modify-write kernel below)
+    const char *k4t = std::getenv("KATS_K4T");
+    if (p.br_monotone && !(k4t && std::string(k4t) == "rmw")) {
+        k_bwd_rebin_cos_T_stream<<<dim3((p.nc + K4T_COLS - 1) / K4T_COLS, p.n_views), K4T_COLS, 0, s>>>(p, qT);
+        return;
+    }
     const char *e = std::getenv("KATS_K4T_VPB");            // A/B: two views per thread
     if (e && std::atoi(e) == 2) {
         k_bwd_rebin_cos_T2<<<dim3((p.nc + 127) / 128, (p.n_views + 1) / 2), 128, 0, s>>>(p, qT);

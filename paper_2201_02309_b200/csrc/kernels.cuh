@@ -42,6 +42,7 @@ struct FilterParams {
     int flat;                 // NEXT-4: flat detector (K12 flat: derivative at constant ray direction, 2-D length weight)
     const float *flat_a;      // flat: u_l / D per column
     float D, dw_over_D, inv_dw, inv_2dw;   // flat K12
+    int br_monotone;          // T_br's κ-line index nondecreasing down every column (K4^T streams its lines)
 };
 
 void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s);   // K12: Eqs. 8, 9, 10-11

@@ -34,6 +34,7 @@ struct HostTables {
     int32_t fp_cols = 0, fp_rows = 0;       // quad box (columns x quad rows) covering any CTA's interior samples of one view
     int32_t max_active = 0;                 // max slices of one column whose interior windows share a view
     bool windows_monotone = false;          // per column: k_first, k_last nondecreasing in z, interior windows non-empty
+    bool br_monotone = false;               // per column: T_br's κ-line index nondecreasing in the row (K4^T streams)
     int32_t fp_cols_column = 0;             // quad columns covering a tile's full-column samples of one view
     int32_t warp_span = 0;                  // max live slices of one warp (8x4 columns): newest open .. oldest unflushed
     int32_t warp_span2 = 0;                 // same for two consecutive views done together: open at k+1 .. unflushed at k

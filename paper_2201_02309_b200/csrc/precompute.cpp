@@ -255,6 +255,19 @@ int compute_host_tables(const katsevich_geometry &g, HostTables &t, std::string 
             }
         }
 
+    // K4^T writes each κ-line of a column once, walking the rows, when T_br's index never decreases
+    // down a column (rows without a root are skipped)
+    t.br_monotone = true;
+    for (int l = 0; l < nc && t.br_monotone; ++l) {
+        int32_t prev = -1;
+        for (int m = 0; m < nr; ++m) {
+            const int32_t i = t.br_idx[(size_t)m * nc + l];
+            if (i < 0) continue;
+            if (i < prev) { t.br_monotone = false; break; }
+            prev = i;
+        }
+    }
+
     // ---- T_pi: PI-line limits per voxel of pitch 0 (P:l.194-202) ----
     const size_t nvox = (size_t)o.nx * o.ny * o.nz;
     t.pi_first.assign(nvox, 0);
