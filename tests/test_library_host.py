@@ -114,7 +114,7 @@ def test_td_warning_when_rows_too_short():
 
 @pytest.mark.parametrize("field,value", [("R", -1.0), ("D", 0.0), ("pitch", 0.0), ("views_per_turn", 2),
                                          ("n_cols", 1), ("n_rows", 1), ("d_w", 0.0), ("r_fov", 600.0),
-                                         ("flags", 4), ("n_psi", 1), ("d_alpha", 0.5)])
+                                         ("flags", 8), ("flags", 5), ("n_psi", 1), ("d_alpha", 0.5)])
 def test_invalid_geometry_rejected(field, value):
     g = k.geometry_from_config(configs.get("T1"))
     setattr(g, field, value)
