@@ -166,6 +166,14 @@ def get(name: str) -> dict:
                    views_per_turn=200, nx=61, ny=53, dx=4.1, nz=19, n_pitches=3,
                    phantom=shepp_logan(110.0, 80.0, 1.5 * P), lambda0=-1.3, z0=-7.0, flags=FLAT,
                    desc="flat-detector ragged config, 3 pitches")
+    if n == "TF2":
+        # T2's paper-like helix and slab with a flat detector: 157 x 2.6 mm columns (u* up to 178 mm) and 18
+        # rows (the flat Tam-Danielsson window is ~9 % taller at the edge columns than the curved one)
+        P = 7.0 * math.pi
+        return _mk("TF2", R=1085.6, D=595.0, P=P, n_rows=18, d_w=0.5176, n_cols=157,
+                   d_alpha=2.6, views_per_turn=90, nx=48, ny=40, dx=10.0, nz=10,
+                   n_pitches=2, phantom=shepp_logan(300.0, 300.0, P), flags=FLAT,
+                   desc="paper-like geometry, flat detector, small grid, 2 pitches")
     if n == "C2F":
         # C2's volume and scan with a flat 36 x 368 detector (2 mm columns: u* up to 346 mm; 36 rows for
         # the flat Tam-Danielsson window, which widens by 1 + u^2/D^2 towards the edges)

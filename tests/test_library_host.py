@@ -39,7 +39,7 @@ def test_library_is_sm100a_code():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("name", ["T1", "T2", "T3", "C1", "C5", "TF1", "C2F"])
+@pytest.mark.parametrize("name", ["T1", "T2", "T3", "C1", "C5", "TF1", "TF2", "C2F"])
 def test_host_tables_bit_exact_vs_oracle(name):
     from oracle import oracle
     cfg = configs.get(name)
