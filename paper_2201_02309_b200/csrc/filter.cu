@@ -870,7 +870,7 @@ __global__ void __launch_bounds__(HK_THREADS, 2) k_hilbert_hk(FilterParams p, in
 //               the accumulator, while the tensor core already works on the next item.
 // ---------------------------------------------------------------------------
 // warps 0-7 convert, 8 issues MMAs, 9-12 epilogue, 13 issues the A chunk TMAs
-constexpr int WS_PROD = 8, WS_EPI = 4, WS_THREADS = 32 * (WS_PROD + 1 + WS_EPI + 1), WS_NST = 2, WS_RAW = 4;
+constexpr int WS_PROD = 8, WS_EPI = 4, WS_THREADS = 32 * (WS_PROD + 1 + WS_EPI + 1);
 constexpr unsigned WS_RAWB = TC_M * TC_KC * 4;                    // one raw A chunk: 128 lines x 32 inputs
 // A tiles of this kernel: K-major core matrices with LBO = 144 B (K quads 9 bank groups apart) and
 // SBO = 1152 B, so the 8 K quads of one line a quarter-warp stores hit 8 different 16-B bank groups
@@ -897,6 +897,8 @@ __device__ __forceinline__ void ws_arrive(unsigned bar)
 }
 
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
+// WS_NST converted A stages (hi/lo tiles), WS_RAW raw TMA chunks in flight
+template <int WS_NST, int WS_RAW>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_hilbert_ws(const __grid_constant__ CUtensorMap amap, FilterParams p,
                                                               int64_t n_lines, int nsplit)
 {
@@ -1567,19 +1569,33 @@ int launch_hilbert(const FilterParams &p, cudaStream_t s)
                 const int v = std::atoi(e);
                 if (v >= 1 && NH % (16 * v) == 0 && NH / v <= 256) ns = v;
             }
-            const size_t wsm = taps + (size_t)WS_NST * 2 * WS_ATILE + (size_t)WS_RAW * WS_RAWB + (size_t)WS_EPI * 32 * 17 * 4;
+            // converted A stages / raw chunks: 2 / 4 (KATS_WS_STAGES=3: three A stages, with four raw chunks where
+            // shared memory allows, else three)
+            auto wsm_of = [&](int nst, int raw) {
+                return taps + (size_t)nst * 2 * WS_ATILE + (size_t)raw * WS_RAWB + (size_t)WS_EPI * 32 * 17 * 4;
+            };
+            int nst = 2, nraw = 4;
+            if (const char *e = std::getenv("KATS_WS_STAGES"))
+                if (std::atoi(e) == 3) { nst = 3; nraw = wsm_of(3, 4) <= 225 * 1024 ? 4 : 3; }
+            if (wsm_of(nst, nraw) > 225 * 1024) { nst = 2; nraw = 4; }
+            const size_t wsm = wsm_of(nst, nraw);
             CUtensorMap amap;                                         // the K3 input: [n_lines][2 hp] fp32
             if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M)) {
                 // cannot happen on a driver that has cuTensorMapEncodeTiled (16-B aligned scratch lines);
                 // nothing else reads parity-split lines: the caller turns this into KATS_ERR_CUDA
                 return -1;
             }
-            smem_opt_in((const void *)k_hilbert_ws, 225 * 1024);
             int nsm2 = 148;
             nsm2 = device_sms();
             const int64_t items = (n_lines + TC_M - 1) / TC_M * ns;
             const int per = (int)std::min<int64_t>(items, std::max(1, nsm2 / 2));   // one CTA per SM, half per parity
-            k_hilbert_ws<<<(unsigned)(2 * per), WS_THREADS, wsm, s>>>(amap, p, n_lines, ns);
+            auto go = [&](auto kern) {
+                smem_opt_in((const void *)kern, 225 * 1024);
+                kern<<<(unsigned)(2 * per), WS_THREADS, wsm, s>>>(amap, p, n_lines, ns);
+            };
+            if (nst == 3 && nraw == 4) go(k_hilbert_ws<3, 4>);
+            else if (nst == 3) go(k_hilbert_ws<3, 3>);
+            else go(k_hilbert_ws<2, 4>);
             return 0;
         }
         const int64_t n_items = (n_lines + TC_M - 1) / TC_M * nsplit;
