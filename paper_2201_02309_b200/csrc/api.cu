@@ -187,9 +187,24 @@ int64_t n_union_views(const katsevich_plan *p, int32_t n_pitches)
 size_t raw_view_elems(const katsevich_plan *p) { return (size_t)p->graw.n_rows * p->graw.n_cols; }
 int halo_lo(const katsevich_plan *p) { return p->half ? 0 : 1; }
 
-size_t filter_chunk_bytes(const katsevich_plan *p, int mul = 1)
+size_t chunk_bytes_views(const katsevich_plan *p, int64_t views)
 {
-    return 2 * sizeof(float) * (size_t)filter_chunk_views(p, mul) * p->t.n_psi * g3_line_pitch(p->g.n_cols);
+    return 2 * sizeof(float) * (size_t)views * p->t.n_psi * g3_line_pitch(p->g.n_cols);
+}
+size_t filter_chunk_bytes(const katsevich_plan *p, int mul = 1) { return chunk_bytes_views(p, filter_chunk_views(p, mul)); }
+
+// Filter chunk of the batch entry point: the batch's filtered views in an even number of equal chunks
+// of at most 8 base chunks, alternating over the two filter streams (C5: two chunks of 4640 views, step
+// 3.675 -> 3.59 ms against 3072-view chunks; scripts/ab/gpu_fchunk_c5.sh); KATS_BATCH_CHUNK=0 keeps
+// the device chunk
+static int64_t batch_chunk_views(const katsevich_plan *p, int32_t B)
+{
+    static const bool off = [] { const char *e = std::getenv("KATS_BATCH_CHUNK"); return e && e[0] == '0'; }();
+    const int64_t dev = filter_chunk_views(p, device_chunk_mul());
+    if (off) return dev;
+    const int64_t nb = (p->t.bp_hi - p->t.bp_lo + 1) * (int64_t)B, cap = 8 * (int64_t)filter_chunk_views(p, 1);
+    const int64_t k = (nb + 2 * cap - 1) / (2 * cap);
+    return std::max<int64_t>(1, (nb + 2 * k - 1) / (2 * k));
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -250,7 +265,7 @@ static int filter_streams(katsevich_plan *p)
 // stream waits for all of them at the end).  C5 4.75 -> 4.31 ms per step with two streams.
 int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, float4 *gq,
                float *scratch, float *dbg3, float *dbg4, float *dbgF, cudaStream_t s, bool overlapped = false,
-               int64_t slab_views = 0, bool multi = false, int chunk_mul = 1)
+               int64_t slab_views = 0, bool multi = false, int chunk_mul = 1, int64_t chunk_views = 0)
 {
     FilterParams f = filter_params(p);
     // running concurrently with the TMEM backprojection: K3 uses the fp32 direct convolution
@@ -262,7 +277,7 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
     const size_t qs = quad_view_elems(p);
     const size_t ps_dbg = (size_t)p->t.n_psi * p->g.n_cols;              // debug stage arrays: plain lines
     const size_t ps = (size_t)p->t.n_psi * g3_line_pitch(p->g.n_cols);  // scratch lines
-    const int kFilterChunk = filter_chunk_views(p, chunk_mul);
+    const int64_t kFilterChunk = chunk_views > 0 ? chunk_views : filter_chunk_views(p, chunk_mul);
     const int64_t nchunks = (n_out + kFilterChunk - 1) / kFilterChunk;
     const int ns = multi && !dbg3 && !dbg4 && !dbgF ? (int)std::min<int64_t>(filter_streams(p), nchunks) : 1;
     cudaStream_t st[kFilterStreamsMax] = {s};
@@ -271,7 +286,7 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
         KCHECK(p, cudaEventRecord((cudaEvent_t)p->fork_events[0], s));
         for (int i = 1; i < ns; ++i) KCHECK(p, cudaStreamWaitEvent(st[i], (cudaEvent_t)p->fork_events[0], 0));
     }
-    const size_t chunk_floats = align_up(filter_chunk_bytes(p, chunk_mul)) / sizeof(float);
+    const size_t chunk_floats = align_up(chunk_bytes_views(p, kFilterChunk)) / sizeof(float);
     for (int64_t v0 = 0; v0 < n_out; v0 += kFilterChunk) {
         const int nv = (int)std::min<int64_t>(kFilterChunk, n_out - v0);
         const int c = (int)((v0 / kFilterChunk) % ns);
@@ -557,7 +572,9 @@ int katsevich_workspace_bytes(const katsevich_plan *p, int32_t n_pitches, size_t
     const int64_t nslab = p->t.bp_hi - p->t.bp_lo + 1;
     // reconstruct: filtered quads over the union of views; batch: per slab
     size_t gf = sizeof(float4) * qs * (size_t)std::max<int64_t>(n_union_views(p, n_pitches), nslab * n_pitches);
-    *bytes = align_up(gf) + kFilterStreamsMax * align_up(filter_chunk_bytes(p, device_chunk_mul()));   // chunk scratches (run_filter)
+    // chunk scratches (run_filter): the device chunk, or the batch chunk of B = n_pitches slabs
+    const size_t chunk = std::max(filter_chunk_bytes(p, device_chunk_mul()), chunk_bytes_views(p, batch_chunk_views(p, n_pitches)));
+    *bytes = align_up(gf) + kFilterStreamsMax * align_up(chunk);
     return KATS_OK;
 }
 
@@ -908,7 +925,8 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     if (ng == 1) {
         // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
         // keeps its own +-1 halo)
-        rc = run_filter(p, slabs + halo_lo(p) * rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true, device_chunk_mul());
+        rc = run_filter(p, slabs + halo_lo(p) * rs, nbp * B, gq, scratch, nullptr, nullptr, nullptr, s, false, nbp, true,
+                        device_chunk_mul(), batch_chunk_views(p, B));
         if (rc) return rc;
         BPParams bp = bp_params(p);
         bp.gq = gq;
