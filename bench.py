@@ -446,6 +446,57 @@ def run_ours(args):
                           "what": "alpha stride 4 + 'Gaussian+Poisson' (I0 1e5, var 0.5), Philox4x32-10"}}
         del sino_g, sino_v
 
+    # ---- method variants (NEXT-4): the same step with Noo's half-sample derivative and with the
+    # Hann-apodised filter at this config, and the flat-detector counterpart config where one exists
+    # (C2 -> C2F); device-resident, CUDA events, one process (rank 0 of a single-rank run) ----
+    var = None
+    if world == 1 and not args.no_variants:
+        from synth import configs as _cf
+
+        import paper_2201_02309_b200 as _kpkg
+
+        def vstep(vcfg, reuse_input):
+            vp = _kpkg.Plan(vcfg, device=local)
+            vp.precompute()
+            if batch:
+                a0_, n_ = vp.pitch_views(0)
+                x = dev_in if reuse_input else torch.from_numpy(
+                    np.stack([synth.project(vcfg, phs[b], a0_, n_) for b in range(batch)])).to(dev)
+                o = torch.empty(vol_shape, dtype=torch.float32, device=dev)
+                fn = lambda: vp.reconstruct_batch(x, out=o, stream=stream)
+            else:
+                a0_, n_ = vp.scan_views(first_pitch, pitches)
+                x = dev_in if reuse_input else torch.from_numpy(
+                    synth.project(vcfg, rank_phantom(vcfg, first_pitch - (first_pitch % vcfg["n_pitches"])), a0_, n_)).to(dev)
+                o = torch.empty((pitches * vcfg["nz"], vcfg["ny"], vcfg["nx"]), dtype=torch.float32, device=dev)
+                fn = lambda: vp.reconstruct(x, a0_, first_pitch, pitches, out=o, stream=stream)
+            for _ in range(args.warmup):
+                fn()
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            b1.record(stream)
+            torch.cuda.synchronize()
+            ms = b0.elapsed_time(b1) / args.steps
+            u = count_updates(vp) * n_items
+            del x, o
+            return {"ms_per_step": ms, "value": u / (ms * 1e-3), "unit": "updates/s", "bp_kernel": vp.bp_kernel()}
+
+        var = {"half_sample": dict(vstep(dict(cfg, flags=1), False), flags=1,
+                                   what="Noo's 2x2x2 half-sample derivative (reading A25), same scan"),
+               "hann": dict(vstep(dict(cfg, flags=2), True), flags=2,
+                            what="Hann-apodised Hilbert filter (reading A26), same input")}
+        try:
+            fcfg = _cf.get(cfg["name"] + "F")
+        except KeyError:
+            fcfg = None
+        if fcfg is not None and not batch:
+            var["flat"] = dict(vstep(fcfg, False), config=fcfg["name"],
+                               what="flat-detector counterpart (reading A27): " + fcfg["desc"])
+        torch.cuda.synchronize()
+
     items_all, launches_all = n_items, stats["total_launches"]
     if world > 1:
         tt = torch.tensor([n_items, launches_all], dtype=torch.float64, device=dev)
@@ -537,6 +588,8 @@ def run_ours(args):
     }
     if dg:
         line["datagen"] = dg
+    if var:
+        line["variants"] = var
     if adj:
         line["adjoint"] = {"metric": "voxel-view updates/s (transpose: volume -> sinogram)",
                            "value": U_all / (adj["ms_per_step"] * 1e-3), "unit": "updates/s",
@@ -689,6 +742,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-adjoint", action="store_true", help="skip the adjoint (NEXT-1) measurement")
     ap.add_argument("--no-datagen", action="store_true", help="skip the data-generation (NEXT-3) measurement")
+    ap.add_argument("--no-variants", action="store_true", help="skip the method-variant (NEXT-4) measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
