@@ -324,6 +324,7 @@ def run_ours(args):
     stats = plan.profile_read(reset=True)
     plan.profile_enable(False)
     ms_step = ms / args.steps
+    step_bp_kernel = plan.bp_kernel()          # the timed step's step-7 kernel (before the e2e / adjoint runs)
 
     # ---- K5 in isolation: the same step with one backprojection launch over all of the rank's
     # pitches after all filtering (KATS_PIPELINE=0, the default), so no other kernel shares the GPU
@@ -523,7 +524,7 @@ def run_ours(args):
     fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     smem_peak, smem_src = smem_peak_gbs(peaks.get("sm_max_mhz", 1965.0))
     achieved_smem = U_rank * bp_smem_bytes_per_update() / (k5_busy * 1e-3) / 1e9
-    bp_kernel = plan.bp_kernel()
+    bp_kernel = step_bp_kernel
     share = {s: stats["busy_ms"][s] / args.steps / ms_step for s in stats["busy_ms"] if stats["busy_ms"][s] > 0}
     line = {
         "metric": "voxel-view updates/s",

@@ -2240,7 +2240,10 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
     const bool small_grid = staged_ctas < nsm && !want_tmem && !want_window;
     // TMEM-window kernel for wide windows (accumulators in tensor memory, 3 CTAs per SM); for
     // windows of <= 32 slices the register window is lighter and faster (C2, C5 measured)
-    if (!small_grid && !want_window && (p.max_active > 32 || want_tmem) && p.staged && !p.checked && p.windows_monotone &&
+    // (also for windows of 17-32 slices when the items pair up: the pitch-pair TMEM kernel beats the
+    // register window there, C2 1.70 -> 1.48 ms, scripts/ab/gpu_c2tmem.sh)
+    const bool pairs_help = p.n_items % 2 == 0 && p.max_active > 16 && !std::getenv("KATS_BP_PP");
+    if (!small_grid && !want_window && (p.max_active > 32 || pairs_help || want_tmem) && p.staged && !p.checked && p.windows_monotone &&
         p.warp_span > 0 &&
         2 * p.nq_s <= 256 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
