@@ -838,7 +838,11 @@ size_t tmem_smem_bytes(const BPParams &p)
 // that is shared and only the samples double; each view's slot holds both items' boxes, each item
 // has its own Wc TMEM columns per warp; the flush writes raw interior sums (end views and the
 // Δλ/2π scale follow in k_bp_ends_add_t).  2 CTAs per SM.
-template <bool POLY, int VP, bool ENDS_PRE, int PP = 1>
+// Q44: lanes of the warp's 8 x 4 columns in 4 x 2 quarter-warps / 4 x 4 half-warps instead of rows of 8:
+// LDS.128 serves a half-warp in one wavefront when its adjacent lane pairs share quads and all its quads
+// lie in one 128-byte segment, which compact half-warps meet more often (C3: K5 7.48 -> 7.20 ms; C4 no
+// change, so the pitch-pair kernel keeps rows; scripts/ab/gpu_qmap44.sh, scripts/micro/lds128_merge.cu)
+template <bool POLY, int VP, bool ENDS_PRE, int PP = 1, bool Q44 = false>
 // (the tensor map is the first parameter: it must sit 64-byte aligned in the parameter space)
 __global__ void __launch_bounds__(kWsThreads, PP == 1 ? 3 : 2) k_bp_tmem(const __grid_constant__ QMaps qm, BPParams p)
 {
@@ -856,8 +860,8 @@ __global__ void __launch_bounds__(kWsThreads, PP == 1 ? 3 : 2) k_bp_tmem(const _
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = warp == kConsumerWarps;
-    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (lane & 7);
-    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (lane >> 3);
+    const int ix = blockIdx.x * TX + (warp & 1) * 8 + (Q44 ? (lane & 3) + 4 * (lane >> 4) : lane & 7);
+    const int iy = blockIdx.y * TY + (warp >> 1) * 4 + (Q44 ? (lane >> 2) & 3 : lane >> 3);
     const int item = blockIdx.z * PP;
     const bool inside = !producer && ix < p.nx && iy < p.ny;
     const size_t plane = (size_t)p.nx * p.ny;
@@ -2075,6 +2079,13 @@ void launch_bp_ends(const BPParams &p, cudaStream_t s)
 template <bool POLY, int VP, bool ENDS_PRE, int PP = 1>
 void launch_tmem_kernel(const BPParams &q, dim3 grid, size_t sm, const QMaps &qmap, cudaStream_t s)
 {
+    if constexpr (PP == 1 && VP == 1) {
+        if (q.qmap44) {
+            smem_opt_in((const void *)k_bp_tmem<POLY, VP, ENDS_PRE, PP, true>, 200 * 1024);
+            k_bp_tmem<POLY, VP, ENDS_PRE, PP, true><<<grid, kWsThreads, sm, s>>>(qmap, q);
+            return;
+        }
+    }
     smem_opt_in((const void *)k_bp_tmem<POLY, VP, ENDS_PRE, PP>, 200 * 1024);
     k_bp_tmem<POLY, VP, ENDS_PRE, PP><<<grid, kWsThreads, sm, s>>>(qmap, q);
 }
@@ -2248,8 +2259,11 @@ static int launch_backproject_items(const BPParams &p, cudaStream_t s)
         2 * p.nq_s <= 256 &&
         p.fp_cols_column <= 256 && p.gq_views > 0 && p.pad_quads <= 2048) {
         // TMEM columns, allocation and ring depth for one view (vp 1) or two views (vp 2) per pass
+        int qmap44 = 1;                                           // single items, one view per pass: 4 x 4 half-warps
+        if (const char *qe = std::getenv("KATS_BP_QMAP")) qmap44 = std::atoi(qe) == 44;
         auto size_tmem = [&](int vp) {
             BPParams q = p;
+            q.qmap44 = qmap44;
             const int span = vp == 2 ? std::max(p.warp_span, p.warp_span2) : p.warp_span;
             if (vp == 2) q.pad_quads = p.pad_quads2;
             q.tmem_cols = 16;                                     // power of two >= span + 2 alias-free groups

@@ -105,6 +105,7 @@ struct BPParams {
     int crop;                 // window kernel: crop each view's box to the rows of the tile's open slices
     int ring_bytes;           // window kernel with cropped boxes: byte ring of variable-size view regions
     int ring_prefetch;        // byte ring: L2 prefetch of the boxes this many views ahead (0: none)
+    int qmap44;               // TMEM kernel: lanes in 4x2 quarter-warps / 4x4 half-warps (else 8x1 / 8x2)
     int adj_nqp;              // adjoint: quad-row pitch of a box column in shared memory (set by the launcher)
     bool adj_fixed_ok;        // adjoint: the int32 fixed-point box cannot overflow (<= 2^10 contributions per cell)
     int ends_pre;             // staged kernels: end views written ahead into vol by k_bp_ends (launcher)
