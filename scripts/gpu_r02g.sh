@@ -1,0 +1,20 @@
+# Round 2 final measurement call: GPU tests, smoke, bench lines C1-C5 + reference arm, ncu launch
+# list of the bench command, ncu --set full of K5 (pitch pairs) at C4 and of the adjoint K5^T.
+set -x
+cd $GRAFT_REPO_ROOT
+R=r02g
+make -s all > gpurun_out/build_$R.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$R.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$R.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$R.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$R.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
+for cfg in C1 C2 C3 C5; do
+  timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 > gpurun_out/bench_${R}_$cfg.json 2> gpurun_out/bench_${R}_$cfg.err
+done
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_$R.json 2> gpurun_out/bench_ref_$R.err
+timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-adjoint --no-datagen > gpurun_out/bench_short_$R.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-adjoint --no-datagen > gpurun_out/ncu_launches_$R.log 2>&1
+timeout 120 python scripts/prof_step.py --config C4 --pitches 8 --reps 1 > gpurun_out/prof_C4_$R.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_bp_tmem" -s 0 -c 1 \
+    -o gpurun_out/k5_full_$R -f python scripts/prof_step.py --config C4 --pitches 8 --reps 1 > gpurun_out/ncu_k5_$R.log 2>&1
+echo done
