@@ -188,3 +188,22 @@ def test_flat_with_hann_filter_matches_oracle():
     p = _plan(cfg)
     got = p.reconstruct(torch.from_numpy(sino).cuda(), cfg["scan_v0"], 0, cfg["n_pitches"]).cpu().numpy()
     _check(got, ref, contrast)
+
+
+def test_flat_adjoint_batch_dot_product():
+    """katsevich_adjoint_batch on flat slabs (TF2): <A x, y> = <x, A^T y> with the batch forward."""
+    import torch
+    from synth import configs
+    cfg = configs.get("TF2")
+    p = _plan(cfg)
+    v0, nv = p.pitch_views(0)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn((2, nv, cfg["n_rows"], cfg["n_cols"]), device="cuda", generator=g)
+    y = torch.randn((2, cfg["nz"], cfg["ny"], cfg["nx"]), device="cuda", generator=g)
+    ax = p.reconstruct_batch(x)
+    aty = p.adjoint_batch(y)
+    torch.cuda.synchronize()
+    lhs = float((ax.double() * y.double()).sum())
+    rhs = float((x.double() * aty.double()).sum())
+    scale = float(ax.double().norm() * y.double().norm())
+    assert abs(lhs - rhs) <= 1e-5 * scale, (lhs, rhs, scale)
