@@ -326,6 +326,37 @@ def run_ours(args):
     ms_step = ms / args.steps
     step_bp_kernel = plan.bp_kernel()          # the timed step's step-7 kernel (before the e2e / adjoint runs)
 
+    # ---- the same step replayed from a captured CUDA graph (every device entry point is capturable:
+    # no host synchronisation or allocation inside); single process only ----
+    graph = None
+    if world == 1 and not args.no_graph:
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+
+        def gstep():
+            if batch:
+                plan.reconstruct_batch(dev_in, out=out, stream=gs)
+            else:
+                plan.reconstruct(dev_in, v0, first_pitch, pitches, out=out, stream=gs)
+        gstep()                                              # warm on the capture stream
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg, stream=gs):
+            gstep()
+        with torch.cuda.stream(gs):                          # replays go to the current stream
+            for _ in range(args.warmup):
+                cg.replay()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(gs)
+            for _ in range(args.steps):
+                cg.replay()
+            g1.record(gs)
+        torch.cuda.synchronize()
+        graph = {"ms_per_step": g0.elapsed_time(g1) / args.steps,
+                 "what": "the timed step captured once into a CUDA graph (torch.cuda.graph) and replayed"}
+        del cg
+
     # ---- K5 in isolation: the same step with one backprojection launch over all of the rank's
     # pitches after all filtering (KATS_PIPELINE=0, the default), so no other kernel shares the GPU
     # with it (differs from the timed region only when KATS_PIPELINE=1 is set) ----
@@ -591,6 +622,10 @@ def run_ours(args):
         line["datagen"] = dg
     if var:
         line["variants"] = var
+    if graph:
+        graph["value"] = U_all / (graph["ms_per_step"] * 1e-3)
+        graph["unit"] = "updates/s"
+        line["cuda_graph"] = graph
     if adj:
         line["adjoint"] = {"metric": "voxel-view updates/s (transpose: volume -> sinogram)",
                            "value": U_all / (adj["ms_per_step"] * 1e-3), "unit": "updates/s",
@@ -744,6 +779,7 @@ def main():
     ap.add_argument("--no-adjoint", action="store_true", help="skip the adjoint (NEXT-1) measurement")
     ap.add_argument("--no-datagen", action="store_true", help="skip the data-generation (NEXT-3) measurement")
     ap.add_argument("--no-variants", action="store_true", help="skip the method-variant (NEXT-4) measurements")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -5,6 +5,7 @@ handles; all arithmetic runs in libkatsevich.so's sm_100a kernels.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import warnings
 
@@ -53,6 +54,8 @@ class Plan:
             raise KatsevichError(rc, "katsevich_plan_create")
         self.td_covered = None
         self._ws = None
+        self._ws_home = self._ws_last = self._ws_event = None
+        self._ws_graph = []                    # workspaces a captured CUDA graph uses
 
     # -- lifecycle ---------------------------------------------------------
     def _check(self, rc, what=""):
@@ -126,11 +129,42 @@ class Plan:
         return out
 
     # -- device entry points (torch tensors for memory) --------------------
-    def _workspace(self, nbytes: int):
+    @contextlib.contextmanager
+    def _ws_use(self, nbytes: int, stream):
+        """The plan's one cached workspace for a call on `stream`.  Calls may come on different
+        streams (the default stream, a capture stream): the call waits for the workspace's previous
+        use when that ran on another stream, and the workspace is marked in use on every stream it
+        ran on, so the caching allocator does not hand it out while a kernel still reads it.  Not
+        while a CUDA graph is being captured (torch.cuda.graph synchronises the device on entry):
+        a captured graph keeps using this workspace, so it is then held for the plan's lifetime
+        (a later, larger workspace does not free it), and eager calls on the plan must not run
+        concurrently with the graph's replays."""
         import torch
+        dev = torch.device("cuda", self.device)
+        if stream is None:
+            st = torch.cuda.current_stream(dev)
+        elif isinstance(stream, int):
+            st = torch.cuda.ExternalStream(stream, device=dev)
+        else:
+            st = stream
+        capturing = torch.cuda.is_current_stream_capturing()
         if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=f"cuda:{self.device}")
-        return self._ws
+            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+            self._ws_home = torch.cuda.current_stream(dev)
+            self._ws_last = None
+        if not capturing:
+            if self._ws_last is not None and self._ws_last != st:
+                st.wait_event(self._ws_event)
+            if st != self._ws_home:
+                self._ws.record_stream(st)
+        if capturing and not any(w is self._ws for w in self._ws_graph):
+            self._ws_graph.append(self._ws)
+        yield self._ws
+        if not capturing:
+            if self._ws_event is None:
+                self._ws_event = torch.cuda.Event()
+            self._ws_event.record(st)
+            self._ws_last = st
 
     def _vol_shape(self, n):
         g = self.geometry
@@ -144,10 +178,10 @@ class Plan:
         if out is None:
             out = torch.empty(self._vol_shape(n_pitches), dtype=torch.float32, device=sino.device)
         nb = self.workspace_bytes(n_pitches)
-        ws = self._workspace(nb)
-        self._check(lib().katsevich_reconstruct(self._h, _ptr(sino), sino_first_view, sino.shape[0],
-                                                first_pitch, n_pitches, _ptr(out), _ptr(ws), ws.numel(),
-                                                _stream_handle(stream)))
+        with self._ws_use(nb, stream) as ws:
+            self._check(lib().katsevich_reconstruct(self._h, _ptr(sino), sino_first_view, sino.shape[0],
+                                                    first_pitch, n_pitches, _ptr(out), _ptr(ws), ws.numel(),
+                                                    _stream_handle(stream)))
         return out
 
     def reconstruct_grouped(self, sino, sino_first_view: int, first_pitch: int, n_pitches: int, groups: int,
@@ -159,16 +193,16 @@ class Plan:
         assert sino.is_cuda and sino.dtype == torch.float32 and sino.is_contiguous()
         if out is None:
             out = torch.empty(self._vol_shape(n_pitches), dtype=torch.float32, device=sino.device)
-        ws = self._workspace(self.workspace_bytes(n_pitches))
         evs = None
         if group_events is not None:
             assert len(group_events) == groups
             assert all(e is None or e.cuda_event for e in group_events), "record each event once to create it"
             evs = (ctypes.c_void_p * groups)(*[ctypes.c_void_p(e.cuda_event) if e is not None else None
                                                for e in group_events])
-        self._check(lib().katsevich_reconstruct_grouped(self._h, _ptr(sino), sino_first_view, sino.shape[0],
-                                                        first_pitch, n_pitches, _ptr(out), _ptr(ws), ws.numel(),
-                                                        _stream_handle(stream), groups, evs))
+        with self._ws_use(self.workspace_bytes(n_pitches), stream) as ws:
+            self._check(lib().katsevich_reconstruct_grouped(self._h, _ptr(sino), sino_first_view, sino.shape[0],
+                                                            first_pitch, n_pitches, _ptr(out), _ptr(ws), ws.numel(),
+                                                            _stream_handle(stream), groups, evs))
         return out
 
     def reconstruct_batch(self, slabs, out=None, stream=None):
@@ -180,9 +214,9 @@ class Plan:
         if out is None:
             g = self.geometry
             out = torch.empty((B, g.nz_per_pitch, g.ny, g.nx), dtype=torch.float32, device=slabs.device)
-        ws = self._workspace(self.workspace_bytes(B))
-        self._check(lib().katsevich_reconstruct_batch(self._h, _ptr(slabs), B, _ptr(out), _ptr(ws), ws.numel(),
-                                                      _stream_handle(stream)))
+        with self._ws_use(self.workspace_bytes(B), stream) as ws:
+            self._check(lib().katsevich_reconstruct_batch(self._h, _ptr(slabs), B, _ptr(out), _ptr(ws), ws.numel(),
+                                                          _stream_handle(stream)))
         return out
 
     def reconstruct_batch_host(self, slabs_host, out_host=None, stream=None):
@@ -198,9 +232,9 @@ class Plan:
             out_host = torch.empty((B, g.nz_per_pitch, g.ny, g.nx), dtype=torch.float32)
         b = ctypes.c_size_t()
         self._check(lib().katsevich_workspace_bytes_batch_host(self._h, B, ctypes.byref(b)))
-        ws = self._workspace(b.value)
-        self._check(lib().katsevich_reconstruct_batch_host(self._h, _ptr(slabs_host), B, _ptr(out_host), _ptr(ws),
-                                                           ws.numel(), _stream_handle(stream)))
+        with self._ws_use(b.value, stream) as ws:
+            self._check(lib().katsevich_reconstruct_batch_host(self._h, _ptr(slabs_host), B, _ptr(out_host), _ptr(ws),
+                                                               ws.numel(), _stream_handle(stream)))
         return out_host
 
     def reconstruct_host(self, sino_host, sino_first_view: int, first_pitch: int = 0, n_pitches: int = 1,
@@ -211,10 +245,10 @@ class Plan:
             sino_host = torch.from_numpy(np.ascontiguousarray(sino_host, dtype=np.float32))
         if out_host is None:
             out_host = torch.empty(self._vol_shape(n_pitches), dtype=torch.float32)
-        ws = self._workspace(self.workspace_bytes(n_pitches, host=True))
-        self._check(lib().katsevich_reconstruct_host(self._h, _ptr(sino_host), sino_first_view, sino_host.shape[0],
-                                                     first_pitch, n_pitches, _ptr(out_host), _ptr(ws), ws.numel(),
-                                                     _stream_handle(stream)))
+        with self._ws_use(self.workspace_bytes(n_pitches, host=True), stream) as ws:
+            self._check(lib().katsevich_reconstruct_host(self._h, _ptr(sino_host), sino_first_view, sino_host.shape[0],
+                                                         first_pitch, n_pitches, _ptr(out_host), _ptr(ws), ws.numel(),
+                                                         _stream_handle(stream)))
         return out_host
 
     def adjoint_workspace_bytes(self, n_pitches: int = 1) -> int:
@@ -232,9 +266,9 @@ class Plan:
         g = self.geometry
         if out is None:
             out = torch.empty((n_views, g.n_rows, g.n_cols), dtype=torch.float32, device=vol.device)
-        ws = self._workspace(self.adjoint_workspace_bytes(n_pitches))
-        self._check(lib().katsevich_adjoint(self._h, _ptr(vol), first_pitch, n_pitches, _ptr(out), sino_first_view,
-                                            n_views, _ptr(ws), ws.numel(), _stream_handle(stream)))
+        with self._ws_use(self.adjoint_workspace_bytes(n_pitches), stream) as ws:
+            self._check(lib().katsevich_adjoint(self._h, _ptr(vol), first_pitch, n_pitches, _ptr(out), sino_first_view,
+                                                n_views, _ptr(ws), ws.numel(), _stream_handle(stream)))
         return out
 
     # -- data generation (NEXT-3) -------------------------------------------
@@ -289,9 +323,9 @@ class Plan:
             out = torch.empty((B, nv, g.n_rows, g.n_cols), dtype=torch.float32, device=vols.device)
         b = ctypes.c_size_t()
         self._check(lib().katsevich_adjoint_batch_workspace_bytes(self._h, B, ctypes.byref(b)))
-        ws = self._workspace(b.value)
-        self._check(lib().katsevich_adjoint_batch(self._h, _ptr(vols), B, _ptr(out), _ptr(ws), ws.numel(),
-                                                  _stream_handle(stream)))
+        with self._ws_use(b.value, stream) as ws:
+            self._check(lib().katsevich_adjoint_batch(self._h, _ptr(vols), B, _ptr(out), _ptr(ws), ws.numel(),
+                                                      _stream_handle(stream)))
         return out
 
     def filter(self, sino, sino_first_view: int, out_first_view: int, n_out: int, stages=("gF",), stream=None):
