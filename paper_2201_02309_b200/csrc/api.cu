@@ -919,7 +919,9 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     // groups of slabs (KATS_BATCH_GROUPS, default 1): group g+1 is filtered on the highest-priority
     // stream while group g backprojects on a low-priority one, so the filter fills the SMs the
     // backprojection leaves idle (group sizes stay even for the window kernel's slab pairs)
-    int ng = 1;
+    // (default: two groups for batches of >= 16 slabs in groups of a multiple of 4, the window
+    // kernel's four slabs per CTA — C5 3.58 -> 3.49 ms, scripts/gpu_r02h.sh; four groups: 3.94 ms)
+    int ng = B >= 16 && B % 8 == 0 ? 2 : 1;
     if (const char *e = std::getenv("KATS_BATCH_GROUPS")) ng = std::max(1, std::atoi(e));
     while (ng > 1 && (B % ng != 0 || ((B / ng) % 2 != 0 && B % 2 == 0))) --ng;
     if (ng == 1) {
@@ -944,13 +946,21 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     rc = ensure_events(p, 2 * (size_t)ng + 1);
     if (rc) return rc;
     const int gs = B / ng;
+    // each group's views in device chunks (KATS_BATCH_GCHUNK=1: in the batch chunking, two equal
+    // chunks on the two filter streams, no larger than the chunk the workspace was sized for —
+    // measured slower, C5 3.574 vs 3.497 ms, scripts/gpu_r02i.sh)
+    int64_t gchunk = 0;
+    if (const char *e = std::getenv("KATS_BATCH_GCHUNK"))
+        if (e[0] == '1')
+            gchunk = std::min(batch_chunk_views(p, gs), std::max<int64_t>(filter_chunk_views(p, device_chunk_mul()),
+                                                                          batch_chunk_views(p, B)));
     cudaStream_t fs = (cudaStream_t)p->filter_stream;
     cudaEvent_t e_fork = (cudaEvent_t)p->sync_events[2 * ng];
     KCHECK(p, cudaEventRecord(e_fork, s));
     KCHECK(p, cudaStreamWaitEvent(fs, e_fork, 0));
     for (int g = 0; g < ng; ++g) {
         rc = run_filter(p, slabs + ((size_t)g * gs * nslab + halo_lo(p)) * rs, nbp * gs, gq + (size_t)g * gs * nbp * qs,
-                        scratch, nullptr, nullptr, nullptr, fs, false, nbp, true, device_chunk_mul());
+                        scratch, nullptr, nullptr, nullptr, fs, false, nbp, true, device_chunk_mul(), gchunk);
         if (rc) return rc;
         cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[ng + g];
         KCHECK(p, cudaEventRecord(e_filt, fs));
