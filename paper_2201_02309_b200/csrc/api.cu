@@ -13,6 +13,7 @@
 #include <new>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -921,9 +922,29 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     // backprojection leaves idle (group sizes stay even for the window kernel's slab pairs)
     // (default: two groups for batches of >= 16 slabs in groups of a multiple of 4, the window
     // kernel's four slabs per CTA — C5 3.58 -> 3.49 ms, scripts/gpu_r02h.sh; four groups: 3.94 ms)
-    int ng = B >= 16 && B % 8 == 0 ? 2 : 1;
-    if (const char *e = std::getenv("KATS_BATCH_GROUPS")) ng = std::max(1, std::atoi(e));
-    while (ng > 1 && (B % ng != 0 || ((B / ng) % 2 != 0 && B % 2 == 0))) --ng;
+    std::vector<int> gsz;                                       // slabs per group
+    {
+        int ng = B >= 16 && B % 8 == 0 ? 2 : 1;
+        if (const char *e = std::getenv("KATS_BATCH_GROUPS")) ng = std::max(1, std::atoi(e));
+        while (ng > 1 && (B % ng != 0 || ((B / ng) % 2 != 0 && B % 2 == 0))) --ng;
+        gsz.assign(ng, B / ng);
+        // KATS_BATCH_SPLIT=a,b,...: explicit group sizes (A/B; used when they sum to B)
+        if (const char *e = std::getenv("KATS_BATCH_SPLIT")) {
+            std::vector<int> v;
+            for (const char *c = e; *c;) {
+                char *end;
+                const long n = std::strtol(c, &end, 10);
+                if (end == c || n < 1) { v.clear(); break; }
+                v.push_back((int)n);
+                c = *end == ',' ? end + 1 : end;
+                if (*end && *end != ',') { v.clear(); break; }
+            }
+            int sum = 0;
+            for (int n : v) sum += n;
+            if (sum == B && !v.empty()) gsz = v;
+        }
+    }
+    const int ng = (int)gsz.size();
     if (ng == 1) {
         // every slab's filtered views in one chunked pass (chunks run across slab ends; each slab
         // keeps its own +-1 halo)
@@ -945,21 +966,21 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     if (rc) return rc;
     rc = ensure_events(p, 2 * (size_t)ng + 1);
     if (rc) return rc;
-    const int gs = B / ng;
-    // each group's views in device chunks (KATS_BATCH_GCHUNK=1: in the batch chunking, two equal
-    // chunks on the two filter streams, no larger than the chunk the workspace was sized for —
-    // measured slower, C5 3.574 vs 3.497 ms, scripts/gpu_r02i.sh)
-    int64_t gchunk = 0;
-    if (const char *e = std::getenv("KATS_BATCH_GCHUNK"))
-        if (e[0] == '1')
-            gchunk = std::min(batch_chunk_views(p, gs), std::max<int64_t>(filter_chunk_views(p, device_chunk_mul()),
-                                                                          batch_chunk_views(p, B)));
     cudaStream_t fs = (cudaStream_t)p->filter_stream;
     cudaEvent_t e_fork = (cudaEvent_t)p->sync_events[2 * ng];
     KCHECK(p, cudaEventRecord(e_fork, s));
     KCHECK(p, cudaStreamWaitEvent(fs, e_fork, 0));
-    for (int g = 0; g < ng; ++g) {
-        rc = run_filter(p, slabs + ((size_t)g * gs * nslab + halo_lo(p)) * rs, nbp * gs, gq + (size_t)g * gs * nbp * qs,
+    for (int g = 0, b0 = 0; g < ng; b0 += gsz[g], ++g) {
+        const int gs = gsz[g];
+        // each group's views in device chunks (KATS_BATCH_GCHUNK=1: in the batch chunking, two equal
+        // chunks on the two filter streams, no larger than the chunk the workspace was sized for —
+        // measured slower, C5 3.574 vs 3.497 ms, scripts/gpu_r02i.sh)
+        int64_t gchunk = 0;
+        if (const char *e = std::getenv("KATS_BATCH_GCHUNK"))
+            if (e[0] == '1')
+                gchunk = std::min(batch_chunk_views(p, gs), std::max<int64_t>(filter_chunk_views(p, device_chunk_mul()),
+                                                                              batch_chunk_views(p, B)));
+        rc = run_filter(p, slabs + ((size_t)b0 * nslab + halo_lo(p)) * rs, nbp * gs, gq + (size_t)b0 * nbp * qs,
                         scratch, nullptr, nullptr, nullptr, fs, false, nbp, true, device_chunk_mul(), gchunk);
         if (rc) return rc;
         cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[ng + g];
@@ -969,10 +990,10 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
         BPParams bp = bp_params(p);
         bp.gq = gq;
         bp.gq_views = nbp * B;
-        bp.off0 = -t.bp_lo + (int64_t)g * gs * nbp;
+        bp.off0 = -t.bp_lo + (int64_t)b0 * nbp;
         bp.item_views = nbp;
         bp.n_items = gs;
-        bp.vol = vols + (size_t)g * gs * p->g.nx * p->g.ny * p->g.nz_per_pitch;
+        bp.vol = vols + (size_t)b0 * p->g.nx * p->g.ny * p->g.nz_per_pitch;
         { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(bp, bs); }
         KCHECK(p, cudaGetLastError());
         KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[g], bs));
