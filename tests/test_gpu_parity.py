@@ -206,14 +206,18 @@ def test_coverage_error_names_pitches():
     assert ei.value.code == -4 and "reconstructible" in str(ei.value)
 
 
-@pytest.mark.parametrize("n_slabs,groups", [(4, "2"), (8, "4"), (6, "3")])
-def test_batch_groups_match_oracle(n_slabs, groups, monkeypatch):
+@pytest.mark.parametrize("n_slabs,var,val", [(4, "KATS_BATCH_GROUPS", "2"), (8, "KATS_BATCH_GROUPS", "4"),
+                                              (6, "KATS_BATCH_GROUPS", "3"), (7, "KATS_BATCH_SPLIT", "3,4"),
+                                              (5, "KATS_BATCH_SPLIT", "1,2,2")])
+def test_batch_groups_match_oracle(n_slabs, var, val, monkeypatch):
     """reconstruct_batch in slab groups (KATS_BATCH_GROUPS: group g+1 filtered while group g
-    backprojects) against the oracle per slab."""
+    backprojects; KATS_BATCH_SPLIT: uneven groups) against the oracle per slab."""
     import torch
     from oracle import oracle
     from synth import configs, synth
-    monkeypatch.setenv("KATS_BATCH_GROUPS", groups)
+    monkeypatch.delenv("KATS_BATCH_GROUPS", raising=False)
+    monkeypatch.delenv("KATS_BATCH_SPLIT", raising=False)
+    monkeypatch.setenv(var, val)
     cfg = configs.get("T2")
     p = _plan(cfg)
     v0, nv = p.pitch_views(0)
