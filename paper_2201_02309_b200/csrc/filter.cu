@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(K12_THREADS) k_deriv_fwd_rebin_tile(FilterPara
 // division.  Same fp32 arithmetic as g2_at.
 constexpr int K12R_WARPS = 8, K12R_MAXR = 8;   // rows per warp: nr <= 64
 
-__global__ void __launch_bounds__(32 * K12R_WARPS) k_deriv_fwd_rebin_rows(FilterParams p, int nvb)
+template <int MINB>
+__global__ void __launch_bounds__(32 * K12R_WARPS, MINB) k_deriv_fwd_rebin_rows(FilterParams p, int nvb)
 {
     extern __shared__ float k12s[];
     const int nr = p.nr, nc = p.nc, npsi = p.npsi, rs = nr * nc;
@@ -1428,10 +1429,22 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
         const int nb = (p.nc + 31) / 32;
         int nvb = 16;
         while (nvb > 1 && (int64_t)nb * ((p.n_views + nvb - 1) / nvb) < 4 * device_sms()) nvb /= 2;
+        if (const char *e = std::getenv("KATS_K12R_NVB")) nvb = std::max(1, std::atoi(e));     // A/B
         const size_t smem = sizeof(float) * (2 * (size_t)p.npsi * 32 + 2 * (size_t)p.nr * 32);
         if (smem <= 200 * 1024) {
-            smem_opt_in((const void *)k_deriv_fwd_rebin_rows, smem);
-            k_deriv_fwd_rebin_rows<<<dim3(nb, (p.n_views + nvb - 1) / nvb), 32 * K12R_WARPS, smem, s>>>(p, nvb);
+            // three CTAs per SM (80 registers, no spills): C3 K12 0.402 -> 0.332 ms (0.43 -> 0.52 of
+            // HBM), C4 0.665 -> 0.564 ms; four (64 registers, a small spill) is slower: C3 0.482,
+            // C4 0.789 ms (scripts/gpu_r02n.sh; KATS_K12R_MINB=2|3|4)
+            int minb = 3;
+            if (const char *e = std::getenv("KATS_K12R_MINB")) minb = std::atoi(e);
+            const dim3 g(nb, (p.n_views + nvb - 1) / nvb);
+            auto go = [&](auto kern) {
+                smem_opt_in((const void *)kern, smem);
+                kern<<<g, 32 * K12R_WARPS, smem, s>>>(p, nvb);
+            };
+            if (minb == 4) go(k_deriv_fwd_rebin_rows<4>);
+            else if (minb == 3) go(k_deriv_fwd_rebin_rows<3>);
+            else go(k_deriv_fwd_rebin_rows<2>);
             return;
         }
     }
