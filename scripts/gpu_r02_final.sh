@@ -2,11 +2,11 @@
 # bench command timed, and the ncu launch list of the C4 and C5 bench commands.
 set -x
 cd $GRAFT_REPO_ROOT
-R=r02z
+R=r02z2
 make -s all > gpurun_out/build_$R.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$R.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$R.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$R.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$R.log
-/usr/bin/time -v timeout 900 python bench.py > gpurun_out/bench_default_$R.json 2> gpurun_out/bench_default_$R.err
+timeout 900 python bench.py > gpurun_out/bench_default_$R.json 2> gpurun_out/bench_default_$R.err
 for cfg in C4 C1 C2 C3 C5; do
   timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 > gpurun_out/bench_${R}_$cfg.json 2> gpurun_out/bench_${R}_$cfg.err
 done
