@@ -271,7 +271,11 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
     FilterParams f = filter_params(p);
     // running concurrently with the TMEM backprojection: K3 uses the fp32 direct convolution
     // (launch_hilbert); results then agree with the device path to fp32 rounding, not bitwise
-    f.hilbert_overlap = overlapped ? 1 : 0;
+    // the host path's filter beside the pitch-pair backprojection (2 CTAs per SM) keeps the tensor-core
+    // K3: C4 e2e 51.91 -> 51.23 ms, C2 3.07 -> 2.75 ms (scripts/gpu_r02p.sh); KATS_HOST_TC=0: the fp32
+    // direct K3 there (the round-1 choice next to three one-pitch TMEM CTAs per SM)
+    static const bool host_tc = [] { const char *e = std::getenv("KATS_HOST_TC"); return !(e && e[0] == '0'); }();
+    f.hilbert_overlap = overlapped && !host_tc ? 1 : 0;
     f.hp = g3_half_pitch(p->g.n_cols);
     f.k3_in_split = hilbert_split_input(f) ? 1 : 0;         // K12 writes the lines the chosen K3 reads
     const size_t rs = (size_t)p->g.n_rows * p->g.n_cols;
