@@ -272,7 +272,7 @@ int run_filter(katsevich_plan *p, const float *raw_first_out, int64_t n_out, flo
     // running concurrently with the TMEM backprojection: K3 uses the fp32 direct convolution
     // (launch_hilbert); results then agree with the device path to fp32 rounding, not bitwise
     // the host path's filter beside the pitch-pair backprojection (2 CTAs per SM) keeps the tensor-core
-    // K3: C4 e2e 51.91 -> 51.23 ms, C2 3.07 -> 2.75 ms (scripts/gpu_r02p.sh); KATS_HOST_TC=0: the fp32
+    // K3: C4 e2e 51.91 -> 51.23 ms, C2 3.07 -> 2.75 ms (scripts/ab/gpu_r02p.sh); KATS_HOST_TC=0: the fp32
     // direct K3 there (the round-1 choice next to three one-pitch TMEM CTAs per SM)
     static const bool host_tc = [] { const char *e = std::getenv("KATS_HOST_TC"); return !(e && e[0] == '0'); }();
     f.hilbert_overlap = overlapped && !host_tc ? 1 : 0;
@@ -925,7 +925,7 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     // stream while group g backprojects on a low-priority one, so the filter fills the SMs the
     // backprojection leaves idle (group sizes stay even for the window kernel's slab pairs)
     // (default: two groups for batches of >= 16 slabs in groups of a multiple of 4, the window
-    // kernel's four slabs per CTA — C5 3.58 -> 3.49 ms, scripts/gpu_r02h.sh; four groups: 3.94 ms)
+    // kernel's four slabs per CTA — C5 3.58 -> 3.49 ms, scripts/ab/gpu_r02h.sh; four groups: 3.94 ms)
     std::vector<int> gsz;                                       // slabs per group
     {
         int ng = B >= 16 && B % 8 == 0 ? 2 : 1;
@@ -978,7 +978,7 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
         const int gs = gsz[g];
         // each group's views in device chunks (KATS_BATCH_GCHUNK=1: in the batch chunking, two equal
         // chunks on the two filter streams, no larger than the chunk the workspace was sized for —
-        // measured slower, C5 3.574 vs 3.497 ms, scripts/gpu_r02i.sh)
+        // measured slower, C5 3.574 vs 3.497 ms, scripts/ab/gpu_r02i.sh)
         int64_t gchunk = 0;
         if (const char *e = std::getenv("KATS_BATCH_GCHUNK"))
             if (e[0] == '1')

@@ -1434,7 +1434,7 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
         if (smem <= 200 * 1024) {
             // three CTAs per SM (80 registers, no spills): C3 K12 0.402 -> 0.332 ms (0.43 -> 0.52 of
             // HBM), C4 0.665 -> 0.564 ms; four (64 registers, a small spill) is slower: C3 0.482,
-            // C4 0.789 ms (scripts/gpu_r02n.sh; KATS_K12R_MINB=2|3|4)
+            // C4 0.789 ms (scripts/ab/gpu_r02n.sh; KATS_K12R_MINB=2|3|4)
             int minb = 3;
             if (const char *e = std::getenv("KATS_K12R_MINB")) minb = std::atoi(e);
             const dim3 g(nb, (p.n_views + nvb - 1) / nvb);
