@@ -682,7 +682,7 @@ int katsevich_reconstruct_grouped(katsevich_plan *p, const float *sino, int64_t 
     float4 *gq = (float4 *)workspace;
     float *scratch = (float *)((char *)workspace + align_up(sizeof(float4) * quad_view_elems(p) * (size_t)std::max<int64_t>(nu, (t.bp_hi - t.bp_lo + 1) * n_pitches)));
     const char *pe = std::getenv("KATS_PIPELINE");
-    if (n_pitches == 1 || n_groups > 1 || group_done || !(pe && pe[0] == '1')) {
+    if (n_pitches == 1 || n_groups > 1 || group_done || !(pe && (pe[0] == '1' || pe[0] == '2'))) {
         // filter every needed view once, then one backprojection launch per pitch group (default: one
         // group); group_done[i] marks the end of group i's launch on the caller's stream
         rc = run_filter(p, sino + (u0 - s0) * rs, nu, gq, scratch, nullptr, nullptr, nullptr, s, false, 0, true, dm);
@@ -718,8 +718,11 @@ int katsevich_reconstruct_grouped(katsevich_plan *p, const float *sino, int64_t 
     KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[2 * n_pitches], s));     // fork
     KCHECK(p, cudaStreamWaitEvent(fs, (cudaEvent_t)p->sync_events[2 * n_pitches], 0));
     int64_t c_next = 0;
-    for (int k = 0; k < n_pitches; ++k) {
-        const int64_t filt_end = (int64_t)(first_pitch + k) * vt + t.bp_hi + 1;   // exclusive
+    // KATS_PIPELINE=2: pitch pairs (the pitch-pair kernel) while two or more pitches remain
+    const int G = pe[0] == '2' ? 2 : 1;
+    for (int k = 0, grp = 1; k < n_pitches; k += grp) {
+        grp = std::min(G, n_pitches - k);
+        const int64_t filt_end = (int64_t)(first_pitch + k + grp - 1) * vt + t.bp_hi + 1;   // exclusive
         if (c_next < nchunks && u0 + c_next * kFilterChunk < filt_end) {
             int64_t c_end = c_next;
             while (c_end < nchunks && u0 + c_end * kFilterChunk < filt_end) ++c_end;
@@ -730,21 +733,21 @@ int katsevich_reconstruct_grouped(katsevich_plan *p, const float *sino, int64_t 
         }
         cudaEvent_t e_filt = (cudaEvent_t)p->sync_events[n_pitches + k];
         KCHECK(p, cudaEventRecord(e_filt, fs));
-        cudaStream_t bs = (cudaStream_t)p->bp_streams[k & 1];
+        cudaStream_t bs = (cudaStream_t)p->bp_streams[(k / G) & 1];
         KCHECK(p, cudaStreamWaitEvent(bs, e_filt, 0));
         BPParams b = bp_params(p);
         b.gq = gq;
         b.gq_views = nu;
         b.off0 = (int64_t)(first_pitch + k) * vt - u0;
         b.item_views = vt;
-        b.n_items = 1;
+        b.n_items = grp;
         b.vol = vol + (size_t)k * vpitch;
         { LaunchScope ls(p, ST_K5, bs); p->last_bp_kernel = launch_backproject(b, bs); }
         KCHECK(p, cudaGetLastError());
         KCHECK(p, cudaEventRecord((cudaEvent_t)p->sync_events[k], bs));
     }
-    for (int k = std::max(0, n_pitches - 2); k < n_pitches; ++k)       // join
-        KCHECK(p, cudaStreamWaitEvent(s, (cudaEvent_t)p->sync_events[k], 0));
+    for (int k = 0; k < n_pitches; ++k)                                 // join (each bp stream is in order)
+        if (k % G == 0 && k + 2 * G >= n_pitches) KCHECK(p, cudaStreamWaitEvent(s, (cudaEvent_t)p->sync_events[k], 0));
     return KATS_OK;
 }
 

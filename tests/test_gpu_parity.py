@@ -300,13 +300,13 @@ def test_every_bp_kernel_variant_matches_oracle(variant, vp, kernel, monkeypatch
     _check(vol.cpu().numpy(), ref, contrast)
 
 
-@pytest.mark.parametrize("name", ["T2", "T3"])
-def test_pipelined_reconstruct_matches_oracle(name, monkeypatch):
-    """KATS_PIPELINE=1: per-pitch backprojections on two streams behind a
-    high-priority filter stream (forked from and joined to the caller's stream)
-    give the oracle's volume too."""
+@pytest.mark.parametrize("name,mode", [("T2", "1"), ("T3", "1"), ("T2", "2"), ("T3", "2")])
+def test_pipelined_reconstruct_matches_oracle(name, mode, monkeypatch):
+    """KATS_PIPELINE=1 (per pitch) / 2 (pitch pairs, the odd last pitch alone): backprojections on
+    two streams behind a high-priority filter stream (forked from and joined to the caller's
+    stream) give the oracle's volume too."""
     import torch
-    monkeypatch.setenv("KATS_PIPELINE", "1")
+    monkeypatch.setenv("KATS_PIPELINE", mode)
     cfg, sino, ref, contrast = _case(name)
     p = _plan(cfg)
     s = torch.cuda.Stream()
