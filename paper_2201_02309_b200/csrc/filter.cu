@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(32 * K12R_WARPS, MINB) k_deriv_fwd_rebin_rows(
 // staged once per CTA.  HALF (NEXT-4, reading A25): Noo's 2x2x2 half-sample derivative
 // on the half-shifted grid (the plan's effective geometry: nr, nc are the shifted grid's sizes,
 // raw views have nr + 1 rows and nc + 1 columns; effective view g reads raw views raw(g), raw(g)+1).
-template <bool HALF>
+template <bool HALF, int UR = 4>
 __global__ void __launch_bounds__(256) k_deriv_fwd_rebin_wv(FilterParams p, int vpw)
 {
     extern __shared__ float k12s[];
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(256) k_deriv_fwd_rebin_wv(FilterParams p, int 
         } else {
             const int lp = min(lc + 1, nc - 1), lm = max(lc - 1, 0);
             const float sa = (lp - lm == 2) ? p.inv_2dalpha : p.inv_dalpha, sq = p.inv_2dlam;
-#pragma unroll 4
+#pragma unroll UR
             for (int m = 0; m < nr; ++m) {
                 const float *r = gv + (size_t)m * nc;
                 const float dq = (__ldg(r + lc + rs) - __ldg(r + lc - rs)) * sq;
@@ -1413,13 +1413,22 @@ void launch_deriv_fwd_rebin(const FilterParams &p, cudaStream_t s)
         const int nb = (p.nc + 31) / 32;
         int vpw = 8;
         while (vpw > 1 && (int64_t)nb * ((p.n_views + 8 * vpw - 1) / (8 * vpw)) < 4 * device_sms()) vpw /= 2;
+        if (const char *e = std::getenv("KATS_K12WV_VPW")) vpw = std::max(1, std::atoi(e));     // A/B
         const dim3 grid(nb, (p.n_views + 8 * vpw - 1) / (8 * vpw));
         if (p.half) {
             smem_opt_in((const void *)k_deriv_fwd_rebin_wv<true>, wv_smem);
             k_deriv_fwd_rebin_wv<true><<<grid, 256, wv_smem, s>>>(p, vpw);
         } else {
-            smem_opt_in((const void *)k_deriv_fwd_rebin_wv<false>, wv_smem);
-            k_deriv_fwd_rebin_wv<false><<<grid, 256, wv_smem, s>>>(p, vpw);
+            // KATS_K12WV_UR=8|16 (A/B): deeper unroll of the g2 row loop (more raw loads in flight)
+            const char *ue = std::getenv("KATS_K12WV_UR");
+            const int ur = ue ? std::atoi(ue) : 4;
+            auto go = [&](auto kern) {
+                smem_opt_in((const void *)kern, wv_smem);
+                kern<<<grid, 256, wv_smem, s>>>(p, vpw);
+            };
+            if (ur == 16) go(k_deriv_fwd_rebin_wv<false, 16>);
+            else if (ur == 8) go(k_deriv_fwd_rebin_wv<false, 8>);
+            else go(k_deriv_fwd_rebin_wv<false, 4>);
         }
         return;
     }
