@@ -754,7 +754,9 @@ def run_reference(args):
     value = upd / t
     line = {"impl": "reference", "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "vs_baseline": None, "dtype": "f64",
+            # (our arm's rule for the same config: batches and --scaling weak are weak, else strong)
+            "scaling": "weak" if (args.scaling == "weak" or cfg.get("batch")) else "strong",
             "data": "synthetic (seeded random arrays of the workload's shapes)",
             "config": {"workload": f"{cfg['name']}: {cfg['desc']}",
                        "step": "one whole slice of pitch 0 (all its voxels + the filtering of the views they need)"},

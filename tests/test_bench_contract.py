@@ -31,6 +31,21 @@ def test_reference_arm_line():
     assert d["value"] > 0 and d["higher_is_better"] is True
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["scaling"] == "strong" and d["config"]["workload"].startswith("C1")
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N = 2 through torch.distributed.run (as the driver launches it): rank 0 alone runs the oracle
+    and prints the one JSON line; the other rank exits 0 without output."""
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "bench.py"),
+                          "--impl", "reference", "--config", "C1", "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
 
 
 @pytest.mark.gpu
