@@ -1600,6 +1600,12 @@ int launch_hilbert(const FilterParams &p, cudaStream_t s)
             if (const char *e = std::getenv("KATS_WS_STAGES"))
                 if (std::atoi(e) == 3) { nst = 3; nraw = wsm_of(3, 4) <= 225 * 1024 ? 4 : 3; }
             if (wsm_of(nst, nraw) > 225 * 1024) { nst = 2; nraw = 4; }
+            // KATS_WS_RAW=6|8 (A/B): more raw TMA chunks in flight with two A stages, where they fit
+            if (const char *e = std::getenv("KATS_WS_RAW")) {
+                const int r = std::atoi(e);
+                if (nst == 2 && (r == 6 || r == 8) && wsm_of(2, r) <= 225 * 1024) nraw = r;
+                else if (nst == 2 && r == 8 && wsm_of(2, 6) <= 225 * 1024) nraw = 6;
+            }
             const size_t wsm = wsm_of(nst, nraw);
             CUtensorMap amap;                                         // the K3 input: [n_lines][2 hp] fp32
             if (!make_tensor_map_2d_f32(&amap, p.g3, (uint64_t)2 * p.hp, (uint64_t)n_lines, (uint64_t)8 * p.hp, 32, TC_M)) {
@@ -1617,6 +1623,8 @@ int launch_hilbert(const FilterParams &p, cudaStream_t s)
             };
             if (nst == 3 && nraw == 4) go(k_hilbert_ws<3, 4>);
             else if (nst == 3) go(k_hilbert_ws<3, 3>);
+            else if (nraw == 8) go(k_hilbert_ws<2, 8>);
+            else if (nraw == 6) go(k_hilbert_ws<2, 6>);
             else go(k_hilbert_ws<2, 4>);
             return 0;
         }
