@@ -194,8 +194,10 @@ def ncu_traffic(config_name):
     try:
         with open(path) as f:
             d = json.load(f)
-        if d.get("config") == config_name:
+        if d.get("config") == config_name:                     # (single-config form)
             return d.get("dram_bytes_per_launch")
+        if isinstance(d.get(config_name), dict):               # keyed by config
+            return d[config_name].get("dram_bytes_per_launch")
     except Exception:
         pass
     return None
@@ -603,10 +605,10 @@ def run_ours(args):
                      "k5_ms_per_launch": k5_ms_launch, "k5_updates_per_s": U_rank / (k5_busy * 1e-3),
                      "peak_source": smem_src + "; DESIGN.md §5",
                      "secondary_hbm": None if not ncu_traffic(cfg["name"]) else {
-                         "achieved": ncu_traffic(cfg["name"]) / (iso["k5_ms_per_launch"] * 1e-3) / 1e9
-                         if iso else None,
+                         "achieved": ncu_traffic(cfg["name"]) / (k5_ms_launch * 1e-3) / 1e9,
                          "peak": peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]), "unit": "GB/s",
-                         "note": "ncu DRAM bytes of one 8-pitch K5 launch / its isolated time: far from bound"},
+                         "note": "ncu DRAM bytes of one K5 launch (profiles/ncu_k5_traffic.json) / the timed "
+                                 "region's average K5 launch time: far from bound"},
                      "secondary_alu": {"achieved": achieved_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
                                        "frac": achieved_tflops / fp32_peak,
                                        "flops_per_update": bp_flops_per_update()},
