@@ -59,7 +59,10 @@ def test_graph_replay_reconstruct_and_adjoint(name):
     assert float((aout - aref).double().norm()) <= 1e-5 * float(aref.double().norm())
 
 
-def test_graph_replay_batch():
+@pytest.mark.parametrize("n_slabs", [4, 16])
+def test_graph_replay_batch(n_slabs):
+    """4 slabs: one filter pass and one step-7 launch; 16: the two slab groups (filter of group 2
+    beside the backprojection of group 1 on forked streams, joined by events) captured as graph edges."""
     import numpy as np
     import torch
     import paper_2201_02309_b200 as k
@@ -69,7 +72,7 @@ def test_graph_replay_batch():
     p.precompute()
     v0, nv = p.pitch_views(0)
     slabs = np.stack([synth.project(cfg, configs.random_ellipsoids(b, 5, 180.0, 0.0, cfg["P"]), v0, nv)
-                      for b in range(4)])
+                      for b in range(n_slabs)])
     x = torch.from_numpy(slabs).cuda()
     ref = p.reconstruct_batch(x).clone()
     s = torch.cuda.Stream()
