@@ -147,3 +147,25 @@ def test_no_uninitialised_reads():
         assert torch.equal(r1, r0), name
         assert bool(torch.isfinite(a1).all()), name
         assert float((a1 - a0).double().norm()) <= 1e-5 * float(a0.double().norm()), name
+
+
+def test_graph_replay_adjoint_batch():
+    """katsevich_adjoint_batch captured and replayed: equal to the eager call to fp32 rounding."""
+    import torch
+    import paper_2201_02309_b200 as k
+    from synth import configs
+    cfg = configs.get("T2")
+    p = k.Plan(cfg, device=0)
+    p.precompute()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    y = torch.randn((4, cfg["nz"], cfg["ny"], cfg["nx"]), device="cuda", generator=g)
+    aref = p.adjoint_batch(y).clone()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    out = torch.empty_like(aref)
+    ga = _capture(lambda: p.adjoint_batch(y, out=out, stream=s), s)
+    out.zero_()
+    with torch.cuda.stream(s):
+        ga.replay()
+    torch.cuda.synchronize()
+    assert float((out - aref).double().norm()) <= 1e-5 * float(aref.double().norm())
