@@ -931,9 +931,10 @@ int katsevich_reconstruct_batch(katsevich_plan *p, const float *slabs, int32_t B
     // kernel's four slabs per CTA — C5 3.58 -> 3.49 ms, scripts/ab/gpu_r02h.sh; four groups: 3.94 ms)
     std::vector<int> gsz;                                       // slabs per group
     {
-        // (not with the half-sample derivative or the Hann filter: C5 6.49 -> 6.89 ms and 3.86 -> 3.95 ms
-        // in groups, measured in the bench's variants)
-        int ng = B >= 16 && B % 8 == 0 && !(p->g.flags & (KATS_FLAG_HALF_SAMPLE | KATS_FLAG_HANN)) ? 2 : 1;
+        // (not with the half-sample derivative or the Hann filter: C5 6.49 -> 6.87 ms and 3.86 -> 3.95 ms
+        // in groups, measured in the bench's variants; the caller's flags: the half-sample plan's
+        // effective grid p->g has that flag cleared)
+        int ng = B >= 16 && B % 8 == 0 && !(p->graw.flags & (KATS_FLAG_HALF_SAMPLE | KATS_FLAG_HANN)) ? 2 : 1;
         if (const char *e = std::getenv("KATS_BATCH_GROUPS")) ng = std::max(1, std::atoi(e));
         while (ng > 1 && (B % ng != 0 || ((B / ng) % 2 != 0 && B % 2 == 0))) --ng;
         gsz.assign(ng, B / ng);
