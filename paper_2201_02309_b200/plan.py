@@ -54,7 +54,8 @@ class Plan:
             raise KatsevichError(rc, "katsevich_plan_create")
         self.td_covered = None
         self._ws = None
-        self._ws_home = self._ws_last = self._ws_event = None
+        self._ws_home = self._ws_last = None
+        self._dev = None
         self._ws_graph = []                    # workspaces a captured CUDA graph uses
 
     # -- lifecycle ---------------------------------------------------------
@@ -132,15 +133,18 @@ class Plan:
     @contextlib.contextmanager
     def _ws_use(self, nbytes: int, stream):
         """The plan's one cached workspace for a call on `stream`.  Calls may come on different
-        streams (the default stream, a capture stream): the call waits for the workspace's previous
-        use when that ran on another stream, and the workspace is marked in use on every stream it
-        ran on, so the caching allocator does not hand it out while a kernel still reads it.  Not
-        while a CUDA graph is being captured (torch.cuda.graph synchronises the device on entry):
-        a captured graph keeps using this workspace, so it is then held for the plan's lifetime
-        (a later, larger workspace does not free it), and eager calls on the plan must not run
+        streams (the default stream, a capture stream): a call on another stream than the
+        workspace's previous use first waits for that stream (an event recorded there at the switch,
+        so same-stream calls pay nothing), and the workspace is marked in use on every stream it ran
+        on, so the caching allocator does not hand it out while a kernel still reads it.  Not while
+        a CUDA graph is being captured (torch.cuda.graph synchronises the device on entry): a
+        captured graph keeps using this workspace, so it is then held for the plan's lifetime (a
+        later, larger workspace does not free it), and eager calls on the plan must not run
         concurrently with the graph's replays."""
         import torch
-        dev = torch.device("cuda", self.device)
+        if self._dev is None:
+            self._dev = torch.device("cuda", self.device)
+        dev = self._dev
         if stream is None:
             st = torch.cuda.current_stream(dev)
         elif isinstance(stream, int):
@@ -154,16 +158,15 @@ class Plan:
             self._ws_last = None
         if not capturing:
             if self._ws_last is not None and self._ws_last != st:
-                st.wait_event(self._ws_event)
+                ev = torch.cuda.Event()
+                ev.record(self._ws_last)
+                st.wait_event(ev)
             if st != self._ws_home:
                 self._ws.record_stream(st)
         if capturing and not any(w is self._ws for w in self._ws_graph):
             self._ws_graph.append(self._ws)
         yield self._ws
         if not capturing:
-            if self._ws_event is None:
-                self._ws_event = torch.cuda.Event()
-            self._ws_event.record(st)
             self._ws_last = st
 
     def _vol_shape(self, n):
