@@ -2,7 +2,7 @@
 # bench command timed, and the ncu launch list of the C4 and C5 bench commands.
 set -x
 cd $GRAFT_REPO_ROOT
-R=r02z3
+R=r02zf
 make -s all > gpurun_out/build_$R.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$R.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$R.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$R.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$R.log
